@@ -1,0 +1,187 @@
+/*
+ * aires_b200.h -- C ABI of the B200-native AIRES out-of-core A·X SpGEMM path.
+ *
+ * The reference (arxiv 2507.02006, /root/reference/proj) is a header-only C++20
+ * library with no FFI; its "operator API" is the free functions of namespace
+ * aires.  This C ABI is the thin layer those functions now forward to (the
+ * drop-in C++ headers in include/aires/ call it; see INTEGRATION.md for the
+ * ctypes / C++ bindings).  Plain pointers and sizes only; no torch types.
+ *
+ * Entry point  -> reference interface it replaces
+ *   aires_b200_spgemm        -> aires::spgemm_block (raw spans)  spgemm.hpp:60-132
+ *                               aires::spgemm_block (segment)    spgemm.hpp:134-139
+ *                               aires::spgemm_full (Csr,Csc)     spgemm.hpp:142-146
+ *                               aires::spgemm_full (Csr,Csr)     spgemm.hpp:148-151
+ *   aires_b200_operand_*     -> the resident B of run_aires Phase I (scheduler.hpp:89-96)
+ *   aires_b200_spgemm_op     -> spgemm_block against a resident B (scheduler.hpp:124)
+ *   aires_b200_robw_cuts     -> aires::robw_partition cut search partition.hpp:52-74
+ *   aires_b200_run           -> aires::run_aires Phases I-III    scheduler.hpp:72-168
+ *                               (real multi-stream tile pipeline, C-aware tiles)
+ *   aires_b200_last_error    -> the what() string of aires::error error.hpp:53-62
+ *
+ * Status codes: 0 = OK, otherwise 1 + (int)aires::errc (error.hpp:9-27), so
+ * errc::index_out_of_range (0) is 1.  Codes >= 100 are device/runtime failures
+ * with no errc equivalent.  CUDA out-of-memory maps to
+ * insufficient_device_memory.  Every entry point is reentrant:
+ * each host thread gets its own CUDA stream and workspace on the current device.
+ */
+#ifndef AIRES_B200_H
+#define AIRES_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AIRES_B200_ABI_VERSION 1
+
+/* status codes (1 + errc) */
+enum {
+  AIRES_B200_OK = 0,
+  AIRES_B200_INDEX_OUT_OF_RANGE = 1,
+  AIRES_B200_UNSUPPORTED_FORMAT = 3,
+  AIRES_B200_INSUFFICIENT_DEVICE_MEMORY = 5,
+  AIRES_B200_ROW_TOO_LARGE = 6,
+  AIRES_B200_DIMENSION_MISMATCH = 8,
+  AIRES_B200_CAPACITY_EXCEEDED = 9,
+  AIRES_B200_CONFIG_ERROR = 17,
+  AIRES_B200_CUDA_ERROR = 100,
+  AIRES_B200_NO_DEVICE = 101,
+  AIRES_B200_INVALID_ARGUMENT = 102
+};
+
+/* where a buffer lives */
+enum { AIRES_B200_HOST = 0, AIRES_B200_DEVICE = 1 };
+/* sparse layouts */
+enum { AIRES_B200_CSR = 0, AIRES_B200_CSC = 1 };
+/* arithmetic modes */
+enum {
+  AIRES_B200_MODE_AUTO = 0,     /* FP64_EXACT if the values are 8 bytes wide, else FP32 */
+  AIRES_B200_MODE_FP32 = 1,     /* fp32 products and sums; order-free accumulation;
+                                   values within 1e-5 relative of the reference */
+  AIRES_B200_MODE_FP64_EXACT = 2 /* fp64, no FMA, each cell summed in ascending k from
+                                   +0.0: bit-identical to the reference (spgemm.hpp:21-42) */
+};
+
+/*
+ * A borrowed sparse matrix.  CSR: ptr has n_rows+1 entries, idx holds column
+ * indices.  CSC: ptr has n_cols+1 entries, idx holds row indices.  ptr is
+ * always 64-bit (index_t); it may be absolute, i.e. ptr[0] != 0, indexing into
+ * idx/val directly (spgemm.hpp:79-84).  idx_bytes in {4, 8}; val_bytes in {4, 8}.
+ * span = number of idx/val entries addressable (>= ptr[last]).
+ */
+typedef struct aires_b200_matrix {
+  uint64_t n_rows;
+  uint64_t n_cols;
+  uint32_t layout;
+  uint32_t location;
+  uint32_t idx_bytes;
+  uint32_t val_bytes;
+  const uint64_t* ptr;
+  const void* idx;
+  const void* val;
+  uint64_t span;
+} aires_b200_matrix;
+
+/*
+ * Output allocator.  Called once per product, after the symbolic pass, with
+ * the exact row and nnz counts (the exact allocation of spgemm.hpp:111-112).
+ * Must return buffers in out->location of n_rows+1 u64, nnz idx_bytes-wide
+ * and nnz val_bytes-wide entries.  Return 0 on success; any other value is
+ * passed back to the caller as the status.
+ */
+typedef int (*aires_b200_alloc_fn)(void* user, uint64_t n_rows, uint64_t nnz, void** ptr,
+                                   void** idx, void** val);
+
+typedef struct aires_b200_output {
+  uint32_t location;  /* where alloc() places C */
+  uint32_t idx_bytes; /* C col_idx width: 4 or 8 */
+  uint32_t val_bytes; /* C value width: 4 or 8 */
+  uint32_t reserved;
+  aires_b200_alloc_fn alloc;
+  void* user;
+  /* filled by the call */
+  uint64_t n_rows;
+  uint64_t n_cols;
+  uint64_t nnz;
+  uint64_t flops; /* multiply-accumulate count == CsrBlockResult.flops (spgemm.hpp:51) */
+} aires_b200_output;
+
+/* ---- library ----------------------------------------------------------- */
+int aires_b200_abi_version(void);
+const char* aires_b200_last_error(void);
+int aires_b200_device_count(int* count);
+/* Selects the CUDA device used by the calling thread (default 0). */
+int aires_b200_set_device(int device);
+
+/* ---- in-core product: C = A(rows) * B --------------------------------- */
+/*
+ * A: CSR rows (spgemm_block's row_ptr/col_idx/values spans; a->n_cols is a_n_cols).
+ * B: CSR or CSC, host or device.  Result columns are sorted ascending per row and
+ * cells with a structural hit are kept even when their sum is zero.
+ */
+int aires_b200_spgemm(const aires_b200_matrix* a, const aires_b200_matrix* b, uint32_t mode,
+                      aires_b200_output* c);
+
+/* ---- resident right operand -------------------------------------------- */
+typedef struct aires_b200_operand_s* aires_b200_operand;
+/* Uploads / converts B once (B200 row-major feature layout) on the current device. */
+int aires_b200_operand_create(const aires_b200_matrix* b, uint32_t mode,
+                              aires_b200_operand* out);
+int aires_b200_operand_destroy(aires_b200_operand op);
+int aires_b200_operand_info(aires_b200_operand op, uint64_t* n_rows, uint64_t* n_cols,
+                            uint64_t* nnz, uint32_t* mode, uint64_t* device_bytes);
+int aires_b200_spgemm_op(const aires_b200_matrix* a, aires_b200_operand b,
+                         aires_b200_output* c);
+
+/* ---- RoBW tiler (Alg. 1) ------------------------------------------------ */
+/*
+ * Greedy maximal whole-row segments with calc_mem(k,q) = (k+1)*I + q*(I+V) <= m_a,
+ * computed on the device (search over F(r) = r*I + row_ptr[r]*(I+V)).  cuts gets
+ * n_segs+1 boundaries (cuts[0] = 0, cuts[n_segs] = n_rows); cap = capacity of cuts.
+ * Returns AIRES_B200_ROW_TOO_LARGE with *bad_row set exactly as robw_partition
+ * throws (partition.hpp:64-69).  row_ptr may be host or device (location).
+ */
+int aires_b200_robw_cuts(const uint64_t* row_ptr, uint64_t n_rows, uint64_t m_a,
+                         uint64_t index_bytes, uint64_t value_bytes, uint32_t location,
+                         uint64_t* cuts, uint64_t cap, uint64_t* n_segs, uint64_t* bad_row);
+
+/* ---- out-of-core run (Alg. 2 as a real multi-stream pipeline) ---------- */
+typedef struct aires_b200_run_config {
+  uint64_t device_budget; /* bytes the run may hold on the device at once (0 = no cap) */
+  uint32_t mode;          /* AIRES_B200_MODE_* */
+  uint32_t c_aware;       /* 1: tiles sized by A + C bytes (default); 0: RoBW by A only */
+  uint32_t n_buffers;     /* tile ring depth (default 2) */
+  uint32_t reserved;
+} aires_b200_run_config;
+
+typedef struct aires_b200_run_report {
+  uint64_t segments;
+  uint64_t h2d_bytes; /* bytes actually copied host -> device */
+  uint64_t d2h_bytes; /* bytes actually copied device -> host */
+  uint64_t flops;
+  uint64_t c_nnz;
+  uint64_t peak_device_bytes;
+  double total_ms;   /* first H2D to last D2H, CUDA events */
+  double phase1_ms;  /* operand upload + symbolic sizing + cut */
+  double phase2_ms;  /* tile streaming */
+  double phase3_ms;  /* final drain / assembly */
+} aires_b200_run_report;
+
+/* A in host memory (CSR); B host or device; C written through c->alloc (host). */
+int aires_b200_run(const aires_b200_matrix* a, const aires_b200_matrix* b,
+                   const aires_b200_run_config* cfg, aires_b200_output* c,
+                   aires_b200_run_report* report);
+
+/* ---- timing helpers for harnesses (not part of the reference surface) --- */
+/* Elapsed ms of the last aires_b200_spgemm/_op on this thread (CUDA events). */
+double aires_b200_last_kernel_ms(void);
+/* Per-kernel ms of the last product on this thread: [classify, symbolic, scan, numeric,
+   x_prep, h2d, d2h]; returns the number of entries written (<= cap). */
+int aires_b200_last_profile(double* ms, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AIRES_B200_H */

@@ -1,0 +1,419 @@
+"""paper_2507_02006_b200 -- B200-native AIRES out-of-core A·X SpGEMM (arXiv 2507.02006).
+
+Python mirror of the reference's operator API for the hot path (namespace ``aires``,
+/root/reference/proj/include/aires/): ``CsrMatrix``/``CscMatrix`` (sparse.hpp:29-52),
+``spgemm_block`` (spgemm.hpp:60-139), ``spgemm_full`` (spgemm.hpp:142-151),
+``robw_partition`` (partition.hpp:52-74) and ``run_aires``-style out-of-core runs
+(scheduler.hpp:72-168), all backed by the C ABI of ``include/aires_b200.h``
+(``libaires_b200.so``, hand-written sm_100a kernels).  Errors are raised as
+``AiresError`` carrying the reference's ``errc`` code (error.hpp:9-27).
+
+There is no CPU fallback: if the CUDA library is missing or no device is visible,
+every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import enum
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libaires_b200.so")
+
+
+class errc(enum.IntEnum):
+    """aires::errc (error.hpp:9-27); the C ABI returns 1 + errc."""
+
+    index_out_of_range = 0
+    parse_error = 1
+    unsupported_format = 2
+    dense_too_large = 3
+    insufficient_device_memory = 4
+    row_too_large = 5
+    non_adjacent_fragments = 6
+    dimension_mismatch = 7
+    capacity_exceeded = 8
+    buffer_not_resident = 9
+    operand_not_on_device = 10
+    same_channel_conflict = 11
+    invalid_density = 12
+    non_square = 13
+    negative_weight = 14
+    io_error = 15
+    config_error = 16
+
+
+class AiresError(RuntimeError):
+    """aires::error (error.hpp:53-62): what() is "<errc name>: <detail>"."""
+
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        self.code: Optional[errc] = errc(status - 1) if 1 <= status <= 17 else None
+        name = self.code.name if self.code is not None else f"b200_status_{status}"
+        super().__init__(f"{name}: {detail}")
+
+
+HOST, DEVICE = 0, 1
+CSR, CSC = 0, 1
+MODE_AUTO, MODE_FP32, MODE_FP64_EXACT = 0, 1, 2
+
+
+class _Matrix(C.Structure):
+    _fields_ = [
+        ("n_rows", C.c_uint64), ("n_cols", C.c_uint64), ("layout", C.c_uint32),
+        ("location", C.c_uint32), ("idx_bytes", C.c_uint32), ("val_bytes", C.c_uint32),
+        ("ptr", C.c_void_p), ("idx", C.c_void_p), ("val", C.c_void_p), ("span", C.c_uint64),
+    ]
+
+
+_ALLOC_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_void_p),
+                        C.POINTER(C.c_void_p), C.POINTER(C.c_void_p))
+
+
+class _Output(C.Structure):
+    _fields_ = [
+        ("location", C.c_uint32), ("idx_bytes", C.c_uint32), ("val_bytes", C.c_uint32),
+        ("reserved", C.c_uint32), ("alloc", _ALLOC_FN), ("user", C.c_void_p),
+        ("n_rows", C.c_uint64), ("n_cols", C.c_uint64), ("nnz", C.c_uint64), ("flops", C.c_uint64),
+    ]
+
+
+class _RunConfig(C.Structure):
+    _fields_ = [("device_budget", C.c_uint64), ("mode", C.c_uint32), ("c_aware", C.c_uint32),
+                ("n_buffers", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+class _RunReport(C.Structure):
+    _fields_ = [("segments", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("flops", C.c_uint64), ("c_nnz", C.c_uint64), ("peak_device_bytes", C.c_uint64),
+                ("total_ms", C.c_double), ("phase1_ms", C.c_double), ("phase2_ms", C.c_double),
+                ("phase3_ms", C.c_double)]
+
+
+class _GraphSpec(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("target_nnz", C.c_uint64), ("alpha", C.c_double),
+                ("degree_cap", C.c_uint64), ("seed", C.c_uint64), ("relabel_seed", C.c_uint64),
+                ("relabel", C.c_int32), ("normalize", C.c_int32), ("threads", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads libaires_b200.so; raises (never falls back) if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the B200 path has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    L.aires_b200_abi_version.restype = C.c_int
+    L.aires_b200_last_error.restype = C.c_char_p
+    L.aires_b200_device_count.argtypes = [P(C.c_int)]
+    L.aires_b200_set_device.argtypes = [C.c_int]
+    L.aires_b200_spgemm.argtypes = [P(_Matrix), P(_Matrix), C.c_uint32, P(_Output)]
+    L.aires_b200_operand_create.argtypes = [P(_Matrix), C.c_uint32, P(C.c_void_p)]
+    L.aires_b200_operand_destroy.argtypes = [C.c_void_p]
+    L.aires_b200_operand_info.argtypes = [C.c_void_p, P(C.c_uint64), P(C.c_uint64), P(C.c_uint64),
+                                          P(C.c_uint32), P(C.c_uint64)]
+    L.aires_b200_spgemm_op.argtypes = [P(_Matrix), C.c_void_p, P(_Output)]
+    L.aires_b200_robw_cuts.argtypes = [P(C.c_uint64), C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                       C.c_uint32, P(C.c_uint64), C.c_uint64, P(C.c_uint64),
+                                       P(C.c_uint64)]
+    L.aires_b200_run.argtypes = [P(_Matrix), P(_Matrix), P(_RunConfig), P(_Output), P(_RunReport)]
+    L.aires_b200_last_kernel_ms.restype = C.c_double
+    L.aires_b200_last_profile.argtypes = [P(C.c_double), C.c_int]
+    L.aires_b200_synth_graph.argtypes = [P(_GraphSpec), P(_Output), P(C.c_double)]
+    L.aires_b200_synth_features.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, P(_Output)]
+    L.aires_b200_synth_last_error.restype = C.c_char_p
+    _lib = L
+    return L
+
+
+def _check(rc: int, synth: bool = False) -> None:
+    if rc != 0:
+        L = lib()
+        msg = (L.aires_b200_synth_last_error() if synth else L.aires_b200_last_error()) or b""
+        raise AiresError(rc, msg.decode(errors="replace"))
+
+
+# ---------------------------------------------------------------------------
+# containers (sparse.hpp:29-52), numpy-backed at API widths by default
+# ---------------------------------------------------------------------------
+
+@dataclasses.dataclass
+class CsrMatrix:
+    n_rows: int
+    n_cols: int
+    row_ptr: np.ndarray  # uint64, n_rows+1
+    col_idx: np.ndarray  # uint64 (or uint32)
+    values: np.ndarray   # float64 (or float32)
+
+    def nnz(self) -> int:
+        return int(self.col_idx.shape[0])
+
+    def __eq__(self, o) -> bool:  # operator== (sparse.hpp:38): bit equality of every array
+        return (self.n_rows == o.n_rows and self.n_cols == o.n_cols
+                and np.array_equal(self.row_ptr.astype(np.uint64), o.row_ptr.astype(np.uint64))
+                and np.array_equal(self.col_idx.astype(np.uint64), o.col_idx.astype(np.uint64))
+                and self.values.dtype == o.values.dtype
+                and np.array_equal(self.values.view(np.uint8), o.values.view(np.uint8)))
+
+
+@dataclasses.dataclass
+class CscMatrix:
+    n_rows: int
+    n_cols: int
+    col_ptr: np.ndarray
+    row_idx: np.ndarray
+    values: np.ndarray
+
+    def nnz(self) -> int:
+        return int(self.row_idx.shape[0])
+
+
+@dataclasses.dataclass
+class CsrBlockResult:
+    """spgemm.hpp:47-52"""
+    start_row: int
+    end_row: int
+    fragment: CsrMatrix
+    flops: int
+
+
+@dataclasses.dataclass
+class ElementSizes:
+    """sparse.hpp:21-24"""
+    index_bytes: int = 8
+    value_bytes: int = 8
+
+
+def _np_view(arr: np.ndarray) -> int:
+    return arr.ctypes.data if arr.size else 0
+
+
+def _matrix_from_np(n_rows, n_cols, layout, ptr, idx, val) -> tuple:
+    ptr = np.ascontiguousarray(ptr, dtype=np.uint64)
+    idx = np.ascontiguousarray(idx)
+    val = np.ascontiguousarray(val)
+    if idx.dtype not in (np.uint32, np.uint64, np.int32, np.int64):
+        idx = idx.astype(np.uint64)
+    if val.dtype not in (np.float32, np.float64):
+        val = val.astype(np.float64)
+    m = _Matrix(n_rows, n_cols, layout, HOST, idx.dtype.itemsize, val.dtype.itemsize,
+                _np_view(ptr), _np_view(idx), _np_view(val), idx.shape[0])
+    return m, (ptr, idx, val)
+
+
+class _HostAlloc:
+    """Output allocator handing out numpy arrays (the exact allocation, spgemm.hpp:111-112)."""
+
+    def __init__(self, idx_dtype, val_dtype):
+        self.idx_dtype, self.val_dtype = idx_dtype, val_dtype
+        self.ptr = self.idx = self.val = None
+        self.fn = _ALLOC_FN(self._alloc)
+
+    def _alloc(self, user, n_rows, nnz, pptr, pidx, pval):
+        try:
+            self.ptr = np.zeros(n_rows + 1, dtype=np.uint64)
+            self.idx = np.empty(max(nnz, 1), dtype=self.idx_dtype)
+            self.val = np.empty(max(nnz, 1), dtype=self.val_dtype)
+            self.nnz = nnz
+            pptr[0] = self.ptr.ctypes.data
+            pidx[0] = self.idx.ctypes.data
+            pval[0] = self.val.ctypes.data
+            return 0
+        except MemoryError:
+            return 9  # 1 + capacity_exceeded
+
+    def output(self, location=HOST) -> _Output:
+        return _Output(location, np.dtype(self.idx_dtype).itemsize, np.dtype(self.val_dtype).itemsize, 0,
+                       self.fn, None, 0, 0, 0, 0)
+
+
+def _mode_for(values: np.ndarray, mode: int) -> int:
+    if mode != MODE_AUTO:
+        return mode
+    return MODE_FP64_EXACT if values.dtype == np.float64 else MODE_FP32
+
+
+def spgemm_rows(row_ptr, col_idx, values, rows: int, a_n_cols: int, b, mode: int = MODE_AUTO,
+                idx_dtype=None) -> tuple:
+    """Raw-span product (spgemm.hpp:60-132).  ``b`` is a CscMatrix, CsrMatrix or Operand.
+    Returns (CsrMatrix fragment with rebased row_ptr, flops)."""
+    L = lib()
+    a, keep_a = _matrix_from_np(rows, a_n_cols, CSR, row_ptr, col_idx, values)
+    mode = _mode_for(keep_a[2], mode)
+    vdt = np.float64 if mode == MODE_FP64_EXACT else np.float32
+    al = _HostAlloc(idx_dtype or keep_a[1].dtype, vdt)
+    out = al.output()
+    if isinstance(b, Operand):
+        _check(L.aires_b200_spgemm_op(C.byref(a), b.handle, C.byref(out)))
+        bcols = b.n_cols
+    else:
+        bm, keep_b = _operand_matrix(b)
+        _check(L.aires_b200_spgemm(C.byref(a), C.byref(bm), mode, C.byref(out)))
+        bcols = b.n_cols
+    frag = CsrMatrix(rows, bcols, al.ptr, al.idx[: out.nnz], al.val[: out.nnz])
+    return frag, int(out.flops)
+
+
+def _operand_matrix(b):
+    if isinstance(b, CscMatrix):
+        return _matrix_from_np(b.n_rows, b.n_cols, CSC, b.col_ptr, b.row_idx, b.values)
+    if isinstance(b, CsrMatrix):
+        return _matrix_from_np(b.n_rows, b.n_cols, CSR, b.row_ptr, b.col_idx, b.values)
+    raise TypeError("operand must be CsrMatrix or CscMatrix")
+
+
+def spgemm_block(row_ptr, col_idx, values, rows: int, a_n_cols: int, b, start_row: int = 0,
+                 tile_cols: int = 256, mode: int = MODE_AUTO) -> CsrBlockResult:
+    """spgemm.hpp:60-132 (tile_cols only changes traversal order in the reference; the
+    B200 kernels have no column tiling, results are identical by construction)."""
+    del tile_cols
+    frag, flops = spgemm_rows(row_ptr, col_idx, values, rows, a_n_cols, b, mode)
+    return CsrBlockResult(start_row, start_row + rows, frag, flops)
+
+
+def spgemm_full(a: CsrMatrix, b, tile_cols: int = 256, mode: int = MODE_AUTO) -> CsrMatrix:
+    """spgemm.hpp:142-151: one block spanning every row; b is CSC or CSR."""
+    return spgemm_block(a.row_ptr, a.col_idx, a.values, a.n_rows, a.n_cols, b, 0, tile_cols, mode).fragment
+
+
+class Operand:
+    """A resident right operand (the device-resident B of run_aires Phase I)."""
+
+    def __init__(self, b, mode: int = MODE_AUTO):
+        L = lib()
+        bm, self._keep = _operand_matrix(b)
+        self.n_rows, self.n_cols = b.n_rows, b.n_cols
+        h = C.c_void_p()
+        _check(L.aires_b200_operand_create(C.byref(bm), _mode_for(self._keep[2], mode), C.byref(h)))
+        self.handle = h
+        self._keep = None
+
+    def info(self) -> dict:
+        L = lib()
+        r, c, z, b = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        m = C.c_uint32()
+        _check(L.aires_b200_operand_info(self.handle, C.byref(r), C.byref(c), C.byref(z), C.byref(m), C.byref(b)))
+        return dict(n_rows=r.value, n_cols=c.value, nnz=z.value, mode=m.value, device_bytes=b.value)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().aires_b200_operand_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def robw_cuts(row_ptr: np.ndarray, m_a: int, sizes: ElementSizes = ElementSizes()) -> np.ndarray:
+    """Device RoBW cut search (partition.hpp:52-74); returns the n_segs+1 boundaries."""
+    L = lib()
+    rp = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+    n = rp.shape[0] - 1
+    cuts = np.zeros(n + 1, dtype=np.uint64)
+    ns, bad = C.c_uint64(), C.c_uint64()
+    P = C.POINTER(C.c_uint64)
+    rc = L.aires_b200_robw_cuts(rp.ctypes.data_as(P), n, m_a, sizes.index_bytes, sizes.value_bytes, HOST,
+                                cuts.ctypes.data_as(P), cuts.shape[0], C.byref(ns), C.byref(bad))
+    if rc == 6:
+        raise AiresError(rc, f"row {bad.value} needs more than the block budget {m_a}")
+    _check(rc)
+    return cuts[: ns.value + 1].copy()
+
+
+@dataclasses.dataclass
+class RobwSegment:
+    """partition.hpp:20-31"""
+    seg_index: int
+    start_row: int
+    end_row: int
+    row_ptr_local: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+    byte_size: int
+
+    def rows(self) -> int:
+        return self.end_row - self.start_row
+
+    def nnz(self) -> int:
+        return int(self.col_idx.shape[0])
+
+
+def calc_mem(k: int, q: int, s: ElementSizes = ElementSizes()) -> int:
+    """memory_model.hpp:84-86"""
+    return (k + 1) * s.index_bytes + q * (s.index_bytes + s.value_bytes)
+
+
+def robw_partition(a: CsrMatrix, m_a: int, s: ElementSizes = ElementSizes()) -> list:
+    """partition.hpp:52-74: cuts from the device tiler, segments sliced like slice_rows (:33-47)."""
+    cuts = robw_cuts(a.row_ptr, m_a, s)
+    segs = []
+    for i in range(len(cuts) - 1):
+        r0, r1 = int(cuts[i]), int(cuts[i + 1])
+        base = int(a.row_ptr[r0])
+        end = int(a.row_ptr[r1])
+        local = (a.row_ptr[r0:r1 + 1] - np.uint64(base)).astype(np.uint64)
+        segs.append(RobwSegment(i, r0, r1, local, a.col_idx[base:end].copy(), a.values[base:end].copy(),
+                                calc_mem(r1 - r0, end - base, s)))
+    return segs
+
+
+def last_profile() -> dict:
+    L = lib()
+    arr = (C.c_double * 7)()
+    n = L.aires_b200_last_profile(arr, 7)
+    names = ["classify", "symbolic", "scan", "numeric", "x_prep", "h2d", "d2h"]
+    d = {names[i]: arr[i] for i in range(n)}
+    d["total"] = L.aires_b200_last_kernel_ms()
+    return d
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(lib().aires_b200_device_count(C.byref(n)))
+    return n.value
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs
+# ---------------------------------------------------------------------------
+
+def synth_graph(n: int, target_nnz: int, alpha: float = 0.75, degree_cap: int = 20000, seed: int = 1,
+                relabel_seed: int = 2, relabel: bool = True, normalize: bool = True, threads: int = 0,
+                idx_dtype=np.uint32, val_dtype=np.float64) -> tuple:
+    """Chung-Lu power-law graph -> (CsrMatrix Ã (or A), stats dict)."""
+    L = lib()
+    al = _HostAlloc(idx_dtype, val_dtype)
+    out = al.output()
+    spec = _GraphSpec(n, target_nnz, alpha, degree_cap, seed, relabel_seed, int(relabel), int(normalize),
+                      threads, 0)
+    st = (C.c_double * 8)()
+    _check(L.aires_b200_synth_graph(C.byref(spec), C.byref(out), st), synth=True)
+    m = CsrMatrix(n, n, al.ptr, al.idx[: out.nnz], al.val[: out.nnz])
+    stats = dict(nnz_a=int(st[0]), max_degree=int(st[1]), mean_degree=st[2], rounds=int(st[3]),
+                 seconds=st[4], i0=st[5])
+    return m, stats
+
+
+def synth_features(n: int, dim: int, sparsity_pct: float = 99.0, seed: int = 3, idx_dtype=np.uint32,
+                   val_dtype=np.float64) -> CsrMatrix:
+    """gen_features (synth.hpp:73-78), draw-for-draw identical."""
+    L = lib()
+    al = _HostAlloc(idx_dtype, val_dtype)
+    out = al.output()
+    _check(L.aires_b200_synth_features(n, dim, sparsity_pct, seed, C.byref(out)), synth=True)
+    return CsrMatrix(n, dim, al.ptr, al.idx[: out.nnz], al.val[: out.nnz])

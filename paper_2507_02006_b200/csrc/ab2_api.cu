@@ -1,0 +1,249 @@
+// ab2_api.cu -- the extern "C" boundary (include/aires_b200.h) and per-thread contexts.
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "ab2_internal.h"
+
+namespace ab2 {
+
+namespace {
+thread_local std::string tl_error;
+thread_local int tl_device = 0;
+thread_local std::map<int, std::unique_ptr<Ctx>> tl_ctx;
+}  // namespace
+
+void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();
+  int code = e == cudaErrorMemoryAllocation ? AIRES_B200_INSUFFICIENT_DEVICE_MEMORY
+             : (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) ? AIRES_B200_NO_DEVICE
+                                                                             : AIRES_B200_CUDA_ERROR;
+  fail(code, std::string(cudaGetErrorString(e)) + " in " + what + " (" + file + ":" + std::to_string(line) + ")");
+}
+
+int64_t env_int(const char* name, int64_t def) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return def;
+  return std::strtoll(v, nullptr, 10);
+}
+
+void* DevBuf::get(size_t bytes) {
+  bytes = std::max<size_t>(bytes, 256);
+  if (bytes <= cap) return p;
+  release();
+  size_t want = bytes + bytes / 8;
+  cudaError_t e = cudaMalloc(&p, want);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    p = nullptr;
+    e = cudaMalloc(&p, bytes);
+    want = bytes;
+  }
+  if (e != cudaSuccess) {
+    p = nullptr;
+    cap = 0;
+    check_cuda(e, "cudaMalloc(workspace)", __FILE__, __LINE__);
+  }
+  cap = want;
+  return p;
+}
+
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+}
+
+void* HostBuf::get(size_t bytes) {
+  bytes = std::max<size_t>(bytes, 256);
+  if (bytes <= cap) return p;
+  release();
+  AB2_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
+  cap = bytes;
+  return p;
+}
+
+void HostBuf::release() {
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  cap = 0;
+}
+
+Ctx::Ctx(int dev) : device(dev) {
+  AB2_CUDA(cudaSetDevice(dev));
+  AB2_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  AB2_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  for (auto& e : ev) AB2_CUDA(cudaEventCreate(&e));
+}
+
+Ctx::~Ctx() {
+  // Best effort: the CUDA runtime may already be torn down at thread/process exit.
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+int current_device() { return tl_device; }
+
+Ctx& ctx_for_thread() {
+  auto it = tl_ctx.find(tl_device);
+  if (it != tl_ctx.end()) {
+    AB2_CUDA(cudaSetDevice(tl_device));
+    return *it->second;
+  }
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    fail(AIRES_B200_NO_DEVICE, "no CUDA device is visible (the B200 path has no CPU fallback)");
+  }
+  auto c = std::make_unique<Ctx>(tl_device);
+  Ctx& ref = *c;
+  tl_ctx[tl_device] = std::move(c);
+  return ref;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    tl_error.clear();
+    return AIRES_B200_OK;
+  } catch (const Error& e) {
+    tl_error = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    tl_error = e.what();
+    return AIRES_B200_CUDA_ERROR;
+  } catch (...) {
+    tl_error = "unknown failure";
+    return AIRES_B200_CUDA_ERROR;
+  }
+}
+
+}  // namespace ab2
+
+struct aires_b200_operand_s {
+  std::unique_ptr<ab2::XOperand> x;
+};
+
+extern "C" {
+
+int aires_b200_abi_version(void) { return AIRES_B200_ABI_VERSION; }
+
+const char* aires_b200_last_error(void) { return ab2::tl_error.c_str(); }
+
+int aires_b200_device_count(int* count) {
+  return ab2::guarded([&] {
+    if (!count) ab2::fail(AIRES_B200_INVALID_ARGUMENT, "count is null");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *count = n;
+  });
+}
+
+int aires_b200_set_device(int device) {
+  return ab2::guarded([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+      cudaGetLastError();
+      ab2::fail(AIRES_B200_NO_DEVICE, "device " + std::to_string(device) + " is not visible");
+    }
+    ab2::tl_device = device;
+  });
+}
+
+int aires_b200_spgemm(const aires_b200_matrix* a, const aires_b200_matrix* b, uint32_t mode,
+                      aires_b200_output* c) {
+  return ab2::guarded([&] {
+    if (!a || !b || !c) ab2::fail(AIRES_B200_INVALID_ARGUMENT, "null argument");
+    if (a->n_cols != b->n_rows)
+      ab2::fail(AIRES_B200_DIMENSION_MISMATCH, "inner dimensions " + std::to_string(a->n_cols) + " and " +
+                                                   std::to_string(b->n_rows) + " differ");
+    ab2::Ctx& ctx = ab2::ctx_for_thread();
+    if (mode == AIRES_B200_MODE_AUTO) mode = c->val_bytes == 8 ? AIRES_B200_MODE_FP64_EXACT : AIRES_B200_MODE_FP32;
+    cudaEvent_t t0 = ctx.ev[10], t1 = ctx.ev[11];
+    AB2_CUDA(cudaEventRecord(t0, ctx.stream));
+    auto x = ab2::make_operand(ctx, *b, mode);
+    AB2_CUDA(cudaEventRecord(t1, ctx.stream));
+    AB2_CUDA(cudaEventSynchronize(t1));
+    float ms = 0;
+    AB2_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+    ab2::spgemm_rows(ctx, *a, *x, *c);
+    ctx.prof[ab2::kPXPrep] = ms;
+  });
+}
+
+int aires_b200_operand_create(const aires_b200_matrix* b, uint32_t mode, aires_b200_operand* out) {
+  return ab2::guarded([&] {
+    if (!b || !out) ab2::fail(AIRES_B200_INVALID_ARGUMENT, "null argument");
+    ab2::Ctx& ctx = ab2::ctx_for_thread();
+    auto op = std::make_unique<aires_b200_operand_s>();
+    op->x = ab2::make_operand(ctx, *b, mode);
+    *out = op.release();
+  });
+}
+
+int aires_b200_operand_destroy(aires_b200_operand op) {
+  return ab2::guarded([&] { delete op; });
+}
+
+int aires_b200_operand_info(aires_b200_operand op, uint64_t* n_rows, uint64_t* n_cols, uint64_t* nnz,
+                            uint32_t* mode, uint64_t* device_bytes) {
+  return ab2::guarded([&] {
+    if (!op || !op->x) ab2::fail(AIRES_B200_INVALID_ARGUMENT, "null operand");
+    if (n_rows) *n_rows = static_cast<uint64_t>(op->x->K);
+    if (n_cols) *n_cols = static_cast<uint64_t>(op->x->n_cols);
+    if (nnz) *nnz = static_cast<uint64_t>(op->x->nnz);
+    if (mode) *mode = op->x->mode;
+    if (device_bytes) *device_bytes = op->x->bytes;
+  });
+}
+
+int aires_b200_spgemm_op(const aires_b200_matrix* a, aires_b200_operand b, aires_b200_output* c) {
+  return ab2::guarded([&] {
+    if (!a || !b || !b->x || !c) ab2::fail(AIRES_B200_INVALID_ARGUMENT, "null argument");
+    ab2::Ctx& ctx = ab2::ctx_for_thread();
+    if (b->x->device != ctx.device)
+      ab2::fail(AIRES_B200_INVALID_ARGUMENT, "operand lives on another device");
+    ab2::spgemm_rows(ctx, *a, *b->x, *c);
+    ctx.prof[ab2::kPXPrep] = 0.0;
+  });
+}
+
+int aires_b200_robw_cuts(const uint64_t* row_ptr, uint64_t n_rows, uint64_t m_a, uint64_t index_bytes,
+                         uint64_t value_bytes, uint32_t location, uint64_t* cuts, uint64_t cap,
+                         uint64_t* n_segs, uint64_t* bad_row) {
+  int rc = AIRES_B200_OK;
+  int g = ab2::guarded([&] {
+    if (!row_ptr || !cuts || !n_segs) ab2::fail(AIRES_B200_INVALID_ARGUMENT, "null argument");
+    ab2::Ctx& ctx = ab2::ctx_for_thread();
+    rc = ab2::robw_cuts(ctx, row_ptr, n_rows, m_a, index_bytes, value_bytes, location, cuts, cap, n_segs,
+                        bad_row);
+  });
+  return g != AIRES_B200_OK ? g : rc;
+}
+
+double aires_b200_last_kernel_ms(void) {
+  auto it = ab2::tl_ctx.find(ab2::tl_device);
+  return it == ab2::tl_ctx.end() ? 0.0 : it->second->last_ms;
+}
+
+int aires_b200_last_profile(double* ms, int cap) {
+  auto it = ab2::tl_ctx.find(ab2::tl_device);
+  int n = 0;
+  for (; n < cap && n < ab2::kPCount; n++) ms[n] = it == ab2::tl_ctx.end() ? 0.0 : it->second->prof[n];
+  return n;
+}
+
+}  // extern "C"

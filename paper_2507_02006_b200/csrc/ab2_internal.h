@@ -1,0 +1,86 @@
+// ab2_internal.h -- host-side internals shared by the library translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "ab2_common.cuh"
+
+namespace ab2 {
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes);
+  template <class T>
+  T* as(size_t n) {
+    return static_cast<T*>(get(n * sizeof(T)));
+  }
+  void release();
+  ~DevBuf() { release(); }
+};
+
+// Grow-only pinned host buffer.
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes);
+  void release();
+  ~HostBuf() { release(); }
+};
+
+enum ProfSlot { kPClassify, kPSymbolic, kPScan, kPNumeric, kPXPrep, kPH2D, kPD2H, kPCount };
+
+// Per-thread, per-device execution context (reentrancy: SURVEY.md §8b Threading).
+struct Ctx {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[2 * kPCount + 2] = {};
+  DevBuf a_ptr, a_col, a_val, a_col2, a_val2;  // uploaded / converted A
+  DevBuf cnt, rflops, cptr, scan_part, sym_heavy, num_heavy, fix_rows, ctl;
+  DevBuf c_col, c_val;                          // C staging for host outputs
+  DevBuf x_ptr, x_idx, x_val;                   // raw X upload (host operands)
+  HostBuf h_ctl;
+  double prof[kPCount] = {};
+  double last_ms = 0.0;
+  explicit Ctx(int dev);
+  ~Ctx();
+};
+
+Ctx& ctx_for_thread();
+int current_device();
+
+// A prepared right operand (B200 feature layout), see ab2_operand.cuh.
+struct XOperand {
+  int device = 0;
+  uint32_t mode = 0;  // AIRES_B200_MODE_FP32 or _FP64_EXACT
+  int64_t K = 0, n_cols = 0, nnz = 0;
+  int W = 0;
+  void* ptr = nullptr;     // int64 K+1
+  void* col = nullptr;     // int32 nnz
+  void* val = nullptr;     // V nnz
+  void* slots = nullptr;   // K*W entries
+  void* cslots = nullptr;  // K*W u16
+  size_t bytes = 0;
+  ~XOperand();
+};
+
+// Builds an operand from a matrix view (host or device, CSR or CSC).
+std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode);
+
+// C = A * X; A is a CSR rows view (host or device).
+void spgemm_rows(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_b200_output& out);
+
+// RoBW cuts on the device.
+int robw_cuts(Ctx& ctx, const uint64_t* row_ptr, uint64_t n_rows, uint64_t m_a, uint64_t I,
+              uint64_t V, uint32_t location, uint64_t* cuts, uint64_t cap, uint64_t* n_segs,
+              uint64_t* bad_row);
+
+int64_t env_int(const char* name, int64_t def);
+
+}  // namespace ab2

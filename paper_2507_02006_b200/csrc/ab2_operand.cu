@@ -1,0 +1,360 @@
+// ab2_operand.cu -- builds the B200 feature layout of X (ab2_operand.cuh) on the device.
+//
+// Accepts X as CSR (spgemm_full(Csr,Csr), spgemm.hpp:148-151) or CSC (the form the
+// reference kernel takes, spgemm.hpp:63); CSC is transposed on the device (the
+// reference's csc_to_csr, sparse.hpp:142-163: columns ascend within each row).
+#include <algorithm>
+#include <cstring>
+
+#include "ab2_internal.h"
+#include "ab2_kernels.cuh"
+
+namespace ab2 {
+
+namespace {
+
+template <class IdxT, class VIn, class V>
+__global__ void k_x_from_csr(const uint64_t* __restrict__ ptr, uint64_t p0, int64_t K,
+                             const IdxT* __restrict__ idx, const VIn* __restrict__ val, int64_t nnz,
+                             int64_t n_cols, int64_t* __restrict__ xptr, int32_t* __restrict__ xcol,
+                             V* __restrict__ xval, Ctl* __restrict__ ctl) {
+  int64_t n = max(K + 1, nnz);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i <= K) xptr[i] = static_cast<int64_t>(ptr[i] - p0);
+    if (i < nnz) {
+      uint64_t c = static_cast<uint64_t>(idx[i]);
+      if (c >= static_cast<uint64_t>(n_cols)) ctl->bad_row = 1;
+      xcol[i] = static_cast<int32_t>(c);
+      xval[i] = static_cast<V>(val[i]);
+    }
+  }
+}
+
+template <class IdxT>
+__global__ void k_csc_count(const IdxT* __restrict__ ridx, int64_t nnz, int64_t K,
+                            int32_t* __restrict__ counts, Ctl* __restrict__ ctl) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t r = static_cast<uint64_t>(ridx[i]);
+    if (r >= static_cast<uint64_t>(K)) {
+      ctl->bad_row = 1;
+      continue;
+    }
+    atomicAdd(&counts[r], 1);
+  }
+}
+
+template <class IdxT, class VIn, class V>
+__global__ void k_csc_scatter(const uint64_t* __restrict__ cptr, uint64_t p0, int64_t n_cols,
+                              const IdxT* __restrict__ ridx, const VIn* __restrict__ val, int64_t nnz,
+                              int64_t K, const int64_t* __restrict__ xptr, int32_t* __restrict__ cursor,
+                              int32_t* __restrict__ xcol, V* __restrict__ xval) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t q = p0 + static_cast<uint64_t>(i);
+    int64_t lo = 0, hi = n_cols + 1;  // upper_bound(q) over cptr[0..n_cols]
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (cptr[mid] <= q)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    int64_t c = lo - 1;
+    uint64_t r = static_cast<uint64_t>(ridx[i]);
+    if (r >= static_cast<uint64_t>(K)) continue;
+    int64_t pos = xptr[r] + atomicAdd(&cursor[r], 1);
+    xcol[pos] = static_cast<int32_t>(c);
+    xval[pos] = static_cast<V>(val[i]);
+  }
+}
+
+// Rows of X are short on the dense path; insertion sort restores ascending columns
+// after the unordered scatter (columns are unique per row, so the result is unique).
+template <class V>
+__global__ void k_row_sort(const int64_t* __restrict__ xptr, int64_t K, int32_t* __restrict__ xcol,
+                           V* __restrict__ xval) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t s = xptr[k], e = xptr[k + 1];
+    for (int64_t i = s + 1; i < e; i++) {
+      int32_t c = xcol[i];
+      V v = xval[i];
+      int64_t j = i - 1;
+      while (j >= s && xcol[j] > c) {
+        xcol[j + 1] = xcol[j];
+        xval[j + 1] = xval[j];
+        j--;
+      }
+      xcol[j + 1] = c;
+      xval[j + 1] = v;
+    }
+  }
+}
+
+__global__ void k_len_hist(const int64_t* __restrict__ xptr, int64_t K,
+                           unsigned long long* __restrict__ h) {
+  __shared__ int64_t tmp[32];
+  int64_t c[5] = {0, 0, 0, 0, 0};
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t n = xptr[k + 1] - xptr[k];
+    c[0] += n > 2;
+    c[1] += n > 4;
+    c[2] += n > 8;
+    c[3] += n > 16;
+    c[4] = max(c[4], n);
+  }
+  for (int j = 0; j < 4; j++) {
+    int64_t s = block_sum<int64_t>(c[j], tmp);
+    if (threadIdx.x == 0 && s) atomicAdd(&h[j], static_cast<unsigned long long>(s));
+  }
+  int64_t m = c[4];
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&h[4], static_cast<unsigned long long>(m));
+}
+
+template <class V, int W>
+__global__ void k_x_slots(const int64_t* __restrict__ xptr, const int32_t* __restrict__ xcol,
+                          const V* __restrict__ xval, int64_t K, typename SlotOf<V>::type* __restrict__ slots,
+                          uint16_t* __restrict__ cslots) {
+  using S = typename SlotOf<V>::type;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t s = xptr[k], n = xptr[k + 1] - s;
+    S* out = slots + k * W;
+    uint16_t* cout = cslots + k * W;
+    const bool ovf = n > W;
+    const int inl = ovf ? W - 1 : static_cast<int>(n);
+#pragma unroll
+    for (int e = 0; e < W; e++) {
+      S en{};
+      uint16_t ce = kCEmpty;
+      if (e < inl) {
+        en.col = static_cast<uint32_t>(xcol[s + e]);
+        en.val = xval[s + e];
+        ce = static_cast<uint16_t>(xcol[s + e]);
+      } else if (ovf && e == W - 1) {
+        en.col = kSlotOvf | static_cast<uint32_t>(n - (W - 1));
+        if constexpr (sizeof(V) == 4)
+          en.val = __uint_as_float(static_cast<uint32_t>(s + W - 1));
+        else
+          en.val = __longlong_as_double(static_cast<long long>(s + W - 1));
+        ce = kCOvf;
+      } else {
+        en.col = kSlotEmpty;
+        en.val = V(0);
+      }
+      out[e] = en;
+      cout[e] = ce;
+    }
+  }
+}
+
+int grid_for(int64_t n, int threads, int sms) {
+  int64_t b = (n + threads - 1) / threads;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, static_cast<int64_t>(sms) * 32)));
+}
+
+template <class V>
+void build_slots(Ctx& ctx, XOperand& x) {
+  int g = grid_for(x.K, 256, ctx.sms);
+  using S = typename SlotOf<V>::type;
+  auto* sl = static_cast<S*>(x.slots);
+  auto* cs = static_cast<uint16_t*>(x.cslots);
+  auto* xp = static_cast<int64_t*>(x.ptr);
+  auto* xc = static_cast<int32_t*>(x.col);
+  auto* xv = static_cast<V*>(x.val);
+  switch (x.W) {
+    case 2: k_x_slots<V, 2><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, sl, cs); break;
+    case 4: k_x_slots<V, 4><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, sl, cs); break;
+    case 8: k_x_slots<V, 8><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, sl, cs); break;
+    default: k_x_slots<V, 16><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, sl, cs); break;
+  }
+  AB2_CUDA(cudaGetLastError());
+}
+
+template <class IdxT, class VIn, class V>
+void fill_plain(Ctx& ctx, XOperand& x, const aires_b200_matrix& b, const uint64_t* dptr, uint64_t p0,
+                const void* didx, const void* dval, Ctl* ctl) {
+  const IdxT* idx = static_cast<const IdxT*>(didx);
+  const VIn* val = static_cast<const VIn*>(dval);
+  auto* xp = static_cast<int64_t*>(x.ptr);
+  auto* xc = static_cast<int32_t*>(x.col);
+  auto* xv = static_cast<V*>(x.val);
+  if (b.layout == AIRES_B200_CSR) {
+    int g = grid_for(std::max<int64_t>(x.K + 1, x.nnz), 256, ctx.sms);
+    k_x_from_csr<IdxT, VIn, V><<<g, 256, 0, ctx.stream>>>(dptr, p0, x.K, idx, val, x.nnz, x.n_cols, xp,
+                                                          xc, xv, ctl);
+    AB2_CUDA(cudaGetLastError());
+    return;
+  }
+  // CSC -> CSR: count, scan, scatter, sort.
+  int32_t* counts = ctx.cnt.as<int32_t>(std::max<int64_t>(x.K, 1));
+  int32_t* cursor = reinterpret_cast<int32_t*>(ctx.rflops.as<int64_t>(std::max<int64_t>(x.K, 1)));
+  AB2_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * std::max<int64_t>(x.K, 1), ctx.stream));
+  AB2_CUDA(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * std::max<int64_t>(x.K, 1), ctx.stream));
+  if (x.nnz > 0) {
+    k_csc_count<IdxT><<<grid_for(x.nnz, 256, ctx.sms), 256, 0, ctx.stream>>>(idx, x.nnz, x.K, counts, ctl);
+    AB2_CUDA(cudaGetLastError());
+  }
+  int64_t nb = (x.K + kScanTile - 1) / kScanTile;
+  int64_t* part = ctx.scan_part.as<int64_t>(std::max<int64_t>(nb, 1));
+  if (x.K > 0) {
+    k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(counts, x.K, part);
+    k_scan_part<<<1, 1024, 0, ctx.stream>>>(part, nb, ctl);
+    k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(counts, x.K, part, xp);
+  } else {
+    AB2_CUDA(cudaMemsetAsync(xp, 0, sizeof(int64_t), ctx.stream));
+  }
+  AB2_CUDA(cudaGetLastError());
+  if (x.nnz > 0) {
+    k_csc_scatter<IdxT, VIn, V><<<grid_for(x.nnz, 256, ctx.sms), 256, 0, ctx.stream>>>(
+        dptr, p0, x.n_cols, idx, val, x.nnz, x.K, xp, cursor, xc, xv);
+    k_row_sort<V><<<grid_for(x.K, 128, ctx.sms), 128, 0, ctx.stream>>>(xp, x.K, xc, xv);
+    AB2_CUDA(cudaGetLastError());
+  }
+}
+
+template <class V>
+void fill_dispatch(Ctx& ctx, XOperand& x, const aires_b200_matrix& b, const uint64_t* dptr, uint64_t p0,
+                   const void* didx, const void* dval, Ctl* ctl) {
+  if (b.idx_bytes == 4 && b.val_bytes == 4)
+    fill_plain<uint32_t, float, V>(ctx, x, b, dptr, p0, didx, dval, ctl);
+  else if (b.idx_bytes == 4)
+    fill_plain<uint32_t, double, V>(ctx, x, b, dptr, p0, didx, dval, ctl);
+  else if (b.val_bytes == 4)
+    fill_plain<uint64_t, float, V>(ctx, x, b, dptr, p0, didx, dval, ctl);
+  else
+    fill_plain<uint64_t, double, V>(ctx, x, b, dptr, p0, didx, dval, ctl);
+}
+
+void* dmalloc(size_t bytes, size_t* total) {
+  void* p = nullptr;
+  bytes = std::max<size_t>(bytes, 16);
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY, "cudaMalloc of operand failed");
+  }
+  AB2_CUDA(e);
+  *total += bytes;
+  return p;
+}
+
+}  // namespace
+
+XOperand::~XOperand() {
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (prev != device) cudaSetDevice(device);
+  for (void* p : {ptr, col, val, slots, cslots})
+    if (p) cudaFree(p);
+  if (prev != device && prev >= 0) cudaSetDevice(prev);
+}
+
+std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode) {
+  if (b.layout != AIRES_B200_CSR && b.layout != AIRES_B200_CSC)
+    fail(AIRES_B200_INVALID_ARGUMENT, "operand layout must be CSR or CSC");
+  if ((b.idx_bytes != 4 && b.idx_bytes != 8) || (b.val_bytes != 4 && b.val_bytes != 8))
+    fail(AIRES_B200_INVALID_ARGUMENT, "operand idx_bytes/val_bytes must be 4 or 8");
+  if (mode == AIRES_B200_MODE_AUTO) mode = b.val_bytes == 8 ? AIRES_B200_MODE_FP64_EXACT : AIRES_B200_MODE_FP32;
+  if (mode != AIRES_B200_MODE_FP32 && mode != AIRES_B200_MODE_FP64_EXACT)
+    fail(AIRES_B200_INVALID_ARGUMENT, "unknown arithmetic mode");
+  auto x = std::make_unique<XOperand>();
+  x->device = ctx.device;
+  x->mode = mode;
+  x->K = static_cast<int64_t>(b.n_rows);
+  x->n_cols = static_cast<int64_t>(b.n_cols);
+  const uint64_t nptr = (b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols) + 1;
+  const int64_t dense_max = mode == AIRES_B200_MODE_FP32 ? kMaxDenseColsF32 : kMaxDenseColsF64;
+  if (x->n_cols > dense_max)
+    fail(AIRES_B200_UNSUPPORTED_FORMAT,
+         "feature matrix has " + std::to_string(x->n_cols) + " columns; the dense-accumulator path supports " +
+             std::to_string(dense_max));
+  if (b.ptr == nullptr) fail(AIRES_B200_INVALID_ARGUMENT, "operand ptr is null");
+
+  // pointer ends (host read or a tiny D2H)
+  uint64_t p0, p1;
+  if (b.location == AIRES_B200_HOST) {
+    p0 = b.ptr[0];
+    p1 = b.ptr[nptr - 1];
+  } else {
+    AB2_CUDA(cudaMemcpyAsync(&p0, b.ptr, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    AB2_CUDA(cudaMemcpyAsync(&p1, b.ptr + nptr - 1, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  }
+  if (p1 < p0 || p1 > b.span) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "operand pointer array exceeds its span");
+  x->nnz = static_cast<int64_t>(p1 - p0);
+  if (x->nnz >= (int64_t(1) << 31)) fail(AIRES_B200_CAPACITY_EXCEEDED, "operand nnz exceeds 2^31");
+
+  // stage host arrays on the device
+  const uint64_t* dptr = b.ptr;
+  const void* didx = b.idx;
+  const void* dval = b.val;
+  if (b.location == AIRES_B200_HOST) {
+    uint64_t* up = ctx.x_ptr.as<uint64_t>(nptr);
+    void* ui = ctx.x_idx.get(std::max<uint64_t>(x->nnz, 1) * b.idx_bytes);
+    void* uv = ctx.x_val.get(std::max<uint64_t>(x->nnz, 1) * b.val_bytes);
+    AB2_CUDA(cudaMemcpyAsync(up, b.ptr, nptr * 8, cudaMemcpyHostToDevice, ctx.stream));
+    if (x->nnz) {
+      AB2_CUDA(cudaMemcpyAsync(ui, static_cast<const char*>(b.idx) + p0 * b.idx_bytes, x->nnz * b.idx_bytes,
+                               cudaMemcpyHostToDevice, ctx.stream));
+      AB2_CUDA(cudaMemcpyAsync(uv, static_cast<const char*>(b.val) + p0 * b.val_bytes, x->nnz * b.val_bytes,
+                               cudaMemcpyHostToDevice, ctx.stream));
+    }
+    dptr = up;
+    didx = ui;
+    dval = uv;
+  } else {
+    didx = static_cast<const char*>(b.idx) + p0 * b.idx_bytes;
+    dval = static_cast<const char*>(b.val) + p0 * b.val_bytes;
+  }
+
+  // choose the slot width from the row-length histogram
+  Ctl* ctl = ctx.ctl.as<Ctl>(1);
+  AB2_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx.stream));
+  const size_t vb = mode == AIRES_B200_MODE_FP32 ? 4 : 8;
+  x->ptr = dmalloc((x->K + 1) * 8, &x->bytes);
+  x->col = dmalloc(std::max<int64_t>(x->nnz, 1) * 4, &x->bytes);
+  x->val = dmalloc(std::max<int64_t>(x->nnz, 1) * vb, &x->bytes);
+  if (mode == AIRES_B200_MODE_FP32)
+    fill_dispatch<float>(ctx, *x, b, dptr, p0, didx, dval, ctl);
+  else
+    fill_dispatch<double>(ctx, *x, b, dptr, p0, didx, dval, ctl);
+
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(&ctl->pad[0]);
+  if (x->K > 0)
+    k_len_hist<<<grid_for(x->K, 256, ctx.sms), 256, 0, ctx.stream>>>(static_cast<int64_t*>(x->ptr), x->K, hist);
+  AB2_CUDA(cudaGetLastError());
+  Ctl* h = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
+  AB2_CUDA(cudaMemcpyAsync(h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (h->bad_row) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "operand index outside its dimensions");
+  const double K = static_cast<double>(std::max<int64_t>(x->K, 1));
+  const double frac[4] = {h->pad[0] / K, h->pad[1] / K, h->pad[2] / K, h->pad[3] / K};
+  int W = 16;
+  const int widths[4] = {2, 4, 8, 16};
+  for (int i = 0; i < 4; i++)
+    if (frac[i] <= 0.2) {
+      W = widths[i];
+      break;
+    }
+  int64_t forced = env_int("AB2_SLOT_W", 0);
+  if (forced == 2 || forced == 4 || forced == 8 || forced == 16) W = static_cast<int>(forced);
+  x->W = W;
+  const size_t sb = mode == AIRES_B200_MODE_FP32 ? sizeof(SlotF) : sizeof(SlotD);
+  x->slots = dmalloc(std::max<int64_t>(x->K, 1) * W * sb, &x->bytes);
+  x->cslots = dmalloc(std::max<int64_t>(x->K, 1) * W * 2, &x->bytes);
+  if (x->K > 0) {
+    if (mode == AIRES_B200_MODE_FP32)
+      build_slots<float>(ctx, *x);
+    else
+      build_slots<double>(ctx, *x);
+  }
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  return x;
+}
+
+}  // namespace ab2

@@ -1,0 +1,342 @@
+// ab2_spgemm.cu -- host orchestration of one A·X product (spgemm_block, spgemm.hpp:60-132).
+//
+//   upload (host A only) -> K_classify -> K_symbolic -> K_scan -> [nnz readback, exact
+//   allocation through the caller's allocator, spgemm.hpp:111-112] -> K_numeric -> [K_fix]
+//   -> row_ptr copy -> (host C) D2H.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <type_traits>
+#include <unordered_map>
+
+#include "ab2_internal.h"
+#include "ab2_kernels.cuh"
+
+namespace ab2 {
+
+namespace {
+
+template <class K>
+int occupancy_grid(K kernel, int threads, size_t smem, int sms) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> attr_set;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = attr_set.find(reinterpret_cast<const void*>(kernel));
+    if (it == attr_set.end() || it->second < smem) {
+      AB2_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      attr_set[reinterpret_cast<const void*>(kernel)] = smem;
+    }
+  }
+  int nb = 0;
+  AB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem));
+  if (nb < 1) fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY, "kernel does not fit on an SM (shared memory)");
+  return nb * sms;
+}
+
+template <class IdxT>
+void launch_symbolic(Ctx& ctx, const SymArgs& p, const IdxT* acol, int W) {
+  const int threads = 256;
+  const size_t smem = static_cast<size_t>(threads / 32) * p.region_bytes;
+  switch (W) {
+#define AB2_SYM(WW)                                                                  \
+  case WW: {                                                                         \
+    auto k = k_symbolic<IdxT, WW>;                                                   \
+    int grid = occupancy_grid(k, threads, smem, ctx.sms);                            \
+    k<<<grid, threads, smem, ctx.stream>>>(p, acol);                                 \
+    break;                                                                           \
+  }
+    AB2_SYM(2)
+    AB2_SYM(4)
+    AB2_SYM(8)
+    AB2_SYM(16)
+#undef AB2_SYM
+    default: fail(AIRES_B200_INVALID_ARGUMENT, "bad slot width");
+  }
+  AB2_CUDA(cudaGetLastError());
+}
+
+template <class V, class IdxT, int W>
+auto numeric_kernel() {
+  if constexpr (std::is_same<V, float>::value)
+    return k_numeric_f32<IdxT, W>;
+  else
+    return k_numeric_f64<IdxT, W>;
+}
+
+template <class V, class IdxT, int W>
+void launch_numeric_w(Ctx& ctx, const NumArgs<V, IdxT>& p, int threads, size_t smem) {
+  auto k = numeric_kernel<V, IdxT, W>();
+  int grid = occupancy_grid(k, threads, smem, ctx.sms);
+  k<<<grid, threads, smem, ctx.stream>>>(p);
+}
+
+template <class V, class IdxT>
+void launch_numeric(Ctx& ctx, const NumArgs<V, IdxT>& p, int W) {
+  const size_t region = static_cast<size_t>(p.region_elems) * sizeof(V);
+  int nw = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / region)));
+  const int threads = nw * 32;
+  const size_t smem = nw * region;
+  switch (W) {
+    case 2: launch_numeric_w<V, IdxT, 2>(ctx, p, threads, smem); break;
+    case 4: launch_numeric_w<V, IdxT, 4>(ctx, p, threads, smem); break;
+    case 8: launch_numeric_w<V, IdxT, 8>(ctx, p, threads, smem); break;
+    case 16: launch_numeric_w<V, IdxT, 16>(ctx, p, threads, smem); break;
+    default: fail(AIRES_B200_INVALID_ARGUMENT, "bad slot width");
+  }
+  AB2_CUDA(cudaGetLastError());
+}
+
+template <class V, class IdxT>
+void launch_fix(Ctx& ctx, const NumArgs<V, IdxT>& p, int64_t n_fix) {
+  size_t smem = static_cast<size_t>(p.region_elems) * sizeof(V) + p.region_elems + 16;
+  auto k = k_fix_rows<V, IdxT>;
+  occupancy_grid(k, 32, smem, ctx.sms);
+  int grid = static_cast<int>(std::min<int64_t>(n_fix, 65535));
+  k<<<grid, 32, smem, ctx.stream>>>(p, n_fix);
+  AB2_CUDA(cudaGetLastError());
+}
+
+template <class Src, class Dst>
+__global__ void k_convert(const Src* __restrict__ in, Dst* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<Dst>(in[i]);
+}
+
+template <class Src, class Dst>
+void convert(Ctx& ctx, const void* in, void* out, int64_t n) {
+  if (n <= 0) return;
+  int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx.sms) * 32));
+  k_convert<Src, Dst><<<grid, 256, 0, ctx.stream>>>(static_cast<const Src*>(in), static_cast<Dst*>(out), n);
+  AB2_CUDA(cudaGetLastError());
+}
+
+
+template <class V, class IdxT>
+void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_b200_output& out,
+                 const uint64_t* aptr, uint64_t abase, const IdxT* acol, const V* aval) {
+  const int64_t rows = static_cast<int64_t>(a.n_rows);
+  const int W = x.W;
+  Ctl* ctl = ctx.ctl.as<Ctl>(1);
+  Ctl* h = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
+  int32_t* cnt = ctx.cnt.as<int32_t>(std::max<int64_t>(rows, 1));
+  int64_t* rflops = ctx.rflops.as<int64_t>(std::max<int64_t>(rows, 1));
+  int64_t* cptr = ctx.cptr.as<int64_t>(rows + 1);
+  int64_t* sym_heavy = ctx.sym_heavy.as<int64_t>(std::max<int64_t>(rows, 1));
+  int64_t* num_heavy = ctx.num_heavy.as<int64_t>(std::max<int64_t>(rows, 1));
+  int64_t* fix_rows = ctx.fix_rows.as<int64_t>(std::max<int64_t>(rows, 1));
+  const int64_t heavy_deg = env_int("AB2_SYM_HEAVY_DEG", 1024);
+  const int64_t heavy_flops = env_int("AB2_NUM_HEAVY_FLOPS", sizeof(V) == 4 ? 8192 : 4096);
+
+  AB2_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx.stream));
+  AB2_CUDA(cudaEventRecord(ctx.ev[0], ctx.stream));
+  if (rows > 0) {
+    int g = static_cast<int>(std::min<int64_t>((rows + 255) / 256, static_cast<int64_t>(ctx.sms) * 16));
+    k_classify<<<g, 256, 0, ctx.stream>>>(aptr, rows, heavy_deg, sym_heavy, ctl);
+    AB2_CUDA(cudaGetLastError());
+  }
+  AB2_CUDA(cudaEventRecord(ctx.ev[1], ctx.stream));
+  SymArgs sp{};
+  sp.aptr = aptr;
+  sp.abase = abase;
+  sp.rows = rows;
+  sp.K = x.K;
+  sp.n_cols = static_cast<int32_t>(x.n_cols);
+  sp.region_bytes = static_cast<int32_t>(std::max<int64_t>(16, (x.n_cols + 15) & ~int64_t(15)));
+  sp.xptr = static_cast<const int64_t*>(x.ptr);
+  sp.xcol = static_cast<const int32_t*>(x.col);
+  sp.cslots = static_cast<const uint16_t*>(x.cslots);
+  sp.cnt = cnt;
+  sp.rflops = rflops;
+  sp.sym_heavy = sym_heavy;
+  sp.heavy_deg = heavy_deg;
+  sp.num_heavy = num_heavy;
+  sp.heavy_flops = heavy_flops;
+  sp.ctl = ctl;
+  if (rows > 0) launch_symbolic<IdxT>(ctx, sp, acol, W);
+  AB2_CUDA(cudaEventRecord(ctx.ev[2], ctx.stream));
+  const int64_t nb = (rows + kScanTile - 1) / kScanTile;
+  int64_t* part = ctx.scan_part.as<int64_t>(std::max<int64_t>(nb, 1));
+  if (rows > 0) {
+    k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(cnt, rows, part);
+    k_scan_part<<<1, 1024, 0, ctx.stream>>>(part, nb, ctl);
+    k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(cnt, rows, part, cptr);
+    AB2_CUDA(cudaGetLastError());
+  } else {
+    AB2_CUDA(cudaMemsetAsync(cptr, 0, sizeof(int64_t), ctx.stream));
+  }
+  AB2_CUDA(cudaEventRecord(ctx.ev[3], ctx.stream));
+  AB2_CUDA(cudaMemcpyAsync(h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  const uint64_t nnz = h->nnz;
+  const uint64_t flops = h->flops;
+
+  // exact allocation by the caller (spgemm.hpp:111-112)
+  void *optr = nullptr, *oidx = nullptr, *oval = nullptr;
+  int rc = out.alloc(out.user, static_cast<uint64_t>(rows), nnz, &optr, &oidx, &oval);
+  if (rc != 0) fail(rc, "output allocator failed for " + std::to_string(nnz) + " nonzeros");
+  IdxT* ccol;
+  V* cval;
+  if (out.location == AIRES_B200_DEVICE) {
+    ccol = static_cast<IdxT*>(oidx);
+    cval = static_cast<V*>(oval);
+  } else {
+    ccol = ctx.c_col.as<IdxT>(std::max<uint64_t>(nnz, 1));
+    cval = ctx.c_val.as<V>(std::max<uint64_t>(nnz, 1));
+  }
+
+  NumArgs<V, IdxT> np{};
+  np.aptr = aptr;
+  np.abase = abase;
+  np.acol = acol;
+  np.aval = aval;
+  np.rows = rows;
+  np.x.K = x.K;
+  np.x.n_cols = static_cast<int32_t>(x.n_cols);
+  np.x.W = x.W;
+  np.x.ptr = static_cast<const int64_t*>(x.ptr);
+  np.x.col = static_cast<const int32_t*>(x.col);
+  np.x.val = static_cast<const V*>(x.val);
+  np.x.slots = static_cast<const typename SlotOf<V>::type*>(x.slots);
+  np.x.cslots = static_cast<const uint16_t*>(x.cslots);
+  np.region_elems = static_cast<int32_t>(std::max<int64_t>(4, (x.n_cols + 3) & ~int64_t(3)));
+  np.cnt = cnt;
+  np.cptr = cptr;
+  np.rflops = rflops;
+  np.num_heavy = num_heavy;
+  np.heavy_flops = heavy_flops;
+  np.ccol = ccol;
+  np.cval = cval;
+  np.fix_rows = fix_rows;
+  np.ctl = ctl;
+  AB2_CUDA(cudaEventRecord(ctx.ev[4], ctx.stream));
+  if (rows > 0 && nnz > 0) launch_numeric<V, IdxT>(ctx, np, W);
+  AB2_CUDA(cudaEventRecord(ctx.ev[5], ctx.stream));
+  AB2_CUDA(cudaMemcpyAsync(h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (h->n_fix > 0) {
+    launch_fix<V, IdxT>(ctx, np, static_cast<int64_t>(h->n_fix));
+  }
+  // row_ptr (int64 == u64 bits; all values are >= 0)
+  if (out.location == AIRES_B200_DEVICE) {
+    AB2_CUDA(cudaMemcpyAsync(optr, cptr, (rows + 1) * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+    AB2_CUDA(cudaEventRecord(ctx.ev[6], ctx.stream));
+  } else {
+    AB2_CUDA(cudaEventRecord(ctx.ev[6], ctx.stream));
+    AB2_CUDA(cudaMemcpyAsync(optr, cptr, (rows + 1) * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    if (nnz) {
+      AB2_CUDA(cudaMemcpyAsync(oidx, ccol, nnz * sizeof(IdxT), cudaMemcpyDeviceToHost, ctx.stream));
+      AB2_CUDA(cudaMemcpyAsync(oval, cval, nnz * sizeof(V), cudaMemcpyDeviceToHost, ctx.stream));
+    }
+  }
+  AB2_CUDA(cudaEventRecord(ctx.ev[7], ctx.stream));
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  float ms = 0;
+  auto el = [&](int a0, int b0) {
+    AB2_CUDA(cudaEventElapsedTime(&ms, ctx.ev[a0], ctx.ev[b0]));
+    return static_cast<double>(ms);
+  };
+  ctx.prof[kPClassify] = el(0, 1);
+  ctx.prof[kPSymbolic] = el(1, 2);
+  ctx.prof[kPScan] = el(2, 3);
+  ctx.prof[kPNumeric] = el(4, 5);
+  ctx.prof[kPD2H] = el(6, 7);
+  ctx.last_ms = el(0, 7);
+  out.n_rows = static_cast<uint64_t>(rows);
+  out.n_cols = static_cast<uint64_t>(x.n_cols);
+  out.nnz = nnz;
+  out.flops = flops;
+}
+
+}  // namespace
+
+void spgemm_rows(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_b200_output& out) {
+  if (a.layout != AIRES_B200_CSR) fail(AIRES_B200_INVALID_ARGUMENT, "A must be CSR");
+  if ((a.idx_bytes != 4 && a.idx_bytes != 8) || (a.val_bytes != 4 && a.val_bytes != 8))
+    fail(AIRES_B200_INVALID_ARGUMENT, "A idx_bytes/val_bytes must be 4 or 8");
+  if ((out.idx_bytes != 4 && out.idx_bytes != 8) || (out.val_bytes != 4 && out.val_bytes != 8))
+    fail(AIRES_B200_INVALID_ARGUMENT, "output idx_bytes/val_bytes must be 4 or 8");
+  if (!out.alloc) fail(AIRES_B200_INVALID_ARGUMENT, "output allocator is null");
+  if (a.n_cols != static_cast<uint64_t>(x.K))
+    fail(AIRES_B200_DIMENSION_MISMATCH, "inner dimensions " + std::to_string(a.n_cols) + " and " +
+                                            std::to_string(x.K) + " differ");
+  if (a.ptr == nullptr) fail(AIRES_B200_INVALID_ARGUMENT, "A ptr is null");
+  const size_t vsize = x.mode == AIRES_B200_MODE_FP32 ? 4 : 8;
+  if (out.val_bytes != vsize)
+    fail(AIRES_B200_INVALID_ARGUMENT, "output value width must match the operand's arithmetic mode");
+  const int64_t rows = static_cast<int64_t>(a.n_rows);
+
+  // Stage A on the device.
+  const uint64_t* aptr = a.ptr;
+  uint64_t abase = 0;
+  const void* acol = a.idx;
+  const void* aval = a.val;
+  uint64_t p0 = 0, p1 = 0;
+  AB2_CUDA(cudaEventRecord(ctx.ev[8], ctx.stream));
+  if (a.location == AIRES_B200_HOST) {
+    p0 = a.ptr[0];
+    p1 = a.ptr[rows];
+    if (p1 < p0 || p1 > a.span) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "A row pointers exceed the index span");
+    uint64_t* dptr = ctx.a_ptr.as<uint64_t>(rows + 1);
+    void* dcol = ctx.a_col.get(std::max<uint64_t>(p1 - p0, 1) * a.idx_bytes);
+    void* dval = ctx.a_val.get(std::max<uint64_t>(p1 - p0, 1) * a.val_bytes);
+    AB2_CUDA(cudaMemcpyAsync(dptr, a.ptr, (rows + 1) * 8, cudaMemcpyHostToDevice, ctx.stream));
+    if (p1 > p0) {
+      AB2_CUDA(cudaMemcpyAsync(dcol, static_cast<const char*>(a.idx) + p0 * a.idx_bytes, (p1 - p0) * a.idx_bytes,
+                               cudaMemcpyHostToDevice, ctx.stream));
+      AB2_CUDA(cudaMemcpyAsync(dval, static_cast<const char*>(a.val) + p0 * a.val_bytes, (p1 - p0) * a.val_bytes,
+                               cudaMemcpyHostToDevice, ctx.stream));
+    }
+    aptr = dptr;
+    abase = p0;
+    acol = dcol;
+    aval = dval;
+  } else if (a.idx_bytes != out.idx_bytes || a.val_bytes != vsize) {
+    // conversions need the span ends
+    AB2_CUDA(cudaMemcpyAsync(&p0, a.ptr, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    AB2_CUDA(cudaMemcpyAsync(&p1, a.ptr + rows, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (p1 < p0 || p1 > a.span) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "A row pointers exceed the index span");
+    abase = p0;
+    acol = static_cast<const char*>(a.idx) + p0 * a.idx_bytes;
+    aval = static_cast<const char*>(a.val) + p0 * a.val_bytes;
+  }
+  AB2_CUDA(cudaEventRecord(ctx.ev[9], ctx.stream));
+  // Width conversions: kernels read A's columns at the output index width and A's
+  // values at the arithmetic width.
+  const int64_t span = static_cast<int64_t>(p1 - p0);
+  if (a.idx_bytes != out.idx_bytes) {
+    void* c2 = ctx.a_col2.get(std::max<int64_t>(span, 1) * out.idx_bytes);
+    if (a.idx_bytes == 8)
+      convert<uint64_t, uint32_t>(ctx, acol, c2, span);
+    else
+      convert<uint32_t, uint64_t>(ctx, acol, c2, span);
+    acol = c2;
+  }
+  if (a.val_bytes != vsize) {
+    void* v2 = ctx.a_val2.get(std::max<int64_t>(span, 1) * vsize);
+    if (a.val_bytes == 8)
+      convert<double, float>(ctx, aval, v2, span);
+    else
+      convert<float, double>(ctx, aval, v2, span);
+    aval = v2;
+  }
+  if (out.idx_bytes == 4 && vsize == 4)
+    run_product<float, uint32_t>(ctx, a, x, out, aptr, abase, static_cast<const uint32_t*>(acol),
+                                 static_cast<const float*>(aval));
+  else if (out.idx_bytes == 4)
+    run_product<double, uint32_t>(ctx, a, x, out, aptr, abase, static_cast<const uint32_t*>(acol),
+                                  static_cast<const double*>(aval));
+  else if (vsize == 4)
+    run_product<float, uint64_t>(ctx, a, x, out, aptr, abase, static_cast<const uint64_t*>(acol),
+                                 static_cast<const float*>(aval));
+  else
+    run_product<double, uint64_t>(ctx, a, x, out, aptr, abase, static_cast<const uint64_t*>(acol),
+                                  static_cast<const double*>(aval));
+  float ms = 0;
+  AB2_CUDA(cudaEventElapsedTime(&ms, ctx.ev[8], ctx.ev[9]));
+  ctx.prof[kPH2D] = ms;
+}
+
+}  // namespace ab2

@@ -1,0 +1,226 @@
+"""GPU parity: the B200 kernels (through the C ABI) against the CPU oracle.
+
+Known answers follow the reference's own unit tests (spgemm_test.cpp); random cases follow
+its property tests.  fp64-exact mode must be bit-identical to the reference (values and
+structure); fp32 mode must match structure exactly and values within 1e-5 relative to the
+cell's sum of |terms| (north_star tolerance).
+"""
+import numpy as np
+import pytest
+
+import paper_2507_02006_b200 as ab
+from oracle import pyoracle as po
+from tests._util import (assert_close_fp32, assert_structure_equal, bits_equal, oracle_product, random_csr,
+                         to_csc)
+
+pytestmark = pytest.mark.gpu
+
+
+def csr(nr, nc, ptr, idx, val):
+    return ab.CsrMatrix(nr, nc, np.asarray(ptr, np.uint64), np.asarray(idx, np.uint64), np.asarray(val))
+
+
+def csc_of(nr, nc, ptr, idx, val):
+    cp, ri, cv = to_csc(nr, nc, ptr, idx, val)
+    return ab.CscMatrix(nr, nc, cp, ri, cv)
+
+
+def triplets(rows, cols, vals, nr, nc):
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = np.asarray(rows)[order], np.asarray(cols)[order], np.asarray(vals, float)[order]
+    ptr = np.zeros(nr + 1, np.uint64)
+    np.add.at(ptr, np.asarray(rows) + 1, 1)
+    return np.cumsum(ptr).astype(np.uint64), np.asarray(cols, np.uint64), vals
+
+
+def test_tiny_hand_product():
+    # spgemm_test.cpp:43-53: [[1,2],[0,3]] * [[4,0],[5,6]] = [[14,12],[15,18]]
+    a = csr(2, 2, *triplets([0, 0, 1], [0, 1, 1], [1, 2, 3], 2, 2))
+    b = csr(2, 2, *triplets([0, 1, 1], [0, 0, 1], [4, 5, 6], 2, 2))
+    for bb in (b, csc_of(2, 2, b.row_ptr, b.col_idx, b.values)):
+        c = ab.spgemm_full(a, bb)
+        assert list(c.row_ptr) == [0, 2, 4]
+        assert list(c.col_idx) == [0, 1, 0, 1]
+        assert list(c.values) == [14.0, 12.0, 15.0, 18.0]
+
+
+def test_identity_is_neutral():
+    # spgemm_test.cpp:55-60
+    rng = np.random.default_rng(3)
+    p, i, v = random_csr(rng, 9, 9, 0.4)
+    a = csr(9, 9, p, i, v)
+    eye = csr(9, 9, np.arange(10, dtype=np.uint64), np.arange(9, dtype=np.uint64), np.ones(9))
+    assert ab.spgemm_full(eye, csc_of(9, 9, p, i, v)) == a
+    assert ab.spgemm_full(a, csc_of(9, 9, eye.row_ptr, eye.col_idx, eye.values)) == a
+
+
+def test_keeps_computed_structural_zeros():
+    # spgemm_test.cpp:62-70
+    a = csr(1, 2, *triplets([0, 0], [0, 1], [1, -1], 1, 2))
+    b = csr(2, 1, *triplets([0, 1], [0, 0], [1, 1], 2, 1))
+    for mode in (ab.MODE_FP64_EXACT, ab.MODE_FP32):
+        c = ab.spgemm_full(a, b, mode=mode)
+        assert c.nnz() == 1 and c.values[0] == 0.0
+
+
+def test_all_negative_zero_contributions_keep_structure():
+    # every contribution to cell (0,0) is -0.0: the reference stores +0.0 (sum starts at 0.0)
+    a = csr(1, 2, *triplets([0, 0], [0, 1], [-1.0, -2.0], 1, 2))
+    b = csr(2, 2, np.array([0, 2, 3], np.uint64), np.array([0, 1, 0], np.uint64), np.array([0.0, 3.0, 0.0]))
+    for mode in (ab.MODE_FP64_EXACT, ab.MODE_FP32):
+        c = ab.spgemm_full(a, b, mode=mode)
+        assert list(c.col_idx) == [0, 1]
+        assert np.signbit(c.values[0]) == False and c.values[0] == 0.0  # noqa: E712
+        assert c.values[1] == -3.0
+
+
+def test_flops_count_structural_matches():
+    # spgemm_test.cpp:72-83
+    rng = np.random.default_rng(7)
+    for _ in range(25):
+        a = random_csr(rng, 8, 6, 0.5)
+        b = random_csr(rng, 6, 7, 0.5)
+        want, macs = oracle_product(8, 6, 7, a, b)
+        blk = ab.spgemm_block(a[0], a[1], a[2], 8, 6, csc_of(6, 7, *b))
+        assert blk.flops == macs
+
+
+@pytest.mark.parametrize("seed", [13, 14])
+def test_matches_oracle_bit_exact_fp64(seed):
+    # spgemm_test.cpp:85-95 shapes; fp64-exact must be bit-identical, not just within 1e-12
+    rng = np.random.default_rng(seed)
+    for _ in range(120):
+        nr, ni, nc = (int(x) for x in rng.integers(1, 25, 3))
+        d = 0.05 + 0.4 * rng.random()
+        a = random_csr(rng, nr, ni, d)
+        b = random_csr(rng, ni, nc, d)
+        (wp, wi, wv), macs = oracle_product(nr, ni, nc, a, b)
+        blk = ab.spgemm_block(a[0], a[1], a[2], nr, ni, csc_of(ni, nc, *b))
+        assert_structure_equal(blk.fragment.row_ptr, blk.fragment.col_idx, wp, wi)
+        assert bits_equal(blk.fragment.values, wv)
+        assert blk.flops == macs
+
+
+def test_matches_oracle_fp32_tolerance():
+    rng = np.random.default_rng(21)
+    for _ in range(80):
+        nr, ni, nc = (int(x) for x in rng.integers(1, 40, 3))
+        d = 0.05 + 0.4 * rng.random()
+        a = random_csr(rng, nr, ni, d)
+        b = random_csr(rng, ni, nc, d)
+        (wp, wi, wv), _ = oracle_product(nr, ni, nc, a, b)
+        (_, _, sv), _ = oracle_product(nr, ni, nc, (a[0], a[1], np.abs(a[2])), (b[0], b[1], np.abs(b[2])))
+        c = ab.spgemm_full(csr(nr, ni, a[0], a[1], a[2].astype(np.float32)),
+                           csr(ni, nc, b[0], b[1], b[2].astype(np.float32)))
+        assert c.values.dtype == np.float32
+        assert_structure_equal(c.row_ptr, c.col_idx, wp, wi)
+        assert_close_fp32(c.values, wv, sv)
+
+
+def test_csr_and_csc_operands_agree():
+    rng = np.random.default_rng(5)
+    a = random_csr(rng, 30, 40, 0.2)
+    b = random_csr(rng, 40, 50, 0.2)
+    c1 = ab.spgemm_full(csr(30, 40, *a), csr(40, 50, *b))
+    c2 = ab.spgemm_full(csr(30, 40, *a), csc_of(40, 50, *b))
+    assert c1 == c2
+
+
+def test_absolute_row_pointer_span():
+    # spgemm.hpp:79-84: row_ptr need not start at 0; it indexes the spans directly
+    rng = np.random.default_rng(9)
+    ptr, idx, val = random_csr(rng, 20, 15, 0.3)
+    b = random_csr(rng, 15, 12, 0.3)
+    full = ab.spgemm_full(csr(20, 15, ptr, idx, val), csr(15, 12, *b))
+    blk = ab.spgemm_block(ptr[5:12], idx, val, 7, 15, csr(15, 12, *b), start_row=5)
+    lo, hi = int(full.row_ptr[5]), int(full.row_ptr[12])
+    assert list(blk.fragment.row_ptr) == list(full.row_ptr[5:13] - full.row_ptr[5])
+    assert np.array_equal(blk.fragment.col_idx, full.col_idx[lo:hi])
+    assert bits_equal(blk.fragment.values, full.values[lo:hi])
+    assert (blk.start_row, blk.end_row) == (5, 12)
+
+
+def test_partition_independent_bit_exact():
+    # spgemm_test.cpp:97-115 with the device RoBW tiler
+    rng = np.random.default_rng(19)
+    for _ in range(20):
+        n = int(rng.integers(4, 24))
+        ap = random_csr(rng, n, n, 0.3)
+        a = csr(n, n, *ap)
+        b = csc_of(n, n, *random_csr(rng, n, n, 0.3))
+        whole = ab.spgemm_full(a, b)
+        need = max(ab.calc_mem(1, int(ap[0][r + 1] - ap[0][r])) for r in range(n))
+        for _ in range(3):
+            m_a = need + int(rng.integers(0, 300))
+            parts = [ab.spgemm_block(s.row_ptr_local, s.col_idx, s.values, s.rows(), n, b, s.start_row)
+                     for s in ab.robw_partition(a, m_a)]
+            ptr = np.concatenate([[0], np.cumsum(np.concatenate([np.diff(p.fragment.row_ptr) for p in parts]))])
+            assert np.array_equal(ptr.astype(np.uint64), whole.row_ptr)
+            assert np.array_equal(np.concatenate([p.fragment.col_idx for p in parts]), whole.col_idx)
+            assert bits_equal(np.concatenate([p.fragment.values for p in parts]), whole.values)
+
+
+def test_mismatched_inner_dimension_raises():
+    # spgemm_test.cpp:125-129
+    a = csr(3, 3, np.arange(4, dtype=np.uint64), np.arange(3, dtype=np.uint64), np.ones(3))
+    b = csr(4, 4, np.arange(5, dtype=np.uint64), np.arange(4, dtype=np.uint64), np.ones(4))
+    with pytest.raises(ab.AiresError) as e:
+        ab.spgemm_full(a, b)
+    assert e.value.code == ab.errc.dimension_mismatch
+
+
+def test_empty_operands():
+    # spgemm_test.cpp:156-169
+    a = csr(3, 4, np.zeros(4, np.uint64), np.zeros(0, np.uint64), np.zeros(0))
+    b = ab.CscMatrix(4, 2, np.zeros(3, np.uint64), np.zeros(0, np.uint64), np.zeros(0))
+    c = ab.spgemm_full(a, b)
+    assert (c.n_rows, c.n_cols, c.nnz()) == (3, 2, 0)
+    assert list(c.row_ptr) == [0, 0, 0, 0]
+
+
+def test_robw_cuts_match_reference_greedy():
+    # partition_test.cpp:50-62 golden + random agreement with the oracle (incl. row_too_large)
+    p, i, v = triplets([0, 0, 1, 1, 1, 2, 3, 3, 3], [0, 1, 0, 1, 2, 3, 1, 2, 3], list(range(1, 10)), 4, 4)
+    segs = ab.robw_partition(csr(4, 4, p, i, v), 120)
+    assert [(s.start_row, s.end_row, s.byte_size) for s in segs] == [(0, 2, 104), (2, 4, 88)]
+    with pytest.raises(ab.AiresError) as e:
+        ab.robw_cuts(p, 63)
+    assert e.value.code == ab.errc.row_too_large
+    rng = np.random.default_rng(23)
+    for _ in range(200):
+        n = int(rng.integers(1, 300))
+        lens = rng.integers(0, 20, n) * (rng.random(n) < 0.7)
+        ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+        I, V = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        m_a = int(rng.integers(1, 4000))
+        rc, cuts, bad = po.robw_cuts(ptr, m_a, I, V)
+        if rc == 0:
+            got = ab.robw_cuts(ptr, m_a, ab.ElementSizes(I, V))
+            assert np.array_equal(got, cuts)
+        else:
+            with pytest.raises(ab.AiresError) as e:
+                ab.robw_cuts(ptr, m_a, ab.ElementSizes(I, V))
+            assert e.value.code == ab.errc.row_too_large and f"row {bad} " in str(e.value)
+
+
+@pytest.mark.parametrize("mode", [ab.MODE_FP64_EXACT, ab.MODE_FP32])
+def test_power_law_cfg1_shape(mode):
+    """cfg1 shape (100K nodes / 1M edges, X 100K x 512 @1%): fp64 bit-exact checksum, fp32 tolerance."""
+    g, st = ab.synth_graph(100_000, 1_000_000, degree_cap=20_000, idx_dtype=np.uint64)
+    x = ab.synth_features(100_000, 512, 99.0, 3, idx_dtype=np.uint64)
+    rc, (wp, wi, wv), macs = po.spgemm_rowwise(g.row_ptr, g.col_idx, g.values, g.n_rows, g.n_cols, x.n_rows,
+                                               x.n_cols, x.row_ptr, x.col_idx, x.values, nthreads=8)
+    assert rc == 0
+    if mode == ab.MODE_FP64_EXACT:
+        c = ab.spgemm_full(g, x)
+        assert c.values.dtype == np.float64
+        assert po.checksum(c.n_rows, c.n_cols, c.row_ptr, c.col_idx, c.values) == \
+            po.checksum(g.n_rows, x.n_cols, wp, wi, wv)
+    else:
+        g32 = ab.CsrMatrix(g.n_rows, g.n_cols, g.row_ptr, g.col_idx.astype(np.uint32), g.values.astype(np.float32))
+        x32 = ab.CsrMatrix(x.n_rows, x.n_cols, x.row_ptr, x.col_idx.astype(np.uint32), x.values.astype(np.float32))
+        c = ab.spgemm_full(g32, x32)
+        assert_structure_equal(c.row_ptr, c.col_idx, wp, wi)
+        assert_close_fp32(c.values, wv, wv)  # all terms positive: scale == value
+    blk = ab.spgemm_block(g.row_ptr, g.col_idx, g.values, g.n_rows, g.n_cols, x)
+    assert blk.flops == macs
