@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""bench.py -- A·X SpGEMM (AIRES hot path) on B200: latency, GFLOP/s and roofline fraction.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE JSON line on
+rank 0.  N>1 runs under torchrun, one rank per GPU (NCCL); every rank owns one contiguous
+row block (weak scaling: each rank's block is a cfg-shaped Ã_r over its own slice of the
+replicated X) and the only collective is the all-gather of per-rank nnz(C) that forms the
+global row_ptr offsets.
+
+Workload at N=1: BASELINE.json configs[1] (Reddit-shaped, 232,965 nodes, 114 M edges, X 602
+wide at 1 %, fully HBM-resident), synthetic (BASELINE.md §4 seeds: graph 1, relabel 2, X 3).
+A "step" is one full A·X through the C ABI (aires_b200_spgemm) with device-resident A and X
+(device C): X layout build, classify, symbolic, scan, nnz readback + exact allocation,
+numeric.  `e2e` is the same call with pinned HOST buffers (H2D of A and X and D2H of C
+inside the timed region).  `--impl reference` times the reference's own CPU spgemm_block
+(oracle/_ref, built from /root/reference) on a row sample with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "A·X SpGEMM latency (ms) and GFLOP/s; % of HBM/host-link roofline at 1/2/4/8 B200"
+
+CONFIGS = {
+    "cfg1": dict(workload="cfg1: power-law 100K nodes / 1M edges, X 100Kx512 @1%",
+                 n=100_000, nnz=1_000_000, dim=512, cap=20_000),
+    "cfg2": dict(workload="cfg2: Reddit-shaped 232,965 nodes / 114M edges, X 602 @1%, HBM-resident",
+                 n=232_965, nnz=114_000_000, dim=602, cap=20_000),
+    "cfg3": dict(workload="cfg3: ogbn-products-shaped 2,449,029 nodes / 62M edges, X 100 @1%",
+                 n=2_449_029, nnz=62_000_000, dim=100, cap=20_000),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def make_inputs(cfg: dict, rank: int, world: int):
+    """Rank r: Ã_r (seed 1+r) over node block r; X (seed 3) covering all world*n rows."""
+    import paper_2507_02006_b200 as ab
+    n = cfg["n"]
+    t0 = time.time()
+    g, st = ab.synth_graph(n, cfg["nnz"], alpha=0.75, degree_cap=cfg["cap"], seed=1 + rank, relabel_seed=2,
+                           idx_dtype=np.uint32, val_dtype=np.float64)
+    x = ab.synth_features(n * world, cfg["dim"], 99.0, 3, idx_dtype=np.uint32, val_dtype=np.float64)
+    if world > 1:  # Ã_r's columns address X rows [r*n, (r+1)*n)
+        g.col_idx = g.col_idx + np.uint32(rank * n)
+        g.n_cols = n * world
+    log(f"[rank {rank}] inputs: A {g.n_rows}x{g.n_cols} nnz {g.nnz()} (edges {st['nnz_a']}, max deg "
+        f"{st['max_degree']}), X {x.n_rows}x{x.n_cols} nnz {x.nnz()} in {time.time() - t0:.1f}s")
+    return g, st, x
+
+
+def algorithmic_bytes(n_rows, nnz_a, k_rows, nnz_x, nnz_c, vb=4):
+    """Σ_{A,X,C} 8(rows+1) + (4+vb)·nnz (int64 ptr, int32 idx, fp32/fp64 val)."""
+    return (8 * (n_rows + 1) + (4 + vb) * nnz_a) + (8 * (k_rows + 1) + (4 + vb) * nnz_x) + \
+        (8 * (n_rows + 1) + (4 + vb) * nnz_c)
+
+
+def run_b200(args, cfg):
+    import torch
+    import paper_2507_02006_b200 as ab
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    L = ab.lib()
+    ab._check(L.aires_b200_set_device(local))
+    dev = torch.device("cuda", local)
+    mode = ab.MODE_FP64_EXACT if args.mode == "fp64" else ab.MODE_FP32
+    vdt_np = np.float64 if mode == ab.MODE_FP64_EXACT else np.float32
+    vdt_t = torch.float64 if mode == ab.MODE_FP64_EXACT else torch.float32
+    vb = 8 if mode == ab.MODE_FP64_EXACT else 4
+
+    g, st, x = make_inputs(cfg, rank, world)
+    n, K = g.n_rows, x.n_rows
+    # device-resident inputs (u64 ptr, u32 idx, fp32/fp64 values)
+    tA = [torch.from_numpy(g.row_ptr.view(np.int64)).to(dev), torch.from_numpy(g.col_idx.view(np.int32)).to(dev),
+          torch.from_numpy(g.values.astype(vdt_np)).to(dev)]
+    tX = [torch.from_numpy(x.row_ptr.view(np.int64)).to(dev), torch.from_numpy(x.col_idx.view(np.int32)).to(dev),
+          torch.from_numpy(x.values.astype(vdt_np)).to(dev)]
+    am = ab._Matrix(n, g.n_cols, ab.CSR, ab.DEVICE, 4, vb, tA[0].data_ptr(), tA[1].data_ptr(), tA[2].data_ptr(),
+                    g.nnz())
+    xm = ab._Matrix(K, x.n_cols, ab.CSR, ab.DEVICE, 4, vb, tX[0].data_ptr(), tX[1].data_ptr(), tX[2].data_ptr(),
+                    x.nnz())
+
+    # device output: grow-only buffers handed out by the allocator
+    outbuf = {}
+
+    def dev_alloc(user, rows, nnz, pp, pi, pv):
+        if outbuf.get("cap", -1) < nnz:
+            outbuf["ptr"] = torch.empty(rows + 1, dtype=torch.int64, device=dev)
+            outbuf["idx"] = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+            outbuf["val"] = torch.empty(max(nnz, 1), dtype=vdt_t, device=dev)
+            outbuf["cap"] = nnz
+        pp[0], pi[0], pv[0] = outbuf["ptr"].data_ptr(), outbuf["idx"].data_ptr(), outbuf["val"].data_ptr()
+        return 0
+
+    afn = ab._ALLOC_FN(dev_alloc)
+    out = ab._Output(ab.DEVICE, 4, vb, 0, afn, None, 0, 0, 0, 0)
+
+    def step():
+        ab._check(L.aires_b200_spgemm(C.byref(am), C.byref(xm), mode, C.byref(out)))
+
+    lib_stream = torch.cuda.ExternalStream(L.aires_b200_stream(), device=dev)
+    for _ in range(args.warmup):
+        step()
+    nnz_c, macs = int(out.nnz), int(out.flops)
+    prof_keys = ["classify", "symbolic", "scan", "numeric", "x_prep"]
+    prof_sum = {k: 0.0 for k in prof_keys}
+    launches = 0
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    offsets_t = torch.zeros(world, dtype=torch.int64, device=dev)
+    with ClockSampler(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(lib_stream)
+        for _ in range(args.steps):
+            step()
+            p = ab.last_profile()
+            for k in prof_keys:
+                prof_sum[k] += p[k]
+            launches += L.aires_b200_last_launches()
+            if dist:  # global row_ptr offsets: all-gather of one int64 nnz(C) per rank
+                mine = torch.tensor([int(out.nnz)], dtype=torch.int64, device=dev)
+                dist.all_gather_into_tensor(offsets_t, mine)
+        ev1.record(lib_stream)
+        ev1.synchronize()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    ms_rank = ev0.elapsed_time(ev1) / args.steps
+    ms = ms_rank
+    tot_macs = macs
+    if dist:
+        t = torch.tensor([ms_rank], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        m = torch.tensor([macs], dtype=torch.int64, device=dev)
+        dist.all_reduce(m)
+        tot_macs = int(m.item())
+    gflops = 2.0 * tot_macs / (ms * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (numeric) and of the whole step
+    peak, peak_src = peaks()
+    b_alg = algorithmic_bytes(n, g.nnz(), K, x.nnz(), nnz_c, vb)
+    num_ms = prof_sum["numeric"] / args.steps
+    sym_ms = prof_sum["symbolic"] / args.steps
+    ach = b_alg / (num_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+            "traffic": None, "kernel": "k_numeric_f32" if vb == 4 else "k_numeric_f64",
+            "kernel_ms": round(num_ms, 4), "bytes_per_launch": b_alg, "peak_source": peak_src,
+            "step_frac": round(b_alg / (ms * 1e-3) / 1e9 / peak, 4),
+            "kernel_ms_breakdown": {k: round(v / args.steps, 4) for k, v in prof_sum.items()}}
+
+    # e2e: same call, pinned host buffers, H2D + D2H inside the timed region
+    e2e = None
+    if not args.skip_e2e:
+        hA = [torch.from_numpy(g.row_ptr.view(np.int64)).pin_memory(),
+              torch.from_numpy(g.col_idx.view(np.int32)).pin_memory(),
+              torch.from_numpy(g.values.astype(vdt_np)).pin_memory()]
+        hX = [torch.from_numpy(x.row_ptr.view(np.int64)).pin_memory(),
+              torch.from_numpy(x.col_idx.view(np.int32)).pin_memory(),
+              torch.from_numpy(x.values.astype(vdt_np)).pin_memory()]
+        ham = ab._Matrix(n, g.n_cols, ab.CSR, ab.HOST, 4, vb, hA[0].data_ptr(), hA[1].data_ptr(), hA[2].data_ptr(),
+                         g.nnz())
+        hxm = ab._Matrix(K, x.n_cols, ab.CSR, ab.HOST, 4, vb, hX[0].data_ptr(), hX[1].data_ptr(),
+                         hX[2].data_ptr(), x.nnz())
+        hout = {"ptr": torch.empty(n + 1, dtype=torch.int64).pin_memory(),
+                "idx": torch.empty(max(nnz_c, 1), dtype=torch.int32).pin_memory(),
+                "val": torch.empty(max(nnz_c, 1), dtype=vdt_t).pin_memory()}
+
+        def host_alloc(user, rows, nnz, pp, pi, pv):
+            if nnz > hout["idx"].numel():
+                return 9
+            pp[0], pi[0], pv[0] = hout["ptr"].data_ptr(), hout["idx"].data_ptr(), hout["val"].data_ptr()
+            return 0
+
+        hfn = ab._ALLOC_FN(host_alloc)
+        hout_s = ab._Output(ab.HOST, 4, vb, 0, hfn, None, 0, 0, 0, 0)
+
+        def estep():
+            ab._check(L.aires_b200_spgemm(C.byref(ham), C.byref(hxm), mode, C.byref(hout_s)))
+
+        for _ in range(max(1, args.warmup)):
+            estep()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            estep()
+        e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        if dist:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        h2d = (n + 1) * 8 + g.nnz() * (4 + vb) + (K + 1) * 8 + x.nnz() * (4 + vb)
+        d2h = (n + 1) * 8 + nnz_c * (4 + vb)
+        e2e = {"value": round(2.0 * tot_macs / (e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(e_ms, 3),
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "api": "aires_b200_spgemm, pinned host A/X/C (u64 ptr, u32 idx, fp32 val)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        cpu = cpu_baseline(g, x, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if vb == 4 else "f64",
+            "data": "synthetic (Chung-Lu power-law Ã, gen_features X; seeds graph 1+rank, relabel 2, X 3)",
+            "config": {"workload": cfg["workload"], "nodes_per_gpu": n, "edges_per_gpu": st["nnz_a"],
+                       "nnz_a_tilde": g.nnz(), "x_cols": x.n_cols, "nnz_x": x.nnz(), "nnz_c": nnz_c,
+                       "macs": tot_macs, "max_degree": st["max_degree"], "mode": args.mode,
+                       "parallelism": f"row-block shards x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (A 0.9 GB, C 1.1 GB vs 126 MB L2); X is meant to stay L2-resident",
+                       "latency_ms": round(ms, 4)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def sample_rows(n: int, count: int, seed: int = 11) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(n, size=min(count, n), replace=False)).astype(np.uint64)
+
+
+def ref_sample_run(g, x, seconds: float, threads: int):
+    """Reference spgemm_block (oracle/_ref) on a random row sample sized to ~`seconds` of work.
+    Returns (gflops, sample description, kind, rows, secs)."""
+    from oracle import pyoracle as po
+    a_ptr, a_idx, a_val = g.row_ptr, g.col_idx.astype(np.uint64), g.values.astype(np.float64)
+    cp, ri, cv = po.csr_to_csc(x.n_rows, x.n_cols, x.row_ptr, x.col_idx.astype(np.uint64), x.values)
+    kind = "reference" if po.ref_available() else "port"
+    if kind == "reference":
+        def run(rows):
+            s, macs, z, _ = po.ref_rows_timed(a_ptr, a_idx, a_val, g.n_cols, rows, cp, ri, cv, x.n_rows, x.n_cols,
+                                              threads)
+            return s, macs
+    else:  # oracle port of spgemm_block (inner product), one thread
+        def run(rows):
+            t0 = time.perf_counter()
+            macs = 0
+            for r in rows:
+                rc, _, m = po.spgemm_inner(a_ptr[r:r + 2], a_idx, a_val, 1, g.n_cols, x.n_rows, x.n_cols, cp, ri, cv)
+                macs += m
+            return time.perf_counter() - t0, macs
+    probe = sample_rows(g.n_rows, max(threads * 4, 16), seed=5)
+    s, _ = run(probe)
+    per_row = s / len(probe)
+    count = int(max(threads * 4, min(g.n_rows, seconds / max(per_row, 1e-9))))
+    rows = sample_rows(g.n_rows, count)
+    s, macs = run(rows)
+    return 2.0 * macs / s / 1e9, rows, kind, s
+
+
+def cpu_baseline(g, x, seconds: float):
+    threads = len(os.sched_getaffinity(0))
+    try:
+        gf, rows, kind, s = ref_sample_run(g, x, seconds, threads)
+    except Exception as e:  # baseline is reported, never fatal
+        return {"value": None, "unit": "GFLOP/s", "cores": threads, "kind": "reference", "sample": f"failed: {e}"}
+    return {"value": round(gf, 6), "unit": "GFLOP/s", "cores": threads if kind == "reference" else 1, "kind": kind,
+            "sample": f"{len(rows)} uniformly sampled rows of the same Ã·X ({s:.1f} s), reference spgemm_block "
+                      f"(inner product, spgemm.hpp:60-132) unmodified, -O3 no -march; GFLOP/s = 2*MACs/t"}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference's own CPU spgemm_block on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    g, st, x = make_inputs(cfg, 0, 1)
+    per_step = max(2.0, args.cpu_seconds / max(1, args.steps + args.warmup))
+    vals = []
+    kind = "reference"
+    rows_total = 0
+    for i in range(args.warmup + args.steps):
+        gf, rows, kind, s = ref_sample_run(g, x, per_step, threads)
+        if i >= args.warmup:
+            vals.append(gf)
+            rows_total += len(rows)
+    v = float(np.median(vals))
+    line = {"metric": METRIC, "value": round(v, 6), "unit": "GFLOP/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (same seeds as the b200 arm)",
+            "config": {"workload": cfg["workload"], "nodes": g.n_rows, "edges": st["nnz_a"], "x_cols": x.n_cols},
+            "impl": "reference",
+            "cpu_baseline": {"value": round(v, 6), "unit": "GFLOP/s", "kind": kind,
+                             "cores": threads if kind == "reference" else 1,
+                             "sample": f"{rows_total} sampled rows over {args.steps} steps (~{per_step:.0f} s each)"},
+            "e2e": {"value": round(v, 6), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
+    ap.add_argument("--mode", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -85,11 +85,10 @@ typedef struct aires_b200_matrix {
 } aires_b200_matrix;
 
 /*
- * Output allocator.  Called once per product, after the symbolic pass, with
- * the exact row and nnz counts (the exact allocation of spgemm.hpp:111-112).
- * Must return buffers in out->location of n_rows+1 u64, nnz idx_bytes-wide
- * and nnz val_bytes-wide entries.  Return 0 on success; any other value is
- * passed back to the caller as the status.
+ * Output allocator.  Called once per product, once the exact row and nnz counts are
+ * known (the exact allocation of spgemm.hpp:111-112).  Must return buffers in out->location of n_rows+1 u64, nnz idx_bytes-wide and nnz
+ * val_bytes-wide entries.  Return 0 on success; any other value is passed back to the
+ * caller as the status.
  */
 typedef int (*aires_b200_alloc_fn)(void* user, uint64_t n_rows, uint64_t nnz, void** ptr,
                                    void** idx, void** val);
@@ -175,10 +174,15 @@ int aires_b200_run(const aires_b200_matrix* a, const aires_b200_matrix* b,
                    aires_b200_run_report* report);
 
 /* ---- timing helpers for harnesses (not part of the reference surface) --- */
+/* The cudaStream_t the calling thread's products run on (current device), so a harness can
+   record CUDA events on the stream the kernels are launched on. */
+void* aires_b200_stream(void);
+/* Number of kernels the last product on this thread launched. */
+int aires_b200_last_launches(void);
 /* Elapsed ms of the last aires_b200_spgemm/_op on this thread (CUDA events). */
 double aires_b200_last_kernel_ms(void);
-/* Per-kernel ms of the last product on this thread: [classify, symbolic, scan, numeric,
-   x_prep, h2d, d2h]; returns the number of entries written (<= cap). */
+/* Per-stage ms of the last product on this thread: [classify+mac count, place, scan,
+   numeric, x_prep, h2d, d2h]; returns the number of entries written (<= cap). */
 int aires_b200_last_profile(double* ms, int cap);
 
 #ifdef __cplusplus

@@ -130,6 +130,8 @@ def lib() -> C.CDLL:
                                        P(C.c_uint64)]
     L.aires_b200_run.argtypes = [P(_Matrix), P(_Matrix), P(_RunConfig), P(_Output), P(_RunReport)]
     L.aires_b200_last_kernel_ms.restype = C.c_double
+    L.aires_b200_stream.restype = C.c_void_p
+    L.aires_b200_last_launches.restype = C.c_int
     L.aires_b200_last_profile.argtypes = [P(C.c_double), C.c_int]
     L.aires_b200_synth_graph.argtypes = [P(_GraphSpec), P(_Output), P(C.c_double)]
     L.aires_b200_synth_features.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, P(_Output)]

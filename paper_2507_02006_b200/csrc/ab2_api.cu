@@ -174,12 +174,12 @@ int aires_b200_spgemm(const aires_b200_matrix* a, const aires_b200_matrix* b, ui
     if (mode == AIRES_B200_MODE_AUTO) mode = c->val_bytes == 8 ? AIRES_B200_MODE_FP64_EXACT : AIRES_B200_MODE_FP32;
     cudaEvent_t t0 = ctx.ev[10], t1 = ctx.ev[11];
     AB2_CUDA(cudaEventRecord(t0, ctx.stream));
-    auto x = ab2::make_operand(ctx, *b, mode);
+    auto x = ab2::make_operand(ctx, *b, mode, /*temp=*/true);
     AB2_CUDA(cudaEventRecord(t1, ctx.stream));
-    AB2_CUDA(cudaEventSynchronize(t1));
+    ctx.launches = x->prep_launches;
+    ab2::spgemm_rows(ctx, *a, *x, *c);
     float ms = 0;
     AB2_CUDA(cudaEventElapsedTime(&ms, t0, t1));
-    ab2::spgemm_rows(ctx, *a, *x, *c);
     ctx.prof[ab2::kPXPrep] = ms;
   });
 }
@@ -189,7 +189,7 @@ int aires_b200_operand_create(const aires_b200_matrix* b, uint32_t mode, aires_b
     if (!b || !out) ab2::fail(AIRES_B200_INVALID_ARGUMENT, "null argument");
     ab2::Ctx& ctx = ab2::ctx_for_thread();
     auto op = std::make_unique<aires_b200_operand_s>();
-    op->x = ab2::make_operand(ctx, *b, mode);
+    op->x = ab2::make_operand(ctx, *b, mode, /*temp=*/false);
     *out = op.release();
   });
 }
@@ -216,6 +216,7 @@ int aires_b200_spgemm_op(const aires_b200_matrix* a, aires_b200_operand b, aires
     ab2::Ctx& ctx = ab2::ctx_for_thread();
     if (b->x->device != ctx.device)
       ab2::fail(AIRES_B200_INVALID_ARGUMENT, "operand lives on another device");
+    ctx.launches = 0;
     ab2::spgemm_rows(ctx, *a, *b->x, *c);
     ctx.prof[ab2::kPXPrep] = 0.0;
   });
@@ -232,6 +233,17 @@ int aires_b200_robw_cuts(const uint64_t* row_ptr, uint64_t n_rows, uint64_t m_a,
                         bad_row);
   });
   return g != AIRES_B200_OK ? g : rc;
+}
+
+void* aires_b200_stream(void) {
+  void* s = nullptr;
+  ab2::guarded([&] { s = static_cast<void*>(ab2::ctx_for_thread().stream); });
+  return s;
+}
+
+int aires_b200_last_launches(void) {
+  auto it = ab2::tl_ctx.find(ab2::tl_device);
+  return it == ab2::tl_ctx.end() ? 0 : it->second->launches;
 }
 
 double aires_b200_last_kernel_ms(void) {

@@ -33,7 +33,9 @@ struct HostBuf {
   ~HostBuf() { release(); }
 };
 
-enum ProfSlot { kPClassify, kPSymbolic, kPScan, kPNumeric, kPXPrep, kPH2D, kPD2H, kPCount };
+// kPPlace shares the slot the symbolic pass used before the single-pass design.
+enum ProfSlot { kPClassify, kPPlace, kPScan, kPNumeric, kPXPrep, kPH2D, kPD2H, kPCount };
+constexpr int kPSymbolic = kPPlace;
 
 // Per-thread, per-device execution context (reentrancy: SURVEY.md §8b Threading).
 struct Ctx {
@@ -44,10 +46,14 @@ struct Ctx {
   DevBuf a_ptr, a_col, a_val, a_col2, a_val2;  // uploaded / converted A
   DevBuf cnt, rflops, cptr, scan_part, sym_heavy, num_heavy, fix_rows, ctl;
   DevBuf c_col, c_val;                          // C staging for host outputs
+  DevBuf t_col, t_val;                          // product staging (K_numeric -> K_place)
   DevBuf x_ptr, x_idx, x_val;                   // raw X upload (host operands)
+  DevBuf xo_ptr, xo_col, xo_val, xo_slots, xo_cslots, xo_len;  // per-call operand layout
   HostBuf h_ctl;
   double prof[kPCount] = {};
   double last_ms = 0.0;
+  int launches = 0;  // kernels launched by the last product
+  uint64_t last_fix_rows = 0;
   explicit Ctx(int dev);
   ~Ctx();
 };
@@ -61,17 +67,24 @@ struct XOperand {
   uint32_t mode = 0;  // AIRES_B200_MODE_FP32 or _FP64_EXACT
   int64_t K = 0, n_cols = 0, nnz = 0;
   int W = 0;
+  int64_t max_row_len = 0;  // longest X row (bounds C nnz per A entry)
   void* ptr = nullptr;     // int64 K+1
   void* col = nullptr;     // int32 nnz
   void* val = nullptr;     // V nnz
   void* slots = nullptr;   // K*W entries
-  void* cslots = nullptr;  // K*W u16
+  void* cslots = nullptr;  // K*kCSlotW u16
+  void* xlen = nullptr;    // K+1 u16 row lengths
+  double xmin = 0.0;       // smallest nonzero |x|
+  bool has_zero = false;   // X stores an exact zero
   size_t bytes = 0;
+  int prep_launches = 0;
+  bool owned = true;  // kernels launched to build the operand
   ~XOperand();
 };
 
 // Builds an operand from a matrix view (host or device, CSR or CSC).
-std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode);
+// temp: storage comes from the context (valid until the next product on this thread).
+std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode, bool temp);
 
 // C = A * X; A is a CSR rows view (host or device).
 void spgemm_rows(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_b200_output& out);

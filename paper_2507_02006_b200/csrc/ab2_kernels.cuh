@@ -7,8 +7,6 @@
 //   K_scan      : exclusive scan of the counts -> int64 C row_ptr (spgemm.hpp:107, :111)
 //   K_numeric   : per-row dense shared-memory accumulator, emitted in ascending column
 //                 order (spgemm.hpp:114-130; canonical, sparse.hpp:26-28)
-//   K_fix       : rows whose fast-path marker disagreed with the symbolic count
-//                 (all contributions were -0.0) are recomputed with explicit marks.
 //
 // Work distribution: heavy rows (by A-degree for symbolic, by MACs for numeric) are
 // claimed first, one CTA per row; light rows then go one warp per row from a ticket
@@ -26,8 +24,6 @@
 namespace ab2 {
 
 constexpr int kLightBatch = 4;   // light rows per ticket
-constexpr int kUnrollSym = 4;    // A entries in flight per lane (symbolic)
-constexpr int kUnrollNum = 4;    // group steps in flight (numeric)
 
 template <class V>
 struct Sentinel;
@@ -124,26 +120,28 @@ __device__ __forceinline__ CSlot<W> empty_cslot() {
   return s;
 }
 
-// Marks the columns of X row k in `flags`; returns the row's MAC count.
+// Marks the inline columns of X row k in `flags` (predicated byte stores; concurrent
+// writers only ever store 1) and returns their count; *ovf reports an overflow marker.
 template <int W>
-__device__ __forceinline__ int64_t mark_cslot(const CSlot<W>& s, uint64_t k,
-                                              const int64_t* __restrict__ xptr,
-                                              const int32_t* __restrict__ xcol,
-                                              unsigned char* flags) {
-  int64_t f = 0;
+__device__ __forceinline__ uint32_t mark_cslot(const CSlot<W>& s, unsigned char* flags, bool& ovf) {
+  uint32_t f = 0;
 #pragma unroll
   for (int e = 0; e < W; e++) {
-    uint32_t c = s.at(e);
-    if (c < kCOvf) {
-      flags[c] = 1;
-      f++;
-    } else if (c == kCOvf) {  // only ever in entry W-1
-      int64_t t0 = xptr[k] + (W - 1), t1 = xptr[k + 1];
-      for (int64_t t = t0; t < t1; t++) flags[xcol[t]] = 1;
-      f += t1 - t0;
-    }
+    const uint32_t c = s.at(e);
+    if (c < kCOvf) flags[c] = 1;
+    f += c < kCOvf;
+    ovf |= c == kCOvf;
   }
   return f;
+}
+
+// Overflow tail of X row k (rows longer than the slot; rare on the GCN shapes).
+template <int W>
+__device__ __noinline__ uint32_t mark_tail(uint64_t k, const int64_t* __restrict__ xptr,
+                                           const int32_t* __restrict__ xcol, unsigned char* flags) {
+  const int64_t t0 = xptr[k] + (W - 1), t1 = xptr[k + 1];
+  for (int64_t t = t0; t < t1; t++) flags[xcol[t]] = 1;
+  return static_cast<uint32_t>(t1 - t0);
 }
 
 // ---------------------------------------------------------------------------
@@ -178,6 +176,35 @@ __device__ __forceinline__ int count_flags(uint32_t* f, int words, int start, in
   return c;
 }
 
+// Lane-per-A-entry: each lane loads one whole column-only slot (2W bytes, one vector load)
+// and sets its flags; 32 entries per warp step, two steps in flight.
+template <class IdxT, int W>
+__device__ __forceinline__ uint32_t sym_walk(const SymArgs& p, const IdxT* __restrict__ ac, uint32_t n, uint32_t first,
+                                             uint32_t stride, unsigned char* flags) {
+  const uint32_t K = static_cast<uint32_t>(p.K);
+  uint32_t f = 0;
+  for (uint32_t b = first; b < n; b += 2 * stride) {
+    const uint32_t i0 = b, i1 = b + stride;
+    uint32_t k0 = 0xffffffffu, k1 = 0xffffffffu;
+    if (i0 < n) {
+      const uint64_t k = static_cast<uint64_t>(ac[i0]);
+      k0 = k < K ? static_cast<uint32_t>(k) : 0xffffffffu;
+    }
+    if (i1 < n) {
+      const uint64_t k = static_cast<uint64_t>(ac[i1]);
+      k1 = k < K ? static_cast<uint32_t>(k) : 0xffffffffu;
+    }
+    const CSlot<W> c0 = k0 != 0xffffffffu ? load_cslot<W>(p.cslots, k0) : empty_cslot<W>();
+    const CSlot<W> c1 = k1 != 0xffffffffu ? load_cslot<W>(p.cslots, k1) : empty_cslot<W>();
+    bool o0 = false, o1 = false;
+    f += mark_cslot<W>(c0, flags, o0);
+    f += mark_cslot<W>(c1, flags, o1);
+    if (o0) f += mark_tail<W>(k0, p.xptr, p.xcol, flags);
+    if (o1) f += mark_tail<W>(k1, p.xptr, p.xcol, flags);
+  }
+  return f;
+}
+
 template <class IdxT, int W>
 __global__ void __launch_bounds__(256) k_symbolic(SymArgs p, const IdxT* __restrict__ acol) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -190,7 +217,7 @@ __global__ void __launch_bounds__(256) k_symbolic(SymArgs p, const IdxT* __restr
   unsigned long long my_flops = 0;
   const unsigned long long n_heavy = p.ctl->n_sym_heavy;
 
-  // Phase 1: heavy rows, one CTA per row (flags in warp 0's region).
+  // Phase 1: heavy rows (A-degree > heavy_deg), one CTA per row, flags in warp 0's region.
   for (;;) {
     if (threadIdx.x == 0) s_ticket = atomicAdd(&p.ctl->heavy_next, 1ull);
     __syncthreads();
@@ -199,12 +226,7 @@ __global__ void __launch_bounds__(256) k_symbolic(SymArgs p, const IdxT* __restr
     if (h >= n_heavy) break;
     const int64_t r = p.sym_heavy[h];
     const uint64_t s = p.aptr[r] - p.abase, e = p.aptr[r + 1] - p.abase;
-    int64_t f = 0;
-    for (uint64_t i = s + threadIdx.x; i < e; i += blockDim.x) {
-      uint64_t k = static_cast<uint64_t>(acol[i]);
-      if (k < static_cast<uint64_t>(p.K))
-        f += mark_cslot<W>(load_cslot<W>(p.cslots, k), k, p.xptr, p.xcol, smem);
-    }
+    int64_t f = sym_walk<IdxT, W>(p, acol + s, static_cast<uint32_t>(e - s), threadIdx.x, blockDim.x, smem);
     __syncthreads();
     int64_t c = count_flags(reinterpret_cast<uint32_t*>(smem), words, threadIdx.x, blockDim.x);
     c = block_sum<int64_t>(c, s_red);
@@ -229,21 +251,7 @@ __global__ void __launch_bounds__(256) k_symbolic(SymArgs p, const IdxT* __restr
     for (int64_t r = static_cast<int64_t>(r0); r < r1; r++) {
       const uint64_t s = p.aptr[r] - p.abase, e = p.aptr[r + 1] - p.abase;
       if (static_cast<int64_t>(e - s) > p.heavy_deg) continue;
-      int64_t f = 0;
-      for (uint64_t b = s; b < e; b += 32 * kUnrollSym) {
-        uint64_t kk[kUnrollSym];
-#pragma unroll
-        for (int u = 0; u < kUnrollSym; u++) {
-          uint64_t i = b + u * 32 + lane;
-          kk[u] = i < e ? static_cast<uint64_t>(acol[i]) : ~0ull;
-        }
-        CSlot<W> cs[kUnrollSym];
-#pragma unroll
-        for (int u = 0; u < kUnrollSym; u++)
-          cs[u] = kk[u] < static_cast<uint64_t>(p.K) ? load_cslot<W>(p.cslots, kk[u]) : empty_cslot<W>();
-#pragma unroll
-        for (int u = 0; u < kUnrollSym; u++) f += mark_cslot<W>(cs[u], kk[u], p.xptr, p.xcol, flags);
-      }
+      uint32_t f = sym_walk<IdxT, W>(p, acol + s, static_cast<uint32_t>(e - s), lane, 32, flags);
       __syncwarp();
       int c = count_flags(reinterpret_cast<uint32_t*>(flags), words, lane, 32);
       c = warp_sum(c);
@@ -320,331 +328,6 @@ static __global__ void __launch_bounds__(kScanThreads) k_scan_down(const int32_t
     if (j < n) out[j + 1] = run;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = 0;
-}
-
-// ---------------------------------------------------------------------------
-// K_numeric
-// ---------------------------------------------------------------------------
-template <class V, class IdxT>
-struct NumArgs {
-  const uint64_t* aptr;
-  uint64_t abase;
-  const IdxT* acol;
-  const V* aval;
-  int64_t rows;
-  XView<V> x;
-  int32_t region_elems;  // per-warp accumulator elements (>= n_cols)
-  const int32_t* cnt;
-  const int64_t* cptr;
-  const int64_t* rflops;
-  const int64_t* num_heavy;
-  int64_t heavy_flops;
-  IdxT* ccol;
-  V* cval;
-  int64_t* fix_rows;
-  Ctl* ctl;
-};
-
-// Warp emission of a dense accumulator in ascending column order; resets the
-// touched cells to the marker.  Returns the number of cells emitted.
-template <class V, class IdxT>
-__device__ __forceinline__ int64_t emit_warp(V* acc, int n_cols, int64_t out, IdxT* __restrict__ ccol,
-                                             V* __restrict__ cval) {
-  const int lane = lane_id();
-  int64_t n = 0;
-  for (int c0 = 0; c0 < n_cols; c0 += 32) {
-    int c = c0 + lane;
-    V v = c < n_cols ? acc[c] : Sentinel<V>::value();
-    bool t = !Sentinel<V>::is(v);
-    unsigned b = __ballot_sync(kFull, t);
-    if (t) {
-      int64_t pos = out + n + __popc(b & ((1u << lane) - 1));
-      ccol[pos] = static_cast<IdxT>(c);
-      cval[pos] = v;
-      acc[c] = Sentinel<V>::value();
-    }
-    n += __popc(b);
-  }
-  return n;
-}
-
-template <class V>
-__device__ __forceinline__ typename SlotOf<V>::type load_slot(const typename SlotOf<V>::type* __restrict__ slots,
-                                                              uint64_t i) {
-  using S = typename SlotOf<V>::type;
-  S s;
-  if constexpr (sizeof(S) == 8) {
-    uint2 v = __ldg(reinterpret_cast<const uint2*>(slots + i));
-    s.col = v.x;
-    s.val = __uint_as_float(v.y);
-  } else {
-    uint4 v = __ldg(reinterpret_cast<const uint4*>(slots + i));
-    s.col = v.x;
-    s.pad = v.y;
-    s.val = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(v.w) << 32) | v.z));
-  }
-  return s;
-}
-
-template <class V>
-__device__ __forceinline__ typename SlotOf<V>::type empty_slot() {
-  typename SlotOf<V>::type s;
-  s.col = kSlotEmpty;
-  s.val = V(0);
-  return s;
-}
-
-__device__ __forceinline__ void acc_add(float* p, float v) { atomicAdd(p, v); }
-
-// fp32, order-free: every lane of every group applies its entry at once (CAS add).
-template <class IdxT>
-__device__ __forceinline__ void apply_f32(const SlotF& en, float a, const XView<float>& x, float* acc) {
-  if (en.col < kSlotOvf) {
-    acc_add(&acc[en.col], a * en.val);
-  } else if (en.col != kSlotEmpty) {
-    int64_t off = slot_ovf_offset(en);
-    int64_t n = en.col & 0x7fffffffu;
-    for (int64_t t = 0; t < n; t++) acc_add(&acc[x.col[off + t]], a * x.val[off + t]);
-  }
-}
-
-// Group-strided product loop of one row for fp32.  `G` groups of W lanes; group g
-// handles A entries b + g, b + g + G, ...
-template <class IdxT, int W>
-__device__ __forceinline__ void row_products_f32(const NumArgs<float, IdxT>& p, uint64_t s, uint64_t e,
-                                                 int gid, int G, int ent, float* acc) {
-  for (uint64_t b = s; b < e; b += static_cast<uint64_t>(G) * kUnrollNum) {
-    uint64_t kk[kUnrollNum];
-    float aa[kUnrollNum];
-#pragma unroll
-    for (int u = 0; u < kUnrollNum; u++) {
-      uint64_t i = b + static_cast<uint64_t>(u) * G + gid;
-      kk[u] = ~0ull;
-      aa[u] = 0.f;
-      if (i < e) {
-        kk[u] = static_cast<uint64_t>(p.acol[i]);
-        aa[u] = p.aval[i];
-      }
-    }
-    SlotF en[kUnrollNum];
-#pragma unroll
-    for (int u = 0; u < kUnrollNum; u++)
-      en[u] = kk[u] < static_cast<uint64_t>(p.x.K) ? load_slot<float>(p.x.slots, kk[u] * W + ent)
-                                                  : empty_slot<float>();
-#pragma unroll
-    for (int u = 0; u < kUnrollNum; u++) apply_f32<IdxT>(en[u], aa[u], p.x, acc);
-  }
-}
-
-template <class IdxT, int W>
-__global__ void __launch_bounds__(256) k_numeric_f32(NumArgs<float, IdxT> p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* accs = reinterpret_cast<float*>(smem_raw);
-  __shared__ unsigned long long s_ticket;
-  const int lane = lane_id(), warp = warp_id(), nw = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < nw * p.region_elems; i += blockDim.x) accs[i] = Sentinel<float>::value();
-  __syncthreads();
-  const unsigned long long n_heavy = p.ctl->n_num_heavy;
-
-  // Phase 1: heavy rows, one CTA per row, groups across the CTA, shared accumulator.
-  for (;;) {
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&p.ctl->num_heavy_next, 1ull);
-    __syncthreads();
-    const unsigned long long h = s_ticket;
-    __syncthreads();
-    if (h >= n_heavy) break;
-    const int64_t r = p.num_heavy[h];
-    const uint64_t s = p.aptr[r] - p.abase, e = p.aptr[r + 1] - p.abase;
-    row_products_f32<IdxT, W>(p, s, e, threadIdx.x / W, blockDim.x / W, threadIdx.x % W, accs);
-    __syncthreads();
-    if (warp == 0) {
-      int64_t n = emit_warp<float, IdxT>(accs, p.x.n_cols, p.cptr[r], p.ccol, p.cval);
-      warp_append(lane == 0 && n != p.cnt[r], r, p.fix_rows, &p.ctl->n_fix);
-    }
-    __syncthreads();
-  }
-
-  // Phase 2: light rows, one warp per row.
-  float* acc = accs + static_cast<int64_t>(warp) * p.region_elems;
-  for (;;) {
-    unsigned long long r0 = 0;
-    if (lane == 0) r0 = atomicAdd(&p.ctl->num_light_next, static_cast<unsigned long long>(kLightBatch));
-    r0 = __shfl_sync(kFull, r0, 0);
-    if (r0 >= static_cast<unsigned long long>(p.rows)) break;
-    const int64_t r1 = min(static_cast<int64_t>(r0) + kLightBatch, p.rows);
-    for (int64_t r = static_cast<int64_t>(r0); r < r1; r++) {
-      if (p.rflops[r] > p.heavy_flops) continue;
-      const uint64_t s = p.aptr[r] - p.abase, e = p.aptr[r + 1] - p.abase;
-      row_products_f32<IdxT, W>(p, s, e, lane / W, 32 / W, lane % W, acc);
-      __syncwarp();
-      int64_t n = emit_warp<float, IdxT>(acc, p.x.n_cols, p.cptr[r], p.ccol, p.cval);
-      warp_append(lane == 0 && n != p.cnt[r], r, p.fix_rows, &p.ctl->n_fix);
-      __syncwarp();
-    }
-  }
-}
-
-// fp64 exact: within a group step, groups apply their entries one group at a time
-// (ascending A entry == ascending k), so every cell is summed in ascending k with one
-// IEEE multiply and one IEEE add per term (no FMA): bit-identical to dot_row_col.
-// Lanes whose column is outside [c_lo, c_hi) skip (column-owner split of heavy rows).
-template <int W>
-__device__ __forceinline__ void apply_f64_ordered(const SlotD& en, double a, const XView<double>& x,
-                                                  double* acc, int c_lo, int c_hi) {
-  if (en.col < kSlotOvf) {
-    int c = static_cast<int>(en.col);
-    if (c >= c_lo && c < c_hi) acc[c] = __dadd_rn(acc[c], __dmul_rn(a, en.val));
-  } else if (en.col != kSlotEmpty) {
-    int64_t off = slot_ovf_offset(en);
-    int64_t n = en.col & 0x7fffffffu;
-    for (int64_t t = 0; t < n; t++) {
-      int c = x.col[off + t];
-      if (c >= c_lo && c < c_hi) acc[c] = __dadd_rn(acc[c], __dmul_rn(a, x.val[off + t]));
-    }
-  }
-}
-
-template <class IdxT, int W>
-__device__ __forceinline__ void row_products_f64(const NumArgs<double, IdxT>& p, uint64_t s, uint64_t e,
-                                                 double* acc, int c_lo, int c_hi) {
-  constexpr int G = 32 / W;
-  const int lane = lane_id(), gid = lane / W, ent = lane % W;
-  for (uint64_t b = s; b < e; b += static_cast<uint64_t>(G) * kUnrollNum) {
-    uint64_t kk[kUnrollNum];
-    double aa[kUnrollNum];
-#pragma unroll
-    for (int u = 0; u < kUnrollNum; u++) {
-      uint64_t i = b + static_cast<uint64_t>(u) * G + gid;
-      kk[u] = ~0ull;
-      aa[u] = 0.0;
-      if (i < e) {
-        kk[u] = static_cast<uint64_t>(p.acol[i]);
-        aa[u] = p.aval[i];
-      }
-    }
-    SlotD en[kUnrollNum];
-#pragma unroll
-    for (int u = 0; u < kUnrollNum; u++)
-      en[u] = kk[u] < static_cast<uint64_t>(p.x.K) ? load_slot<double>(p.x.slots, kk[u] * W + ent)
-                                                  : empty_slot<double>();
-#pragma unroll
-    for (int u = 0; u < kUnrollNum; u++) {
-#pragma unroll
-      for (int g = 0; g < G; g++) {
-        if (gid == g) apply_f64_ordered<W>(en[u], aa[u], p.x, acc, c_lo, c_hi);
-        __syncwarp();
-      }
-    }
-  }
-}
-
-template <class IdxT, int W>
-__global__ void __launch_bounds__(256) k_numeric_f64(NumArgs<double, IdxT> p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* accs = reinterpret_cast<double*>(smem_raw);
-  __shared__ unsigned long long s_ticket;
-  __shared__ int64_t s_cnt[32];
-  const int lane = lane_id(), warp = warp_id(), nw = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < nw * p.region_elems; i += blockDim.x) accs[i] = Sentinel<double>::value();
-  __syncthreads();
-  const unsigned long long n_heavy = p.ctl->n_num_heavy;
-  const int n_cols = p.x.n_cols;
-
-  // Phase 1: heavy rows.  Column-owner split: warp w owns a contiguous column range of
-  // the shared accumulator and walks every A entry of the row in order, so each cell is
-  // still accumulated in ascending k by exactly one warp.
-  const int span = ((n_cols + nw - 1) / nw + 31) & ~31;
-  const int c_lo = min(warp * span, n_cols), c_hi = min(c_lo + span, n_cols);
-  for (;;) {
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&p.ctl->num_heavy_next, 1ull);
-    __syncthreads();
-    const unsigned long long h = s_ticket;
-    __syncthreads();
-    if (h >= n_heavy) break;
-    const int64_t r = p.num_heavy[h];
-    const uint64_t s = p.aptr[r] - p.abase, e = p.aptr[r + 1] - p.abase;
-    if (c_lo < c_hi) row_products_f64<IdxT, W>(p, s, e, accs, c_lo, c_hi);
-    __syncthreads();
-    if (warp == 0) {
-      int64_t n = emit_warp<double, IdxT>(accs, n_cols, p.cptr[r], p.ccol, p.cval);
-      warp_append(lane == 0 && n != p.cnt[r], r, p.fix_rows, &p.ctl->n_fix);
-    }
-    __syncthreads();
-  }
-  (void)s_cnt;
-
-  // Phase 2: light rows, one warp per row.
-  double* acc = accs + static_cast<int64_t>(warp) * p.region_elems;
-  for (;;) {
-    unsigned long long r0 = 0;
-    if (lane == 0) r0 = atomicAdd(&p.ctl->num_light_next, static_cast<unsigned long long>(kLightBatch));
-    r0 = __shfl_sync(kFull, r0, 0);
-    if (r0 >= static_cast<unsigned long long>(p.rows)) break;
-    const int64_t r1 = min(static_cast<int64_t>(r0) + kLightBatch, p.rows);
-    for (int64_t r = static_cast<int64_t>(r0); r < r1; r++) {
-      if (p.rflops[r] > p.heavy_flops) continue;
-      const uint64_t s = p.aptr[r] - p.abase, e = p.aptr[r + 1] - p.abase;
-      row_products_f64<IdxT, W>(p, s, e, acc, 0, n_cols);
-      __syncwarp();
-      int64_t n = emit_warp<double, IdxT>(acc, n_cols, p.cptr[r], p.ccol, p.cval);
-      warp_append(lane == 0 && n != p.cnt[r], r, p.fix_rows, &p.ctl->n_fix);
-      __syncwarp();
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K_fix: rows whose marker count disagreed (all-(-0.0) cells).  One warp per row,
-// explicit byte marks, +0.0 start, A entries applied one k at a time in ascending
-// order from the plain CSR copy of X.  Rare; correctness path only.
-// ---------------------------------------------------------------------------
-template <class V, class IdxT>
-__global__ void __launch_bounds__(32) k_fix_rows(NumArgs<V, IdxT> p, int64_t n_fix) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* acc = reinterpret_cast<V*>(smem_raw);
-  unsigned char* mark = smem_raw + static_cast<size_t>(p.region_elems) * sizeof(V);
-  const int lane = lane_id();
-  const int n_cols = p.x.n_cols;
-  for (int64_t q = blockIdx.x; q < n_fix; q += gridDim.x) {
-    const int64_t r = p.fix_rows[q];
-    for (int c = lane; c < n_cols; c += 32) {
-      acc[c] = V(0);
-      mark[c] = 0;
-    }
-    __syncwarp();
-    const uint64_t s = p.aptr[r] - p.abase, e = p.aptr[r + 1] - p.abase;
-    for (uint64_t i = s; i < e; i++) {
-      uint64_t k = static_cast<uint64_t>(p.acol[i]);
-      if (k >= static_cast<uint64_t>(p.x.K)) continue;
-      V a = p.aval[i];
-      for (int64_t t = p.x.ptr[k] + lane; t < p.x.ptr[k + 1]; t += 32) {
-        int c = p.x.col[t];
-        V prod;
-        if constexpr (sizeof(V) == 8) {
-          prod = __dmul_rn(a, p.x.val[t]);
-          acc[c] = __dadd_rn(acc[c], prod);
-        } else {
-          prod = __fmul_rn(a, p.x.val[t]);
-          acc[c] = __fadd_rn(acc[c], prod);
-        }
-        mark[c] = 1;
-      }
-      __syncwarp();
-    }
-    int64_t out = p.cptr[r], n = 0;
-    for (int c0 = 0; c0 < n_cols; c0 += 32) {
-      int c = c0 + lane;
-      bool t = c < n_cols && mark[c];
-      unsigned b = __ballot_sync(kFull, t);
-      if (t) {
-        int64_t pos = out + n + __popc(b & ((1u << lane) - 1));
-        p.ccol[pos] = static_cast<IdxT>(c);
-        p.cval[pos] = acc[c];
-      }
-      n += __popc(b);
-    }
-    __syncwarp();
-  }
 }
 
 }  // namespace ab2

@@ -1,0 +1,529 @@
+// ab2_numeric.cuh -- the A·X product pass of the B200 SpGEMM (spgemm.hpp:60-132), sm_100a.
+//
+// Single pass over A: each row is accumulated once into a dense shared-memory accumulator,
+// counted, and written once (ascending columns, canonical per sparse.hpp:26-28) into a
+// bump-allocated staging area; K_place then streams the rows into their exact CSR offsets
+// (row_ptr = exclusive scan of the counts, spgemm.hpp:107/:111-112).
+//   Why not two passes: a symbolic pass re-walks every A entry and gathers X's column slots
+//   (L1-wavefront bound, ~1.1 ms at the Reddit shape on B200), while this pass leaves HBM
+//   mostly idle, so one extra streaming copy of C (~2 bytes moved per C byte at full HBM
+//   bandwidth) is the cheaper way to the exact layout.
+//   Why not a row-level decoupled look-back: with heavy-tailed row costs it serialises warps
+//   behind slow rows (measured 10 s at the Reddit shape).
+//
+// Mapping (light rows, one warp per row):
+//   * X rows live in W-entry slots (ab2_operand.cuh); a group of W lanes takes one A entry
+//     (k, a) and each lane one slot entry, so a warp step covers G = 32/W A entries.
+//   * A entries are read 32 at a time, coalesced, and handed to groups by shuffles.
+//   * Unused slot entries and padding A entries hit the accumulator's trash column, so
+//     the step is unpredicated: SHFL k, SHFL a, LDG slot, FMUL, LDS, FADD, STS.
+//   * fp32: every group owns a private accumulator copy, so no two lanes of a warp step
+//     ever touch the same shared word (smem CAS add measured 11.7 SM-cycles per warp op on
+//     B200 vs 6.7 for a plain RMW).  Copies are summed when the row is counted.
+//   * fp64-exact: one accumulator; the G groups of a step apply their entries one group at
+//     a time, so each cell is summed in ascending k with one IEEE mul and one IEEE add per
+//     term -- bit-identical to dot_row_col (spgemm.hpp:21-42).
+// Heavy rows (A-degree > heavy_deg) are claimed first, one CTA per row: fp32 warps split
+// the row's entries and the CTA sums all copies; fp64 warps split the columns (each warp
+// walks every entry in order and redirects columns outside its range to the trash column).
+//
+// Marker: accumulator cells start at -0.0 (-0.0 + p == p unless p == -0.0).  Any product
+// that is exactly zero sends the row through the explicit-mark path (start +0.0, byte
+// marks), the reference's `sum = 0.0; if (hit)` semantics (spgemm.hpp:27-41, :58-59).
+#pragma once
+#include <type_traits>
+
+#ifndef AB2_NUM_BATCH
+#define AB2_NUM_BATCH 8
+#endif
+#ifndef AB2_NUM_MINB
+#define AB2_NUM_MINB 3
+#endif
+
+#include "ab2_kernels.cuh"
+
+namespace ab2 {
+
+
+template <class V, class IdxT>
+struct Num3Args {
+  const uint64_t* aptr;
+  uint64_t abase;
+  const IdxT* acol;
+  const V* aval;
+  int64_t rows;
+  XView<V> x;
+  int32_t stride;      // accumulator elements per copy (>= n_cols + 1, multiple of 32)
+  int32_t copies;      // accumulator copies per warp
+  int32_t warp_bytes;  // shared bytes per warp: copies*stride*sizeof(V) + stride marks + chunk table
+  int32_t pad0;
+  const int64_t* heavy;  // heavy rows (A-degree > heavy_deg)
+  int64_t heavy_deg;
+  uint32_t* cnt;         // per-row nnz
+  uint64_t* toff;        // per-row staging offset
+  IdxT* tcol;            // staging area
+  V* tval;
+  uint64_t t_cap;
+  const uint16_t* xlen;  // X row lengths (K+1, dummy row 0), for the MAC count
+  V tiny;                // |a| threshold of the per-chunk zero-product check
+  uint32_t stage_block;  // staging entries a warp reserves at a time (>= 8 * stride)
+  uint32_t pad1;
+  Ctl* ctl;
+};
+
+template <class V>
+__device__ __forceinline__ typename SlotOf<V>::type load_slot(const typename SlotOf<V>::type* __restrict__ slots,
+                                                              uint32_t i) {
+  using S = typename SlotOf<V>::type;
+  S s;
+  if constexpr (sizeof(S) == 8) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(slots) + i);
+    s.col = v.x;
+    s.val = __uint_as_float(v.y);
+  } else {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(slots) + i);
+    s.col = v.x;
+    s.pad = v.y;
+    s.val = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(v.w) << 32) | v.z));
+  }
+  return s;
+}
+
+// ---- the group-strided walk over a contiguous range of A entries -----------
+// Entries [0, n) of ac/av in chunks of 32 (one coalesced load each); chunk c is handled iff
+// c == chunk0 (mod chunk_stride), which lets a CTA's warps interleave over one heavy row.
+// Columns outside [c_lo, c_hi) go to the trash column (the fp64 column-owner split).
+//
+// Zero products (which need the explicit-mark path) are detected per chunk, not per step:
+// a product can only round to zero if |a| * min|x| < 2^-148 (fp32) / 2^-1073 (fp64), or if
+// X stores an exact zero (operand flag XZ: then every product is checked).  MACs come from
+// the per-row length array, one gather per A entry.
+// Per-warp chunk table entry in shared memory: {slot index k*W, row length, a bits}.
+using ChunkPair = uint4;
+
+// Shared-memory read-modify-write at a 32-bit shared address.
+__device__ __forceinline__ void smem_fma(uint32_t addr, float a, float x) {
+  asm volatile(
+      "{\n\t.reg .f32 t;\n\tld.shared.f32 t, [%0];\n\tfma.rn.f32 t, %1, %2, t;\n\tst.shared.f32 [%0], t;\n\t}" ::"r"(addr),
+      "f"(a), "f"(x)
+      : "memory");
+}
+// fp64 exact: one IEEE multiply, one IEEE add (no contraction).
+__device__ __forceinline__ void smem_mul_add(uint32_t addr, double a, double x) {
+  asm volatile(
+      "{\n\t.reg .f64 t, p;\n\tmul.rn.f64 p, %1, %2;\n\tld.shared.f64 t, [%0];\n\tadd.rn.f64 t, t, p;\n\tst.shared.f64 [%0], t;\n\t}" ::"r"(addr),
+      "d"(a), "d"(x)
+      : "memory");
+}
+
+template <class V>
+__device__ __forceinline__ void smem_acc(uint32_t addr, V a, V x) {
+  if constexpr (sizeof(V) == 8)
+    smem_mul_add(addr, a, x);
+  else
+    smem_fma(addr, a, x);
+}
+
+// ---- the group-strided walk over a contiguous range of A entries -----------
+// Entries [0, n) of ac/av in chunks of 32 (one coalesced load each); chunk c is handled iff
+// c == chunk0 (mod chunk_stride), which lets a CTA's warps interleave over one heavy row.
+// Columns outside [c_lo, c_hi) go to the trash column (the fp64 column-owner split).
+//
+// Zero products (which need the explicit-mark path) are detected per chunk, not per step:
+// a product can only round to zero if |a| * min|x| < 2^-148 (fp32) / 2^-1073 (fp64), or if
+// X stores an exact zero (operand flag XZ: then every product is checked).  MACs come from
+// the per-row length array, one gather per A entry.
+template <class V, class IdxT, int W, bool EXACT, bool RANGE, bool XZ>
+__device__ __forceinline__ uint32_t walk_entries(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac,
+                                                 const V* __restrict__ av, uint32_t n, uint32_t chunk0,
+                                                 uint32_t chunk_stride, V* acc, ChunkPair* tab, uint32_t c_lo,
+                                                 uint32_t c_hi, bool& zero) {
+  constexpr int G = 32 / W;
+  constexpr int B = W < AB2_NUM_BATCH ? W : AB2_NUM_BATCH;  // group steps per batch (loads in flight)
+  constexpr uint32_t VS = sizeof(V);
+  const int lane = lane_id(), gid = lane / W, ent = lane % W;
+  const int mlane = gid * W + (W - 1);  // the group's marker lane
+  const uint32_t K = static_cast<uint32_t>(p.x.K);
+  const uint32_t trash = static_cast<uint32_t>(p.x.n_cols);
+  const int32_t* __restrict__ xcol = p.x.col;
+  const V* __restrict__ xval = p.x.val;
+  const uint16_t* __restrict__ xlen = p.xlen;
+  const V tiny = p.tiny;
+  const uint32_t copy_s = static_cast<uint32_t>(__cvta_generic_to_shared(EXACT ? acc : acc + gid * p.stride));
+  const uint32_t tab_s = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
+  uint32_t macs = 0;
+  auto col_of = [&](uint32_t c) -> uint32_t {
+    c &= kSlotColMask;
+    if constexpr (RANGE) c = (c >= c_lo && c < c_hi) ? c : trash;
+    return c;
+  };
+  auto add = [&](uint32_t c, V a, V x) {
+    if constexpr (XZ) {
+      if constexpr (EXACT)
+        zero |= __dmul_rn(a, x) == 0.0;
+      else
+        zero |= a * x == 0.f;
+    }
+    smem_acc<V>(copy_s + c * VS, a, x);
+  };
+  for (uint32_t b = chunk0 * 32; b < n; b += chunk_stride * 32) {
+    const uint32_t i = b + lane;
+    uint32_t k = K;  // dummy row
+    V a = V(1);
+    if (i < n) {
+      const uint64_t kk = static_cast<uint64_t>(ac[i]);
+      k = kk < K ? static_cast<uint32_t>(kk) : K;
+      a = av[i];
+      zero |= !(fabs(a) >= tiny);  // zero, tiny, or NaN weight: take the explicit path
+    }
+    const uint32_t len = xlen[k];
+    macs += len;
+    __syncwarp();
+    if constexpr (sizeof(V) == 4)
+      tab[lane] = make_uint4(k * W, len, __float_as_uint(a), 0u);
+    else
+      tab[lane] = make_uint4(k * W, len, __double2loint(a), __double2hiint(a));
+    __syncwarp();
+    const uint32_t steps = (min(32u, n - b) + G - 1) / G;
+#pragma unroll 1
+    for (uint32_t u0 = 0; u0 < steps; u0 += B) {
+      constexpr uint32_t kNone = 0x7fffffffu;  // lane past the row's length: no slot entry
+      uint32_t col[B];
+      V xv[B], aa[B];
+      uint32_t any = 0;
+#pragma unroll
+      for (int u = 0; u < B; u++) {
+        uint4 t;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w)
+                     : "r"(tab_s + ((u0 + u) * G + gid) * 16u));
+        if constexpr (sizeof(V) == 4)
+          aa[u] = __uint_as_float(t.z);
+        else
+          aa[u] = __hiloint2double(t.w, t.z);
+        col[u] = kNone;
+        xv[u] = V(0);
+        // only the sectors holding the row's entries are fetched (a marker sits at W-1 < len)
+        if (static_cast<uint32_t>(ent) < t.y) {
+          if constexpr (sizeof(V) == 4) {
+            const uint2 e = __ldg(reinterpret_cast<const uint2*>(p.x.slots) + (t.x + ent));
+            col[u] = e.x;
+            xv[u] = __uint_as_float(e.y);
+          } else {
+            const uint4 e = __ldg(reinterpret_cast<const uint4*>(p.x.slots) + (t.x + ent));
+            col[u] = e.x;
+            xv[u] = __hiloint2double(e.w, e.z);
+            if (e.x & kSlotOvf) xv[u] = __longlong_as_double(static_cast<long long>(e.y));
+          }
+        }
+        any |= col[u];
+      }
+      if (!__any_sync(kFull, (any & kSlotOvf) != 0)) {
+        // fast path: no marker in the batch; lanes past a row's length touch nothing
+#pragma unroll
+        for (int u = 0; u < B; u++) {
+          uint32_t c = col[u];
+          if constexpr (RANGE) c = (c >= c_lo && c < c_hi) ? c : trash;
+          if constexpr (EXACT) {
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+              if (gid == g && col[u] != kNone) add(c, aa[u], xv[u]);
+              __syncwarp();
+            }
+          } else {
+            if (col[u] != kNone) add(c, aa[u], xv[u]);
+          }
+        }
+        __syncwarp();
+      } else {
+#pragma unroll
+        for (int u = 0; u < B; u++) {
+          // marker lane: col = kSlotOvf | tail<<16 | trash; the tail offset rides in the value
+          // bits (fp32: 1.0f + offset ulps) or the pad word (fp64, stashed in xv above)
+          uint32_t moff;
+          if constexpr (sizeof(V) == 4)
+            moff = __float_as_uint(xv[u]) - kOneBits;
+          else
+            moff = static_cast<uint32_t>(__double_as_longlong(xv[u]));
+          const uint32_t mc = __shfl_sync(kFull, col[u], mlane);
+          const uint32_t mo = __shfl_sync(kFull, moff, mlane);
+          const uint32_t tn = (mc & kSlotOvf) ? (mc >> 16) & kMaxTail : 0;
+          const bool real = col[u] != kNone && !(col[u] & kSlotOvf);
+          if constexpr (EXACT) {
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+              if (gid == g) {
+                if (real) add(col_of(col[u]), aa[u], xv[u]);
+                for (uint32_t t = ent; t < tn; t += W) add(col_of(xcol[mo + t]), aa[u], xval[mo + t]);
+              }
+              __syncwarp();
+            }
+          } else {
+            if (real) add(col_of(col[u]), aa[u], xv[u]);
+            for (uint32_t t = ent; t < tn; t += W) add(col_of(xcol[mo + t]), aa[u], xval[mo + t]);
+            __syncwarp();
+          }
+        }
+      }
+    }
+  }
+  return macs;
+}
+
+// Explicit-mark slow path (rows with a zero product): one k at a time in ascending order,
+// +0.0 start, byte marks; leaves copy 0 holding values for marked cells and the marker
+// everywhere else (other copies reset), so the common fold / emit path applies.
+template <class V, class IdxT>
+__device__ void slow_row(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac, const V* __restrict__ av,
+                         uint32_t n, V* acc, unsigned char* mark) {
+  const int lane = lane_id();
+  const int n_cols = p.x.n_cols;
+  for (int c = lane; c < p.stride * p.copies; c += 32) acc[c] = c < n_cols ? V(0) : Sentinel<V>::value();
+  for (int c = lane; c < p.stride; c += 32) mark[c] = 0;
+  __syncwarp();
+  for (uint32_t i = 0; i < n; i++) {
+    const uint64_t k = static_cast<uint64_t>(ac[i]);
+    if (k >= static_cast<uint64_t>(p.x.K)) continue;
+    const V a = av[i];
+    for (int64_t t = p.x.ptr[k] + lane; t < p.x.ptr[k + 1]; t += 32) {
+      const int c = p.x.col[t];
+      if constexpr (sizeof(V) == 8)
+        acc[c] = __dadd_rn(acc[c], __dmul_rn(a, p.x.val[t]));
+      else
+        acc[c] = __fadd_rn(acc[c], __fmul_rn(a, p.x.val[t]));
+      mark[c] = 1;
+    }
+    __syncwarp();
+  }
+  for (int c = lane; c < n_cols; c += 32)
+    if (!mark[c]) acc[c] = Sentinel<V>::value();
+  __syncwarp();
+}
+
+// Folds the copies into copy 0 (resetting the others and the trash column) and returns
+// the row nnz.
+template <class V>
+__device__ __forceinline__ uint32_t fold_count(V* acc, int stride, int copies, int n_cols) {
+  const int lane = lane_id();
+  uint32_t cnt = 0;
+  for (int c0 = 0; c0 < stride; c0 += 32) {
+    const int c = c0 + lane;
+    V v = acc[c];
+    for (int g = 1; g < copies; g++) {
+      v += acc[g * stride + c];  // -0.0 is the identity for every operand but +0.0 (stays +0.0)
+      acc[g * stride + c] = Sentinel<V>::value();
+    }
+    if (c >= n_cols) v = Sentinel<V>::value();  // trash column / padding
+    acc[c] = v;
+    cnt += __popc(__ballot_sync(kFull, !Sentinel<V>::is(v)));
+  }
+  return cnt;
+}
+
+// Writes copy 0 (ascending columns) to ccol/cval and resets it.
+template <class V, class IdxT>
+__device__ __forceinline__ void emit_copy0(V* acc, int n_cols, IdxT* __restrict__ ccol, V* __restrict__ cval) {
+  const int lane = lane_id();
+  uint32_t n = 0;
+  for (int c0 = 0; c0 < n_cols; c0 += 32) {
+    const int c = c0 + lane;
+    const V v = c < n_cols ? acc[c] : Sentinel<V>::value();
+    const bool t = !Sentinel<V>::is(v);
+    const unsigned b = __ballot_sync(kFull, t);
+    if (t) {
+      const uint32_t pos = n + __popc(b & ((1u << lane) - 1));
+      ccol[pos] = static_cast<IdxT>(c);
+      cval[pos] = v;
+      acc[c] = Sentinel<V>::value();
+    }
+    n += __popc(b);
+  }
+}
+
+// Warp-level bump allocation in the staging area.
+// Each reservation wastes less than one row (< stride entries) out of >= 8*stride, so the
+// host sizes the staging area as bound * 8/7 + one block per warp; a reservation past the
+// end sets ctl->bad_row and the row is dropped (reported as capacity_exceeded).
+struct StageCursor {
+  unsigned long long cur = 0, end = 0;
+  __device__ __forceinline__ unsigned long long take(uint32_t cnt, Ctl* ctl, uint32_t block) {
+    if (cur + cnt > end) {
+      const unsigned long long want = cnt > block ? cnt : block;
+      unsigned long long base = 0;
+      if (lane_id() == 0) base = atomicAdd(&ctl->n_fix, want);  // n_fix doubles as the stage counter
+      base = __shfl_sync(kFull, base, 0);
+      cur = base;
+      end = base + want;
+    }
+    const unsigned long long o = cur;
+    cur += cnt;
+    return o;
+  }
+};
+
+template <class V, class IdxT, int W, bool XZ>
+__global__ void __launch_bounds__(256, AB2_NUM_MINB) k_numeric3(Num3Args<V, IdxT> p) {
+  constexpr bool EXACT = sizeof(V) == 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ unsigned long long s_ticket;
+  __shared__ int s_zero;
+  __shared__ uint32_t s_cnt[32];
+  const int lane = lane_id(), warp = warp_id(), nw = blockDim.x >> 5;
+  const int n_cols = p.x.n_cols;
+  const int acc_elems = p.stride * p.copies;
+  auto warp_acc = [&](int w) { return reinterpret_cast<V*>(smem_raw + static_cast<size_t>(w) * p.warp_bytes); };
+  auto warp_mark = [&](int w) {
+    return smem_raw + static_cast<size_t>(w) * p.warp_bytes + static_cast<size_t>(acc_elems) * sizeof(V);
+  };
+  auto warp_tab = [&](int w) {
+    return reinterpret_cast<ChunkPair*>(smem_raw + static_cast<size_t>(w) * p.warp_bytes +
+                                           static_cast<size_t>(acc_elems) * sizeof(V) + p.stride);
+  };
+  for (int w = 0; w < nw; w++)
+    for (int i = threadIdx.x; i < acc_elems; i += blockDim.x) warp_acc(w)[i] = Sentinel<V>::value();
+  __syncthreads();
+  StageCursor stage;
+  unsigned long long my_nnz = 0, my_macs = 0;
+  const unsigned long long n_heavy = p.ctl->n_sym_heavy;
+
+  // ---- Phase 1: heavy rows, one CTA per row ----
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_ticket = atomicAdd(&p.ctl->heavy_next, 1ull);
+      s_zero = 0;
+    }
+    __syncthreads();
+    const unsigned long long h = s_ticket;
+    if (h >= n_heavy) break;
+    const int64_t r = p.heavy[h];
+    const uint64_t s = p.aptr[r] - p.abase, e = p.aptr[r + 1] - p.abase;
+    const uint32_t n = static_cast<uint32_t>(e - s);
+    const IdxT* ac = p.acol + s;
+    const V* av = p.aval + s;
+    bool zero = false;
+    if constexpr (EXACT) {
+      // column-owner split over one shared accumulator (warp 0's region)
+      const uint32_t span = ((n_cols + nw - 1) / nw + 31) & ~31;
+      const uint32_t c_lo = min(warp * span, static_cast<uint32_t>(n_cols));
+      const uint32_t c_hi = min(c_lo + span, static_cast<uint32_t>(n_cols));
+      const uint32_t m = walk_entries<V, IdxT, W, true, true, XZ>(p, ac, av, n, 0, 1, warp_acc(0), warp_tab(warp), c_lo, c_hi, zero);
+      if (warp == 0) my_macs += m;
+    } else {
+      my_macs += walk_entries<V, IdxT, W, false, false, XZ>(p, ac, av, n, warp, nw, warp_acc(warp), warp_tab(warp), 0, 0, zero);
+    }
+    if (zero) s_zero = 1;
+    __syncthreads();
+    if (s_zero) {
+      if (warp == 0) slow_row<V, IdxT>(p, ac, av, n, warp_acc(0), warp_mark(0));
+      if (!EXACT && warp != 0)
+        for (int i = lane; i < acc_elems; i += 32) warp_acc(warp)[i] = Sentinel<V>::value();
+    } else if constexpr (!EXACT) {
+      // CTA fold: every warp's copies into warp 0's copy 0
+      for (int c = threadIdx.x; c < p.stride; c += blockDim.x) {
+        V v = Sentinel<V>::value();
+        for (int w = 0; w < nw; w++)
+          for (int g = 0; g < p.copies; g++) {
+            V* q = warp_acc(w) + g * p.stride + c;
+            v += *q;
+            *q = Sentinel<V>::value();
+          }
+        warp_acc(0)[c] = v;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t cnt = fold_count<V>(warp_acc(0), p.stride, 1, n_cols);
+      const unsigned long long off = stage.take(cnt, p.ctl, p.stage_block);
+      if (off + cnt <= p.t_cap) {
+        emit_copy0<V, IdxT>(warp_acc(0), n_cols, p.tcol + off, p.tval + off);
+      } else {
+        fold_count<V>(warp_acc(0), p.stride, 1, 0);  // reset
+        if (lane == 0) p.ctl->bad_row = 1;
+      }
+      if (lane == 0) {
+        p.cnt[r] = cnt;
+        p.toff[r] = off;
+        my_nnz += cnt;
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- Phase 2: light rows, one warp per row ----
+  V* acc = warp_acc(warp);
+  for (;;) {
+    unsigned long long r0 = 0;
+    if (lane == 0) r0 = atomicAdd(&p.ctl->light_next, static_cast<unsigned long long>(kLightBatch));
+    r0 = __shfl_sync(kFull, r0, 0);
+    if (r0 >= static_cast<unsigned long long>(p.rows)) break;
+    const int64_t r1 = min(static_cast<int64_t>(r0) + kLightBatch, p.rows);
+    for (int64_t r = static_cast<int64_t>(r0); r < r1; r++) {
+      const uint64_t s = p.aptr[r] - p.abase, e = p.aptr[r + 1] - p.abase;
+      if (static_cast<int64_t>(e - s) > p.heavy_deg) continue;
+      const uint32_t n = static_cast<uint32_t>(e - s);
+      const IdxT* ac = p.acol + s;
+      const V* av = p.aval + s;
+      bool zero = false;
+      my_macs += walk_entries<V, IdxT, W, EXACT, false, XZ>(p, ac, av, n, 0, 1, acc, warp_tab(warp), 0, 0, zero);
+      if (__any_sync(kFull, zero)) slow_row<V, IdxT>(p, ac, av, n, acc, warp_mark(warp));
+      const uint32_t cnt = fold_count<V>(acc, p.stride, EXACT ? 1 : p.copies, n_cols);
+      const unsigned long long off = stage.take(cnt, p.ctl, p.stage_block);
+      if (off + cnt <= p.t_cap) {
+        emit_copy0<V, IdxT>(acc, n_cols, p.tcol + off, p.tval + off);
+      } else {
+        fold_count<V>(acc, p.stride, 1, 0);  // reset
+        if (lane == 0) p.ctl->bad_row = 1;
+      }
+      if (lane == 0) {
+        p.cnt[r] = cnt;
+        p.toff[r] = off;
+        my_nnz += cnt;
+      }
+    }
+  }
+  my_macs = warp_sum(my_macs);
+  if (lane == 0 && my_nnz) atomicAdd(&p.ctl->nnz, my_nnz);
+  if (lane == 0 && my_macs) atomicAdd(&p.ctl->flops, my_macs);
+  (void)s_cnt;
+}
+
+// MACs of the product: sum over A entries of the X row length (spgemm.hpp:51 `flops`).
+template <class IdxT>
+__global__ void __launch_bounds__(256) k_count_macs(const uint64_t* __restrict__ aptr, uint64_t abase,
+                                                    const IdxT* __restrict__ acol, int64_t rows,
+                                                    const int64_t* __restrict__ xptr, int64_t K,
+                                                    Ctl* __restrict__ ctl) {
+  __shared__ int64_t tmp[32];
+  const uint64_t s = aptr[0] - abase, e = aptr[rows] - abase;
+  int64_t m = 0;
+  for (uint64_t i = s + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < e;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = static_cast<uint64_t>(acol[i]);
+    if (k < static_cast<uint64_t>(K)) m += xptr[k + 1] - xptr[k];
+  }
+  m = block_sum<int64_t>(m, tmp);
+  if (threadIdx.x == 0 && m) atomicAdd(&ctl->flops, static_cast<unsigned long long>(m));
+}
+
+// K_place: staging -> exact CSR offsets.  One warp per row, 16-byte vector copies when the
+// source and destination share alignment.
+template <class V, class IdxT>
+__global__ void __launch_bounds__(256) k_place(const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ toff,
+                                               const int64_t* __restrict__ cptr, const IdxT* __restrict__ tcol,
+                                               const V* __restrict__ tval, int64_t rows, IdxT* __restrict__ ccol,
+                                               V* __restrict__ cval) {
+  const int lane = lane_id();
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = wid; r < rows; r += nwarps) {
+    const uint32_t n = cnt[r];
+    const uint64_t src = toff[r];
+    const int64_t dst = cptr[r];
+    for (uint32_t i = lane; i < n; i += 32) {
+      ccol[dst + i] = tcol[src + i];
+      cval[dst + i] = tval[src + i];
+    }
+  }
+}
+
+}  // namespace ab2

@@ -13,20 +13,23 @@ namespace ab2 {
 
 namespace {
 
+// ptr holds absolute offsets into idx/val (spgemm.hpp:79-84); nnz = ptr[K] - ptr[0] is read
+// on the device so a device-resident operand needs no host round trip.
 template <class IdxT, class VIn, class V>
-__global__ void k_x_from_csr(const uint64_t* __restrict__ ptr, uint64_t p0, int64_t K,
-                             const IdxT* __restrict__ idx, const VIn* __restrict__ val, int64_t nnz,
-                             int64_t n_cols, int64_t* __restrict__ xptr, int32_t* __restrict__ xcol,
-                             V* __restrict__ xval, Ctl* __restrict__ ctl) {
+__global__ void k_x_from_csr(const uint64_t* __restrict__ ptr, int64_t K, const IdxT* __restrict__ idx,
+                             const VIn* __restrict__ val, int64_t n_cols, int64_t* __restrict__ xptr,
+                             int32_t* __restrict__ xcol, V* __restrict__ xval, Ctl* __restrict__ ctl) {
+  const uint64_t p0 = ptr[0];
+  const int64_t nnz = static_cast<int64_t>(ptr[K] - p0);
   int64_t n = max(K + 1, nnz);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     if (i <= K) xptr[i] = static_cast<int64_t>(ptr[i] - p0);
     if (i < nnz) {
-      uint64_t c = static_cast<uint64_t>(idx[i]);
+      uint64_t c = static_cast<uint64_t>(idx[p0 + i]);
       if (c >= static_cast<uint64_t>(n_cols)) ctl->bad_row = 1;
       xcol[i] = static_cast<int32_t>(c);
-      xval[i] = static_cast<V>(val[i]);
+      xval[i] = static_cast<V>(val[p0 + i]);
     }
   }
 }
@@ -106,6 +109,7 @@ __global__ void k_len_hist(const int64_t* __restrict__ xptr, int64_t K,
     c[3] += n > 16;
     c[4] = max(c[4], n);
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) h[5] = static_cast<unsigned long long>(xptr[K]);
   for (int j = 0; j < 4; j++) {
     int64_t s = block_sum<int64_t>(c[j], tmp);
     if (threadIdx.x == 0 && s) atomicAdd(&h[j], static_cast<unsigned long long>(s));
@@ -115,40 +119,83 @@ __global__ void k_len_hist(const int64_t* __restrict__ xptr, int64_t K,
   if ((threadIdx.x & 31) == 0) atomicMax(&h[4], static_cast<unsigned long long>(m));
 }
 
+// Slot rows 0..K-1 from the plain CSR, plus the dummy row K (see ab2_operand.cuh).
+// Smallest nonzero |x| (bit patterns of non-negative floats order like the values) and an
+// exact-zero flag: they decide how the product pass guards against zero products.
+template <class V>
+__global__ void k_x_val_stats(const V* __restrict__ xval, const int64_t* __restrict__ xptr, int64_t K,
+                              unsigned long long* __restrict__ st) {
+  const int64_t nnz = xptr[K];
+  unsigned long long mn = ~0ull;
+  int z = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < nnz;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = fabs(static_cast<double>(xval[i]));
+    if (v == 0.0)
+      z = 1;
+    else
+      mn = min(mn, static_cast<unsigned long long>(__double_as_longlong(v)));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(kFull, mn, o));
+    z |= __shfl_xor_sync(kFull, z, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mn != ~0ull) atomicMin(&st[0], mn);
+    if (z) st[1] = 1;
+  }
+}
+
 template <class V, int W>
 __global__ void k_x_slots(const int64_t* __restrict__ xptr, const int32_t* __restrict__ xcol,
-                          const V* __restrict__ xval, int64_t K, typename SlotOf<V>::type* __restrict__ slots,
-                          uint16_t* __restrict__ cslots) {
+                          const V* __restrict__ xval, int64_t K, uint32_t trash,
+                          typename SlotOf<V>::type* __restrict__ slots, uint16_t* __restrict__ xlen) {
   using S = typename SlotOf<V>::type;
-  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k <= K;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int64_t s = xptr[k], n = xptr[k + 1] - s;
+    const int64_t s = k < K ? xptr[k] : 0, n = k < K ? xptr[k + 1] - s : 0;
     S* out = slots + k * W;
-    uint16_t* cout = cslots + k * W;
+    xlen[k] = static_cast<uint16_t>(n);
     const bool ovf = n > W;
     const int inl = ovf ? W - 1 : static_cast<int>(n);
 #pragma unroll
     for (int e = 0; e < W; e++) {
       S en{};
-      uint16_t ce = kCEmpty;
+      en.val = V(1);
+      en.col = trash;
       if (e < inl) {
         en.col = static_cast<uint32_t>(xcol[s + e]);
         en.val = xval[s + e];
-        ce = static_cast<uint16_t>(xcol[s + e]);
       } else if (ovf && e == W - 1) {
-        en.col = kSlotOvf | static_cast<uint32_t>(n - (W - 1));
+        const uint32_t tail = static_cast<uint32_t>(n - (W - 1));
+        const uint32_t off = static_cast<uint32_t>(s + W - 1);
+        en.col = kSlotOvf | (tail << 16) | trash;
         if constexpr (sizeof(V) == 4)
-          en.val = __uint_as_float(static_cast<uint32_t>(s + W - 1));
+          en.val = __uint_as_float(kOneBits + off);
         else
-          en.val = __longlong_as_double(static_cast<long long>(s + W - 1));
-        ce = kCOvf;
-      } else {
-        en.col = kSlotEmpty;
-        en.val = V(0);
+          en.pad = off;
       }
       out[e] = en;
-      cout[e] = ce;
     }
+  }
+}
+
+// Column-only slots for the symbolic pass (kCSlotW entries, one 32 B sector per row).
+__global__ void k_x_cslots(const int64_t* __restrict__ xptr, const int32_t* __restrict__ xcol, int64_t K,
+                           uint16_t* __restrict__ cslots) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = xptr[k], n = xptr[k + 1] - s;
+    const bool ovf = n > kCSlotW;
+    const int inl = ovf ? kCSlotW - 1 : static_cast<int>(n);
+    uint16_t v[kCSlotW];
+#pragma unroll
+    for (int e = 0; e < kCSlotW; e++)
+      v[e] = e < inl ? static_cast<uint16_t>(xcol[s + e]) : (ovf && e == kCSlotW - 1 ? kCOvf : kCEmpty);
+    uint4* o = reinterpret_cast<uint4*>(cslots + k * kCSlotW);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(v);
+    o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    o[1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
 }
 
@@ -159,19 +206,21 @@ int grid_for(int64_t n, int threads, int sms) {
 
 template <class V>
 void build_slots(Ctx& ctx, XOperand& x) {
-  int g = grid_for(x.K, 256, ctx.sms);
+  int g = grid_for(x.K + 1, 256, ctx.sms);
   using S = typename SlotOf<V>::type;
   auto* sl = static_cast<S*>(x.slots);
   auto* cs = static_cast<uint16_t*>(x.cslots);
   auto* xp = static_cast<int64_t*>(x.ptr);
   auto* xc = static_cast<int32_t*>(x.col);
   auto* xv = static_cast<V*>(x.val);
+  const uint32_t trash = static_cast<uint32_t>(x.n_cols);
   switch (x.W) {
-    case 2: k_x_slots<V, 2><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, sl, cs); break;
-    case 4: k_x_slots<V, 4><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, sl, cs); break;
-    case 8: k_x_slots<V, 8><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, sl, cs); break;
-    default: k_x_slots<V, 16><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, sl, cs); break;
+    case 2: k_x_slots<V, 2><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, trash, sl, static_cast<uint16_t*>(x.xlen)); break;
+    case 4: k_x_slots<V, 4><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, trash, sl, static_cast<uint16_t*>(x.xlen)); break;
+    case 8: k_x_slots<V, 8><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, trash, sl, static_cast<uint16_t*>(x.xlen)); break;
+    default: k_x_slots<V, 16><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, trash, sl, static_cast<uint16_t*>(x.xlen)); break;
   }
+  k_x_cslots<<<g, 256, 0, ctx.stream>>>(xp, xc, x.K, cs);
   AB2_CUDA(cudaGetLastError());
 }
 
@@ -185,12 +234,13 @@ void fill_plain(Ctx& ctx, XOperand& x, const aires_b200_matrix& b, const uint64_
   auto* xv = static_cast<V*>(x.val);
   if (b.layout == AIRES_B200_CSR) {
     int g = grid_for(std::max<int64_t>(x.K + 1, x.nnz), 256, ctx.sms);
-    k_x_from_csr<IdxT, VIn, V><<<g, 256, 0, ctx.stream>>>(dptr, p0, x.K, idx, val, x.nnz, x.n_cols, xp,
-                                                          xc, xv, ctl);
+    k_x_from_csr<IdxT, VIn, V><<<g, 256, 0, ctx.stream>>>(dptr, x.K, idx, val, x.n_cols, xp, xc, xv, ctl);
     AB2_CUDA(cudaGetLastError());
     return;
   }
-  // CSC -> CSR: count, scan, scatter, sort.
+  // CSC -> CSR: count, scan, scatter, sort (entries addressed from p0).
+  idx += p0;
+  val += p0;
   int32_t* counts = ctx.cnt.as<int32_t>(std::max<int64_t>(x.K, 1));
   int32_t* cursor = reinterpret_cast<int32_t*>(ctx.rflops.as<int64_t>(std::max<int64_t>(x.K, 1)));
   AB2_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * std::max<int64_t>(x.K, 1), ctx.stream));
@@ -246,15 +296,16 @@ void* dmalloc(size_t bytes, size_t* total) {
 }  // namespace
 
 XOperand::~XOperand() {
+  if (!owned) return;
   int prev = -1;
   cudaGetDevice(&prev);
   if (prev != device) cudaSetDevice(device);
-  for (void* p : {ptr, col, val, slots, cslots})
+  for (void* p : {ptr, col, val, slots, cslots, xlen})
     if (p) cudaFree(p);
   if (prev != device && prev >= 0) cudaSetDevice(prev);
 }
 
-std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode) {
+std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode, bool temp) {
   if (b.layout != AIRES_B200_CSR && b.layout != AIRES_B200_CSC)
     fail(AIRES_B200_INVALID_ARGUMENT, "operand layout must be CSR or CSC");
   if ((b.idx_bytes != 4 && b.idx_bytes != 8) || (b.val_bytes != 4 && b.val_bytes != 8))
@@ -265,6 +316,7 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
   auto x = std::make_unique<XOperand>();
   x->device = ctx.device;
   x->mode = mode;
+  x->owned = !temp;
   x->K = static_cast<int64_t>(b.n_rows);
   x->n_cols = static_cast<int64_t>(b.n_cols);
   const uint64_t nptr = (b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols) + 1;
@@ -274,70 +326,96 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
          "feature matrix has " + std::to_string(x->n_cols) + " columns; the dense-accumulator path supports " +
              std::to_string(dense_max));
   if (b.ptr == nullptr) fail(AIRES_B200_INVALID_ARGUMENT, "operand ptr is null");
+  if (b.span >= (uint64_t(1) << 31)) fail(AIRES_B200_CAPACITY_EXCEEDED, "operand span exceeds 2^31 entries");
 
-  // pointer ends (host read or a tiny D2H)
-  uint64_t p0, p1;
-  if (b.location == AIRES_B200_HOST) {
-    p0 = b.ptr[0];
-    p1 = b.ptr[nptr - 1];
-  } else {
-    AB2_CUDA(cudaMemcpyAsync(&p0, b.ptr, 8, cudaMemcpyDeviceToHost, ctx.stream));
-    AB2_CUDA(cudaMemcpyAsync(&p1, b.ptr + nptr - 1, 8, cudaMemcpyDeviceToHost, ctx.stream));
-    AB2_CUDA(cudaStreamSynchronize(ctx.stream));
-  }
-  if (p1 < p0 || p1 > b.span) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "operand pointer array exceeds its span");
-  x->nnz = static_cast<int64_t>(p1 - p0);
-  if (x->nnz >= (int64_t(1) << 31)) fail(AIRES_B200_CAPACITY_EXCEEDED, "operand nnz exceeds 2^31");
-
-  // stage host arrays on the device
+  // Host operands: stage the used span.  Device CSR operands are read in place (the
+  // kernels read ptr[0] / ptr[K] themselves); device CSC needs the span ends on the host.
+  uint64_t p0 = 0, p1 = b.span;
   const uint64_t* dptr = b.ptr;
   const void* didx = b.idx;
   const void* dval = b.val;
   if (b.location == AIRES_B200_HOST) {
+    p0 = b.ptr[0];
+    p1 = b.ptr[nptr - 1];
+    if (p1 < p0 || p1 > b.span) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "operand pointer array exceeds its span");
     uint64_t* up = ctx.x_ptr.as<uint64_t>(nptr);
-    void* ui = ctx.x_idx.get(std::max<uint64_t>(x->nnz, 1) * b.idx_bytes);
-    void* uv = ctx.x_val.get(std::max<uint64_t>(x->nnz, 1) * b.val_bytes);
+    void* ui = ctx.x_idx.get(std::max<uint64_t>(p1, 1) * b.idx_bytes);
+    void* uv = ctx.x_val.get(std::max<uint64_t>(p1, 1) * b.val_bytes);
     AB2_CUDA(cudaMemcpyAsync(up, b.ptr, nptr * 8, cudaMemcpyHostToDevice, ctx.stream));
-    if (x->nnz) {
-      AB2_CUDA(cudaMemcpyAsync(ui, static_cast<const char*>(b.idx) + p0 * b.idx_bytes, x->nnz * b.idx_bytes,
+    if (p1 > p0) {  // same absolute positions as on the host
+      AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(ui) + p0 * b.idx_bytes,
+                               static_cast<const char*>(b.idx) + p0 * b.idx_bytes, (p1 - p0) * b.idx_bytes,
                                cudaMemcpyHostToDevice, ctx.stream));
-      AB2_CUDA(cudaMemcpyAsync(uv, static_cast<const char*>(b.val) + p0 * b.val_bytes, x->nnz * b.val_bytes,
+      AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(uv) + p0 * b.val_bytes,
+                               static_cast<const char*>(b.val) + p0 * b.val_bytes, (p1 - p0) * b.val_bytes,
                                cudaMemcpyHostToDevice, ctx.stream));
     }
     dptr = up;
     didx = ui;
     dval = uv;
-  } else {
-    didx = static_cast<const char*>(b.idx) + p0 * b.idx_bytes;
-    dval = static_cast<const char*>(b.val) + p0 * b.val_bytes;
+  } else if (b.layout == AIRES_B200_CSC) {
+    AB2_CUDA(cudaMemcpyAsync(&p0, b.ptr, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    AB2_CUDA(cudaMemcpyAsync(&p1, b.ptr + nptr - 1, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (p1 < p0 || p1 > b.span) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "operand pointer array exceeds its span");
   }
+  // nnz upper bound until the histogram readback reports the exact count
+  x->nnz = static_cast<int64_t>(b.location == AIRES_B200_HOST || b.layout == AIRES_B200_CSC ? p1 - p0 : b.span);
 
-  // choose the slot width from the row-length histogram
   Ctl* ctl = ctx.ctl.as<Ctl>(1);
   AB2_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx.stream));
   const size_t vb = mode == AIRES_B200_MODE_FP32 ? 4 : 8;
-  x->ptr = dmalloc((x->K + 1) * 8, &x->bytes);
-  x->col = dmalloc(std::max<int64_t>(x->nnz, 1) * 4, &x->bytes);
-  x->val = dmalloc(std::max<int64_t>(x->nnz, 1) * vb, &x->bytes);
+  auto alloc = [&](DevBuf& cache, size_t bytes) -> void* {
+    if (temp) return cache.get(bytes);
+    return dmalloc(bytes, &x->bytes);
+  };
+  x->ptr = alloc(ctx.xo_ptr, (x->K + 1) * 8);
+  x->col = alloc(ctx.xo_col, std::max<int64_t>(x->nnz, 1) * 4);
+  x->val = alloc(ctx.xo_val, std::max<int64_t>(x->nnz, 1) * vb);
   if (mode == AIRES_B200_MODE_FP32)
     fill_dispatch<float>(ctx, *x, b, dptr, p0, didx, dval, ctl);
   else
     fill_dispatch<double>(ctx, *x, b, dptr, p0, didx, dval, ctl);
 
+  // choose the slot width from the row-length histogram (one readback)
   unsigned long long* hist = reinterpret_cast<unsigned long long*>(&ctl->pad[0]);
-  if (x->K > 0)
-    k_len_hist<<<grid_for(x->K, 256, ctx.sms), 256, 0, ctx.stream>>>(static_cast<int64_t*>(x->ptr), x->K, hist);
+  AB2_CUDA(cudaMemsetAsync(&ctl->bad_row + 0, 0, 8, ctx.stream));
+  AB2_CUDA(cudaMemsetAsync(&ctl->flops, 0xff, 8, ctx.stream));  // min |x| bits
+  {
+    const int g = grid_for(std::max<int64_t>(x->nnz, 1), 256, ctx.sms);
+    auto* xp = static_cast<const int64_t*>(x->ptr);
+    if (mode == AIRES_B200_MODE_FP32)
+      k_x_val_stats<float><<<g, 256, 0, ctx.stream>>>(static_cast<float*>(x->val), xp, x->K, &ctl->flops);
+    else
+      k_x_val_stats<double><<<g, 256, 0, ctx.stream>>>(static_cast<double*>(x->val), xp, x->K, &ctl->flops);
+  }
+  k_len_hist<<<grid_for(std::max<int64_t>(x->K, 1), 256, ctx.sms), 256, 0, ctx.stream>>>(
+      static_cast<int64_t*>(x->ptr), x->K, hist);
   AB2_CUDA(cudaGetLastError());
   Ctl* h = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
   AB2_CUDA(cudaMemcpyAsync(h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
   AB2_CUDA(cudaStreamSynchronize(ctx.stream));
   if (h->bad_row) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "operand index outside its dimensions");
+  x->nnz = static_cast<int64_t>(h->pad[5]);
+  {
+    const unsigned long long bits = h->flops;
+    double mn;
+    std::memcpy(&mn, &bits, 8);
+    x->xmin = bits == ~0ull ? 0.0 : mn;
+    x->has_zero = h->num_light_next != 0;
+  }
+  if (static_cast<int64_t>(h->pad[4]) > kMaxTail)
+    fail(AIRES_B200_UNSUPPORTED_FORMAT, "feature row longer than " + std::to_string(kMaxTail) + " entries");
+  x->max_row_len = static_cast<int64_t>(h->pad[4]);
   const double K = static_cast<double>(std::max<int64_t>(x->K, 1));
   const double frac[4] = {h->pad[0] / K, h->pad[1] / K, h->pad[2] / K, h->pad[3] / K};
   int W = 16;
   const int widths[4] = {2, 4, 8, 16};
+  // Tails cost a dependent round trip for the whole warp step, so the slot must hold
+  // all but ~1% of rows (measured: 8-wide slots on the Reddit shape put a tail in 48%
+  // of warp steps and doubled the numeric pass's instruction count).
   for (int i = 0; i < 4; i++)
-    if (frac[i] <= 0.2) {
+    if (frac[i] <= 0.01) {
       W = widths[i];
       break;
     }
@@ -345,15 +423,17 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
   if (forced == 2 || forced == 4 || forced == 8 || forced == 16) W = static_cast<int>(forced);
   x->W = W;
   const size_t sb = mode == AIRES_B200_MODE_FP32 ? sizeof(SlotF) : sizeof(SlotD);
-  x->slots = dmalloc(std::max<int64_t>(x->K, 1) * W * sb, &x->bytes);
-  x->cslots = dmalloc(std::max<int64_t>(x->K, 1) * W * 2, &x->bytes);
-  if (x->K > 0) {
+  x->slots = alloc(ctx.xo_slots, (x->K + 1) * W * sb);
+  x->cslots = alloc(ctx.xo_cslots, std::max<int64_t>(x->K, 1) * kCSlotW * 2);
+  x->xlen = alloc(ctx.xo_len, (x->K + 1) * 2);
+  {
     if (mode == AIRES_B200_MODE_FP32)
       build_slots<float>(ctx, *x);
     else
       build_slots<double>(ctx, *x);
   }
-  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  x->prep_launches = (b.layout == AIRES_B200_CSR ? 1 : 6) + 4;
+  if (!temp) AB2_CUDA(cudaStreamSynchronize(ctx.stream));
   return x;
 }
 

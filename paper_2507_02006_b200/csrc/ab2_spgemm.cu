@@ -4,13 +4,14 @@
 //   allocation through the caller's allocator, spgemm.hpp:111-112] -> K_numeric -> [K_fix]
 //   -> row_ptr copy -> (host C) D2H.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
 #include <unordered_map>
 
 #include "ab2_internal.h"
-#include "ab2_kernels.cuh"
+#include "ab2_numeric.cuh"
 
 namespace ab2 {
 
@@ -34,66 +35,31 @@ int occupancy_grid(K kernel, int threads, size_t smem, int sms) {
   return nb * sms;
 }
 
-template <class IdxT>
-void launch_symbolic(Ctx& ctx, const SymArgs& p, const IdxT* acol, int W) {
-  const int threads = 256;
-  const size_t smem = static_cast<size_t>(threads / 32) * p.region_bytes;
-  switch (W) {
-#define AB2_SYM(WW)                                                                  \
-  case WW: {                                                                         \
-    auto k = k_symbolic<IdxT, WW>;                                                   \
-    int grid = occupancy_grid(k, threads, smem, ctx.sms);                            \
-    k<<<grid, threads, smem, ctx.stream>>>(p, acol);                                 \
-    break;                                                                           \
-  }
-    AB2_SYM(2)
-    AB2_SYM(4)
-    AB2_SYM(8)
-    AB2_SYM(16)
-#undef AB2_SYM
-    default: fail(AIRES_B200_INVALID_ARGUMENT, "bad slot width");
-  }
-  AB2_CUDA(cudaGetLastError());
-}
-
 template <class V, class IdxT, int W>
-auto numeric_kernel() {
-  if constexpr (std::is_same<V, float>::value)
-    return k_numeric_f32<IdxT, W>;
-  else
-    return k_numeric_f64<IdxT, W>;
-}
-
-template <class V, class IdxT, int W>
-void launch_numeric_w(Ctx& ctx, const NumArgs<V, IdxT>& p, int threads, size_t smem) {
-  auto k = numeric_kernel<V, IdxT, W>();
+void launch_numeric_w(Ctx& ctx, const Num3Args<V, IdxT>& p, int threads, size_t smem, bool xz) {
+  auto k = xz ? k_numeric3<V, IdxT, W, true> : k_numeric3<V, IdxT, W, false>;
   int grid = occupancy_grid(k, threads, smem, ctx.sms);
   k<<<grid, threads, smem, ctx.stream>>>(p);
 }
 
 template <class V, class IdxT>
-void launch_numeric(Ctx& ctx, const NumArgs<V, IdxT>& p, int W) {
-  const size_t region = static_cast<size_t>(p.region_elems) * sizeof(V);
-  int nw = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / region)));
-  const int threads = nw * 32;
-  const size_t smem = nw * region;
-  switch (W) {
-    case 2: launch_numeric_w<V, IdxT, 2>(ctx, p, threads, smem); break;
-    case 4: launch_numeric_w<V, IdxT, 4>(ctx, p, threads, smem); break;
-    case 8: launch_numeric_w<V, IdxT, 8>(ctx, p, threads, smem); break;
-    case 16: launch_numeric_w<V, IdxT, 16>(ctx, p, threads, smem); break;
-    default: fail(AIRES_B200_INVALID_ARGUMENT, "bad slot width");
-  }
-  AB2_CUDA(cudaGetLastError());
+int numeric_warps(const Num3Args<V, IdxT>& p) {
+  int nw = static_cast<int>(env_int("AB2_NUM_WARPS", 8));
+  return std::max(1, std::min<int>(nw, static_cast<int>((200 * 1024) / p.warp_bytes)));
 }
 
 template <class V, class IdxT>
-void launch_fix(Ctx& ctx, const NumArgs<V, IdxT>& p, int64_t n_fix) {
-  size_t smem = static_cast<size_t>(p.region_elems) * sizeof(V) + p.region_elems + 16;
-  auto k = k_fix_rows<V, IdxT>;
-  occupancy_grid(k, 32, smem, ctx.sms);
-  int grid = static_cast<int>(std::min<int64_t>(n_fix, 65535));
-  k<<<grid, 32, smem, ctx.stream>>>(p, n_fix);
+void launch_numeric(Ctx& ctx, const Num3Args<V, IdxT>& p, int W, bool xz) {
+  const int nw = numeric_warps(p);
+  const int threads = nw * 32;
+  const size_t smem = static_cast<size_t>(nw) * p.warp_bytes;
+  switch (W) {
+    case 2: launch_numeric_w<V, IdxT, 2>(ctx, p, threads, smem, xz); break;
+    case 4: launch_numeric_w<V, IdxT, 4>(ctx, p, threads, smem, xz); break;
+    case 8: launch_numeric_w<V, IdxT, 8>(ctx, p, threads, smem, xz); break;
+    case 16: launch_numeric_w<V, IdxT, 16>(ctx, p, threads, smem, xz); break;
+    default: fail(AIRES_B200_INVALID_ARGUMENT, "bad slot width");
+  }
   AB2_CUDA(cudaGetLastError());
 }
 
@@ -109,59 +75,85 @@ void convert(Ctx& ctx, const void* in, void* out, int64_t n) {
   if (n <= 0) return;
   int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(ctx.sms) * 32));
   k_convert<Src, Dst><<<grid, 256, 0, ctx.stream>>>(static_cast<const Src*>(in), static_cast<Dst*>(out), n);
+  ctx.launches++;
   AB2_CUDA(cudaGetLastError());
 }
 
 
+// One product: classify -> MAC count -> K_numeric (staging) -> scan -> [nnz readback,
+// exact allocation through the caller's allocator, spgemm.hpp:111-112] -> K_place.
 template <class V, class IdxT>
 void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_b200_output& out,
-                 const uint64_t* aptr, uint64_t abase, const IdxT* acol, const V* aval) {
+                 const uint64_t* aptr, uint64_t abase, const IdxT* acol, const V* aval, uint64_t span_hint) {
   const int64_t rows = static_cast<int64_t>(a.n_rows);
   const int W = x.W;
+  if (x.K >= (int64_t(1) << 31) / 16) fail(AIRES_B200_CAPACITY_EXCEEDED, "inner dimension too large for slot indexing");
   Ctl* ctl = ctx.ctl.as<Ctl>(1);
   Ctl* h = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
-  int32_t* cnt = ctx.cnt.as<int32_t>(std::max<int64_t>(rows, 1));
-  int64_t* rflops = ctx.rflops.as<int64_t>(std::max<int64_t>(rows, 1));
+  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 4096);
+  int64_t* heavy = ctx.sym_heavy.as<int64_t>(std::max<int64_t>(rows, 1));
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(ctx.cnt.as<int32_t>(std::max<int64_t>(rows, 1)));
+  uint64_t* toff = reinterpret_cast<uint64_t*>(ctx.rflops.as<int64_t>(std::max<int64_t>(rows, 1)));
   int64_t* cptr = ctx.cptr.as<int64_t>(rows + 1);
-  int64_t* sym_heavy = ctx.sym_heavy.as<int64_t>(std::max<int64_t>(rows, 1));
-  int64_t* num_heavy = ctx.num_heavy.as<int64_t>(std::max<int64_t>(rows, 1));
-  int64_t* fix_rows = ctx.fix_rows.as<int64_t>(std::max<int64_t>(rows, 1));
-  const int64_t heavy_deg = env_int("AB2_SYM_HEAVY_DEG", 1024);
-  const int64_t heavy_flops = env_int("AB2_NUM_HEAVY_FLOPS", sizeof(V) == 4 ? 8192 : 4096);
+  const uint64_t n_cols = static_cast<uint64_t>(x.n_cols);
+
+  Num3Args<V, IdxT> np{};
+  np.aptr = aptr;
+  np.abase = abase;
+  np.acol = acol;
+  np.aval = aval;
+  np.rows = rows;
+  np.x.K = x.K;
+  np.x.n_cols = static_cast<int32_t>(x.n_cols);
+  np.x.W = x.W;
+  np.x.ptr = static_cast<const int64_t*>(x.ptr);
+  np.x.col = static_cast<const int32_t*>(x.col);
+  np.x.val = static_cast<const V*>(x.val);
+  np.x.slots = static_cast<const typename SlotOf<V>::type*>(x.slots);
+  np.x.cslots = static_cast<const uint16_t*>(x.cslots);
+  np.stride = static_cast<int32_t>((x.n_cols + 1 + 31) & ~int64_t(31));
+  np.copies = sizeof(V) == 8 ? 1 : 32 / W;
+  np.warp_bytes = static_cast<int32_t>(
+      ((static_cast<size_t>(np.copies) * np.stride * sizeof(V) + np.stride + 15) & ~size_t(15)) +
+      32 * sizeof(ChunkPair));
+  np.heavy = heavy;
+  np.heavy_deg = heavy_deg;
+  np.cnt = cnt;
+  np.toff = toff;
+  np.ctl = ctl;
+  np.xlen = static_cast<const uint16_t*>(x.xlen);
+  // |a| below `tiny` may round a*x to zero (fp32: |a*x| < 2^-149 incl. the FFMA path;
+  // fp64: < 2^-1074); such weights send the row to the explicit-mark path.
+  np.tiny = x.xmin > 0 ? static_cast<V>((sizeof(V) == 4 ? std::ldexp(1.0, -147) : std::ldexp(1.0, -1072)) / x.xmin)
+                       : V(0);
+  // staging: nnz bound (dense rows, or A entries x longest X row) * 8/7 + one block per warp
+  const uint64_t maxlen = std::max<int64_t>(x.max_row_len, 1);
+  const uint64_t bound = std::min<uint64_t>(static_cast<uint64_t>(rows) * n_cols, span_hint * maxlen);
+  np.stage_block = static_cast<uint32_t>(std::max<int64_t>(4096, 8 * static_cast<int64_t>(np.stride)));
+  const int nw = numeric_warps(np);
+  const uint64_t warps_total = static_cast<uint64_t>(ctx.sms) * 64;  // upper bound of resident warps
+  np.t_cap = bound + bound / 7 + (warps_total + 1) * np.stage_block;
+  (void)nw;
+  np.tcol = ctx.t_col.as<IdxT>(np.t_cap);
+  np.tval = ctx.t_val.as<V>(np.t_cap);
 
   AB2_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx.stream));
   AB2_CUDA(cudaEventRecord(ctx.ev[0], ctx.stream));
   if (rows > 0) {
     int g = static_cast<int>(std::min<int64_t>((rows + 255) / 256, static_cast<int64_t>(ctx.sms) * 16));
-    k_classify<<<g, 256, 0, ctx.stream>>>(aptr, rows, heavy_deg, sym_heavy, ctl);
+    k_classify<<<g, 256, 0, ctx.stream>>>(aptr, rows, heavy_deg, heavy, ctl);
     AB2_CUDA(cudaGetLastError());
   }
   AB2_CUDA(cudaEventRecord(ctx.ev[1], ctx.stream));
-  SymArgs sp{};
-  sp.aptr = aptr;
-  sp.abase = abase;
-  sp.rows = rows;
-  sp.K = x.K;
-  sp.n_cols = static_cast<int32_t>(x.n_cols);
-  sp.region_bytes = static_cast<int32_t>(std::max<int64_t>(16, (x.n_cols + 15) & ~int64_t(15)));
-  sp.xptr = static_cast<const int64_t*>(x.ptr);
-  sp.xcol = static_cast<const int32_t*>(x.col);
-  sp.cslots = static_cast<const uint16_t*>(x.cslots);
-  sp.cnt = cnt;
-  sp.rflops = rflops;
-  sp.sym_heavy = sym_heavy;
-  sp.heavy_deg = heavy_deg;
-  sp.num_heavy = num_heavy;
-  sp.heavy_flops = heavy_flops;
-  sp.ctl = ctl;
-  if (rows > 0) launch_symbolic<IdxT>(ctx, sp, acol, W);
+  if (rows > 0) launch_numeric<V, IdxT>(ctx, np, W, x.has_zero);
   AB2_CUDA(cudaEventRecord(ctx.ev[2], ctx.stream));
   const int64_t nb = (rows + kScanTile - 1) / kScanTile;
   int64_t* part = ctx.scan_part.as<int64_t>(std::max<int64_t>(nb, 1));
   if (rows > 0) {
-    k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(cnt, rows, part);
+    const int32_t* cin = reinterpret_cast<const int32_t*>(cnt);
+    k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(cin, rows, part);
     k_scan_part<<<1, 1024, 0, ctx.stream>>>(part, nb, ctl);
-    k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(cnt, rows, part, cptr);
+    k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(cin, rows, part, cptr);
     AB2_CUDA(cudaGetLastError());
   } else {
     AB2_CUDA(cudaMemsetAsync(cptr, 0, sizeof(int64_t), ctx.stream));
@@ -169,6 +161,7 @@ void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_
   AB2_CUDA(cudaEventRecord(ctx.ev[3], ctx.stream));
   AB2_CUDA(cudaMemcpyAsync(h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
   AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (h->bad_row) fail(AIRES_B200_CAPACITY_EXCEEDED, "staging area overflow");
   const uint64_t nnz = h->nnz;
   const uint64_t flops = h->flops;
 
@@ -185,39 +178,12 @@ void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_
     ccol = ctx.c_col.as<IdxT>(std::max<uint64_t>(nnz, 1));
     cval = ctx.c_val.as<V>(std::max<uint64_t>(nnz, 1));
   }
-
-  NumArgs<V, IdxT> np{};
-  np.aptr = aptr;
-  np.abase = abase;
-  np.acol = acol;
-  np.aval = aval;
-  np.rows = rows;
-  np.x.K = x.K;
-  np.x.n_cols = static_cast<int32_t>(x.n_cols);
-  np.x.W = x.W;
-  np.x.ptr = static_cast<const int64_t*>(x.ptr);
-  np.x.col = static_cast<const int32_t*>(x.col);
-  np.x.val = static_cast<const V*>(x.val);
-  np.x.slots = static_cast<const typename SlotOf<V>::type*>(x.slots);
-  np.x.cslots = static_cast<const uint16_t*>(x.cslots);
-  np.region_elems = static_cast<int32_t>(std::max<int64_t>(4, (x.n_cols + 3) & ~int64_t(3)));
-  np.cnt = cnt;
-  np.cptr = cptr;
-  np.rflops = rflops;
-  np.num_heavy = num_heavy;
-  np.heavy_flops = heavy_flops;
-  np.ccol = ccol;
-  np.cval = cval;
-  np.fix_rows = fix_rows;
-  np.ctl = ctl;
   AB2_CUDA(cudaEventRecord(ctx.ev[4], ctx.stream));
-  if (rows > 0 && nnz > 0) launch_numeric<V, IdxT>(ctx, np, W);
-  AB2_CUDA(cudaEventRecord(ctx.ev[5], ctx.stream));
-  AB2_CUDA(cudaMemcpyAsync(h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
-  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
-  if (h->n_fix > 0) {
-    launch_fix<V, IdxT>(ctx, np, static_cast<int64_t>(h->n_fix));
+  if (rows > 0 && nnz > 0) {
+    k_place<V, IdxT><<<ctx.sms * 8, 256, 0, ctx.stream>>>(cnt, toff, cptr, np.tcol, np.tval, rows, ccol, cval);
+    AB2_CUDA(cudaGetLastError());
   }
+  AB2_CUDA(cudaEventRecord(ctx.ev[5], ctx.stream));
   // row_ptr (int64 == u64 bits; all values are >= 0)
   if (out.location == AIRES_B200_DEVICE) {
     AB2_CUDA(cudaMemcpyAsync(optr, cptr, (rows + 1) * 8, cudaMemcpyDeviceToDevice, ctx.stream));
@@ -238,13 +204,14 @@ void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_
     return static_cast<double>(ms);
   };
   ctx.prof[kPClassify] = el(0, 1);
-  ctx.prof[kPSymbolic] = el(1, 2);
+  ctx.prof[kPSymbolic] = el(4, 5);  // slot reused: K_place
   ctx.prof[kPScan] = el(2, 3);
-  ctx.prof[kPNumeric] = el(4, 5);
+  ctx.prof[kPNumeric] = el(1, 2);
   ctx.prof[kPD2H] = el(6, 7);
   ctx.last_ms = el(0, 7);
+  ctx.launches += rows > 0 ? 5 + (nnz > 0 ? 1 : 0) : 0;
   out.n_rows = static_cast<uint64_t>(rows);
-  out.n_cols = static_cast<uint64_t>(x.n_cols);
+  out.n_cols = n_cols;
   out.nnz = nnz;
   out.flops = flops;
 }
@@ -322,18 +289,19 @@ void spgemm_rows(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_
       convert<float, double>(ctx, aval, v2, span);
     aval = v2;
   }
+  const uint64_t span_hint = a.location == AIRES_B200_HOST || p1 > p0 ? p1 - p0 : a.span;
   if (out.idx_bytes == 4 && vsize == 4)
     run_product<float, uint32_t>(ctx, a, x, out, aptr, abase, static_cast<const uint32_t*>(acol),
-                                 static_cast<const float*>(aval));
+                             static_cast<const float*>(aval), span_hint);
   else if (out.idx_bytes == 4)
     run_product<double, uint32_t>(ctx, a, x, out, aptr, abase, static_cast<const uint32_t*>(acol),
-                                  static_cast<const double*>(aval));
+                              static_cast<const double*>(aval), span_hint);
   else if (vsize == 4)
     run_product<float, uint64_t>(ctx, a, x, out, aptr, abase, static_cast<const uint64_t*>(acol),
-                                 static_cast<const float*>(aval));
+                             static_cast<const float*>(aval), span_hint);
   else
     run_product<double, uint64_t>(ctx, a, x, out, aptr, abase, static_cast<const uint64_t*>(acol),
-                                  static_cast<const double*>(aval));
+                              static_cast<const double*>(aval), span_hint);
   float ms = 0;
   AB2_CUDA(cudaEventElapsedTime(&ms, ctx.ev[8], ctx.ev[9]));
   ctx.prof[kPH2D] = ms;
