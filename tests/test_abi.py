@@ -1,0 +1,76 @@
+"""CPU tier: the C-ABI library (libaires_b200.so) loads, exports every entry point that
+include/*.h declares, and -- with no GPU visible -- fails loudly (never a CPU fallback)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2507_02006_b200 as ab
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    syms = set()
+    for h in os.listdir(os.path.join(ROOT, "include")):
+        if h.endswith(".h"):
+            txt = open(os.path.join(ROOT, "include", h)).read()
+            txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+            syms |= set(re.findall(r"\b(aires_b200_\w+)\s*\(", txt))
+    return sorted(s for s in syms if not s.endswith("_fn"))
+
+
+def test_library_exports_every_declared_symbol():
+    L = ab.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    missing = [s for s in syms if not hasattr(L, s)]
+    assert not missing, missing
+
+
+def test_abi_version_and_status_mapping():
+    assert ab.lib().aires_b200_abi_version() == 1
+    # status = 1 + errc (error.hpp:9-27)
+    e = ab.AiresError(8, "x")
+    assert e.code == ab.errc.dimension_mismatch and str(e).startswith("dimension_mismatch")
+    assert ab.AiresError(6, "r").code == ab.errc.row_too_large
+    assert ab.AiresError(101, "n").code is None
+
+
+@pytest.mark.skipif(ab.device_count() > 0, reason="a CUDA device is visible")
+def test_no_device_fails_loudly():
+    a = ab.CsrMatrix(2, 2, np.array([0, 1, 2], np.uint64), np.array([0, 1], np.uint64), np.ones(2))
+    with pytest.raises(ab.AiresError) as e:
+        ab.spgemm_full(a, a)
+    assert e.value.status == 101 and "no CUDA device" in str(e.value)
+    with pytest.raises(ab.AiresError):
+        ab.robw_cuts(np.array([0, 1, 2], np.uint64), 100)
+
+
+def test_synth_features_is_reference_gen_features():
+    """The host-side generator the bench uses reproduces gen_features (synth.hpp:73-78) byte for
+    byte (golden fixture made by the reference)."""
+    g = np.load(os.path.join(ROOT, "tests", "golden", "features.npz"))
+    for f in range(int(g["n_cases"][0])):
+        n, dim, sp, seed = g[f"f{f}_spec"]
+        x = ab.synth_features(int(n), int(dim), float(sp), int(seed), idx_dtype=np.uint64)
+        assert np.array_equal(x.row_ptr, g[f"f{f}_ptr"]) and np.array_equal(x.col_idx, g[f"f{f}_idx"])
+        assert np.array_equal(x.values.view(np.uint64), g[f"f{f}_val"].view(np.uint64))
+
+
+def test_synth_graph_shape_and_normalization():
+    """Chung-Lu Ã: symmetric, self-loops present, values 1/sqrt(d_i d_j) (gcn.hpp:29-72)."""
+    g, st = ab.synth_graph(3000, 30000, degree_cap=500, idx_dtype=np.uint64)
+    assert g.row_ptr[-1] == g.nnz()
+    rows = np.repeat(np.arange(g.n_rows), np.diff(g.row_ptr.astype(np.int64)))
+    cols = g.col_idx.astype(np.int64)
+    assert np.all(np.diff(cols)[np.diff(rows) == 0] > 0)  # canonical
+    import scipy.sparse as sp
+    m = sp.csr_matrix((g.values, cols, g.row_ptr.astype(np.int64)), shape=(g.n_rows, g.n_cols))
+    assert abs(m - m.T).max() < 1e-15
+    assert np.all(m.diagonal() > 0)
+    deg = np.diff(g.row_ptr.astype(np.int64)).astype(np.float64)
+    np.testing.assert_allclose(g.values, 1.0 / np.sqrt(deg[rows] * deg[cols]), rtol=1e-15)
+    assert st["nnz_a"] + g.n_rows == g.nnz()
