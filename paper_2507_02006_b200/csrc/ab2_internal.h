@@ -48,7 +48,7 @@ struct Ctx {
   DevBuf c_col, c_val;                          // C staging for host outputs
   DevBuf t_col, t_val;                          // product staging (K_numeric -> K_place)
   DevBuf x_ptr, x_idx, x_val;                   // raw X upload (host operands)
-  DevBuf xo_ptr, xo_col, xo_val, xo_slots, xo_cslots, xo_len;  // per-call operand layout
+  DevBuf xo_ptr, xo_col, xo_val, xo_slots, xo_cslots, xo_len, xo_desc, xo_ent;  // per-call operand layout
   HostBuf h_ctl;
   double prof[kPCount] = {};
   double last_ms = 0.0;
@@ -74,6 +74,8 @@ struct XOperand {
   void* slots = nullptr;   // K*W entries
   void* cslots = nullptr;  // K*kCSlotW u16
   void* xlen = nullptr;    // K+1 u16 row lengths
+  void* xdesc = nullptr;   // fp32: K+1 uint2 {start, len} (row K empty)
+  void* xent = nullptr;    // fp32: nnz uint2 {col, value bits}
   double xmin = 0.0;       // smallest nonzero |x|
   bool has_zero = false;   // X stores an exact zero
   size_t bytes = 0;

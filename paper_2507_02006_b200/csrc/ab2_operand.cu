@@ -180,6 +180,22 @@ __global__ void k_x_slots(const int64_t* __restrict__ xptr, const int32_t* __res
   }
 }
 
+// Flat fp32 layout for the flattened-MAC product pass (ab2_numeric4.cuh): one 8-byte
+// descriptor per X row and the entries interleaved as {col, value} so one 8-byte gather
+// fetches a whole term.
+__global__ void k_x_flat(const int64_t* __restrict__ xptr, const int32_t* __restrict__ xcol,
+                         const float* __restrict__ xval, int64_t K, uint2* __restrict__ desc,
+                         uint2* __restrict__ ent) {
+  const int64_t nnz = xptr[K];
+  const int64_t n = max(K + 1, nnz);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i < K) desc[i] = make_uint2(static_cast<uint32_t>(xptr[i]), static_cast<uint32_t>(xptr[i + 1] - xptr[i]));
+    if (i == K) desc[i] = make_uint2(0u, 0u);
+    if (i < nnz) ent[i] = make_uint2(static_cast<uint32_t>(xcol[i]), __float_as_uint(xval[i]));
+  }
+}
+
 // Column-only slots for the symbolic pass (kCSlotW entries, one 32 B sector per row).
 __global__ void k_x_cslots(const int64_t* __restrict__ xptr, const int32_t* __restrict__ xcol, int64_t K,
                            uint16_t* __restrict__ cslots) {
@@ -300,7 +316,7 @@ XOperand::~XOperand() {
   int prev = -1;
   cudaGetDevice(&prev);
   if (prev != device) cudaSetDevice(device);
-  for (void* p : {ptr, col, val, slots, cslots, xlen})
+  for (void* p : {ptr, col, val, slots, cslots, xlen, xdesc, xent})
     if (p) cudaFree(p);
   if (prev != device && prev >= 0) cudaSetDevice(prev);
 }
@@ -432,7 +448,15 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
     else
       build_slots<double>(ctx, *x);
   }
-  x->prep_launches = (b.layout == AIRES_B200_CSR ? 1 : 6) + 4;
+  if (mode == AIRES_B200_MODE_FP32) {
+    x->xdesc = alloc(ctx.xo_desc, (x->K + 1) * sizeof(uint2));
+    x->xent = alloc(ctx.xo_ent, std::max<int64_t>(x->nnz, 1) * sizeof(uint2));
+    k_x_flat<<<grid_for(std::max<int64_t>(x->K + 1, x->nnz), 256, ctx.sms), 256, 0, ctx.stream>>>(
+        static_cast<const int64_t*>(x->ptr), static_cast<const int32_t*>(x->col), static_cast<const float*>(x->val),
+        x->K, static_cast<uint2*>(x->xdesc), static_cast<uint2*>(x->xent));
+    AB2_CUDA(cudaGetLastError());
+  }
+  x->prep_launches = (b.layout == AIRES_B200_CSR ? 1 : 6) + 4 + (mode == AIRES_B200_MODE_FP32 ? 1 : 0);
   if (!temp) AB2_CUDA(cudaStreamSynchronize(ctx.stream));
   return x;
 }

@@ -12,6 +12,7 @@
 
 #include "ab2_internal.h"
 #include "ab2_numeric.cuh"
+#include "ab2_numeric4.cuh"
 
 namespace ab2 {
 
@@ -60,6 +61,45 @@ void launch_numeric(Ctx& ctx, const Num3Args<V, IdxT>& p, int W, bool xz) {
     case 16: launch_numeric_w<V, IdxT, 16>(ctx, p, threads, smem, xz); break;
     default: fail(AIRES_B200_INVALID_ARGUMENT, "bad slot width");
   }
+  AB2_CUDA(cudaGetLastError());
+}
+
+// fp32 flattened-MAC pass (ab2_numeric4.cuh); shares the staging set-up of the k_numeric3 args.
+template <class IdxT>
+void launch_numeric4(Ctx& ctx, const Num3Args<float, IdxT>& q, const XOperand& x) {
+  Num4Args<IdxT> p{};
+  p.aptr = q.aptr;
+  p.abase = q.abase;
+  p.acol = q.acol;
+  p.aval = q.aval;
+  p.rows = q.rows;
+  p.K = x.K;
+  p.n_cols = static_cast<int32_t>(x.n_cols);
+  p.stride = q.stride;
+  int nc = static_cast<int>(env_int("AB2_N4_COPIES", 4));
+  if (nc != 1 && nc != 2 && nc != 4 && nc != 8 && nc != 16) nc = 4;
+  p.copies = nc;
+  p.log2c = __builtin_ctz(static_cast<unsigned>(nc));
+  p.warp_bytes = static_cast<int32_t>(static_cast<size_t>(nc) * p.stride * 4 + p.stride + 32 * sizeof(uint4));
+  p.xdesc = static_cast<const uint2*>(x.xdesc);
+  p.xent = static_cast<const uint2*>(x.xent);
+  p.heavy = q.heavy;
+  p.heavy_deg = q.heavy_deg;
+  p.cnt = q.cnt;
+  p.toff = q.toff;
+  p.tcol = q.tcol;
+  p.tval = q.tval;
+  p.t_cap = q.t_cap;
+  p.tiny = q.tiny;
+  p.stage_block = q.stage_block;
+  p.ctl = q.ctl;
+  int nw = static_cast<int>(env_int("AB2_N4_WARPS", 8));
+  nw = std::max(1, std::min<int>(nw, static_cast<int>((200 * 1024) / p.warp_bytes)));
+  const int threads = nw * 32;
+  const size_t smem = static_cast<size_t>(nw) * p.warp_bytes;
+  auto k = x.has_zero ? k_numeric4<IdxT, true> : k_numeric4<IdxT, false>;
+  const int grid = occupancy_grid(k, threads, smem, ctx.sms);
+  k<<<grid, threads, smem, ctx.stream>>>(p);
   AB2_CUDA(cudaGetLastError());
 }
 
@@ -145,7 +185,16 @@ void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_
     AB2_CUDA(cudaGetLastError());
   }
   AB2_CUDA(cudaEventRecord(ctx.ev[1], ctx.stream));
-  if (rows > 0) launch_numeric<V, IdxT>(ctx, np, W, x.has_zero);
+  if (rows > 0) {
+    if constexpr (std::is_same<V, float>::value) {
+      if (x.xdesc != nullptr && env_int("AB2_NUMERIC", 4) == 4)
+        launch_numeric4<IdxT>(ctx, np, x);
+      else
+        launch_numeric<V, IdxT>(ctx, np, W, x.has_zero);
+    } else {
+      launch_numeric<V, IdxT>(ctx, np, W, x.has_zero);
+    }
+  }
   AB2_CUDA(cudaEventRecord(ctx.ev[2], ctx.stream));
   const int64_t nb = (rows + kScanTile - 1) / kScanTile;
   int64_t* part = ctx.scan_part.as<int64_t>(std::max<int64_t>(nb, 1));
