@@ -17,6 +17,7 @@
  *   aires_b200_robw_cuts     -> aires::robw_partition cut search partition.hpp:52-74
  *   aires_b200_run           -> aires::run_aires Phases I-III    scheduler.hpp:72-168
  *                               (real multi-stream tile pipeline, C-aware tiles)
+ *   aires_b200_checksum      -> aires::checksum (FNV-1a of C)   serialize.hpp:50-59
  *   aires_b200_last_error    -> the what() string of aires::error error.hpp:53-62
  *
  * Status codes: 0 = OK, otherwise 1 + (int)aires::errc (error.hpp:9-27), so
@@ -172,6 +173,11 @@ typedef struct aires_b200_run_report {
 int aires_b200_run(const aires_b200_matrix* a, const aires_b200_matrix* b,
                    const aires_b200_run_config* cfg, aires_b200_output* c,
                    aires_b200_run_report* report);
+
+/* FNV-1a 64 of a CSR in the reference's canonical byte stream (serialize.hpp:50-59); host only.
+   row_ptr may be absolute (it is rebased); 4-byte indices / values are widened to u64 / f64. */
+uint64_t aires_b200_checksum(uint64_t n_rows, uint64_t n_cols, uint64_t nnz, const uint64_t* row_ptr,
+                             const void* col_idx, uint32_t idx_bytes, const void* values, uint32_t val_bytes);
 
 /* ---- timing helpers for harnesses (not part of the reference surface) --- */
 /* The cudaStream_t the calling thread's products run on (current device), so a harness can

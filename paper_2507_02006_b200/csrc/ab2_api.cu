@@ -235,6 +235,16 @@ int aires_b200_robw_cuts(const uint64_t* row_ptr, uint64_t n_rows, uint64_t m_a,
   return g != AIRES_B200_OK ? g : rc;
 }
 
+int aires_b200_run(const aires_b200_matrix* a, const aires_b200_matrix* b, const aires_b200_run_config* cfg,
+                   aires_b200_output* c, aires_b200_run_report* report) {
+  return ab2::guarded([&] {
+    if (!a || !b || !cfg || !c || !report) ab2::fail(AIRES_B200_INVALID_ARGUMENT, "null argument");
+    ab2::Ctx& ctx = ab2::ctx_for_thread();
+    ctx.launches = 0;
+    ab2::run_pipeline(ctx, *a, *b, *cfg, *c, *report);
+  });
+}
+
 void* aires_b200_stream(void) {
   void* s = nullptr;
   ab2::guarded([&] { s = static_cast<void*>(ab2::ctx_for_thread().stream); });

@@ -91,6 +91,43 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
 // C = A * X; A is a CSR rows view (host or device).
 void spgemm_rows(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_b200_output& out);
 
+// ---- tile passes for the out-of-core pipeline (ab2_pipeline.cu), launched on ctx.stream ----
+// A tile: rows [0, rows) of a device CSR slice; aptr is absolute (abase = aptr[0] of the slice
+// buffer's first entry).  idx_bytes is the width of acol and of the C column output.
+struct TileSym {
+  const uint64_t* aptr;
+  uint64_t abase;
+  const void* acol;
+  int64_t rows;
+  int32_t* cnt;     // rows: C nnz per row (output)
+  int64_t* rflops;  // rows: MACs per row (output)
+  int64_t* heavy;   // rows scratch
+  Ctl* ctl;         // zeroed; ctl->flops accumulates the MACs
+};
+struct TilePass {
+  const uint64_t* aptr;
+  uint64_t abase;
+  const void* acol;
+  const void* aval;
+  int64_t rows;
+  const int64_t* cpos;  // exact C row offsets for these rows (rows+1), absolute
+  int64_t cbase;        // cpos value of the tile's first C entry in ccol/cval
+  void* ccol;
+  void* cval;
+  uint64_t c_cap;
+  int64_t* heavy;   // rows scratch
+  uint32_t* cnt;    // rows scratch
+  uint64_t* toff;   // rows scratch
+  Ctl* ctl;         // zeroed; bad_row != 0 afterwards means a count/capacity failure
+};
+// Both return the number of kernels launched.
+int tile_symbolic(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TileSym& t);
+int tile_product(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TilePass& t);
+
+// Out-of-core run (ab2_pipeline.cu).
+void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b, const aires_b200_run_config& cfg,
+                  aires_b200_output& out, aires_b200_run_report& rep);
+
 // RoBW cuts on the device.
 int robw_cuts(Ctx& ctx, const uint64_t* row_ptr, uint64_t n_rows, uint64_t m_a, uint64_t I,
               uint64_t V, uint32_t location, uint64_t* cuts, uint64_t cap, uint64_t* n_segs,

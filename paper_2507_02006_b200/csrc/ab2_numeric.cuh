@@ -69,6 +69,8 @@ struct Num3Args {
   uint32_t stage_block;  // staging entries a warp reserves at a time (>= 8 * stride)
   uint32_t pad1;
   Ctl* ctl;
+  const int64_t* cpos;  // direct mode: exact C row offsets (symbolic pass), else staging
+  int64_t cbase;
 };
 
 template <class V>
@@ -361,6 +363,22 @@ struct StageCursor {
   }
 };
 
+// Output offset of row r: the exact CSR position when the row counts are known in advance
+// (out-of-core tiles, cpos = C row_ptr from the symbolic pass; a count that disagrees flags
+// ctl->bad_row = 2), else a bump allocation in the staging area.
+template <class P>
+__device__ __forceinline__ unsigned long long out_offset(const P& p, int64_t r, uint32_t cnt, StageCursor& stage) {
+  if (p.cpos != nullptr) {
+    const int64_t o = p.cpos[r] - p.cbase;
+    if (p.cpos[r + 1] - p.cpos[r] != static_cast<int64_t>(cnt)) {
+      if (lane_id() == 0) atomicMax(&p.ctl->bad_row, 2ull);
+      return ~0ull;
+    }
+    return static_cast<unsigned long long>(o);
+  }
+  return stage.take(cnt, p.ctl, p.stage_block);
+}
+
 template <class V, class IdxT, int W, bool XZ>
 __global__ void __launch_bounds__(256, AB2_NUM_MINB) k_numeric3(Num3Args<V, IdxT> p) {
   constexpr bool EXACT = sizeof(V) == 8;
@@ -433,12 +451,12 @@ __global__ void __launch_bounds__(256, AB2_NUM_MINB) k_numeric3(Num3Args<V, IdxT
     __syncthreads();
     if (warp == 0) {
       const uint32_t cnt = fold_count<V>(warp_acc(0), p.stride, 1, n_cols);
-      const unsigned long long off = stage.take(cnt, p.ctl, p.stage_block);
-      if (off + cnt <= p.t_cap) {
+      const unsigned long long off = out_offset(p, r, cnt, stage);
+      if (off <= p.t_cap && off + cnt <= p.t_cap) {
         emit_copy0<V, IdxT>(warp_acc(0), n_cols, p.tcol + off, p.tval + off);
       } else {
         fold_count<V>(warp_acc(0), p.stride, 1, 0);  // reset
-        if (lane == 0) p.ctl->bad_row = 1;
+        if (lane == 0) atomicMax(&p.ctl->bad_row, 1ull);
       }
       if (lane == 0) {
         p.cnt[r] = cnt;
@@ -467,12 +485,12 @@ __global__ void __launch_bounds__(256, AB2_NUM_MINB) k_numeric3(Num3Args<V, IdxT
       my_macs += walk_entries<V, IdxT, W, EXACT, false, XZ>(p, ac, av, n, 0, 1, acc, warp_tab(warp), 0, 0, zero);
       if (__any_sync(kFull, zero)) slow_row<V, IdxT>(p, ac, av, n, acc, warp_mark(warp));
       const uint32_t cnt = fold_count<V>(acc, p.stride, EXACT ? 1 : p.copies, n_cols);
-      const unsigned long long off = stage.take(cnt, p.ctl, p.stage_block);
-      if (off + cnt <= p.t_cap) {
+      const unsigned long long off = out_offset(p, r, cnt, stage);
+      if (off <= p.t_cap && off + cnt <= p.t_cap) {
         emit_copy0<V, IdxT>(acc, n_cols, p.tcol + off, p.tval + off);
       } else {
         fold_count<V>(acc, p.stride, 1, 0);  // reset
-        if (lane == 0) p.ctl->bad_row = 1;
+        if (lane == 0) atomicMax(&p.ctl->bad_row, 1ull);
       }
       if (lane == 0) {
         p.cnt[r] = cnt;

@@ -26,7 +26,7 @@
 #include "ab2_numeric.cuh"
 
 #ifndef AB2_N4_BATCH
-#define AB2_N4_BATCH 4
+#define AB2_N4_BATCH 8
 #endif
 
 namespace ab2 {
@@ -57,6 +57,8 @@ struct Num4Args {
   float tiny;
   uint32_t stage_block;
   Ctl* ctl;
+  const int64_t* cpos;
+  int64_t cbase;
 };
 
 __device__ __forceinline__ void smem_fma_rmw(uint32_t addr, float a, float x) {
@@ -84,16 +86,32 @@ __device__ __forceinline__ uint32_t walk4(const Num4Args<IdxT>& p, const IdxT* _
   const uint2* __restrict__ xent = p.xent;
   const float tiny = p.tiny;
   uint32_t macs = 0;
-  for (uint32_t b = chunk0 * 32; b < n; b += chunk_stride * 32) {
+  // Two-deep prefetch: the descriptor gather of chunk c+1 and the (k, a) loads of chunk c+2 are
+  // in flight while chunk c's terms are gathered and accumulated.
+  const uint32_t step = chunk_stride * 32;
+  auto load_ka = [&](uint32_t b, uint64_t& k, float& a) {
     const uint32_t i = b + lane;
-    uint2 d = make_uint2(0u, 0u);
-    float a = 0.f;
+    k = K;
+    a = 0.f;
     if (i < n) {
-      const uint64_t k = static_cast<uint64_t>(ac[i]);
+      k = static_cast<uint64_t>(ac[i]);
       a = av[i];
-      if (k < K) d = __ldg(p.xdesc + k);
-      zero |= !(fabsf(a) >= tiny);  // zero, tiny or NaN weight: explicit path
     }
+  };
+  auto load_d = [&](uint64_t k) { return k < K ? __ldg(p.xdesc + k) : make_uint2(0u, 0u); };
+  uint64_t k1 = K, k2 = K;
+  float a1 = 0.f, a2 = 0.f;
+  uint32_t b = chunk0 * 32;
+  load_ka(b, k1, a1);
+  uint2 d1 = load_d(k1);
+  load_ka(b + step, k2, a2);
+  for (; b < n; b += step) {
+    const uint2 d = d1;
+    const float a = a1;
+    zero |= (b + lane < n) && !(fabsf(a) >= tiny);  // zero, tiny or NaN weight: explicit path
+    d1 = load_d(k2);
+    a1 = a2;
+    load_ka(b + 2 * step, k2, a2);
     macs += d.y;
     const uint32_t nem = __ballot_sync(kFull, d.y != 0);
     if (nem == 0) continue;
@@ -256,12 +274,12 @@ __global__ void __launch_bounds__(256, 2) k_numeric4(Num4Args<IdxT> p) {
     __syncthreads();
     if (warp == 0) {
       const uint32_t cnt = fold_count<float>(warp_acc(0), p.stride, 1, n_cols);
-      const unsigned long long off = stage.take(cnt, p.ctl, p.stage_block);
-      if (off + cnt <= p.t_cap) {
+      const unsigned long long off = out_offset(p, r, cnt, stage);
+      if (off <= p.t_cap && off + cnt <= p.t_cap) {
         emit_copy0<float, IdxT>(warp_acc(0), n_cols, p.tcol + off, p.tval + off);
       } else {
         fold_count<float>(warp_acc(0), p.stride, 1, 0);
-        if (lane == 0) p.ctl->bad_row = 1;
+        if (lane == 0) atomicMax(&p.ctl->bad_row, 1ull);
       }
       if (lane == 0) {
         p.cnt[r] = cnt;
@@ -290,12 +308,12 @@ __global__ void __launch_bounds__(256, 2) k_numeric4(Num4Args<IdxT> p) {
       my_macs += walk4<IdxT, XZ>(p, ac, av, n, 0, 1, acc, warp_cbuf(warp), zero);
       if (__any_sync(kFull, zero)) slow_row4<IdxT>(p, ac, av, n, acc, warp_mark(warp));
       const uint32_t cnt = fold_count<float>(acc, p.stride, p.copies, n_cols);
-      const unsigned long long off = stage.take(cnt, p.ctl, p.stage_block);
-      if (off + cnt <= p.t_cap) {
+      const unsigned long long off = out_offset(p, r, cnt, stage);
+      if (off <= p.t_cap && off + cnt <= p.t_cap) {
         emit_copy0<float, IdxT>(acc, n_cols, p.tcol + off, p.tval + off);
       } else {
         fold_count<float>(acc, p.stride, 1, 0);
-        if (lane == 0) p.ctl->bad_row = 1;
+        if (lane == 0) atomicMax(&p.ctl->bad_row, 1ull);
       }
       if (lane == 0) {
         p.cnt[r] = cnt;

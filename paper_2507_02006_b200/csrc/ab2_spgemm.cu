@@ -4,6 +4,7 @@
 //   allocation through the caller's allocator, spgemm.hpp:111-112] -> K_numeric -> [K_fix]
 //   -> row_ptr copy -> (host C) D2H.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -93,6 +94,8 @@ void launch_numeric4(Ctx& ctx, const Num3Args<float, IdxT>& q, const XOperand& x
   p.tiny = q.tiny;
   p.stage_block = q.stage_block;
   p.ctl = q.ctl;
+  p.cpos = q.cpos;
+  p.cbase = q.cbase;
   int nw = static_cast<int>(env_int("AB2_N4_WARPS", 8));
   nw = std::max(1, std::min<int>(nw, static_cast<int>((200 * 1024) / p.warp_bytes)));
   const int threads = nw * 32;
@@ -120,23 +123,9 @@ void convert(Ctx& ctx, const void* in, void* out, int64_t n) {
 }
 
 
-// One product: classify -> MAC count -> K_numeric (staging) -> scan -> [nnz readback,
-// exact allocation through the caller's allocator, spgemm.hpp:111-112] -> K_place.
 template <class V, class IdxT>
-void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_b200_output& out,
-                 const uint64_t* aptr, uint64_t abase, const IdxT* acol, const V* aval, uint64_t span_hint) {
-  const int64_t rows = static_cast<int64_t>(a.n_rows);
-  const int W = x.W;
-  if (x.K >= (int64_t(1) << 31) / 16) fail(AIRES_B200_CAPACITY_EXCEEDED, "inner dimension too large for slot indexing");
-  Ctl* ctl = ctx.ctl.as<Ctl>(1);
-  Ctl* h = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
-  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 4096);
-  int64_t* heavy = ctx.sym_heavy.as<int64_t>(std::max<int64_t>(rows, 1));
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(ctx.cnt.as<int32_t>(std::max<int64_t>(rows, 1)));
-  uint64_t* toff = reinterpret_cast<uint64_t*>(ctx.rflops.as<int64_t>(std::max<int64_t>(rows, 1)));
-  int64_t* cptr = ctx.cptr.as<int64_t>(rows + 1);
-  const uint64_t n_cols = static_cast<uint64_t>(x.n_cols);
-
+Num3Args<V, IdxT> make_num3(const XOperand& x, const uint64_t* aptr, uint64_t abase, const IdxT* acol, const V* aval,
+                            int64_t rows, int64_t* heavy, int64_t heavy_deg, uint32_t* cnt, uint64_t* toff, Ctl* ctl) {
   Num3Args<V, IdxT> np{};
   np.aptr = aptr;
   np.abase = abase;
@@ -152,7 +141,7 @@ void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_
   np.x.slots = static_cast<const typename SlotOf<V>::type*>(x.slots);
   np.x.cslots = static_cast<const uint16_t*>(x.cslots);
   np.stride = static_cast<int32_t>((x.n_cols + 1 + 31) & ~int64_t(31));
-  np.copies = sizeof(V) == 8 ? 1 : 32 / W;
+  np.copies = sizeof(V) == 8 ? 1 : 32 / x.W;
   np.warp_bytes = static_cast<int32_t>(
       ((static_cast<size_t>(np.copies) * np.stride * sizeof(V) + np.stride + 15) & ~size_t(15)) +
       32 * sizeof(ChunkPair));
@@ -166,6 +155,40 @@ void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_
   // fp64: < 2^-1074); such weights send the row to the explicit-mark path.
   np.tiny = x.xmin > 0 ? static_cast<V>((sizeof(V) == 4 ? std::ldexp(1.0, -147) : std::ldexp(1.0, -1072)) / x.xmin)
                        : V(0);
+  np.stage_block = static_cast<uint32_t>(std::max<int64_t>(4096, 8 * static_cast<int64_t>(np.stride)));
+  return np;
+}
+
+// The product kernel for the operand's arithmetic (fp32: flattened-MAC k_numeric4 unless
+// AB2_NUMERIC=3; fp64-exact: k_numeric3).
+template <class V, class IdxT>
+void launch_product(Ctx& ctx, const Num3Args<V, IdxT>& np, const XOperand& x) {
+  if constexpr (std::is_same<V, float>::value) {
+    if (x.xdesc != nullptr && env_int("AB2_NUMERIC", 4) == 4) {
+      launch_numeric4<IdxT>(ctx, np, x);
+      return;
+    }
+  }
+  launch_numeric<V, IdxT>(ctx, np, x.W, x.has_zero);
+}
+
+// One product: classify -> MAC count -> K_numeric (staging) -> scan -> [nnz readback,
+// exact allocation through the caller's allocator, spgemm.hpp:111-112] -> K_place.
+template <class V, class IdxT>
+void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_b200_output& out,
+                 const uint64_t* aptr, uint64_t abase, const IdxT* acol, const V* aval, uint64_t span_hint) {
+  const int64_t rows = static_cast<int64_t>(a.n_rows);
+  if (x.K >= (int64_t(1) << 31) / 16) fail(AIRES_B200_CAPACITY_EXCEEDED, "inner dimension too large for slot indexing");
+  Ctl* ctl = ctx.ctl.as<Ctl>(1);
+  Ctl* h = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
+  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 4096);
+  int64_t* heavy = ctx.sym_heavy.as<int64_t>(std::max<int64_t>(rows, 1));
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(ctx.cnt.as<int32_t>(std::max<int64_t>(rows, 1)));
+  uint64_t* toff = reinterpret_cast<uint64_t*>(ctx.rflops.as<int64_t>(std::max<int64_t>(rows, 1)));
+  int64_t* cptr = ctx.cptr.as<int64_t>(rows + 1);
+  const uint64_t n_cols = static_cast<uint64_t>(x.n_cols);
+
+  Num3Args<V, IdxT> np = make_num3<V, IdxT>(x, aptr, abase, acol, aval, rows, heavy, heavy_deg, cnt, toff, ctl);
   // staging: nnz bound (dense rows, or A entries x longest X row) * 8/7 + one block per warp
   const uint64_t maxlen = std::max<int64_t>(x.max_row_len, 1);
   const uint64_t bound = std::min<uint64_t>(static_cast<uint64_t>(rows) * n_cols, span_hint * maxlen);
@@ -185,16 +208,7 @@ void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_
     AB2_CUDA(cudaGetLastError());
   }
   AB2_CUDA(cudaEventRecord(ctx.ev[1], ctx.stream));
-  if (rows > 0) {
-    if constexpr (std::is_same<V, float>::value) {
-      if (x.xdesc != nullptr && env_int("AB2_NUMERIC", 4) == 4)
-        launch_numeric4<IdxT>(ctx, np, x);
-      else
-        launch_numeric<V, IdxT>(ctx, np, W, x.has_zero);
-    } else {
-      launch_numeric<V, IdxT>(ctx, np, W, x.has_zero);
-    }
-  }
+  if (rows > 0) launch_product<V, IdxT>(ctx, np, x);
   AB2_CUDA(cudaEventRecord(ctx.ev[2], ctx.stream));
   const int64_t nb = (rows + kScanTile - 1) / kScanTile;
   int64_t* part = ctx.scan_part.as<int64_t>(std::max<int64_t>(nb, 1));
@@ -266,6 +280,69 @@ void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_
 }
 
 }  // namespace
+
+namespace {
+template <class V, class IdxT>
+int tile_product_t(Ctx& ctx, const XOperand& x, const TilePass& t) {
+  if (t.rows <= 0) return 0;
+  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 4096);
+  const int g = static_cast<int>(std::min<int64_t>((t.rows + 255) / 256, static_cast<int64_t>(ctx.sms) * 16));
+  k_classify<<<g, 256, 0, ctx.stream>>>(t.aptr, t.rows, heavy_deg, t.heavy, t.ctl);
+  AB2_CUDA(cudaGetLastError());
+  Num3Args<V, IdxT> np = make_num3<V, IdxT>(x, t.aptr, t.abase, static_cast<const IdxT*>(t.acol),
+                                            static_cast<const V*>(t.aval), t.rows, t.heavy, heavy_deg, t.cnt,
+                                            t.toff, t.ctl);
+  np.cpos = t.cpos;
+  np.cbase = t.cbase;
+  np.tcol = static_cast<IdxT*>(t.ccol);
+  np.tval = static_cast<V*>(t.cval);
+  np.t_cap = t.c_cap;
+  launch_product<V, IdxT>(ctx, np, x);
+  return 2;
+}
+
+template <class IdxT>
+int tile_symbolic_t(Ctx& ctx, const XOperand& x, const TileSym& t) {
+  if (t.rows <= 0) return 0;
+  const int64_t heavy_deg = env_int("AB2_SYM_HEAVY_DEG", 2048);
+  const int g = static_cast<int>(std::min<int64_t>((t.rows + 255) / 256, static_cast<int64_t>(ctx.sms) * 16));
+  k_classify<<<g, 256, 0, ctx.stream>>>(t.aptr, t.rows, heavy_deg, t.heavy, t.ctl);
+  AB2_CUDA(cudaGetLastError());
+  SymArgs sp{};
+  sp.aptr = t.aptr;
+  sp.abase = t.abase;
+  sp.rows = t.rows;
+  sp.K = x.K;
+  sp.n_cols = static_cast<int32_t>(x.n_cols);
+  sp.region_bytes = static_cast<int32_t>((x.n_cols + 15) & ~int64_t(15));
+  sp.xptr = static_cast<const int64_t*>(x.ptr);
+  sp.xcol = static_cast<const int32_t*>(x.col);
+  sp.cslots = static_cast<const uint16_t*>(x.cslots);
+  sp.cnt = t.cnt;
+  sp.rflops = t.rflops;
+  sp.sym_heavy = t.heavy;
+  sp.heavy_deg = heavy_deg;
+  sp.num_heavy = t.heavy;  // unused: heavy_flops is never exceeded
+  sp.heavy_flops = INT64_MAX;
+  sp.ctl = t.ctl;
+  auto k = k_symbolic<IdxT, kCSlotW>;
+  const size_t smem = 8 * static_cast<size_t>(sp.region_bytes);
+  const int grid = occupancy_grid(k, 256, smem, ctx.sms);
+  k<<<grid, 256, smem, ctx.stream>>>(sp, static_cast<const IdxT*>(t.acol));
+  AB2_CUDA(cudaGetLastError());
+  return 2;
+}
+}  // namespace
+
+int tile_product(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TilePass& t) {
+  const bool f32 = x.mode == AIRES_B200_MODE_FP32;
+  if (idx_bytes == 4) return f32 ? tile_product_t<float, uint32_t>(ctx, x, t) : tile_product_t<double, uint32_t>(ctx, x, t);
+  return f32 ? tile_product_t<float, uint64_t>(ctx, x, t) : tile_product_t<double, uint64_t>(ctx, x, t);
+}
+
+int tile_symbolic(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TileSym& t) {
+  return idx_bytes == 4 ? tile_symbolic_t<uint32_t>(ctx, x, t) : tile_symbolic_t<uint64_t>(ctx, x, t);
+}
 
 void spgemm_rows(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_b200_output& out) {
   if (a.layout != AIRES_B200_CSR) fail(AIRES_B200_INVALID_ARGUMENT, "A must be CSR");

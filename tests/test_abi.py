@@ -74,3 +74,14 @@ def test_synth_graph_shape_and_normalization():
     deg = np.diff(g.row_ptr.astype(np.int64)).astype(np.float64)
     np.testing.assert_allclose(g.values, 1.0 / np.sqrt(deg[rows] * deg[cols]), rtol=1e-15)
     assert st["nnz_a"] + g.n_rows == g.nnz()
+
+
+def test_library_checksum_matches_reference_goldens():
+    """aires_b200_checksum (host) == the reference's checksum of every golden C (serialize.hpp:50-59)."""
+    g = np.load(os.path.join(ROOT, "tests", "golden", "spgemm.npz"))
+    for c in range(int(g["n_cases"][0])):
+        nr, ni, nc, macs, ck = (int(x) for x in g[f"c{c}_dims"])
+        m = ab.CsrMatrix(nr, nc, g[f"c{c}_c_ptr"], g[f"c{c}_c_idx"], g[f"c{c}_c_val"])
+        assert ab.checksum(m) == ck
+        m32 = ab.CsrMatrix(nr, nc, g[f"c{c}_c_ptr"], g[f"c{c}_c_idx"].astype(np.uint32), g[f"c{c}_c_val"])
+        assert ab.checksum(m32) == ck

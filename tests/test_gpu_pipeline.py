@@ -1,0 +1,107 @@
+"""GPU parity of the out-of-core run (aires_b200_run / run_aires, scheduler.hpp:72-168) against
+the oracle: results must not depend on the device budget, tile count or ring depth (the
+partition-independence of spgemm_test.cpp:97-115 and acceptance.cpp:66-103, criterion 2)."""
+import numpy as np
+import pytest
+
+import paper_2507_02006_b200 as ab
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+
+def _graph(n, nnz, dim, seed=1):
+    g, _ = ab.synth_graph(n, nnz, degree_cap=max(50, n // 10), seed=seed, idx_dtype=np.uint64)
+    x = ab.synth_features(n, dim, 99.0 if dim >= 100 else 90.0, 3, idx_dtype=np.uint64)
+    return g, x
+
+
+def _oracle(g, x):
+    rc, (p, i, v), macs = po.spgemm_rowwise(g.row_ptr, g.col_idx, g.values, g.n_rows, g.n_cols, x.n_rows, x.n_cols,
+                                            x.row_ptr, x.col_idx, x.values, nthreads=8)
+    assert rc == 0
+    return p, i, v, macs
+
+
+def _bytes(g, x, want, vb=8):
+    a = 8 * (g.n_rows + 1) + (8 + vb) * g.nnz()
+    c = 8 * (g.n_rows + 1) + (8 + vb) * want[1].shape[0]
+    return a, c
+
+
+@pytest.mark.parametrize("frac", [1.0, 0.5, 0.25, 0.125])
+def test_run_fp64_bit_exact_across_budgets(frac):
+    g, x = _graph(20_000, 300_000, 128)
+    wp, wi, wv, macs = _oracle(g, x)
+    ck = po.checksum(g.n_rows, x.n_cols, wp, wi, wv)
+    a_b, c_b = _bytes(g, x, (wp, wi))
+    budget = ab.MemoryBudget(int(40e6 + frac * (a_b + c_b)))
+    res = ab.run_aires(g, x, budget)
+    if frac < 1.0:
+        assert res.report.segments >= 2
+    assert res.report.c_checksum == ck
+    assert res.report.flops == macs
+    assert np.array_equal(res.c.row_ptr, wp) and np.array_equal(res.c.col_idx, wi)
+    # ledger: A (ptr + one column pass for the symbolic sizing + col/val) and X cross H2D once,
+    # C (ptr + col/val) crosses D2H once
+    rep = res.report.ledger
+    assert rep.d2h.bytes == 8 * (g.n_rows + 1) + 16 * wi.shape[0]
+    assert rep.h2d.bytes == 8 * (g.n_rows + 1) + 8 * g.nnz() + 16 * g.nnz() + 8 * (x.n_rows + 1) + 16 * x.nnz()
+
+
+@pytest.mark.parametrize("n_buffers", [2, 3, 4])
+def test_run_fp32_tolerance_many_tiles(n_buffers):
+    g, x = _graph(30_000, 400_000, 100, seed=4)
+    wp, wi, wv, macs = _oracle(g, x)
+    g32 = ab.CsrMatrix(g.n_rows, g.n_cols, g.row_ptr, g.col_idx.astype(np.uint32), g.values.astype(np.float32))
+    x32 = ab.CsrMatrix(x.n_rows, x.n_cols, x.row_ptr, x.col_idx.astype(np.uint32), x.values.astype(np.float32))
+    a_b = 8 * (g.n_rows + 1) + 8 * g.nnz()
+    c_b = 8 * (g.n_rows + 1) + 8 * wi.shape[0]
+    res = ab.run_aires(g32, x32, ab.MemoryBudget(int(30e6 + (a_b + c_b) / 8)), n_buffers=n_buffers,
+                       with_checksum=False)
+    assert res.report.segments >= 8
+    assert np.array_equal(res.c.row_ptr, wp) and np.array_equal(res.c.col_idx.astype(np.uint64), wi)
+    err = np.abs(res.c.values.astype(np.float64) - wv) / np.abs(wv)
+    assert err.max() <= 1e-5
+    assert res.report.flops == macs
+
+
+def test_run_matches_in_core_product_fp32():
+    g, x = _graph(10_000, 200_000, 64, seed=6)
+    g32 = ab.CsrMatrix(g.n_rows, g.n_cols, g.row_ptr, g.col_idx.astype(np.uint32), g.values.astype(np.float32))
+    x32 = ab.CsrMatrix(x.n_rows, x.n_cols, x.row_ptr, x.col_idx.astype(np.uint32), x.values.astype(np.float32))
+    full = ab.spgemm_full(g32, x32)
+    res = ab.run_aires(g32, x32, ab.MemoryBudget(int(8e6)), with_checksum=False)
+    assert res.report.segments >= 2
+    assert np.array_equal(res.c.row_ptr, full.row_ptr) and np.array_equal(res.c.col_idx, full.col_idx)
+    np.testing.assert_allclose(res.c.values, full.values, rtol=2e-6)
+
+
+def test_run_budget_too_small_raises():
+    g, x = _graph(5_000, 50_000, 64)
+    with pytest.raises(ab.AiresError) as e:
+        ab.run_aires(g, x, ab.MemoryBudget(1000))
+    assert e.value.code == ab.errc.insufficient_device_memory
+
+
+def test_run_a_only_tiling_fails_like_the_reference():
+    """c_aware=False reproduces the reference admission (A-only RoBW segments, C must fit the rest):
+    on a GCN shape with a multi-segment budget it raises insufficient_device_memory."""
+    g, x = _graph(20_000, 300_000, 128)
+    wp, wi, wv, _ = _oracle(g, x)
+    a_b, c_b = _bytes(g, x, (wp, wi))
+    with pytest.raises(ab.AiresError) as e:
+        ab.run_aires(g, x, ab.MemoryBudget(int(40e6 + 0.25 * (a_b + c_b))), c_aware=False)
+    assert e.value.code == ab.errc.insufficient_device_memory
+
+
+def test_run_empty_and_csc_operand():
+    a = ab.CsrMatrix(4, 3, np.zeros(5, np.uint64), np.zeros(0, np.uint64), np.zeros(0))
+    b = ab.CsrMatrix(3, 2, np.array([0, 1, 1, 2], np.uint64), np.array([0, 1], np.uint64), np.array([1.0, 2.0]))
+    res = ab.run_aires(a, b, ab.MemoryBudget(int(1e7)))
+    assert res.c.nnz() == 0 and list(res.c.row_ptr) == [0] * 5
+    g, x = _graph(3_000, 30_000, 32)
+    cp, ri, cv = po.csr_to_csc(x.n_rows, x.n_cols, x.row_ptr, x.col_idx, x.values)
+    res1 = ab.run_aires(g, ab.CscMatrix(x.n_rows, x.n_cols, cp, ri, cv), ab.MemoryBudget(int(2e7)))
+    res2 = ab.run_aires(g, x, ab.MemoryBudget(int(2e7)))
+    assert res1.report.c_checksum == res2.report.c_checksum
