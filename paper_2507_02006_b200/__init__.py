@@ -22,7 +22,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libaires_b200.so")
+LIB_PATH = os.environ.get("AB2_LIB") or os.path.join(_HERE, "libaires_b200.so")
 
 
 class errc(enum.IntEnum):

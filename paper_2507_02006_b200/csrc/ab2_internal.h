@@ -74,8 +74,10 @@ struct XOperand {
   void* slots = nullptr;   // K*W entries
   void* cslots = nullptr;  // K*kCSlotW u16
   void* xlen = nullptr;    // K+1 u16 row lengths
-  void* xdesc = nullptr;   // fp32: K+1 uint2 {start, len} (row K empty)
-  void* xent = nullptr;    // fp32: nnz uint2 {col, value bits}
+  void* xdesc = nullptr;   // fp32: K+1 uint2 {slot start, nslot | len << 16} (row K empty)
+  void* xent = nullptr;    // fp32: padded W5-entry slots of uint2 {col, value bits}
+  int W5 = 0;              // fp32 step-list slot width
+  int64_t dummy_slot = 0;  // fp32: index of the all-trash slot
   double xmin = 0.0;       // smallest nonzero |x|
   bool has_zero = false;   // X stores an exact zero
   size_t bytes = 0;

@@ -180,19 +180,37 @@ __global__ void k_x_slots(const int64_t* __restrict__ xptr, const int32_t* __res
   }
 }
 
-// Flat fp32 layout for the flattened-MAC product pass (ab2_numeric4.cuh): one 8-byte
-// descriptor per X row and the entries interleaved as {col, value} so one 8-byte gather
-// fetches a whole term.
-__global__ void k_x_flat(const int64_t* __restrict__ xptr, const int32_t* __restrict__ xcol,
-                         const float* __restrict__ xval, int64_t K, uint2* __restrict__ desc,
-                         uint2* __restrict__ ent) {
-  const int64_t nnz = xptr[K];
-  const int64_t n = max(K + 1, nnz);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    if (i < K) desc[i] = make_uint2(static_cast<uint32_t>(xptr[i]), static_cast<uint32_t>(xptr[i + 1] - xptr[i]));
-    if (i == K) desc[i] = make_uint2(0u, 0u);
-    if (i < nnz) ent[i] = make_uint2(static_cast<uint32_t>(xcol[i]), __float_as_uint(xval[i]));
+// Padded fp32 layout for the step-list product pass (ab2_numeric5.cuh): X row k occupies
+// nslot = ceil(len / W5) consecutive W5-entry slots starting at slot pstart[k]; an entry is
+// {accumulator byte offset col * 4, value bits}; entries past len point at the trash column
+// (value 1.0), so a W5-lane group always loads and adds a full slot.  The last slot is an
+// all-trash dummy used to pad step lists.
+// desc[k] = {pstart[k], nslot | len << 16}; desc[K] = {0, 0} (the dummy row).
+__global__ void k_x_pcount(const int64_t* __restrict__ xptr, int64_t K, int w5, int32_t* __restrict__ cnt) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    cnt[k] = static_cast<int32_t>((xptr[k + 1] - xptr[k] + w5 - 1) / w5);
+}
+
+__global__ void k_x_pfill(const int64_t* __restrict__ xptr, const int32_t* __restrict__ xcol,
+                          const float* __restrict__ xval, int64_t K, int w5, uint32_t trash,
+                          const int64_t* __restrict__ pstart, uint2* __restrict__ desc, uint2* __restrict__ ent,
+                          int64_t dummy) {
+  if (blockIdx.x == 0 && threadIdx.x < w5) ent[dummy * w5 + threadIdx.x] = make_uint2(trash * 4u, kOneBits);
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k <= K;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (k == K) {
+      desc[k] = make_uint2(0u, 0u);
+      continue;
+    }
+    const int64_t s = xptr[k], len = xptr[k + 1] - s;
+    const int64_t ns = (len + w5 - 1) / w5;
+    const int64_t p = pstart[k];
+    desc[k] = make_uint2(static_cast<uint32_t>(p), static_cast<uint32_t>(ns | (len << 16)));
+    uint2* o = ent + p * w5;
+    for (int64_t e = 0; e < ns * w5; e++)
+      o[e] = e < len ? make_uint2(static_cast<uint32_t>(xcol[s + e]) * 4u, __float_as_uint(xval[s + e]))
+                     : make_uint2(trash * 4u, kOneBits);
   }
 }
 
@@ -449,14 +467,36 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
       build_slots<double>(ctx, *x);
   }
   if (mode == AIRES_B200_MODE_FP32) {
+    // step-list layout: W5 ~ the mean row length, copies = 32 / W5 accumulators per warp
+    const double mean = static_cast<double>(x->nnz) / K;
+    int w5 = mean >= 4.0 ? 8 : (mean >= 2.0 ? 4 : 2);
+    const int64_t stride = (x->n_cols + 1 + 31) & ~int64_t(31);
+    while (w5 < 32 && (32 / w5) * stride * 4 > 24 * 1024) w5 *= 2;
+    const int64_t fw = env_int("AB2_W5", 0);
+    if (fw == 2 || fw == 4 || fw == 8 || fw == 16 || fw == 32) w5 = static_cast<int>(fw);
+    x->W5 = w5;
+    int32_t* pc = ctx.cnt.as<int32_t>(std::max<int64_t>(x->K, 1));
+    int64_t* ps = ctx.cptr.as<int64_t>(x->K + 1);
+    const int g = grid_for(std::max<int64_t>(x->K + 1, 1), 256, ctx.sms);
+    k_x_pcount<<<g, 256, 0, ctx.stream>>>(static_cast<const int64_t*>(x->ptr), x->K, w5, pc);
+    const int64_t nb = (x->K + kScanTile - 1) / kScanTile;
+    int64_t* part = ctx.scan_part.as<int64_t>(std::max<int64_t>(nb, 1));
+    if (x->K > 0) {
+      k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(pc, x->K, part);
+      k_scan_part<<<1, 1024, 0, ctx.stream>>>(part, nb, ctl);
+      k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(pc, x->K, part, ps);
+    }
+    const int64_t slots_ub = x->nnz / w5 + x->K + 2;  // + the dummy slot
+    x->dummy_slot = slots_ub - 1;
     x->xdesc = alloc(ctx.xo_desc, (x->K + 1) * sizeof(uint2));
-    x->xent = alloc(ctx.xo_ent, std::max<int64_t>(x->nnz, 1) * sizeof(uint2));
-    k_x_flat<<<grid_for(std::max<int64_t>(x->K + 1, x->nnz), 256, ctx.sms), 256, 0, ctx.stream>>>(
-        static_cast<const int64_t*>(x->ptr), static_cast<const int32_t*>(x->col), static_cast<const float*>(x->val),
-        x->K, static_cast<uint2*>(x->xdesc), static_cast<uint2*>(x->xent));
+    x->xent = alloc(ctx.xo_ent, slots_ub * w5 * sizeof(uint2));
+    k_x_pfill<<<g, 256, 0, ctx.stream>>>(static_cast<const int64_t*>(x->ptr), static_cast<const int32_t*>(x->col),
+                                           static_cast<const float*>(x->val), x->K, w5,
+                                           static_cast<uint32_t>(x->n_cols), ps, static_cast<uint2*>(x->xdesc),
+                                           static_cast<uint2*>(x->xent), x->dummy_slot);
     AB2_CUDA(cudaGetLastError());
   }
-  x->prep_launches = (b.layout == AIRES_B200_CSR ? 1 : 6) + 4 + (mode == AIRES_B200_MODE_FP32 ? 1 : 0);
+  x->prep_launches = (b.layout == AIRES_B200_CSR ? 1 : 6) + 4 + (mode == AIRES_B200_MODE_FP32 ? (x->K > 0 ? 5 : 2) : 0);
   if (!temp) AB2_CUDA(cudaStreamSynchronize(ctx.stream));
   return x;
 }

@@ -263,7 +263,6 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
       fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY, "ring slot overflow");
   };
 
-  int launches = ctx.launches;
   const uint64_t n_sym = sym_cuts.size() - 1;
   std::vector<Ctl*> sym_ctl(nbuf);
   Ctl* d_ctls = static_cast<Ctl*>(arena.get(sizeof(Ctl) * std::max<uint64_t>(n_sym, 1)));
@@ -331,11 +330,11 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   const uint64_t* cp = static_cast<const uint64_t*>(optr);
 
   // tile cuts: C-aware (A + C + scratch per slot), or RoBW over A alone
-  // (c_aware = 0: RoBW-style cuts over A alone into half a slot, then the C block of each
+  // (c_aware = 0: RoBW-style cuts that fill a slot with A alone, then the C block of each
   // segment must fit the rest -- the reference's admission, which fails on GCN shapes)
   std::vector<uint64_t> cuts;
   if (!greedy_cuts(a.ptr, cfg.c_aware ? cp : nullptr, n, row_bytes, ib + vb, ib + vb,
-                   cfg.c_aware ? slot_budget : slot_budget / 2, cuts, &bad))
+                   cfg.c_aware ? slot_budget : slot_budget - slot_budget / 16, cuts, &bad))
     fail(AIRES_B200_ROW_TOO_LARGE, "row " + std::to_string(bad) + " does not fit a ring slot of " +
                                        std::to_string(slot_budget) + " bytes");
   if (!cfg.c_aware) {
@@ -424,7 +423,6 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   rep.phase3_ms = ms_between(t_p2, t_end);
   rep.total_ms = ms_between(t_begin, t_end);
   ctx.last_ms = rep.total_ms;
-  (void)launches;
   out.n_rows = n;
   out.n_cols = static_cast<uint64_t>(x->n_cols);
   out.nnz = nnz;

@@ -13,7 +13,7 @@
 
 #include "ab2_internal.h"
 #include "ab2_numeric.cuh"
-#include "ab2_numeric4.cuh"
+#include "ab2_numeric5.cuh"
 
 namespace ab2 {
 
@@ -65,10 +65,23 @@ void launch_numeric(Ctx& ctx, const Num3Args<V, IdxT>& p, int W, bool xz) {
   AB2_CUDA(cudaGetLastError());
 }
 
-// fp32 flattened-MAC pass (ab2_numeric4.cuh); shares the staging set-up of the k_numeric3 args.
+// fp32 step-list pass (ab2_numeric5.cuh); shares the staging / direct-offset set-up of the
+// k_numeric3 args.
+template <class IdxT, int W>
+void launch_numeric5_w(Ctx& ctx, const Num5Args<IdxT>& p, bool xz) {
+  int nw = static_cast<int>(env_int("AB2_N5_WARPS", 8));
+  nw = std::max(1, std::min<int>(nw, static_cast<int>((200 * 1024) / p.warp_bytes)));
+  const int threads = nw * 32;
+  const size_t smem = static_cast<size_t>(nw) * p.warp_bytes;
+  auto k = xz ? k_numeric5<IdxT, W, true> : k_numeric5<IdxT, W, false>;
+  const int grid = occupancy_grid(k, threads, smem, ctx.sms);
+  k<<<grid, threads, smem, ctx.stream>>>(p);
+  AB2_CUDA(cudaGetLastError());
+}
+
 template <class IdxT>
-void launch_numeric4(Ctx& ctx, const Num3Args<float, IdxT>& q, const XOperand& x) {
-  Num4Args<IdxT> p{};
+void launch_numeric5(Ctx& ctx, const Num3Args<float, IdxT>& q, const XOperand& x) {
+  Num5Args<IdxT> p{};
   p.aptr = q.aptr;
   p.abase = q.abase;
   p.acol = q.acol;
@@ -77,13 +90,10 @@ void launch_numeric4(Ctx& ctx, const Num3Args<float, IdxT>& q, const XOperand& x
   p.K = x.K;
   p.n_cols = static_cast<int32_t>(x.n_cols);
   p.stride = q.stride;
-  int nc = static_cast<int>(env_int("AB2_N4_COPIES", 4));
-  if (nc != 1 && nc != 2 && nc != 4 && nc != 8 && nc != 16) nc = 4;
-  p.copies = nc;
-  p.log2c = __builtin_ctz(static_cast<unsigned>(nc));
-  p.warp_bytes = static_cast<int32_t>(static_cast<size_t>(nc) * p.stride * 4 + p.stride + 32 * sizeof(uint4));
+  p.warp_bytes = static_cast<int32_t>(static_cast<size_t>(32 / x.W5) * p.stride * 4 + p.stride + kN5List * 8);
   p.xdesc = static_cast<const uint2*>(x.xdesc);
   p.xent = static_cast<const uint2*>(x.xent);
+  p.dummy_slot = static_cast<uint32_t>(x.dummy_slot);
   p.heavy = q.heavy;
   p.heavy_deg = q.heavy_deg;
   p.cnt = q.cnt;
@@ -96,14 +106,14 @@ void launch_numeric4(Ctx& ctx, const Num3Args<float, IdxT>& q, const XOperand& x
   p.ctl = q.ctl;
   p.cpos = q.cpos;
   p.cbase = q.cbase;
-  int nw = static_cast<int>(env_int("AB2_N4_WARPS", 8));
-  nw = std::max(1, std::min<int>(nw, static_cast<int>((200 * 1024) / p.warp_bytes)));
-  const int threads = nw * 32;
-  const size_t smem = static_cast<size_t>(nw) * p.warp_bytes;
-  auto k = x.has_zero ? k_numeric4<IdxT, true> : k_numeric4<IdxT, false>;
-  const int grid = occupancy_grid(k, threads, smem, ctx.sms);
-  k<<<grid, threads, smem, ctx.stream>>>(p);
-  AB2_CUDA(cudaGetLastError());
+  switch (x.W5) {
+    case 2: launch_numeric5_w<IdxT, 2>(ctx, p, x.has_zero); break;
+    case 4: launch_numeric5_w<IdxT, 4>(ctx, p, x.has_zero); break;
+    case 8: launch_numeric5_w<IdxT, 8>(ctx, p, x.has_zero); break;
+    case 16: launch_numeric5_w<IdxT, 16>(ctx, p, x.has_zero); break;
+    case 32: launch_numeric5_w<IdxT, 32>(ctx, p, x.has_zero); break;
+    default: fail(AIRES_B200_INVALID_ARGUMENT, "bad step-list slot width");
+  }
 }
 
 template <class Src, class Dst>
@@ -159,13 +169,14 @@ Num3Args<V, IdxT> make_num3(const XOperand& x, const uint64_t* aptr, uint64_t ab
   return np;
 }
 
-// The product kernel for the operand's arithmetic (fp32: flattened-MAC k_numeric4 unless
-// AB2_NUMERIC=3; fp64-exact: k_numeric3).
+// The product kernel: k_numeric3 (W-lane slot groups; fp32 and fp64-exact) by default, the fp32
+// step-list k_numeric5 with AB2_NUMERIC=5 (measured 3.5 ms vs 3.0 ms at cfg2: both are bound by
+// L1/shared-memory wavefronts, profiles/r01*).
 template <class V, class IdxT>
 void launch_product(Ctx& ctx, const Num3Args<V, IdxT>& np, const XOperand& x) {
   if constexpr (std::is_same<V, float>::value) {
-    if (x.xdesc != nullptr && env_int("AB2_NUMERIC", 4) == 4) {
-      launch_numeric4<IdxT>(ctx, np, x);
+    if (x.xdesc != nullptr && env_int("AB2_NUMERIC", 3) == 5) {
+      launch_numeric5<IdxT>(ctx, np, x);
       return;
     }
   }

@@ -35,7 +35,7 @@ def test_run_fp64_bit_exact_across_budgets(frac):
     wp, wi, wv, macs = _oracle(g, x)
     ck = po.checksum(g.n_rows, x.n_cols, wp, wi, wv)
     a_b, c_b = _bytes(g, x, (wp, wi))
-    budget = ab.MemoryBudget(int(40e6 + frac * (a_b + c_b)))
+    budget = ab.MemoryBudget(int(3e6 + frac * (a_b + c_b)))
     res = ab.run_aires(g, x, budget)
     if frac < 1.0:
         assert res.report.segments >= 2
@@ -57,7 +57,7 @@ def test_run_fp32_tolerance_many_tiles(n_buffers):
     x32 = ab.CsrMatrix(x.n_rows, x.n_cols, x.row_ptr, x.col_idx.astype(np.uint32), x.values.astype(np.float32))
     a_b = 8 * (g.n_rows + 1) + 8 * g.nnz()
     c_b = 8 * (g.n_rows + 1) + 8 * wi.shape[0]
-    res = ab.run_aires(g32, x32, ab.MemoryBudget(int(30e6 + (a_b + c_b) / 8)), n_buffers=n_buffers,
+    res = ab.run_aires(g32, x32, ab.MemoryBudget(int(3e6 + (a_b + c_b) / 8)), n_buffers=n_buffers,
                        with_checksum=False)
     assert res.report.segments >= 8
     assert np.array_equal(res.c.row_ptr, wp) and np.array_equal(res.c.col_idx.astype(np.uint64), wi)
@@ -91,7 +91,7 @@ def test_run_a_only_tiling_fails_like_the_reference():
     wp, wi, wv, _ = _oracle(g, x)
     a_b, c_b = _bytes(g, x, (wp, wi))
     with pytest.raises(ab.AiresError) as e:
-        ab.run_aires(g, x, ab.MemoryBudget(int(40e6 + 0.25 * (a_b + c_b))), c_aware=False)
+        ab.run_aires(g, x, ab.MemoryBudget(int(3e6 + 0.25 * (a_b + c_b))), c_aware=False)
     assert e.value.code == ab.errc.insufficient_device_memory
 
 

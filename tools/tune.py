@@ -37,6 +37,7 @@ def main():
     for vals in itertools.product(*[v.split(",") for _, v in knobs]):
         for k, v in zip(names, vals):
             os.environ[k] = v
+        op = ab.Operand(x32)  # layout knobs are read when the operand is built
         ts = []
         for it in range(6):
             ab.spgemm_full(g32, op)
