@@ -279,6 +279,11 @@ def run_b200(args, cfg):
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         cpu = cpu_baseline(g, x, args.cpu_seconds)
+    ooc = None
+    if world == 1 and not args.skip_ooc:
+        tA.clear(); tX.clear(); outbuf.clear()
+        torch.cuda.empty_cache()
+        ooc = out_of_core_leg(args, dev, L, ab, torch)
 
     if rank == 0:
         line = {
@@ -292,12 +297,99 @@ def run_b200(args, cfg):
                        "parallelism": f"row-block shards x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (A 0.9 GB, C 1.1 GB vs 126 MB L2); X is meant to stay L2-resident",
                        "latency_ms": round(ms, 4)},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "out_of_core": ooc,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def link_bandwidth(dev, nbytes=512 << 20, reps=5):
+    """Pinned cudaMemcpy H2D / D2H GB/s (best of reps, CUDA events) -- the host-link roofline."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        best = 1e9
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        out[name] = nbytes / (best * 1e-3) / 1e9
+    del h, d
+    return out
+
+
+def out_of_core_leg(args, dev, L, ab, torch):
+    """cfg3 (ogbn-products-shaped) through aires_b200_run with the device budget capped to
+    args.ooc_frac of B_A + B_X + B_C: A and X in pinned host memory, C drained to pinned host
+    memory tile by tile.  Roofline = the host link (measured in this run)."""
+    cfg = CONFIGS["cfg3"]
+    g, st, x = make_inputs(cfg, 0, 1)
+    n, K = g.n_rows, x.n_rows
+    hA = [torch.from_numpy(g.row_ptr.view(np.int64)).pin_memory(), torch.from_numpy(g.col_idx.view(np.int32)).pin_memory(),
+          torch.from_numpy(g.values.astype(np.float32)).pin_memory()]
+    hX = [torch.from_numpy(x.row_ptr.view(np.int64)).pin_memory(), torch.from_numpy(x.col_idx.view(np.int32)).pin_memory(),
+          torch.from_numpy(x.values.astype(np.float32)).pin_memory()]
+    am = ab._Matrix(n, g.n_cols, ab.CSR, ab.HOST, 4, 4, hA[0].data_ptr(), hA[1].data_ptr(), hA[2].data_ptr(), g.nnz())
+    xm = ab._Matrix(K, x.n_cols, ab.CSR, ab.HOST, 4, 4, hX[0].data_ptr(), hX[1].data_ptr(), hX[2].data_ptr(), x.nnz())
+    hout = {}
+
+    def alloc(user, rows, nnz, pp, pi, pv):
+        if hout.get("cap", -1) < nnz:
+            hout["ptr"] = torch.empty(rows + 1, dtype=torch.int64).pin_memory()
+            hout["idx"] = torch.empty(max(nnz, 1), dtype=torch.int32).pin_memory()
+            hout["val"] = torch.empty(max(nnz, 1), dtype=torch.float32).pin_memory()
+            hout["cap"] = nnz
+        pp[0], pi[0], pv[0] = hout["ptr"].data_ptr(), hout["idx"].data_ptr(), hout["val"].data_ptr()
+        return 0
+
+    afn = ab._ALLOC_FN(alloc)
+    out = ab._Output(ab.HOST, 4, 4, 0, afn, None, 0, 0, 0, 0)
+    rep = ab._RunReport()
+    # size the budget from a first unconstrained run (C bytes are only known after it)
+    ab._check(L.aires_b200_run(C.byref(am), C.byref(xm), C.byref(ab._RunConfig(0, ab.MODE_FP32, 1, 2, 0)),
+                               C.byref(out), C.byref(rep)))
+    nnz_c, macs = int(out.nnz), int(out.flops)
+    b_a = 8 * (n + 1) + 8 * g.nnz()
+    b_x = 8 * (K + 1) + 8 * x.nnz()
+    b_c = 8 * (n + 1) + 8 * nnz_c
+    budget = int(args.ooc_frac * (b_a + b_x + b_c))
+    rc = ab._RunConfig(budget, ab.MODE_FP32, 1, args.ooc_buffers, 0)
+    for _ in range(max(1, args.warmup)):
+        ab._check(L.aires_b200_run(C.byref(am), C.byref(xm), C.byref(rc), C.byref(out), C.byref(rep)))
+    dev_ms, wall_ms, segs, launches = [], [], 0, 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ab._check(L.aires_b200_run(C.byref(am), C.byref(xm), C.byref(rc), C.byref(out), C.byref(rep)))
+        wall_ms.append((time.perf_counter() - t0) * 1e3)
+        dev_ms.append(rep.total_ms)
+        segs = int(rep.segments)
+        launches += L.aires_b200_last_launches()
+    h2d_b, d2h_b = int(rep.h2d_bytes), int(rep.d2h_bytes)
+    bw = link_bandwidth(dev)
+    ms = float(np.median(dev_ms))
+    t_roof = (b_a + b_x + b_c) / (bw["h2d"] * 1e9) * 1e3
+    t_duplex = max(h2d_b / (bw["h2d"] * 1e9), d2h_b / (bw["d2h"] * 1e9)) * 1e3
+    return {
+        "workload": cfg["workload"] + f", device budget {args.ooc_frac:.3g} x (B_A+B_X+B_C) = {budget / 1e6:.1f} MB",
+        "metric": "A·X latency (ms) and GFLOP/s, out-of-core", "ms": round(ms, 3),
+        "gflops": round(2.0 * macs / (ms * 1e-3) / 1e9, 3), "wall_ms": round(float(np.median(wall_ms)), 3),
+        "segments": segs, "n_buffers": args.ooc_buffers, "nnz_a": g.nnz(), "nnz_x": x.nnz(), "nnz_c": nnz_c,
+        "macs": macs, "h2d_bytes": h2d_b, "d2h_bytes": d2h_b, "gpu_launches_per_run": launches // args.steps,
+        "phase_ms": {"phase1": round(rep.phase1_ms, 3), "phase2": round(rep.phase2_ms, 3),
+                     "phase3": round(rep.phase3_ms, 3)},
+        "roofline": {"bound": "host-link", "achieved": round((b_a + b_x + b_c) / (ms * 1e-3) / 1e9, 2),
+                     "peak": round(bw["h2d"], 2), "unit": "GB/s", "frac": round(t_roof / ms, 4),
+                     "frac_full_duplex": round(t_duplex / ms, 4), "link_gbs": {k: round(v, 2) for k, v in bw.items()},
+                     "basis": "(B_A+B_X+B_C) / measured pinned H2D GB/s; full duplex: max(H2D bytes/H2D, D2H bytes/D2H)"},
+        "storage": "pinned host memory (GPUDirect Storage not used: operands arrive through the host API)",
+    }
 
 
 def sample_rows(n: int, count: int, seed: int = 11) -> np.ndarray:
@@ -385,6 +477,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-ooc", action="store_true", help="skip the cfg3 out-of-core leg")
+    ap.add_argument("--ooc-frac", type=float, default=0.25, help="cfg3 device budget / (B_A+B_X+B_C)")
+    ap.add_argument("--ooc-buffers", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]

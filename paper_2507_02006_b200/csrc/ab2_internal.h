@@ -80,7 +80,7 @@ struct XOperand {
   int64_t dummy_slot = 0;  // fp32: index of the all-trash slot
   double xmin = 0.0;       // smallest nonzero |x|
   bool has_zero = false;   // X stores an exact zero
-  size_t bytes = 0;
+  size_t bytes = 0;        // device bytes of every layout built
   int prep_launches = 0;
   bool owned = true;  // kernels launched to build the operand
   ~XOperand();
@@ -88,7 +88,15 @@ struct XOperand {
 
 // Builds an operand from a matrix view (host or device, CSR or CSC).
 // temp: storage comes from the context (valid until the next product on this thread).
-std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode, bool temp);
+// Which device layouts of X to build (the plain CSR is always built).
+enum OperandPlan : uint32_t {
+  kPlanSlots = 1,   // W-slot groups (k_numeric3)
+  kPlanCSlots = 2,  // 16-wide column-only slots (symbolic pass over slots)
+  kPlanStep = 4,    // padded step-list slots (k_numeric5, fp32 only)
+  kPlanAuto = 0     // the in-core default for the mode (AB2_NUMERIC selects the fp32 kernel)
+};
+std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode, bool temp,
+                                       uint32_t plan = kPlanAuto);
 
 // C = A * X; A is a CSR rows view (host or device).
 void spgemm_rows(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_b200_output& out);

@@ -205,6 +205,33 @@ __device__ __forceinline__ uint32_t sym_walk(const SymArgs& p, const IdxT* __res
   return f;
 }
 
+// Lane-per-A-entry over the plain CSR of X (W == 0): each lane marks its X row's columns.  Used
+// by the out-of-core sizing pass, whose operand carries no column slots (short X rows, e.g. the
+// ogbn-products shape with ~1 entry per row, make 32-byte slots mostly padding).
+template <class IdxT>
+__device__ __forceinline__ uint32_t sym_walk_plain(const SymArgs& p, const IdxT* __restrict__ ac, uint32_t n,
+                                                   uint32_t first, uint32_t stride, unsigned char* flags) {
+  const uint64_t K = static_cast<uint64_t>(p.K);
+  uint32_t f = 0;
+  for (uint32_t i = first; i < n; i += stride) {
+    const uint64_t k = static_cast<uint64_t>(ac[i]);
+    if (k >= K) continue;
+    const int64_t s = p.xptr[k], e = p.xptr[k + 1];
+    f += static_cast<uint32_t>(e - s);
+    for (int64_t t = s; t < e; t++) flags[p.xcol[t]] = 1;
+  }
+  return f;
+}
+
+template <class IdxT, int W>
+__device__ __forceinline__ uint32_t sym_any(const SymArgs& p, const IdxT* __restrict__ ac, uint32_t n, uint32_t first,
+                                            uint32_t stride, unsigned char* flags) {
+  if constexpr (W == 0)
+    return sym_walk_plain<IdxT>(p, ac, n, first, stride, flags);
+  else
+    return sym_walk<IdxT, W>(p, ac, n, first, stride, flags);
+}
+
 template <class IdxT, int W>
 __global__ void __launch_bounds__(256) k_symbolic(SymArgs p, const IdxT* __restrict__ acol) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -226,7 +253,7 @@ __global__ void __launch_bounds__(256) k_symbolic(SymArgs p, const IdxT* __restr
     if (h >= n_heavy) break;
     const int64_t r = p.sym_heavy[h];
     const uint64_t s = p.aptr[r] - p.abase, e = p.aptr[r + 1] - p.abase;
-    int64_t f = sym_walk<IdxT, W>(p, acol + s, static_cast<uint32_t>(e - s), threadIdx.x, blockDim.x, smem);
+    int64_t f = sym_any<IdxT, W>(p, acol + s, static_cast<uint32_t>(e - s), threadIdx.x, blockDim.x, smem);
     __syncthreads();
     int64_t c = count_flags(reinterpret_cast<uint32_t*>(smem), words, threadIdx.x, blockDim.x);
     c = block_sum<int64_t>(c, s_red);
@@ -251,7 +278,7 @@ __global__ void __launch_bounds__(256) k_symbolic(SymArgs p, const IdxT* __restr
     for (int64_t r = static_cast<int64_t>(r0); r < r1; r++) {
       const uint64_t s = p.aptr[r] - p.abase, e = p.aptr[r + 1] - p.abase;
       if (static_cast<int64_t>(e - s) > p.heavy_deg) continue;
-      uint32_t f = sym_walk<IdxT, W>(p, acol + s, static_cast<uint32_t>(e - s), lane, 32, flags);
+      uint32_t f = sym_any<IdxT, W>(p, acol + s, static_cast<uint32_t>(e - s), lane, 32, flags);
       __syncwarp();
       int c = count_flags(reinterpret_cast<uint32_t*>(flags), words, lane, 32);
       c = warp_sum(c);

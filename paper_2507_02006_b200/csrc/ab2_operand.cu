@@ -248,13 +248,13 @@ void build_slots(Ctx& ctx, XOperand& x) {
   auto* xc = static_cast<int32_t*>(x.col);
   auto* xv = static_cast<V*>(x.val);
   const uint32_t trash = static_cast<uint32_t>(x.n_cols);
-  switch (x.W) {
+  if (x.slots) switch (x.W) {
     case 2: k_x_slots<V, 2><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, trash, sl, static_cast<uint16_t*>(x.xlen)); break;
     case 4: k_x_slots<V, 4><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, trash, sl, static_cast<uint16_t*>(x.xlen)); break;
     case 8: k_x_slots<V, 8><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, trash, sl, static_cast<uint16_t*>(x.xlen)); break;
     default: k_x_slots<V, 16><<<g, 256, 0, ctx.stream>>>(xp, xc, xv, x.K, trash, sl, static_cast<uint16_t*>(x.xlen)); break;
   }
-  k_x_cslots<<<g, 256, 0, ctx.stream>>>(xp, xc, x.K, cs);
+  if (x.cslots) k_x_cslots<<<g, 256, 0, ctx.stream>>>(xp, xc, x.K, cs);
   AB2_CUDA(cudaGetLastError());
 }
 
@@ -339,7 +339,7 @@ XOperand::~XOperand() {
   if (prev != device && prev >= 0) cudaSetDevice(prev);
 }
 
-std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode, bool temp) {
+std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode, bool temp, uint32_t plan) {
   if (b.layout != AIRES_B200_CSR && b.layout != AIRES_B200_CSC)
     fail(AIRES_B200_INVALID_ARGUMENT, "operand layout must be CSR or CSC");
   if ((b.idx_bytes != 4 && b.idx_bytes != 8) || (b.val_bytes != 4 && b.val_bytes != 8))
@@ -387,6 +387,7 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
     dptr = up;
     didx = ui;
     dval = uv;
+    x->bytes += nptr * 8 + std::max<uint64_t>(p1, 1) * (b.idx_bytes + b.val_bytes);  // raw upload
   } else if (b.layout == AIRES_B200_CSC) {
     AB2_CUDA(cudaMemcpyAsync(&p0, b.ptr, 8, cudaMemcpyDeviceToHost, ctx.stream));
     AB2_CUDA(cudaMemcpyAsync(&p1, b.ptr + nptr - 1, 8, cudaMemcpyDeviceToHost, ctx.stream));
@@ -399,8 +400,14 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
   Ctl* ctl = ctx.ctl.as<Ctl>(1);
   AB2_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx.stream));
   const size_t vb = mode == AIRES_B200_MODE_FP32 ? 4 : 8;
+  if (plan == kPlanAuto)
+    plan = mode == AIRES_B200_MODE_FP32 && env_int("AB2_NUMERIC", 3) == 5 ? kPlanStep : kPlanSlots;
+  if (mode != AIRES_B200_MODE_FP32) plan &= ~static_cast<uint32_t>(kPlanStep);
   auto alloc = [&](DevBuf& cache, size_t bytes) -> void* {
-    if (temp) return cache.get(bytes);
+    if (temp) {
+      x->bytes += std::max<size_t>(bytes, 256);
+      return cache.get(bytes);
+    }
     return dmalloc(bytes, &x->bytes);
   };
   x->ptr = alloc(ctx.xo_ptr, (x->K + 1) * 8);
@@ -456,17 +463,21 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
   int64_t forced = env_int("AB2_SLOT_W", 0);
   if (forced == 2 || forced == 4 || forced == 8 || forced == 16) W = static_cast<int>(forced);
   x->W = W;
-  const size_t sb = mode == AIRES_B200_MODE_FP32 ? sizeof(SlotF) : sizeof(SlotD);
-  x->slots = alloc(ctx.xo_slots, (x->K + 1) * W * sb);
-  x->cslots = alloc(ctx.xo_cslots, std::max<int64_t>(x->K, 1) * kCSlotW * 2);
-  x->xlen = alloc(ctx.xo_len, (x->K + 1) * 2);
-  {
-    if (mode == AIRES_B200_MODE_FP32)
-      build_slots<float>(ctx, *x);
-    else
-      build_slots<double>(ctx, *x);
+  if (plan & kPlanSlots) {
+    const size_t sb = mode == AIRES_B200_MODE_FP32 ? sizeof(SlotF) : sizeof(SlotD);
+    x->slots = alloc(ctx.xo_slots, (x->K + 1) * W * sb);
+    x->xlen = alloc(ctx.xo_len, (x->K + 1) * 2);
+    x->prep_launches += 1;
   }
-  if (mode == AIRES_B200_MODE_FP32) {
+  if (plan & kPlanCSlots) {
+    x->cslots = alloc(ctx.xo_cslots, std::max<int64_t>(x->K, 1) * kCSlotW * 2);
+    x->prep_launches += 1;
+  }
+  if (mode == AIRES_B200_MODE_FP32)
+    build_slots<float>(ctx, *x);
+  else
+    build_slots<double>(ctx, *x);
+  if (plan & kPlanStep) {
     // step-list layout: W5 ~ the mean row length, copies = 32 / W5 accumulators per warp
     const double mean = static_cast<double>(x->nnz) / K;
     int w5 = mean >= 4.0 ? 8 : (mean >= 2.0 ? 4 : 2);
@@ -495,8 +506,9 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
                                            static_cast<uint32_t>(x->n_cols), ps, static_cast<uint2*>(x->xdesc),
                                            static_cast<uint2*>(x->xent), x->dummy_slot);
     AB2_CUDA(cudaGetLastError());
+    x->prep_launches += x->K > 0 ? 5 : 2;
   }
-  x->prep_launches = (b.layout == AIRES_B200_CSR ? 1 : 6) + 4 + (mode == AIRES_B200_MODE_FP32 ? (x->K > 0 ? 5 : 2) : 0);
+  x->prep_launches += (b.layout == AIRES_B200_CSR ? 1 : 6) + 2;
   if (!temp) AB2_CUDA(cudaStreamSynchronize(ctx.stream));
   return x;
 }

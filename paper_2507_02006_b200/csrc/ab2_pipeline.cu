@@ -179,10 +179,10 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   // ---------------- Phase I ----------------
   AB2_CUDA(cudaEventRecord(t_begin, cs));
   AB2_CUDA(cudaStreamWaitEvent(st.h2d, t_begin, 0));
-  auto x = make_operand(ctx, b, mode, /*temp=*/true);  // H2D of X + layout build on cs
-  uint64_t x_bytes = (static_cast<uint64_t>(x->K) + 1) * 8 + static_cast<uint64_t>(x->nnz) * (4 + vb);
-  uint64_t x_dev = x_bytes + (static_cast<uint64_t>(x->K) + 1) * (x->W * (vb == 4 ? 8 : 16) + 2) +
-                   static_cast<uint64_t>(x->K) * 32 + (vb == 4 ? (x->K + 1) * 8 + x->nnz * 8 : 0);
+  // lean operand: the step-list layout (fp32) or W-slots (fp64-exact) plus the plain CSR, which
+  // the sizing pass reads directly
+  auto x = make_operand(ctx, b, mode, /*temp=*/true, mode == AIRES_B200_MODE_FP32 ? kPlanStep : kPlanSlots);
+  const uint64_t x_dev = x->bytes;
   rep.h2d_bytes += b.location == AIRES_B200_HOST ? (b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols) * 8 + 8 +
                                                        static_cast<uint64_t>(x->nnz) * (b.idx_bytes + b.val_bytes)
                                                  : 0;

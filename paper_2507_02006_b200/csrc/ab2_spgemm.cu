@@ -175,7 +175,7 @@ Num3Args<V, IdxT> make_num3(const XOperand& x, const uint64_t* aptr, uint64_t ab
 template <class V, class IdxT>
 void launch_product(Ctx& ctx, const Num3Args<V, IdxT>& np, const XOperand& x) {
   if constexpr (std::is_same<V, float>::value) {
-    if (x.xdesc != nullptr && env_int("AB2_NUMERIC", 3) == 5) {
+    if (x.xdesc != nullptr && (x.slots == nullptr || env_int("AB2_NUMERIC", 3) == 5)) {
       launch_numeric5<IdxT>(ctx, np, x);
       return;
     }
@@ -336,7 +336,7 @@ int tile_symbolic_t(Ctx& ctx, const XOperand& x, const TileSym& t) {
   sp.num_heavy = t.heavy;  // unused: heavy_flops is never exceeded
   sp.heavy_flops = INT64_MAX;
   sp.ctl = t.ctl;
-  auto k = k_symbolic<IdxT, kCSlotW>;
+  auto k = x.cslots ? k_symbolic<IdxT, kCSlotW> : k_symbolic<IdxT, 0>;
   const size_t smem = 8 * static_cast<size_t>(sp.region_bytes);
   const int grid = occupancy_grid(k, 256, smem, ctx.sms);
   k<<<grid, 256, smem, ctx.stream>>>(sp, static_cast<const IdxT*>(t.acol));
