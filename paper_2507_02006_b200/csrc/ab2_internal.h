@@ -77,6 +77,7 @@ struct XOperand {
   void* xdesc = nullptr;   // fp32: K+1 uint2 {slot start, nslot | len << 16} (row K empty)
   void* xent = nullptr;    // fp32: padded W5-entry slots of uint2 {col, value bits}
   int W5 = 0;              // fp32 step-list slot width
+  bool wide = false;       // n_cols beyond the dense accumulator: plain CSR only, column-tiled product
   int64_t dummy_slot = 0;  // fp32: index of the all-trash slot
   double xmin = 0.0;       // smallest nonzero |x|
   bool has_zero = false;   // X stores an exact zero
@@ -95,6 +96,8 @@ enum OperandPlan : uint32_t {
   kPlanStep = 4,    // padded step-list slots (k_numeric5, fp32 only)
   kPlanAuto = 0     // the in-core default for the mode (AB2_NUMERIC selects the fp32 kernel)
 };
+// Widest X handled by the dense accumulator (wider operands run in column tiles).
+int64_t wide_threshold(uint32_t mode);
 std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode, bool temp,
                                        uint32_t plan = kPlanAuto);
 

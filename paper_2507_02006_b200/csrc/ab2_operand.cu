@@ -339,6 +339,11 @@ XOperand::~XOperand() {
   if (prev != device && prev >= 0) cudaSetDevice(prev);
 }
 
+int64_t wide_threshold(uint32_t mode) {
+  const int64_t dense_max = mode == AIRES_B200_MODE_FP32 ? kMaxDenseColsF32 : kMaxDenseColsF64;
+  return std::max<int64_t>(32, std::min<int64_t>(dense_max, env_int("AB2_WIDE_AT", dense_max)));
+}
+
 std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode, bool temp, uint32_t plan) {
   if (b.layout != AIRES_B200_CSR && b.layout != AIRES_B200_CSC)
     fail(AIRES_B200_INVALID_ARGUMENT, "operand layout must be CSR or CSC");
@@ -354,11 +359,12 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
   x->K = static_cast<int64_t>(b.n_rows);
   x->n_cols = static_cast<int64_t>(b.n_cols);
   const uint64_t nptr = (b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols) + 1;
-  const int64_t dense_max = mode == AIRES_B200_MODE_FP32 ? kMaxDenseColsF32 : kMaxDenseColsF64;
-  if (x->n_cols > dense_max)
-    fail(AIRES_B200_UNSUPPORTED_FORMAT,
-         "feature matrix has " + std::to_string(x->n_cols) + " columns; the dense-accumulator path supports " +
-             std::to_string(dense_max));
+  const int64_t dense_max = wide_threshold(mode);
+  // wide X: only the plain CSR is built; the product runs in column tiles (wide_product)
+  x->wide = x->n_cols > dense_max;
+  if (x->wide && (plan & (kPlanStep | kPlanCSlots)))
+    fail(AIRES_B200_UNSUPPORTED_FORMAT, "feature matrix has " + std::to_string(x->n_cols) +
+                                            " columns; the out-of-core path supports " + std::to_string(dense_max));
   if (b.ptr == nullptr) fail(AIRES_B200_INVALID_ARGUMENT, "operand ptr is null");
   if (b.span >= (uint64_t(1) << 31)) fail(AIRES_B200_CAPACITY_EXCEEDED, "operand span exceeds 2^31 entries");
 
@@ -463,6 +469,7 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
   int64_t forced = env_int("AB2_SLOT_W", 0);
   if (forced == 2 || forced == 4 || forced == 8 || forced == 16) W = static_cast<int>(forced);
   x->W = W;
+  if (x->wide) plan = 0;
   if (plan & kPlanSlots) {
     const size_t sb = mode == AIRES_B200_MODE_FP32 ? sizeof(SlotF) : sizeof(SlotD);
     x->slots = alloc(ctx.xo_slots, (x->K + 1) * W * sb);

@@ -343,6 +343,206 @@ int tile_symbolic_t(Ctx& ctx, const XOperand& x, const TileSym& t) {
   AB2_CUDA(cudaGetLastError());
   return 2;
 }
+// ---------------------------------------------------------------------------
+// Wide operands (n_cols(X) beyond the dense shared-memory accumulator): C is computed in column
+// tiles of X -- the reference's own B column tiling (spgemm.hpp:94-130, tile_cols), which never
+// changes a cell's terms or their ascending-k order -- each tile through the regular product
+// pass into its own staging area; the tiles' row counts are summed, scanned, and every tile is
+// placed at row offset cptr[r] + (entries of earlier tiles in row r), so each row comes out in
+// ascending column order.
+// ---------------------------------------------------------------------------
+template <class V>
+__global__ void k_tile_count(const int64_t* __restrict__ xptr, const int32_t* __restrict__ xcol, int64_t K,
+                             int32_t c0, int32_t c1, int32_t* __restrict__ cnt) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t n = 0;
+    for (int64_t t = xptr[k]; t < xptr[k + 1]; t++) n += xcol[t] >= c0 && xcol[t] < c1;
+    cnt[k] = static_cast<int32_t>(n);
+  }
+}
+
+template <class V>
+__global__ void k_tile_fill(const int64_t* __restrict__ xptr, const int32_t* __restrict__ xcol,
+                            const V* __restrict__ xval, int64_t K, int32_t c0, int32_t c1,
+                            const int64_t* __restrict__ tptr, uint32_t* __restrict__ tcol, V* __restrict__ tval) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < K;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t o = tptr[k];
+    for (int64_t t = xptr[k]; t < xptr[k + 1]; t++)
+      if (xcol[t] >= c0 && xcol[t] < c1) {
+        tcol[o] = static_cast<uint32_t>(xcol[t] - c0);
+        tval[o] = xval[t];
+        o++;
+      }
+  }
+}
+
+__global__ void k_add_counts(uint32_t* __restrict__ acc, const uint32_t* __restrict__ add, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    acc[i] += add[i];
+}
+
+template <class V, class IdxT>
+__global__ void __launch_bounds__(256) k_place_tile(const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ toff,
+                                                    const int64_t* __restrict__ cptr, uint32_t* __restrict__ roff,
+                                                    const IdxT* __restrict__ tcol, const V* __restrict__ tval,
+                                                    int64_t rows, IdxT col0, IdxT* __restrict__ ccol,
+                                                    V* __restrict__ cval) {
+  const int lane = lane_id();
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = wid; r < rows; r += nwarps) {
+    const uint32_t n = cnt[r];
+    const uint64_t src = toff[r];
+    const int64_t dst = cptr[r] + roff[r];
+    for (uint32_t i = lane; i < n; i += 32) {
+      ccol[dst + i] = tcol[src + i] + col0;
+      cval[dst + i] = tval[src + i];
+    }
+    __syncwarp();
+    if (lane == 0) roff[r] += n;
+  }
+}
+
+template <class V, class IdxT>
+void wide_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_b200_output& out,
+                  const uint64_t* aptr, uint64_t abase, const IdxT* acol, const V* aval, uint64_t span_hint) {
+  const int64_t rows = static_cast<int64_t>(a.n_rows);
+  const int64_t n_cols = x.n_cols;
+  const int64_t tw = std::min<int64_t>(wide_threshold(x.mode), std::max<int64_t>(32, env_int("AB2_WIDE_TILE", 2048)));
+  const int64_t T = (n_cols + tw - 1) / tw;
+  const int64_t K = x.K;
+  const uint32_t mode = x.mode;
+  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 4096);
+  int64_t* heavy = ctx.sym_heavy.as<int64_t>(std::max<int64_t>(rows, 1));
+  struct Tile {
+    DevBuf ptr, col, val, cnt, toff, tcol, tval;
+    int64_t c0 = 0;
+  };
+  std::vector<Tile> tiles(T);
+  DevBuf ctl_buf, cnt_sum, roff;
+  Ctl* ctls = static_cast<Ctl*>(ctl_buf.get(sizeof(Ctl) * (T + 1)));
+  AB2_CUDA(cudaMemsetAsync(ctls, 0, sizeof(Ctl) * (T + 1), ctx.stream));
+  const auto* xp = static_cast<const int64_t*>(x.ptr);
+  const auto* xc = static_cast<const int32_t*>(x.col);
+  const auto* xv = static_cast<const V*>(x.val);
+  const int gK = static_cast<int>(std::min<int64_t>((K + 255) / 256 + 1, static_cast<int64_t>(ctx.sms) * 32));
+  const int64_t nbK = (K + kScanTile - 1) / kScanTile;
+  int64_t* partK = ctx.scan_part.as<int64_t>(std::max<int64_t>(nbK, 1) + 1);
+  for (int64_t t = 0; t < T; t++) {
+    Tile& tl = tiles[t];
+    tl.c0 = t * tw;
+    const int32_t c0 = static_cast<int32_t>(tl.c0), c1 = static_cast<int32_t>(std::min(n_cols, tl.c0 + tw));
+    // one buffer: X-row counts of the tile first, then the product's C row counts
+    int32_t* kc = static_cast<int32_t*>(tl.cnt.get(std::max<int64_t>(std::max<int64_t>(rows, K), 1) * 4));
+    int64_t* tp = static_cast<int64_t*>(tl.ptr.get((K + 1) * 8));
+    k_tile_count<V><<<gK, 256, 0, ctx.stream>>>(xp, xc, K, c0, c1, kc);
+    if (K > 0) {
+      k_scan_reduce<<<static_cast<unsigned>(nbK), kScanThreads, 0, ctx.stream>>>(kc, K, partK);
+      k_scan_part<<<1, 1024, 0, ctx.stream>>>(partK, nbK, ctls + T);
+      k_scan_down<<<static_cast<unsigned>(nbK), kScanThreads, 0, ctx.stream>>>(kc, K, partK, tp);
+    } else {
+      AB2_CUDA(cudaMemsetAsync(tp, 0, 8, ctx.stream));
+    }
+    auto* tc = static_cast<uint32_t*>(tl.col.get(std::max<int64_t>(x.nnz, 1) * 4));
+    auto* tv = static_cast<V*>(tl.val.get(std::max<int64_t>(x.nnz, 1) * sizeof(V)));
+    k_tile_fill<V><<<gK, 256, 0, ctx.stream>>>(xp, xc, xv, K, c0, c1, tp, tc, tv);
+    AB2_CUDA(cudaGetLastError());
+    aires_b200_matrix tv_m{};
+    tv_m.n_rows = static_cast<uint64_t>(K);
+    tv_m.n_cols = static_cast<uint64_t>(c1 - c0);
+    tv_m.layout = AIRES_B200_CSR;
+    tv_m.location = AIRES_B200_DEVICE;
+    tv_m.idx_bytes = 4;
+    tv_m.val_bytes = sizeof(V);
+    tv_m.ptr = reinterpret_cast<const uint64_t*>(tp);
+    tv_m.idx = tc;
+    tv_m.val = tv;
+    tv_m.span = static_cast<uint64_t>(std::max<int64_t>(x.nnz, 1));
+    auto xt = make_operand(ctx, tv_m, mode, /*temp=*/false, kPlanSlots);
+    ctx.launches += xt->prep_launches + 6;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(kc);
+    uint64_t* toff = static_cast<uint64_t*>(tl.toff.get(std::max<int64_t>(rows, 1) * 8));
+    Num3Args<V, IdxT> np =
+        make_num3<V, IdxT>(*xt, aptr, abase, acol, aval, rows, heavy, heavy_deg, cnt, toff, ctls + t);
+    const uint64_t maxlen = std::max<int64_t>(xt->max_row_len, 1);
+    const uint64_t bound = std::min<uint64_t>(static_cast<uint64_t>(rows) * (c1 - c0), span_hint * maxlen);
+    np.t_cap = bound + bound / 7 + (static_cast<uint64_t>(ctx.sms) * 64 + 1) * np.stage_block;
+    np.tcol = static_cast<IdxT*>(tl.tcol.get(np.t_cap * sizeof(IdxT)));
+    np.tval = static_cast<V*>(tl.tval.get(np.t_cap * sizeof(V)));
+    if (rows > 0) {
+      const int g = static_cast<int>(std::min<int64_t>((rows + 255) / 256, static_cast<int64_t>(ctx.sms) * 16));
+      k_classify<<<g, 256, 0, ctx.stream>>>(aptr, rows, heavy_deg, heavy, ctls + t);
+      launch_product<V, IdxT>(ctx, np, *xt);
+    }
+    AB2_CUDA(cudaStreamSynchronize(ctx.stream));  // xt is freed at scope exit
+  }
+  // row counts -> row_ptr
+  uint32_t* csum = static_cast<uint32_t*>(cnt_sum.get(std::max<int64_t>(rows, 1) * 4));
+  uint32_t* ro = static_cast<uint32_t*>(roff.get(std::max<int64_t>(rows, 1) * 4));
+  AB2_CUDA(cudaMemsetAsync(csum, 0, std::max<int64_t>(rows, 1) * 4, ctx.stream));
+  AB2_CUDA(cudaMemsetAsync(ro, 0, std::max<int64_t>(rows, 1) * 4, ctx.stream));
+  const int gR = static_cast<int>(std::min<int64_t>((rows + 255) / 256 + 1, static_cast<int64_t>(ctx.sms) * 32));
+  for (int64_t t = 0; t < T && rows > 0; t++)
+    k_add_counts<<<gR, 256, 0, ctx.stream>>>(csum, static_cast<uint32_t*>(tiles[t].cnt.p), rows);
+  int64_t* cptr = ctx.cptr.as<int64_t>(rows + 1);
+  const int64_t nb = (rows + kScanTile - 1) / kScanTile;
+  int64_t* part = ctx.scan_part.as<int64_t>(std::max<int64_t>(nb, 1));
+  if (rows > 0) {
+    const int32_t* cin = reinterpret_cast<const int32_t*>(csum);
+    k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(cin, rows, part);
+    k_scan_part<<<1, 1024, 0, ctx.stream>>>(part, nb, ctls + T);
+    k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(cin, rows, part, cptr);
+  } else {
+    AB2_CUDA(cudaMemsetAsync(cptr, 0, 8, ctx.stream));
+  }
+  AB2_CUDA(cudaGetLastError());
+  std::vector<Ctl> h(T + 1);
+  AB2_CUDA(cudaMemcpyAsync(h.data(), ctls, sizeof(Ctl) * (T + 1), cudaMemcpyDeviceToHost, ctx.stream));
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  uint64_t flops = 0;
+  for (int64_t t = 0; t < T; t++) {
+    if (h[t].bad_row) fail(AIRES_B200_CAPACITY_EXCEEDED, "staging area overflow");
+    flops += h[t].flops;
+  }
+  const uint64_t nnz = rows > 0 ? h[T].nnz : 0;
+  void *optr = nullptr, *oidx = nullptr, *oval = nullptr;
+  int rc = out.alloc(out.user, static_cast<uint64_t>(rows), nnz, &optr, &oidx, &oval);
+  if (rc != 0) fail(rc, "output allocator failed for " + std::to_string(nnz) + " nonzeros");
+  IdxT* ccol;
+  V* cval;
+  if (out.location == AIRES_B200_DEVICE) {
+    ccol = static_cast<IdxT*>(oidx);
+    cval = static_cast<V*>(oval);
+  } else {
+    ccol = ctx.c_col.as<IdxT>(std::max<uint64_t>(nnz, 1));
+    cval = ctx.c_val.as<V>(std::max<uint64_t>(nnz, 1));
+  }
+  for (int64_t t = 0; t < T && rows > 0 && nnz > 0; t++)
+    k_place_tile<V, IdxT><<<ctx.sms * 8, 256, 0, ctx.stream>>>(
+        static_cast<const uint32_t*>(tiles[t].cnt.p), static_cast<const uint64_t*>(tiles[t].toff.p), cptr, ro,
+        static_cast<const IdxT*>(tiles[t].tcol.p), static_cast<const V*>(tiles[t].tval.p), rows,
+        static_cast<IdxT>(tiles[t].c0), ccol, cval);
+  AB2_CUDA(cudaGetLastError());
+  if (out.location == AIRES_B200_DEVICE) {
+    AB2_CUDA(cudaMemcpyAsync(optr, cptr, (rows + 1) * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+  } else {
+    AB2_CUDA(cudaMemcpyAsync(optr, cptr, (rows + 1) * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    if (nnz) {
+      AB2_CUDA(cudaMemcpyAsync(oidx, ccol, nnz * sizeof(IdxT), cudaMemcpyDeviceToHost, ctx.stream));
+      AB2_CUDA(cudaMemcpyAsync(oval, cval, nnz * sizeof(V), cudaMemcpyDeviceToHost, ctx.stream));
+    }
+  }
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  ctx.launches += static_cast<int>(2 * T + 3);
+  out.n_rows = static_cast<uint64_t>(rows);
+  out.n_cols = static_cast<uint64_t>(n_cols);
+  out.nnz = nnz;
+  out.flops = flops;
+}
+
 }  // namespace
 
 int tile_product(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TilePass& t) {
@@ -427,7 +627,20 @@ void spgemm_rows(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_
     aval = v2;
   }
   const uint64_t span_hint = a.location == AIRES_B200_HOST || p1 > p0 ? p1 - p0 : a.span;
-  if (out.idx_bytes == 4 && vsize == 4)
+  if (x.wide) {
+    if (out.idx_bytes == 4 && vsize == 4)
+      wide_product<float, uint32_t>(ctx, a, x, out, aptr, abase, static_cast<const uint32_t*>(acol),
+                                    static_cast<const float*>(aval), span_hint);
+    else if (out.idx_bytes == 4)
+      wide_product<double, uint32_t>(ctx, a, x, out, aptr, abase, static_cast<const uint32_t*>(acol),
+                                     static_cast<const double*>(aval), span_hint);
+    else if (vsize == 4)
+      wide_product<float, uint64_t>(ctx, a, x, out, aptr, abase, static_cast<const uint64_t*>(acol),
+                                    static_cast<const float*>(aval), span_hint);
+    else
+      wide_product<double, uint64_t>(ctx, a, x, out, aptr, abase, static_cast<const uint64_t*>(acol),
+                                     static_cast<const double*>(aval), span_hint);
+  } else if (out.idx_bytes == 4 && vsize == 4)
     run_product<float, uint32_t>(ctx, a, x, out, aptr, abase, static_cast<const uint32_t*>(acol),
                              static_cast<const float*>(aval), span_hint);
   else if (out.idx_bytes == 4)

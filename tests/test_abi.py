@@ -85,3 +85,14 @@ def test_library_checksum_matches_reference_goldens():
         assert ab.checksum(m) == ck
         m32 = ab.CsrMatrix(nr, nc, g[f"c{c}_c_ptr"], g[f"c{c}_c_idx"].astype(np.uint32), g[f"c{c}_c_val"])
         assert ab.checksum(m32) == ck
+
+
+def test_dropin_binaries_fail_loudly_without_a_device():
+    """The reference's spgemm_test built on the drop-in headers aborts (no CPU fallback) when no
+    CUDA device is visible."""
+    import subprocess
+    exe = os.path.join(ROOT, "oracle", "_ref", "dropin_spgemm_test")
+    if not os.path.exists(exe) or ab.device_count() > 0:
+        pytest.skip("drop-in binary absent or a device is visible")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0 and "no CUDA device" in (r.stdout + r.stderr)

@@ -224,3 +224,28 @@ def test_power_law_cfg1_shape(mode):
         assert_close_fp32(c.values, wv, wv)  # all terms positive: scale == value
     blk = ab.spgemm_block(g.row_ptr, g.col_idx, g.values, g.n_rows, g.n_cols, x)
     assert blk.flops == macs
+
+
+@pytest.mark.parametrize("mode", [ab.MODE_FP64_EXACT, ab.MODE_FP32])
+def test_wide_operand_column_tiles(mode, monkeypatch):
+    """X wider than the dense accumulator: the product runs in column tiles of X (the reference's
+    B column tiling, spgemm.hpp:94-130) and must still match bit for bit (fp64) / 1e-5 (fp32)."""
+    rng = np.random.default_rng(31)
+    for nc, tile in ((12000, "2048"), (300, "64"), (97, "32")):
+        monkeypatch.setenv("AB2_WIDE_TILE", tile)
+        if nc < 4096:
+            monkeypatch.setenv("AB2_WIDE_AT", "64")
+        a = random_csr(rng, 40, 50, 0.2)
+        b = random_csr(rng, 50, nc, min(0.5, 30.0 / nc + 0.02))
+        (wp, wi, wv), macs = oracle_product(40, 50, nc, a, b, inner=False)
+        if mode == ab.MODE_FP64_EXACT:
+            blk = ab.spgemm_block(a[0], a[1], a[2], 40, 50, csc_of(50, nc, *b))
+            assert_structure_equal(blk.fragment.row_ptr, blk.fragment.col_idx, wp, wi)
+            assert bits_equal(blk.fragment.values, wv) and blk.flops == macs
+        else:
+            c = ab.spgemm_full(csr(40, 50, a[0], a[1], a[2].astype(np.float32)),
+                               csr(50, nc, b[0], b[1], b[2].astype(np.float32)))
+            (_, _, sv), _ = oracle_product(40, 50, nc, (a[0], a[1], np.abs(a[2])), (b[0], b[1], np.abs(b[2])),
+                                           inner=False)
+            assert_structure_equal(c.row_ptr, c.col_idx, wp, wi)
+            assert_close_fp32(c.values, wv, sv)
