@@ -69,8 +69,8 @@ void launch_numeric(Ctx& ctx, const Num3Args<V, IdxT>& p, int W, bool xz) {
 // k_numeric3 args.
 template <class IdxT, int W>
 void launch_numeric5_w(Ctx& ctx, const Num5Args<IdxT>& p, bool xz) {
-  int nw = static_cast<int>(env_int("AB2_N5_WARPS", 8));
-  nw = std::max(1, std::min<int>(nw, static_cast<int>((200 * 1024) / p.warp_bytes)));
+  int nw = static_cast<int>(env_int("AB2_N5_WARPS", AB2_N5_MAXT / 32));
+  nw = std::max(1, std::min<int>({nw, AB2_N5_MAXT / 32, static_cast<int>((200 * 1024) / p.warp_bytes)}));
   const int threads = nw * 32;
   const size_t smem = static_cast<size_t>(nw) * p.warp_bytes;
   auto k = xz ? k_numeric5<IdxT, W, true> : k_numeric5<IdxT, W, false>;
