@@ -37,7 +37,7 @@
 #define AB2_NUM_BATCH 8
 #endif
 #ifndef AB2_NUM_MINB
-#define AB2_NUM_MINB 3
+#define AB2_NUM_MINB 4
 #endif
 
 #include "ab2_kernels.cuh"
@@ -168,17 +168,33 @@ __device__ __forceinline__ uint32_t walk_entries(const Num3Args<V, IdxT>& p, con
     }
     smem_acc<V>(copy_s + c * VS, a, x);
   };
-  for (uint32_t b = chunk0 * 32; b < n; b += chunk_stride * 32) {
-    const uint32_t i = b + lane;
-    uint32_t k = K;  // dummy row
-    V a = V(1);
+  // Two-deep prefetch: the (k, a) loads of chunk c+2 (HBM stream) and the X row-length gather of
+  // chunk c+1 are in flight while chunk c runs (without it the A load and the length gather were
+  // ~25% of the stall samples, profiles/r01a).
+  const uint32_t step = chunk_stride * 32;
+  auto load_ka = [&](uint32_t bb, uint32_t& k, V& a) {
+    const uint32_t i = bb + lane;
+    k = K;  // dummy row
+    a = V(1);
     if (i < n) {
       const uint64_t kk = static_cast<uint64_t>(ac[i]);
       k = kk < K ? static_cast<uint32_t>(kk) : K;
       a = av[i];
-      zero |= !(fabs(a) >= tiny);  // zero, tiny, or NaN weight: take the explicit path
     }
-    const uint32_t len = xlen[k];
+  };
+  uint32_t k1, k2;
+  V a1, a2;
+  load_ka(chunk0 * 32, k1, a1);
+  uint32_t len1 = xlen[k1];
+  load_ka(chunk0 * 32 + step, k2, a2);
+  for (uint32_t b = chunk0 * 32; b < n; b += step) {
+    const uint32_t k = k1, len = len1;
+    const V a = a1;
+    if (b + lane < n) zero |= !(fabs(a) >= tiny);  // zero, tiny, or NaN weight: take the explicit path
+    len1 = xlen[k2];
+    k1 = k2;
+    a1 = a2;
+    load_ka(b + 2 * step, k2, a2);
     macs += len;
     __syncwarp();
     if constexpr (sizeof(V) == 4)
