@@ -258,23 +258,43 @@ def run_b200(args, cfg):
         def estep():
             ab._check(L.aires_b200_spgemm(C.byref(ham), C.byref(hxm), mode, C.byref(hout_s)))
 
+        # the public entry point for host-resident operands is the out-of-core run (run_aires,
+        # aires_b200_run): uncapped, it keeps A's columns resident after the sizing pass and cuts
+        # ~8 tiles so H2D of A, the product and the D2H of C overlap on the two copy engines
+        rrep = ab._RunReport()
+        rcfg = ab._RunConfig(0, mode, 1, 3, 0)
+
+        def rstep():
+            ab._check(L.aires_b200_run(C.byref(ham), C.byref(hxm), C.byref(rcfg), C.byref(hout_s), C.byref(rrep)))
+
         for _ in range(max(1, args.warmup)):
             estep()
+            rstep()
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             estep()
+        s_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            rstep()
         e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        if int(hout_s.nnz) != nnz_c:
+            raise RuntimeError(f"run_aires nnz {int(hout_s.nnz)} != spgemm nnz {nnz_c}")
         if dist:
             t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        h2d = (n + 1) * 8 + g.nnz() * (4 + vb) + (K + 1) * 8 + x.nnz() * (4 + vb)
-        d2h = (n + 1) * 8 + nnz_c * (4 + vb)
+        h2d = int(rrep.h2d_bytes)
+        d2h = int(rrep.d2h_bytes)
         e2e = {"value": round(2.0 * tot_macs / (e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(e_ms, 3),
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "api": "aires_b200_spgemm, pinned host A/X/C (u64 ptr, u32 idx, fp32 val)"}
+               "api": "aires_b200_run (run_aires), pinned host A/X/C (u64 ptr, u32 idx, fp32 val), wall clock",
+               "segments": int(rrep.segments), "device_ms": round(rrep.total_ms, 3),
+               "spgemm_call": {"api": "aires_b200_spgemm with host buffers (one-shot H2D, product, D2H)",
+                               "ms_per_step": round(s_ms, 3),
+                               "value": round(2.0 * tot_macs / (s_ms * 1e-3) / 1e9, 3)}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:

@@ -84,6 +84,7 @@ Ctx::Ctx(int dev) : device(dev) {
 
 Ctx::~Ctx() {
   // Best effort: the CUDA runtime may already be torn down at thread/process exit.
+  if (pipe) destroy_pipe_cache(pipe);
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
   if (stream) cudaStreamDestroy(stream);

@@ -53,6 +53,7 @@ struct Ctx {
   double prof[kPCount] = {};
   double last_ms = 0.0;
   int launches = 0;  // kernels launched by the last product
+  void* pipe = nullptr;  // out-of-core pipeline cache (ab2_pipeline.cu)
   uint64_t last_fix_rows = 0;
   explicit Ctx(int dev);
   ~Ctx();
@@ -138,6 +139,7 @@ int tile_symbolic(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TileSym
 int tile_product(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TilePass& t);
 
 // Out-of-core run (ab2_pipeline.cu).
+void destroy_pipe_cache(void* p);
 void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b, const aires_b200_run_config& cfg,
                   aires_b200_output& out, aires_b200_run_report& rep);
 

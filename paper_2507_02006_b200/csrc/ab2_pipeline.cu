@@ -55,50 +55,70 @@ struct Pinned {
   }
 };
 
-struct Streams {
+// Streams, events and device buffers of the pipeline, cached per (thread, device) context so
+// repeated runs pay no cudaMalloc / stream creation on the host path.
+struct PipeCacheImpl {
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  std::vector<cudaEvent_t> ev;
-  cudaEvent_t make() {
-    cudaEvent_t e;
-    AB2_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    ev.push_back(e);
-    return e;
-  }
-  cudaEvent_t make_timed() {
-    cudaEvent_t e;
-    AB2_CUDA(cudaEventCreate(&e));
-    ev.push_back(e);
-    return e;
-  }
-  Streams() {
+  std::vector<cudaEvent_t> ev, tev;  // disable-timing / timing
+  std::vector<DevBuf> bufs;
+  PipeCacheImpl() {
     AB2_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
     AB2_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    bufs.resize(32);
   }
-  ~Streams() {
+  ~PipeCacheImpl() {
     for (auto e : ev) cudaEventDestroy(e);
+    for (auto e : tev) cudaEventDestroy(e);
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
   }
 };
 
-// Device allocations of the run, charged against the budget.
-struct Arena {
-  std::vector<void*> ptrs;
-  uint64_t used = 0;
-  void* get(size_t bytes) {
-    void* p = nullptr;
-    bytes = std::max<size_t>(bytes, 256);
-    cudaError_t e = cudaMalloc(&p, bytes);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+struct Streams {
+  PipeCacheImpl& c;
+  cudaStream_t h2d, d2h;
+  size_t ne = 0, nt = 0;
+  explicit Streams(PipeCacheImpl& pc) : c(pc), h2d(pc.h2d), d2h(pc.d2h) {}
+  cudaEvent_t make() {
+    if (ne == c.ev.size()) {
+      cudaEvent_t e;
+      AB2_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c.ev.push_back(e);
     }
-    ptrs.push_back(p);
-    used += bytes;
-    return p;
+    return c.ev[ne++];
   }
-  ~Arena() {
-    for (void* p : ptrs) cudaFree(p);
+  cudaEvent_t make_timed() {
+    if (nt == c.tev.size()) {
+      cudaEvent_t e;
+      AB2_CUDA(cudaEventCreate(&e));
+      c.tev.push_back(e);
+    }
+    return c.tev[nt++];
+  }
+};
+
+// Device allocations of the run (charged against the budget), from the cached grow-only buffers.
+struct Arena {
+  PipeCacheImpl& c;
+  size_t next = 0;
+  uint64_t used = 0;
+  explicit Arena(PipeCacheImpl& pc) : c(pc) {}
+  void* get(size_t bytes) {
+    bytes = std::max<size_t>(bytes, 256);
+    if (next == c.bufs.size()) c.bufs.resize(c.bufs.size() * 2);
+    DevBuf& d = c.bufs[next++];
+    if (d.cap < bytes) {
+      d.release();
+      cudaError_t e = cudaMalloc(&d.p, bytes);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        d.p = nullptr;
+        fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+      }
+      d.cap = bytes;
+    }
+    used += bytes;
+    return d.p;
   }
 };
 
@@ -143,6 +163,8 @@ double ms_between(cudaEvent_t a, cudaEvent_t b) {
 
 }  // namespace
 
+void destroy_pipe_cache(void* p) { delete static_cast<PipeCacheImpl*>(p); }
+
 void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b, const aires_b200_run_config& cfg,
                   aires_b200_output& out, aires_b200_run_report& rep) {
   if (a.layout != AIRES_B200_CSR || a.location != AIRES_B200_HOST)
@@ -166,10 +188,19 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   if (pend < p0 || pend > a.span) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "A row pointers exceed the index span");
   const uint32_t nbuf = std::max<uint32_t>(2, std::min<uint32_t>(cfg.n_buffers ? cfg.n_buffers : 2, 8));
   std::memset(&rep, 0, sizeof(rep));
+  // AB2_TRACE=1: host-side milestones on stderr (where the wall time of a run goes)
+  const bool trace = env_int("AB2_TRACE", 0) != 0;
+  const auto t_host0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+    std::fprintf(stderr, "[ab2 run] %8.3f ms  %s\n", ms, what);
+  };
 
-  Streams st;
+  if (!ctx.pipe) ctx.pipe = new PipeCacheImpl();
+  Streams st(*static_cast<PipeCacheImpl*>(ctx.pipe));
   cudaStream_t cs = ctx.stream;
-  Arena arena;
+  Arena arena(*static_cast<PipeCacheImpl*>(ctx.pipe));
   Pinned pin;
   cudaEvent_t t_begin = st.make_timed(), t_p1 = st.make_timed(), t_p2 = st.make_timed(), t_end = st.make_timed();
   pin.ensure(a.ptr, (n + 1) * 8);
@@ -177,16 +208,57 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   pin.ensure(static_cast<const char*>(a.val) + p0 * vb, (pend - p0) * vb);
 
   // ---------------- Phase I ----------------
+  mark("pinned checks done");
   AB2_CUDA(cudaEventRecord(t_begin, cs));
   AB2_CUDA(cudaStreamWaitEvent(st.h2d, t_begin, 0));
   // lean operand: the step-list layout (fp32) or W-slots (fp64-exact) plus the plain CSR, which
-  // the sizing pass reads directly
-  auto x = make_operand(ctx, b, mode, /*temp=*/true, mode == AIRES_B200_MODE_FP32 ? kPlanStep : kPlanSlots);
-  const uint64_t x_dev = x->bytes;
+  // the sizing pass reads directly (the device staging of a host X's raw arrays is transient and
+  // not charged to the budget)
+  // (+ 16-wide column slots for the sizing pass when X rows average >= 4 entries and the slots take
+  // <= 1/16 of a capped budget: the lane-per-entry walk over the plain CSR serialises long rows)
+  uint32_t plan = mode == AIRES_B200_MODE_FP32 ? kPlanStep : kPlanSlots;
+  {
+    const uint64_t xk = b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols;
+    const uint64_t xnnz = b.location == AIRES_B200_HOST ? b.ptr[(b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols)] - b.ptr[0]
+                                                        : b.span;
+    const uint64_t cs_bytes = xk * kCSlotW * 2;
+    if (xk > 0 && xnnz >= 4 * xk && (cfg.device_budget == 0 || cs_bytes * 16 <= cfg.device_budget) &&
+        env_int("AB2_RUN_CSLOTS", 1) != 0)
+      plan |= kPlanCSlots;
+  }
+  auto x = make_operand(ctx, b, mode, /*temp=*/true, plan);
+  mark("operand built (host synced)");
+  // Uncapped runs keep A's column indices resident and stream them right after X (X first: its
+  // build synchronises the host once and must not queue behind A on the link).
+  const uint64_t a_col_bytes = (pend - p0) * ib;
+  const bool early_cols = cfg.device_budget == 0 && env_int("AB2_RUN_RESIDENT_COLS", 1) != 0 && n > 0;
+  char* d_acol_full = nullptr;
+  std::vector<uint64_t> early_cuts;
+  std::vector<cudaEvent_t> early_ev;
+  uint64_t bad = 0;
+  if (early_cols) {
+    d_acol_full = static_cast<char*>(arena.get(a_col_bytes));
+    if (!greedy_cuts(a.ptr, nullptr, n, 0, ib, 0, std::max<uint64_t>(a_col_bytes / 8, 16ull << 20), early_cuts, &bad))
+      early_cuts = {0, n};  // a row longer than the chunk target: one chunk
+    for (size_t c = 0; c + 1 < early_cuts.size(); c++) {
+      const uint64_t q0 = a.ptr[early_cuts[c]], q1 = a.ptr[early_cuts[c + 1]];
+      if (q1 > q0)
+        AB2_CUDA(cudaMemcpyAsync(d_acol_full + (q0 - p0) * ib, static_cast<const char*>(a.idx) + q0 * ib,
+                                 (q1 - q0) * ib, cudaMemcpyHostToDevice, st.h2d));
+      early_ev.push_back(st.make());
+      AB2_CUDA(cudaEventRecord(early_ev.back(), st.h2d));
+    }
+  }
+  uint64_t x_dev = x->bytes;
+  if (b.location == AIRES_B200_HOST) {
+    const uint64_t raw = ctx.x_ptr.cap + ctx.x_idx.cap + ctx.x_val.cap;
+    x_dev = x_dev > raw ? x_dev - raw : 0;
+  }
   rep.h2d_bytes += b.location == AIRES_B200_HOST ? (b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols) * 8 + 8 +
                                                        static_cast<uint64_t>(x->nnz) * (b.idx_bytes + b.val_bytes)
                                                  : 0;
   // resident per-row arrays: A row_ptr, C row_ptr, counts
+  mark("A columns enqueued");
   uint64_t* d_aptr = static_cast<uint64_t*>(arena.get((n + 1) * 8));
   int64_t* d_cptr = static_cast<int64_t*>(arena.get((n + 1) * 8));
   int32_t* d_cnt = static_cast<int32_t*>(arena.get(std::max<uint64_t>(n, 1) * 4));
@@ -198,23 +270,35 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   // budget left for the ring: per slot A col/val + C col/val + per-row scratch
   const uint64_t fixed = x_dev + arena.used + (64 << 10) + 8 * sizeof(Ctl);
   uint64_t budget = cfg.device_budget;
-  if (budget == 0) {
-    size_t fr = 0, tot = 0;
-    AB2_CUDA(cudaMemGetInfo(&fr, &tot));
-    budget = fixed + static_cast<uint64_t>(fr * 0.8);
-  }
+  // Uncapped (device_budget 0): no cap to divide -- every buffer is sized to what the run needs and
+  // an allocation failure surfaces as insufficient_device_memory (cudaMemGetInfo would wait for
+  // the copies already in flight).
+  if (budget == 0) budget = fixed + (uint64_t(1) << 60);
+  mark("budget sized");
   if (budget <= fixed)
     fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY, "device budget " + std::to_string(budget) +
                                                     " does not cover the resident operand and row arrays (" +
                                                     std::to_string(fixed) + " bytes)");
-  const uint64_t slot_budget = (budget - fixed) / nbuf;
+  // A's column indices stay resident after the sizing pass when they take at most half of the
+  // budget left (then Phase II streams only A's values): one column pass over the link instead of two
+  const bool cols_resident =
+      early_cols || (env_int("AB2_RUN_RESIDENT_COLS", 1) != 0 && budget - fixed >= 2 * a_col_bytes + 4096);
+  if (cols_resident && !d_acol_full) d_acol_full = static_cast<char*>(arena.get(a_col_bytes));
+  const uint64_t fixed2 = fixed + (cols_resident && !early_cols ? std::max<uint64_t>(a_col_bytes, 256) : 0);
+  const uint64_t slot_budget = (budget - fixed2) / nbuf;
   // per-row scratch per slot: heavy (8) + cnt (4) + toff (8) + rflops (8)
   const uint64_t row_bytes = 28;
+  const uint64_t a_tile_bytes = cols_resident ? vb : ib + vb;  // A bytes per entry streamed in Phase II
 
   // Symbolic chunks: A columns only, sized like a slot's A + C space.
   std::vector<uint64_t> sym_cuts;
-  uint64_t bad = 0;
-  if (!greedy_cuts(a.ptr, nullptr, n, row_bytes, ib, 0, slot_budget, sym_cuts, &bad))
+  // (uncapped runs: chunks of ~1/8 of A's columns so the copies overlap the sizing kernels)
+  const uint64_t sym_budget = cfg.device_budget == 0
+                                  ? std::min<uint64_t>(slot_budget, std::max<uint64_t>(a_col_bytes / 8, 16ull << 20))
+                                  : slot_budget;
+  if (early_cols)
+    sym_cuts = early_cuts;
+  else if (!greedy_cuts(a.ptr, nullptr, n, row_bytes, ib, 0, sym_budget, sym_cuts, &bad))
     fail(AIRES_B200_ROW_TOO_LARGE, "row " + std::to_string(bad) + " does not fit a ring slot of " +
                                        std::to_string(slot_budget) + " bytes");
   // shift to relative offsets: greedy_cuts used absolute pointers; differences are what count
@@ -233,9 +317,23 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   };
   // Slot memory is carved from one allocation per slot (reused by both phases).
   std::vector<Slot> slot(nbuf);
+  // Capped runs give every slot the whole per-slot budget once; uncapped runs size the slots to
+  // the largest chunk (Phase I) and again to the largest tile (Phase II).
+  auto carve_bytes = [&](uint64_t rows, uint64_t a_nnz, bool with_val, uint64_t c_nnz) {
+    auto r = [](uint64_t b) { return (b + 255) & ~uint64_t(255); };
+    return (cols_resident ? 0 : r(a_nnz * ib)) + (with_val ? r(a_nnz * vb) : 0) + (c_nnz ? r(c_nnz * ib) + r(c_nnz * vb) : 0) +
+           r(std::max<uint64_t>(rows, 1) * 8) * 3 + r(std::max<uint64_t>(rows, 1) * 4);
+  };
+  uint64_t slot_cap = slot_budget;
+  if (cfg.device_budget == 0) {
+    slot_cap = 0;
+    for (size_t c = 0; c + 1 < sym_cuts.size(); c++)
+      slot_cap = std::max(slot_cap, carve_bytes(sym_cuts[c + 1] - sym_cuts[c], a.ptr[sym_cuts[c + 1]] - a.ptr[sym_cuts[c]],
+                                                false, 0));
+  }
   std::vector<char*> slot_mem(nbuf);
   for (uint32_t s = 0; s < nbuf; s++) {
-    slot_mem[s] = static_cast<char*>(arena.get(slot_budget + 4096));
+    slot_mem[s] = static_cast<char*>(arena.get(slot_cap + 4096));
     slot[s].loaded = st.make();
     slot[s].computed = st.make();
     slot[s].drained = st.make();
@@ -251,7 +349,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
       return static_cast<void*>(p);
     };
     Slot& sl = slot[s];
-    sl.acol = take(a_nnz * ib);
+    sl.acol = cols_resident ? nullptr : take(a_nnz * ib);
     sl.aval = with_val ? take(a_nnz * vb) : nullptr;
     sl.ccol = c_nnz ? take(c_nnz * ib) : nullptr;
     sl.cval = c_nnz ? take(c_nnz * vb) : nullptr;
@@ -259,7 +357,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
     sl.cnt = static_cast<uint32_t*>(take(std::max<uint64_t>(rows, 1) * 4));
     sl.toff = static_cast<uint64_t*>(take(std::max<uint64_t>(rows, 1) * 8));
     sl.rflops = static_cast<int64_t*>(take(std::max<uint64_t>(rows, 1) * 8));
-    if (static_cast<uint64_t>(m - slot_mem[s]) > slot_budget + 4096)
+    if (static_cast<uint64_t>(m - slot_mem[s]) > slot_cap + 4096)
       fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY, "ring slot overflow");
   };
 
@@ -276,12 +374,17 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
     const uint64_t q0 = a.ptr[r0], q1 = a.ptr[r1];
     if (c >= nbuf) AB2_CUDA(cudaStreamWaitEvent(st.h2d, slot[s].computed, 0));
     carve(s, r1 - r0, q1 - q0, false, 0);
-    if (q1 > q0)
-      AB2_CUDA(cudaMemcpyAsync(slot[s].acol, static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib,
-                               cudaMemcpyHostToDevice, st.h2d));
+    if (cols_resident) slot[s].acol = d_acol_full + (q0 - p0) * ib;
     rep.h2d_bytes += (q1 - q0) * ib;
-    AB2_CUDA(cudaEventRecord(slot[s].loaded, st.h2d));
-    AB2_CUDA(cudaStreamWaitEvent(cs, slot[s].loaded, 0));
+    if (early_cols) {
+      AB2_CUDA(cudaStreamWaitEvent(cs, early_ev[c], 0));
+    } else {
+      if (q1 > q0)
+        AB2_CUDA(cudaMemcpyAsync(slot[s].acol, static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib,
+                                 cudaMemcpyHostToDevice, st.h2d));
+      AB2_CUDA(cudaEventRecord(slot[s].loaded, st.h2d));
+      AB2_CUDA(cudaStreamWaitEvent(cs, slot[s].loaded, 0));
+    }
     TileSym t{};
     t.aptr = d_aptr + r0;
     t.abase = q0;
@@ -295,6 +398,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
     AB2_CUDA(cudaEventRecord(slot[s].computed, cs));
   }
   // scan -> C row_ptr, total nnz and MACs
+  mark("sizing pass enqueued");
   {
     const int64_t nb = (static_cast<int64_t>(n) + kScanTile - 1) / kScanTile;
     int64_t* part = static_cast<int64_t*>(arena.get(std::max<int64_t>(nb, 1) * 8));
@@ -318,6 +422,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   for (uint64_t c = 0; c < n_sym; c++) flops += h_ctls[c].flops;
 
   // exact allocation by the caller (spgemm.hpp:111-112), C row_ptr straight into it
+  mark("sizing pass done (synced)");
   void *optr = nullptr, *oidx = nullptr, *oval = nullptr;
   int rc = out.alloc(out.user, n, nnz, &optr, &oidx, &oval);
   if (rc != 0) fail(rc, "output allocator failed for " + std::to_string(nnz) + " nonzeros");
@@ -330,28 +435,49 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   const uint64_t* cp = static_cast<const uint64_t*>(optr);
 
   // tile cuts: C-aware (A + C + scratch per slot), or RoBW over A alone
+  mark("allocated + C row_ptr copied");
   // (c_aware = 0: RoBW-style cuts that fill a slot with A alone, then the C block of each
   // segment must fit the rest -- the reference's admission, which fails on GCN shapes)
+  // Uncapped runs (device_budget 0) still cut ~AB2_RUN_TILES (16) tiles so that tile k+1's H2D, tile k's
+  // product and tile k-1's D2H overlap; capped runs use maximal tiles.
+  uint64_t tile_budget = slot_budget;
+  if (cfg.device_budget == 0) {
+    const uint64_t p2_bytes = (pend - p0) * a_tile_bytes + nnz * (ib + vb) + n * row_bytes;
+    const uint64_t want = std::max<uint64_t>(env_int("AB2_RUN_TILES", 16), 1);
+    tile_budget = std::min<uint64_t>(slot_budget, std::max<uint64_t>(p2_bytes / want, 64ull << 20));
+  }
   std::vector<uint64_t> cuts;
-  if (!greedy_cuts(a.ptr, cfg.c_aware ? cp : nullptr, n, row_bytes, ib + vb, ib + vb,
-                   cfg.c_aware ? slot_budget : slot_budget - slot_budget / 16, cuts, &bad))
+  if (!greedy_cuts(a.ptr, cfg.c_aware ? cp : nullptr, n, row_bytes, a_tile_bytes, ib + vb,
+                   cfg.c_aware ? tile_budget : slot_budget - slot_budget / 16, cuts, &bad))
     fail(AIRES_B200_ROW_TOO_LARGE, "row " + std::to_string(bad) + " does not fit a ring slot of " +
                                        std::to_string(slot_budget) + " bytes");
   if (!cfg.c_aware) {
     for (size_t j = 0; j + 1 < cuts.size(); j++) {
       const uint64_t r0 = cuts[j], r1 = cuts[j + 1];
-      const uint64_t need = (r1 - r0) * row_bytes + (a.ptr[r1] - a.ptr[r0]) * (ib + vb) + (cp[r1] - cp[r0]) * (ib + vb);
+      const uint64_t need =
+          (r1 - r0) * row_bytes + (a.ptr[r1] - a.ptr[r0]) * a_tile_bytes + (cp[r1] - cp[r0]) * (ib + vb);
       if (need > slot_budget)
         fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY,
              "segment " + std::to_string(j) + "'s C block does not fit the remaining device memory (A-only tiling)");
     }
   }
   const uint64_t n_tiles = cuts.size() - 1;
+  if (cfg.device_budget == 0) {  // resize the ring to the largest tile
+    uint64_t need = 0;
+    for (uint64_t j = 0; j < n_tiles; j++)
+      need = std::max(need, carve_bytes(cuts[j + 1] - cuts[j], a.ptr[cuts[j + 1]] - a.ptr[cuts[j]], true,
+                                        cp[cuts[j + 1]] - cp[cuts[j]]));
+    if (need > slot_cap) {
+      slot_cap = need;
+      for (uint32_t s = 0; s < nbuf; s++) slot_mem[s] = static_cast<char*>(arena.get(slot_cap + 4096));
+    }
+  }
   Ctl* d_tctl = static_cast<Ctl*>(arena.get(sizeof(Ctl) * std::max<uint64_t>(n_tiles, 1)));
   AB2_CUDA(cudaMemsetAsync(d_tctl, 0, sizeof(Ctl) * std::max<uint64_t>(n_tiles, 1), cs));
   AB2_CUDA(cudaEventRecord(t_p1, cs));
 
   // ---------------- Phase II ----------------
+  mark("tiles cut");
   AB2_CUDA(cudaEventRecord(e_zero, cs));
   AB2_CUDA(cudaStreamWaitEvent(st.h2d, e_zero, 0));
   for (uint64_t j = 0; j < n_tiles; j++) {
@@ -364,13 +490,15 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
     // its C space is free once tile j-nbuf was drained
     if (j >= nbuf) AB2_CUDA(cudaStreamWaitEvent(st.h2d, slot[s].drained, 0));
     carve(s, r1 - r0, q1 - q0, true, c1 - c0);
+    if (cols_resident) slot[s].acol = d_acol_full + (q0 - p0) * ib;
     if (q1 > q0) {
-      AB2_CUDA(cudaMemcpyAsync(slot[s].acol, static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib,
-                               cudaMemcpyHostToDevice, st.h2d));
+      if (!cols_resident)
+        AB2_CUDA(cudaMemcpyAsync(slot[s].acol, static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib,
+                                 cudaMemcpyHostToDevice, st.h2d));
       AB2_CUDA(cudaMemcpyAsync(slot[s].aval, static_cast<const char*>(a.val) + q0 * vb, (q1 - q0) * vb,
                                cudaMemcpyHostToDevice, st.h2d));
     }
-    rep.h2d_bytes += (q1 - q0) * (ib + vb);
+    rep.h2d_bytes += (q1 - q0) * a_tile_bytes;
     AB2_CUDA(cudaEventRecord(slot[s].loaded, st.h2d));
     AB2_CUDA(cudaStreamWaitEvent(cs, slot[s].loaded, 0));
     TilePass t{};
@@ -403,6 +531,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   AB2_CUDA(cudaEventRecord(t_p2, cs));
 
   // ---------------- Phase III ----------------
+  mark("phase II enqueued");
   AB2_CUDA(cudaStreamWaitEvent(cs, slot[0].drained, 0));
   for (uint32_t s = 0; s < nbuf; s++) AB2_CUDA(cudaStreamWaitEvent(cs, slot[s].drained, 0));
   AB2_CUDA(cudaEventRecord(t_end, cs));
@@ -414,6 +543,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
     if (h_t[j].bad_row == 2) fail(AIRES_B200_CUDA_ERROR, "numeric row counts disagree with the symbolic pass");
     if (h_t[j].bad_row) fail(AIRES_B200_CAPACITY_EXCEEDED, "tile output overflow");
   }
+  mark("phase III synced");
   rep.segments = n_tiles;
   rep.flops = flops;
   rep.c_nnz = nnz;

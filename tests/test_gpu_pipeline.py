@@ -46,7 +46,9 @@ def test_run_fp64_bit_exact_across_budgets(frac):
     # C (ptr + col/val) crosses D2H once
     rep = res.report.ledger
     assert rep.d2h.bytes == 8 * (g.n_rows + 1) + 16 * wi.shape[0]
-    assert rep.h2d.bytes == 8 * (g.n_rows + 1) + 8 * g.nnz() + 16 * g.nnz() + 8 * (x.n_rows + 1) + 16 * x.nnz()
+    # A's columns cross once (kept resident after the sizing pass) or twice (sizing + tile)
+    base = 8 * (g.n_rows + 1) + 16 * g.nnz() + 8 * (x.n_rows + 1) + 16 * x.nnz()
+    assert rep.h2d.bytes in (base, base + 8 * g.nnz())
 
 
 @pytest.mark.parametrize("n_buffers", [2, 3, 4])
