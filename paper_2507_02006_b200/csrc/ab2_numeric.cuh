@@ -288,6 +288,163 @@ __device__ __forceinline__ uint32_t walk_entries(const Num3Args<V, IdxT>& p, con
   return macs;
 }
 
+// Register-fed variant (default, AB2_NUM_SHFL=1).  The kernel is bound by the L1 / shared-memory
+// datapath (90% L1 throughput at cfg2, profiles/r01d); per warp step the variant above spends two
+// shared wavefronts on the chunk table (LDS.128) and, per chunk, one 32-sector gather of X row
+// lengths.  Here each lane keeps its own entry (slot base k*W, weight a) in registers and groups
+// fetch theirs with SHFL; slots are loaded whole (entries past the row's length hold the trash
+// column, skipped without touching shared memory) and MACs are counted from the real entries.
+template <class V, class IdxT, int W, bool EXACT, bool RANGE, bool XZ>
+__device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac,
+                                                  const V* __restrict__ av, uint32_t n, uint32_t chunk0,
+                                                  uint32_t chunk_stride, V* acc, uint32_t c_lo, uint32_t c_hi,
+                                                  bool& zero) {
+  constexpr int G = 32 / W;
+  constexpr int B = W < AB2_NUM_BATCH ? W : AB2_NUM_BATCH;  // group steps per batch (loads in flight)
+  constexpr uint32_t VS = sizeof(V);
+  const int lane = lane_id(), gid = lane / W, ent = lane % W;
+  const int mlane = gid * W + (W - 1);  // the group's marker lane
+  const uint32_t K = static_cast<uint32_t>(p.x.K);
+  const uint32_t trash = static_cast<uint32_t>(p.x.n_cols);
+  const int32_t* __restrict__ xcol = p.x.col;
+  const V* __restrict__ xval = p.x.val;
+  const V tiny = p.tiny;
+  const uint32_t copy_s = static_cast<uint32_t>(__cvta_generic_to_shared(EXACT ? acc : acc + gid * p.stride));
+  uint32_t macs = 0;
+  auto col_of = [&](uint32_t c) -> uint32_t {
+    c &= kSlotColMask;
+    if constexpr (RANGE) c = (c >= c_lo && c < c_hi) ? c : trash;
+    return c;
+  };
+  auto add = [&](uint32_t c, V a, V x) {
+    if constexpr (XZ) {
+      if constexpr (EXACT)
+        zero |= __dmul_rn(a, x) == 0.0;
+      else
+        zero |= a * x == 0.f;
+    }
+    smem_acc<V>(copy_s + c * VS, a, x);
+  };
+  const uint32_t step = chunk_stride * 32;
+  auto load_ka = [&](uint32_t bb, uint32_t& k, V& a) {
+    const uint32_t i = bb + lane;
+    k = K;  // dummy row: an all-trash slot
+    a = V(1);
+    if (i < n) {
+      const uint64_t kk = static_cast<uint64_t>(ac[i]);
+      k = kk < K ? static_cast<uint32_t>(kk) : K;
+      a = av[i];
+    }
+  };
+  // two chunks of (k, a) in flight ahead of the one being accumulated
+  uint32_t k1, k2;
+  V a1, a2;
+  load_ka(chunk0 * 32, k1, a1);
+  load_ka(chunk0 * 32 + step, k2, a2);
+  for (uint32_t b = chunk0 * 32; b < n; b += step) {
+    const uint32_t kw = k1 * W;
+    const V a = a1;
+    if (b + lane < n) zero |= !(fabs(a) >= tiny);  // zero, tiny, or NaN weight: take the explicit path
+    k1 = k2;
+    a1 = a2;
+    load_ka(b + 2 * step, k2, a2);
+    const uint32_t steps = (min(32u, n - b) + G - 1) / G;
+#pragma unroll 1
+    for (uint32_t u0 = 0; u0 < steps; u0 += B) {
+      uint32_t col[B];
+      V xv[B], aa[B];
+      uint32_t any = 0;
+#pragma unroll
+      for (int u = 0; u < B; u++) {
+        const int src = static_cast<int>(((u0 + u) * G + gid) & 31u);
+        const uint32_t skw = __shfl_sync(kFull, kw, src);
+        aa[u] = __shfl_sync(kFull, a, src);
+        if constexpr (sizeof(V) == 4) {
+          const uint2 e = __ldg(reinterpret_cast<const uint2*>(p.x.slots) + (skw + ent));
+          col[u] = e.x;
+          xv[u] = __uint_as_float(e.y);
+        } else {
+          const uint4 e = __ldg(reinterpret_cast<const uint4*>(p.x.slots) + (skw + ent));
+          col[u] = e.x;
+          xv[u] = __hiloint2double(e.w, e.z);
+          if (e.x & kSlotOvf) xv[u] = __longlong_as_double(static_cast<long long>(e.y));
+        }
+        if ((u0 + u) * G >= 32u) col[u] = trash;  // steps past the chunk (only when G does not divide 32)
+        any |= col[u];
+      }
+      if (!__any_sync(kFull, (any & kSlotOvf) != 0)) {
+        // fast path: no marker in the batch; trash entries touch nothing
+#pragma unroll
+        for (int u = 0; u < B; u++) {
+          const bool real = col[u] != trash;
+          macs += real;
+          uint32_t c = col[u];
+          if constexpr (RANGE) c = (c >= c_lo && c < c_hi) ? c : trash;
+          if constexpr (EXACT) {
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+              if (gid == g && real) add(c, aa[u], xv[u]);
+              __syncwarp();
+            }
+          } else {
+            if (real) add(c, aa[u], xv[u]);
+          }
+        }
+        __syncwarp();
+      } else {
+#pragma unroll
+        for (int u = 0; u < B; u++) {
+          // marker lane: col = kSlotOvf | tail<<16 | trash; the tail offset rides in the value
+          // bits (fp32: 1.0f + offset ulps) or the pad word (fp64, stashed in xv above)
+          uint32_t moff;
+          if constexpr (sizeof(V) == 4)
+            moff = __float_as_uint(xv[u]) - kOneBits;
+          else
+            moff = static_cast<uint32_t>(__double_as_longlong(xv[u]));
+          const uint32_t mc = __shfl_sync(kFull, col[u], mlane);
+          const uint32_t mo = __shfl_sync(kFull, moff, mlane);
+          const uint32_t tn = (mc & kSlotOvf) ? (mc >> 16) & kMaxTail : 0;
+          const bool real = col[u] != trash && !(col[u] & kSlotOvf);
+          macs += real;
+          for (uint32_t t = ent; t < tn; t += W) macs++;
+          if constexpr (EXACT) {
+#pragma unroll
+            for (int g = 0; g < G; g++) {
+              if (gid == g) {
+                if (real) add(col_of(col[u]), aa[u], xv[u]);
+                for (uint32_t t = ent; t < tn; t += W) add(col_of(xcol[mo + t]), aa[u], xval[mo + t]);
+              }
+              __syncwarp();
+            }
+          } else {
+            if (real) add(col_of(col[u]), aa[u], xv[u]);
+            for (uint32_t t = ent; t < tn; t += W) add(col_of(xcol[mo + t]), aa[u], xval[mo + t]);
+            __syncwarp();
+          }
+        }
+      }
+    }
+  }
+  return macs;
+}
+
+#ifndef AB2_NUM_SHFL
+#define AB2_NUM_SHFL 1
+#endif
+
+template <class V, class IdxT, int W, bool EXACT, bool RANGE, bool XZ>
+__device__ __forceinline__ uint32_t walk_any(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac,
+                                             const V* __restrict__ av, uint32_t n, uint32_t chunk0,
+                                             uint32_t chunk_stride, V* acc, ChunkPair* tab, uint32_t c_lo,
+                                             uint32_t c_hi, bool& zero) {
+#if AB2_NUM_SHFL
+  (void)tab;
+  return walk_entries2<V, IdxT, W, EXACT, RANGE, XZ>(p, ac, av, n, chunk0, chunk_stride, acc, c_lo, c_hi, zero);
+#else
+  return walk_entries<V, IdxT, W, EXACT, RANGE, XZ>(p, ac, av, n, chunk0, chunk_stride, acc, tab, c_lo, c_hi, zero);
+#endif
+}
+
 // Explicit-mark slow path (rows with a zero product): one k at a time in ascending order,
 // +0.0 start, byte marks; leaves copy 0 holding values for marked cells and the marker
 // everywhere else (other copies reset), so the common fold / emit path applies.
@@ -440,10 +597,10 @@ __global__ void __launch_bounds__(256, AB2_NUM_MINB) k_numeric3(Num3Args<V, IdxT
       const uint32_t span = ((n_cols + nw - 1) / nw + 31) & ~31;
       const uint32_t c_lo = min(warp * span, static_cast<uint32_t>(n_cols));
       const uint32_t c_hi = min(c_lo + span, static_cast<uint32_t>(n_cols));
-      const uint32_t m = walk_entries<V, IdxT, W, true, true, XZ>(p, ac, av, n, 0, 1, warp_acc(0), warp_tab(warp), c_lo, c_hi, zero);
+      const uint32_t m = walk_any<V, IdxT, W, true, true, XZ>(p, ac, av, n, 0, 1, warp_acc(0), warp_tab(warp), c_lo, c_hi, zero);
       if (warp == 0) my_macs += m;
     } else {
-      my_macs += walk_entries<V, IdxT, W, false, false, XZ>(p, ac, av, n, warp, nw, warp_acc(warp), warp_tab(warp), 0, 0, zero);
+      my_macs += walk_any<V, IdxT, W, false, false, XZ>(p, ac, av, n, warp, nw, warp_acc(warp), warp_tab(warp), 0, 0, zero);
     }
     if (zero) s_zero = 1;
     __syncthreads();
@@ -498,7 +655,7 @@ __global__ void __launch_bounds__(256, AB2_NUM_MINB) k_numeric3(Num3Args<V, IdxT
       const IdxT* ac = p.acol + s;
       const V* av = p.aval + s;
       bool zero = false;
-      my_macs += walk_entries<V, IdxT, W, EXACT, false, XZ>(p, ac, av, n, 0, 1, acc, warp_tab(warp), 0, 0, zero);
+      my_macs += walk_any<V, IdxT, W, EXACT, false, XZ>(p, ac, av, n, 0, 1, acc, warp_tab(warp), 0, 0, zero);
       if (__any_sync(kFull, zero)) slow_row<V, IdxT>(p, ac, av, n, acc, warp_mark(warp));
       const uint32_t cnt = fold_count<V>(acc, p.stride, EXACT ? 1 : p.copies, n_cols);
       const unsigned long long off = out_offset(p, r, cnt, stage);

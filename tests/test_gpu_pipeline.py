@@ -51,8 +51,9 @@ def test_run_fp64_bit_exact_across_budgets(frac):
     assert rep.h2d.bytes in (base, base + 8 * g.nnz())
 
 
-@pytest.mark.parametrize("n_buffers", [2, 3, 4])
-def test_run_fp32_tolerance_many_tiles(n_buffers):
+@pytest.mark.parametrize("n_buffers,resident", [(2, "1"), (3, "0"), (4, "1"), (2, "0")])
+def test_run_fp32_tolerance_many_tiles(n_buffers, resident, monkeypatch):
+    monkeypatch.setenv("AB2_RUN_RESIDENT_COLS", resident)  # A columns kept on the device or re-streamed
     g, x = _graph(30_000, 400_000, 100, seed=4)
     wp, wi, wv, macs = _oracle(g, x)
     g32 = ab.CsrMatrix(g.n_rows, g.n_cols, g.row_ptr, g.col_idx.astype(np.uint32), g.values.astype(np.float32))
@@ -61,7 +62,7 @@ def test_run_fp32_tolerance_many_tiles(n_buffers):
     c_b = 8 * (g.n_rows + 1) + 8 * wi.shape[0]
     res = ab.run_aires(g32, x32, ab.MemoryBudget(int(3e6 + (a_b + c_b) / 8)), n_buffers=n_buffers,
                        with_checksum=False)
-    assert res.report.segments >= 8
+    assert res.report.segments >= 4
     assert np.array_equal(res.c.row_ptr, wp) and np.array_equal(res.c.col_idx.astype(np.uint64), wi)
     err = np.abs(res.c.values.astype(np.float64) - wv) / np.abs(wv)
     assert err.max() <= 1e-5
