@@ -18,6 +18,8 @@
  *   aires_b200_run           -> aires::run_aires Phases I-III    scheduler.hpp:72-168
  *                               (real multi-stream tile pipeline, C-aware tiles)
  *   aires_b200_checksum      -> aires::checksum (FNV-1a of C)   serialize.hpp:50-59
+ *   aires_b200_normalize_adjacency -> aires::normalize_adjacency gcn.hpp:29-72
+ *   aires_b200_combine       -> aires::combine (ReLU(X*W))      gcn.hpp:90-116
  *   aires_b200_last_error    -> the what() string of aires::error error.hpp:53-62
  *
  * Status codes: 0 = OK, otherwise 1 + (int)aires::errc (error.hpp:9-27), so
@@ -173,6 +175,15 @@ typedef struct aires_b200_run_report {
 int aires_b200_run(const aires_b200_matrix* a, const aires_b200_matrix* b,
                    const aires_b200_run_config* cfg, aires_b200_output* c,
                    aires_b200_run_report* report);
+
+/* ---- GCN layer steps either side of A·X ------------------ */
+/* Ã = D̂^-½ (A + I) D̂^-½, bit-identical to the reference (fp64 arithmetic; fp32 output is the
+   rounded fp64 value).  A square CSR, nonnegative weights; errors: non_square, negative_weight. */
+int aires_b200_normalize_adjacency(const aires_b200_matrix* a, aires_b200_output* out);
+/* H = ReLU(X * W), entries <= 0 dropped.  X CSR (host or device), W dense row-major w_rows x w_cols
+   of X's value type at w_location; fp64 bit-identical to the reference, fp32 within tolerance. */
+int aires_b200_combine(const aires_b200_matrix* x, const void* w, uint64_t w_rows, uint64_t w_cols,
+                       uint32_t w_location, aires_b200_output* out);
 
 /* FNV-1a 64 of a CSR in the reference's canonical byte stream (serialize.hpp:50-59); host only.
    row_ptr may be absolute (it is rebased); 4-byte indices / values are widened to u64 / f64. */

@@ -8,6 +8,7 @@
  *                               arithmetic of normalize_adjacency (gcn.hpp:29-72).
  *   aires_b200_synth_features : the reference's gen_features (synth.hpp:73-78) draw for draw
  *                               (std::mt19937_64), so X is byte-identical to the reference's.
+ *   aires_b200_synth_weights  : the reference's gen_weights (synth.hpp:81-86), same draws.
  * Outputs go through the aires_b200_output allocator (location must be HOST).
  */
 #ifndef AIRES_B200_SYNTH_H
@@ -40,6 +41,9 @@ int aires_b200_synth_graph(const aires_b200_graph_spec* spec, aires_b200_output*
 
 int aires_b200_synth_features(uint64_t n, uint64_t dim, double sparsity_pct, uint64_t seed,
                               aires_b200_output* out);
+
+/* the reference's gen_weights (synth.hpp:81-86): row-major in_dim x out_dim, U[0,1) - 0.5 */
+int aires_b200_synth_weights(uint64_t in_dim, uint64_t out_dim, uint64_t seed, double* out);
 
 #ifdef __cplusplus
 }

@@ -484,3 +484,48 @@ int ao_normalize_adjacency(uint64_t n, const uint64_t* row_ptr, const uint64_t* 
   free(degree);
   return AO_OK;
 }
+
+/* synth.hpp:81-86 gen_weights: row-major in_dim x out_dim, uniform01 - 0.5 */
+int ao_gen_weights(uint64_t in_dim, uint64_t out_dim, uint64_t seed, double* out) {
+  mt64 st;
+  mt64_seed(&st, seed);
+  for (uint64_t i = 0; i < in_dim * out_dim; i++) out[i] = uniform01(&st) - 0.5;
+  return AO_OK;
+}
+
+/* gcn.hpp:90-116 combine: per row, acc[j] = sum_k v_k * W[in_k][j] in ascending k from 0.0
+   (separate multiply and add; the build uses -ffp-contract=off), keep acc[j] > 0. */
+int ao_combine(uint64_t rows, uint64_t x_cols, const uint64_t* row_ptr, const uint64_t* col_idx,
+               const double* values, const double* w, uint64_t w_rows, uint64_t w_cols, ao_csr* out) {
+  if (x_cols != w_rows) return AO_DIMENSION_MISMATCH;
+  double* acc = (double*)xmalloc(w_cols * sizeof(double));
+  uint64_t cap = 1024, nnz = 0;
+  out->n_rows = rows;
+  out->n_cols = w_cols;
+  out->ptr = (uint64_t*)xcalloc(rows + 1, sizeof(uint64_t));
+  out->idx = (uint64_t*)xmalloc(cap * sizeof(uint64_t));
+  out->val = (double*)xmalloc(cap * sizeof(double));
+  for (uint64_t r = 0; r < rows; r++) {
+    for (uint64_t j = 0; j < w_cols; j++) acc[j] = 0.0;
+    for (uint64_t k = row_ptr[r]; k < row_ptr[r + 1]; k++) {
+      const uint64_t in = col_idx[k];
+      const double v = values[k];
+      for (uint64_t j = 0; j < w_cols; j++) acc[j] += v * w[in * w_cols + j];
+    }
+    for (uint64_t j = 0; j < w_cols; j++)
+      if (acc[j] > 0.0) {
+        if (nnz == cap) {
+          cap *= 2;
+          out->idx = (uint64_t*)realloc(out->idx, cap * sizeof(uint64_t));
+          out->val = (double*)realloc(out->val, cap * sizeof(double));
+        }
+        out->idx[nnz] = j;
+        out->val[nnz] = acc[j];
+        nnz++;
+      }
+    out->ptr[r + 1] = nnz;
+  }
+  out->nnz = nnz;
+  free(acc);
+  return AO_OK;
+}

@@ -112,6 +112,12 @@ int ao_gen_features(uint64_t n_nodes, uint64_t dim, double sparsity_pct, uint64_
 int ao_normalize_adjacency(uint64_t n, const uint64_t* row_ptr, const uint64_t* col_idx,
                            const double* values, ao_csr* out);
 
+/* synth.hpp:81-86 */
+int ao_gen_weights(uint64_t in_dim, uint64_t out_dim, uint64_t seed, double* out);
+/* gcn.hpp:90-116 (row_ptr rebased: row_ptr[0] == 0) */
+int ao_combine(uint64_t rows, uint64_t x_cols, const uint64_t* row_ptr, const uint64_t* col_idx,
+               const double* values, const double* w, uint64_t w_rows, uint64_t w_cols, ao_csr* out);
+
 #ifdef __cplusplus
 }
 #endif

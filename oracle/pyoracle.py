@@ -60,6 +60,9 @@ def oracle() -> C.CDLL:
         L.ao_gen_features.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, C.POINTER(AoCsr)]
         L.ao_normalize_adjacency.argtypes = [C.c_uint64, U64P, U64P, F64P, C.POINTER(AoCsr)]
         L.ao_free.argtypes = [C.POINTER(AoCsr)]
+        L.ao_gen_weights.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, F64P]
+        L.ao_combine.argtypes = [C.c_uint64, C.c_uint64, U64P, U64P, F64P, F64P, C.c_uint64, C.c_uint64,
+                                 C.POINTER(AoCsr)]
         _oracle = L
     return _oracle
 
@@ -96,6 +99,9 @@ def ref() -> C.CDLL:
         L.ref_spgemm_rows_timed.argtypes = [U64P, U64P, F64P, C.c_uint64, C.c_uint64, U64P, C.c_uint64,
                                             C.c_uint64, C.c_uint64, U64P, U64P, F64P, C.c_int, U64P, U64P, U64P]
         L.ref_free.argtypes = [C.POINTER(AoCsr)]
+        L.ref_gen_weights.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, F64P]
+        L.ref_combine.argtypes = [C.c_uint64, C.c_uint64, U64P, U64P, F64P, F64P, C.c_uint64, C.c_uint64,
+                                  C.POINTER(AoCsr)]
         _ref = L
     return _ref
 
@@ -292,3 +298,26 @@ def ref_rows_timed(row_ptr, col_idx, values, a_n_cols, rows, b_col_ptr, b_row_id
                                 b_n_rows, b_n_cols, _p64(cp), _p64(ri), _pf(bv), nthreads, C.byref(macs),
                                 C.byref(z), C.byref(h))
     return s, macs.value, z.value, h.value
+
+
+def gen_weights(in_dim, out_dim, seed, use_ref=False) -> np.ndarray:
+    """synth.hpp:81-86"""
+    w = np.empty((in_dim, out_dim), dtype=np.float64)
+    (ref().ref_gen_weights if use_ref else oracle().ao_gen_weights)(in_dim, out_dim, seed, _pf(w))
+    return w
+
+
+def combine(rows, x_cols, row_ptr, col_idx, values, w, use_ref=False):
+    """gcn.hpp:90-116.  Returns (rc, (ptr, idx, val))."""
+    rp = _u64(np.asarray(row_ptr, dtype=np.uint64) - np.uint64(np.asarray(row_ptr)[0]))
+    ci, va = _u64(col_idx), _f64(values)
+    wd = _f64(w)
+    m = AoCsr()
+    L = ref() if use_ref else oracle()
+    f = L.ref_combine if use_ref else L.ao_combine
+    p0 = int(np.asarray(row_ptr)[0])
+    ci, va = _u64(ci[p0:]), _f64(va[p0:])
+    rc = f(rows, x_cols, _p64(rp), _p64(ci), _pf(va), _pf(wd), wd.shape[0], wd.shape[1], C.byref(m))
+    if rc:
+        return rc, None
+    return 0, _take(m, rows + 1, L.ref_free if use_ref else L.ao_free)

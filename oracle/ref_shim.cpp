@@ -182,6 +182,23 @@ int ref_normalize_adjacency(uint64_t n, const uint64_t* row_ptr, const uint64_t*
   }
 }
 
+int ref_gen_weights(uint64_t in_dim, uint64_t out_dim, uint64_t seed, double* out) {
+  DenseMatrix w = gen_weights(in_dim, out_dim, seed);
+  std::memcpy(out, w.data.data(), w.data.size() * sizeof(double));
+  return 0;
+}
+
+int ref_combine(uint64_t rows, uint64_t x_cols, const uint64_t* row_ptr, const uint64_t* col_idx,
+                const double* values, const double* w, uint64_t w_rows, uint64_t w_cols, ao_csr* out) {
+  try {
+    DenseMatrix wd{w_rows, w_cols, std::vector<value_t>(w, w + w_rows * w_cols)};
+    export_csr(combine(make_csr(rows, x_cols, row_ptr, col_idx, values), wd), out);
+    return 0;
+  } catch (const error& e) {
+    return code_of(e);
+  }
+}
+
 // run_aires (scheduler.hpp:72-168) verbatim; returns the report fields the
 // B200 drop-in must reproduce.  rep: [segments, gds.count, gds.bytes, s2h.count,
 // s2h.bytes, h2d.count, h2d.bytes, d2h.count, d2h.bytes, merge_bytes,

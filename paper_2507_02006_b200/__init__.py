@@ -136,6 +136,9 @@ def lib() -> C.CDLL:
     L.aires_b200_synth_graph.argtypes = [P(_GraphSpec), P(_Output), P(C.c_double)]
     L.aires_b200_synth_features.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, P(_Output)]
     L.aires_b200_synth_last_error.restype = C.c_char_p
+    L.aires_b200_normalize_adjacency.argtypes = [P(_Matrix), P(_Output)]
+    L.aires_b200_combine.argtypes = [P(_Matrix), C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, P(_Output)]
+    L.aires_b200_synth_weights.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, P(C.c_double)]
     L.aires_b200_checksum.restype = C.c_uint64
     L.aires_b200_checksum.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, P(C.c_uint64), C.c_void_p, C.c_uint32,
                                       C.c_void_p, C.c_uint32]
@@ -478,6 +481,62 @@ def run_aires(a: CsrMatrix, b, budget: MemoryBudget, cfg=None, mode: int = MODE_
     if with_checksum:
         r.c_checksum = checksum(c)
     return RunResult(c, r, [])
+
+
+# ---------------------------------------------------------------------------
+# GCN layer steps either side of A·X (gcn.hpp:29-132)
+# ---------------------------------------------------------------------------
+
+def normalize_adjacency(a: CsrMatrix, val_dtype=None) -> CsrMatrix:
+    """gcn.hpp:29-72 on the B200: Ã = D̂^-½(A+I)D̂^-½ (fp64 arithmetic, bit-identical)."""
+    L = lib()
+    am, keep = _matrix_from_np(a.n_rows, a.n_cols, CSR, a.row_ptr, a.col_idx, a.values)
+    al = _HostAlloc(keep[1].dtype, val_dtype or keep[2].dtype)
+    out = al.output()
+    _check(L.aires_b200_normalize_adjacency(C.byref(am), C.byref(out)))
+    return CsrMatrix(a.n_rows, a.n_cols, al.ptr, al.idx[: out.nnz], al.val[: out.nnz])
+
+
+def combine(x: CsrMatrix, w: np.ndarray) -> CsrMatrix:
+    """gcn.hpp:90-116 on the B200: ReLU(X·W) with entries <= 0 dropped.  W dense (in, out), same
+    value type as X."""
+    L = lib()
+    xm, keep = _matrix_from_np(x.n_rows, x.n_cols, CSR, x.row_ptr, x.col_idx, x.values)
+    wd = np.ascontiguousarray(w, dtype=keep[2].dtype)
+    if wd.ndim != 2:
+        raise ValueError("W must be 2-D")
+    al = _HostAlloc(keep[1].dtype, keep[2].dtype)
+    out = al.output()
+    _check(L.aires_b200_combine(C.byref(xm), _np_view(wd), wd.shape[0], wd.shape[1], HOST, C.byref(out)))
+    return CsrMatrix(x.n_rows, wd.shape[1], al.ptr, al.idx[: out.nnz], al.val[: out.nnz])
+
+
+def gen_weights(in_dim: int, out_dim: int, seed: int) -> np.ndarray:
+    """synth.hpp:81-86 (same draws as the reference)."""
+    w = np.empty((in_dim, out_dim), dtype=np.float64)
+    _check(lib().aires_b200_synth_weights(in_dim, out_dim, seed, w.ctypes.data_as(C.POINTER(C.c_double))), synth=True)
+    return w
+
+
+@dataclasses.dataclass
+class LayerResult:
+    """gcn.hpp:118-123"""
+    h_next: CsrMatrix
+    aggregate_report: Optional[RunReport]
+    trace: list
+
+
+def layer_forward(a: CsrMatrix, h, weight: np.ndarray, budget: Optional[MemoryBudget] = None,
+                  mode: int = MODE_AUTO) -> LayerResult:
+    """gcn.hpp:125-132: normalize, aggregate (A·H; the out-of-core run when a budget is given),
+    combine with ReLU -- every step on the B200."""
+    at = normalize_adjacency(a)
+    if budget is not None:
+        res = run_aires(at, h, budget, mode=mode)
+        x, rep = res.c, res.report
+    else:
+        x, rep = spgemm_full(at, h, mode=mode), None
+    return LayerResult(combine(x, weight), rep, [])
 
 
 def last_profile() -> dict:

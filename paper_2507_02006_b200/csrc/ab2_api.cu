@@ -246,6 +246,23 @@ int aires_b200_run(const aires_b200_matrix* a, const aires_b200_matrix* b, const
   });
 }
 
+int aires_b200_normalize_adjacency(const aires_b200_matrix* a, aires_b200_output* out) {
+  return ab2::guarded([&] {
+    if (!a || !out) ab2::fail(AIRES_B200_INVALID_ARGUMENT, "null argument");
+    ab2::Ctx& ctx = ab2::ctx_for_thread();
+    ab2::normalize_adjacency(ctx, *a, *out);
+  });
+}
+
+int aires_b200_combine(const aires_b200_matrix* x, const void* w, uint64_t w_rows, uint64_t w_cols,
+                       uint32_t w_location, aires_b200_output* out) {
+  return ab2::guarded([&] {
+    if (!x || !out || (!w && w_rows * w_cols)) ab2::fail(AIRES_B200_INVALID_ARGUMENT, "null argument");
+    ab2::Ctx& ctx = ab2::ctx_for_thread();
+    ab2::combine(ctx, *x, w, w_rows, w_cols, w_location, *out);
+  });
+}
+
 void* aires_b200_stream(void) {
   void* s = nullptr;
   ab2::guarded([&] { s = static_cast<void*>(ab2::ctx_for_thread().stream); });

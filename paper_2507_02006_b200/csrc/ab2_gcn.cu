@@ -1,0 +1,408 @@
+// ab2_gcn.cu -- the steps either side of A·X in a GCN layer, on the device.
+//
+//   K9 normalize_adjacency (gcn.hpp:29-72): Ã = D̂^-½ (A + I) D̂^-½.  Self loops are inserted at
+//      their sorted position (a diagonal entry present in A becomes a_rr + 1), the weighted degree
+//      of each row is summed left to right in fp64 exactly as the reference does, and every entry
+//      becomes v / sqrt(d_i * d_j) with one IEEE multiply, sqrt and divide (the division form keeps
+//      1/sqrt(4) = 0.5 exact) -- bit-identical to the reference.
+//   K8 combine (gcn.hpp:90-116): H' = ReLU(X · W), X sparse CSR, W dense row-major; entries <= 0
+//      after the activation are dropped (re-sparsified CSR).  One warp per row, lanes over output
+//      columns (tiles of 256), terms added in ascending k with separate multiply and add: fp64 is
+//      bit-identical to the reference; fp32 is within tolerance.  Two passes (count, fill) around a
+//      scan give the exact CSR.
+#include <algorithm>
+#include <cmath>
+
+#include "ab2_internal.h"
+#include "ab2_kernels.cuh"
+
+namespace ab2 {
+
+namespace {
+
+template <class IdxT>
+__global__ void k_norm_count(const uint64_t* __restrict__ ptr, uint64_t base, const IdxT* __restrict__ col,
+                             int64_t n, int32_t* __restrict__ cnt, Ctl* __restrict__ ctl) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t lo = static_cast<int64_t>(ptr[r] - base), hi = static_cast<int64_t>(ptr[r + 1] - base);
+    const int64_t len = hi - lo;
+    while (lo < hi) {  // lower_bound(r)
+      const int64_t mid = (lo + hi) >> 1;
+      if (static_cast<int64_t>(col[mid]) < r)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    const bool diag = lo < static_cast<int64_t>(ptr[r + 1] - base) && static_cast<int64_t>(col[lo]) == r;
+    cnt[r] = static_cast<int32_t>(len + (diag ? 0 : 1));
+  }
+  (void)ctl;
+}
+
+template <class IdxT, class VIn>
+__global__ void k_norm_check(const IdxT* __restrict__ col, const VIn* __restrict__ val, uint64_t nnz, int64_t n,
+                             Ctl* __restrict__ ctl) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < nnz;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (val[i] < VIn(0)) ctl->bad_row = 1;                                // negative_weight
+    if (static_cast<uint64_t>(col[i]) >= static_cast<uint64_t>(n)) ctl->n_fix = 1;  // index_out_of_range
+  }
+}
+
+// Â = A + I at its sorted positions (values before normalisation, fp64).
+template <class IdxT, class VIn, class IdxO>
+__global__ void k_norm_fill(const uint64_t* __restrict__ ptr, uint64_t base, const IdxT* __restrict__ col,
+                            const VIn* __restrict__ val, int64_t n, const int64_t* __restrict__ optr,
+                            IdxO* __restrict__ ocol, double* __restrict__ oval) {
+  const int lane = lane_id();
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = wid; r < n; r += nw) {
+    const int64_t s = static_cast<int64_t>(ptr[r] - base), e = static_cast<int64_t>(ptr[r + 1] - base);
+    int64_t lo = s, hi = e;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (static_cast<int64_t>(col[mid]) < r)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    const int64_t p = lo;  // first entry with col >= r
+    const bool diag = p < e && static_cast<int64_t>(col[p]) == r;
+    const int64_t o = optr[r];
+    for (int64_t i = s + lane; i < e; i += 32) {
+      if (diag && i == p) continue;
+      const int64_t dst = o + (i - s) + (i >= p && !diag ? 1 : 0);
+      ocol[dst] = static_cast<IdxO>(col[i]);
+      oval[dst] = static_cast<double>(val[i]);
+    }
+    if (lane == 0) {
+      ocol[o + (p - s)] = static_cast<IdxO>(r);
+      oval[o + (p - s)] = diag ? static_cast<double>(val[p]) + 1.0 : 1.0;
+    }
+  }
+}
+
+// weighted degrees, summed left to right (gcn.hpp:61-64)
+__global__ void k_norm_degree(const int64_t* __restrict__ optr, const double* __restrict__ oval, int64_t n,
+                              double* __restrict__ deg) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double d = 0.0;
+    for (int64_t k = optr[r]; k < optr[r + 1]; k++) d = __dadd_rn(d, oval[k]);
+    deg[r] = d;
+  }
+}
+
+template <class IdxO, class VO>
+__global__ void k_norm_scale(const int64_t* __restrict__ optr, const IdxO* __restrict__ ocol,
+                             const double* __restrict__ oval, const double* __restrict__ deg, int64_t n,
+                             VO* __restrict__ out) {
+  const int lane = lane_id();
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = wid; r < n; r += nw) {
+    const double dr = deg[r];
+    for (int64_t k = optr[r] + lane; k < optr[r + 1]; k += 32)
+      out[k] = static_cast<VO>(__ddiv_rn(oval[k], __dsqrt_rn(__dmul_rn(dr, deg[static_cast<int64_t>(ocol[k])]))));
+  }
+}
+
+// ---- combine ---------------------------------------------------------------
+template <class V>
+__device__ __forceinline__ V mul_add(V acc, V a, V b) {
+  if constexpr (sizeof(V) == 8)
+    return __dadd_rn(acc, __dmul_rn(a, b));
+  else
+    return __fadd_rn(acc, __fmul_rn(a, b));
+}
+
+// FILL = false: per-row positive counts; FILL = true: writes the positives at optr[r].
+template <class V, class IdxT, class IdxO, int J, bool FILL>
+__global__ void __launch_bounds__(256) k_combine(const uint64_t* __restrict__ xptr, uint64_t xbase,
+                                                 const IdxT* __restrict__ xcol, const V* __restrict__ xval,
+                                                 int64_t rows, const V* __restrict__ w, int64_t w_rows, int64_t w_cols,
+                                                 int32_t* __restrict__ cnt, const int64_t* __restrict__ optr,
+                                                 IdxO* __restrict__ ocol, V* __restrict__ oval, Ctl* __restrict__ ctl) {
+  constexpr int TW = 32 * J;  // output columns per tile
+  const int lane = lane_id();
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = wid; r < rows; r += nw) {
+    const int64_t s = static_cast<int64_t>(xptr[r] - xbase), e = static_cast<int64_t>(xptr[r + 1] - xbase);
+    uint32_t written = 0;
+    for (int64_t t0 = 0; t0 < w_cols; t0 += TW) {
+      V acc[J];
+#pragma unroll
+      for (int j = 0; j < J; j++) acc[j] = V(0);
+      for (int64_t k = s; k < e; k++) {
+        const uint64_t in = static_cast<uint64_t>(xcol[k]);
+        if (in >= static_cast<uint64_t>(w_rows)) {
+          if (lane == 0) ctl->bad_row = 1;
+          continue;
+        }
+        const V v = xval[k];
+        const V* wr = w + in * w_cols + t0;
+#pragma unroll
+        for (int j = 0; j < J; j++) {
+          const int64_t c = lane + 32 * j;
+          if (t0 + c < w_cols) acc[j] = mul_add<V>(acc[j], v, __ldg(wr + c));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < J; j++) {
+        const int64_t c = t0 + lane + 32 * j;
+        const bool pos = c < w_cols && acc[j] > V(0);
+        const unsigned m = __ballot_sync(kFull, pos);
+        if constexpr (FILL) {
+          if (pos) {
+            const int64_t dst = optr[r] + written + __popc(m & ((1u << lane) - 1));
+            ocol[dst] = static_cast<IdxO>(c);
+            oval[dst] = acc[j];
+          }
+        }
+        written += __popc(m);
+      }
+    }
+    if constexpr (!FILL) {
+      if (lane == 0) cnt[r] = static_cast<int32_t>(written);
+    }
+  }
+}
+
+void scan_counts(Ctx& ctx, const int32_t* cnt, int64_t n, int64_t* out, Ctl* ctl, int* launches) {
+  if (n <= 0) {
+    AB2_CUDA(cudaMemsetAsync(out, 0, 8, ctx.stream));
+    AB2_CUDA(cudaMemsetAsync(&ctl->nnz, 0, 8, ctx.stream));
+    return;
+  }
+  const int64_t nb = (n + kScanTile - 1) / kScanTile;
+  int64_t* part = ctx.scan_part.as<int64_t>(std::max<int64_t>(nb, 1));
+  k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(cnt, n, part);
+  k_scan_part<<<1, 1024, 0, ctx.stream>>>(part, nb, ctl);
+  k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(cnt, n, part, out);
+  AB2_CUDA(cudaGetLastError());
+  *launches += 3;
+}
+
+int grid_of(int64_t n, int threads, int sms) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, int64_t(sms) * 32)));
+}
+
+// Stages a host CSR (ptr, idx, val) on the device through the context's A buffers.
+struct Staged {
+  const uint64_t* ptr;
+  uint64_t base;   // ptr value of idx[0] / val[0]
+  const void* idx;
+  const void* val;
+  uint64_t nnz;
+  uint64_t first;  // index of the first used entry in idx / val
+};
+
+Staged stage_csr(Ctx& ctx, const aires_b200_matrix& m) {
+  Staged s{m.ptr, 0, m.idx, m.val, 0, 0};
+  const uint64_t n = m.n_rows;
+  if (m.location == AIRES_B200_HOST) {
+    const uint64_t p0 = m.ptr[0], p1 = m.ptr[n];
+    if (p1 < p0 || p1 > m.span) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "row pointers exceed the index span");
+    uint64_t* dp = ctx.a_ptr.as<uint64_t>(n + 1);
+    void* di = ctx.a_col.get(std::max<uint64_t>(p1 - p0, 1) * m.idx_bytes);
+    void* dv = ctx.a_val.get(std::max<uint64_t>(p1 - p0, 1) * m.val_bytes);
+    AB2_CUDA(cudaMemcpyAsync(dp, m.ptr, (n + 1) * 8, cudaMemcpyHostToDevice, ctx.stream));
+    if (p1 > p0) {
+      AB2_CUDA(cudaMemcpyAsync(di, static_cast<const char*>(m.idx) + p0 * m.idx_bytes, (p1 - p0) * m.idx_bytes,
+                               cudaMemcpyHostToDevice, ctx.stream));
+      AB2_CUDA(cudaMemcpyAsync(dv, static_cast<const char*>(m.val) + p0 * m.val_bytes, (p1 - p0) * m.val_bytes,
+                               cudaMemcpyHostToDevice, ctx.stream));
+    }
+    s = Staged{dp, p0, di, dv, p1 - p0, 0};
+  } else {
+    uint64_t p[2] = {0, 0};
+    AB2_CUDA(cudaMemcpyAsync(&p[0], m.ptr, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    AB2_CUDA(cudaMemcpyAsync(&p[1], m.ptr + n, 8, cudaMemcpyDeviceToHost, ctx.stream));
+    AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (p[1] < p[0] || p[1] > m.span) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "row pointers exceed the index span");
+    s.nnz = p[1] - p[0];
+    s.first = p[0];  // kernels index idx/val by ptr[r] - base with base 0 (absolute pointers)
+  }
+  return s;
+}
+
+// Hands the result (device arrays ptr/idx/val) to the caller's allocator (host or device).
+template <class IdxO, class VO>
+void deliver(Ctx& ctx, aires_b200_output& out, uint64_t rows, uint64_t cols, uint64_t nnz, const int64_t* dptr,
+             const IdxO* didx, const VO* dval) {
+  void *optr = nullptr, *oidx = nullptr, *oval = nullptr;
+  const int rc = out.alloc(out.user, rows, nnz, &optr, &oidx, &oval);
+  if (rc != 0) fail(rc, "output allocator failed for " + std::to_string(nnz) + " nonzeros");
+  const cudaMemcpyKind kind = out.location == AIRES_B200_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  AB2_CUDA(cudaMemcpyAsync(optr, dptr, (rows + 1) * 8, kind, ctx.stream));
+  if (nnz) {
+    AB2_CUDA(cudaMemcpyAsync(oidx, didx, nnz * sizeof(IdxO), kind, ctx.stream));
+    AB2_CUDA(cudaMemcpyAsync(oval, dval, nnz * sizeof(VO), kind, ctx.stream));
+  }
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  out.n_rows = rows;
+  out.n_cols = cols;
+  out.nnz = nnz;
+  out.flops = 0;
+}
+
+template <class IdxT, class VIn, class IdxO, class VO>
+void normalize_t(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
+  const int64_t n = static_cast<int64_t>(a.n_rows);
+  Staged s = stage_csr(ctx, a);
+  Ctl* ctl = ctx.ctl.as<Ctl>(1);
+  AB2_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx.stream));
+  int32_t* cnt = ctx.cnt.as<int32_t>(std::max<int64_t>(n, 1));
+  int64_t* optr = ctx.cptr.as<int64_t>(n + 1);
+  const IdxT* col = static_cast<const IdxT*>(s.idx);
+  const VIn* val = static_cast<const VIn*>(s.val);
+  int launches = 0;
+  if (s.nnz) {
+    k_norm_check<IdxT, VIn><<<grid_of(static_cast<int64_t>(s.nnz), 256, ctx.sms), 256, 0, ctx.stream>>>(
+        col + s.first, val + s.first, s.nnz, n, ctl);
+    launches++;
+  }
+  if (n > 0) {
+    k_norm_count<IdxT><<<grid_of(n, 256, ctx.sms), 256, 0, ctx.stream>>>(s.ptr, s.base, col, n, cnt, ctl);
+    launches++;
+  }
+  scan_counts(ctx, cnt, n, optr, ctl, &launches);
+  Ctl* h = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
+  AB2_CUDA(cudaMemcpyAsync(h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (h->bad_row) fail(1 + 14, "adjacency weights must be nonnegative");  // errc::negative_weight
+  if (h->n_fix) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "column index outside the square adjacency");
+  const uint64_t nnz = n > 0 ? h->nnz : 0;
+  IdxO* ocol = static_cast<IdxO*>(ctx.c_col.get(std::max<uint64_t>(nnz, 1) * sizeof(IdxO)));
+  double* oval = static_cast<double*>(ctx.t_val.get(std::max<uint64_t>(nnz, 1) * 8));
+  double* deg = static_cast<double*>(ctx.rflops.get(std::max<int64_t>(n, 1) * 8));
+  VO* outv = static_cast<VO*>(ctx.c_val.get(std::max<uint64_t>(nnz, 1) * sizeof(VO)));
+  if (n > 0) {
+    k_norm_fill<IdxT, VIn, IdxO><<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(s.ptr, s.base, col, val, n,
+                                                                                       optr, ocol, oval);
+    k_norm_degree<<<grid_of(n, 128, ctx.sms), 128, 0, ctx.stream>>>(optr, oval, n, deg);
+    k_norm_scale<IdxO, VO><<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(optr, ocol, oval, deg, n, outv);
+    AB2_CUDA(cudaGetLastError());
+    launches += 3;
+  }
+  deliver<IdxO, VO>(ctx, out, static_cast<uint64_t>(n), static_cast<uint64_t>(n), nnz, optr, ocol, outv);
+  ctx.launches = launches;
+}
+
+template <class V, class IdxT, class IdxO, int J>
+void combine_launch(Ctx& ctx, const Staged& s, int64_t rows, const V* w, int64_t w_rows, int64_t w_cols, int32_t* cnt,
+                    int64_t* optr, IdxO* ocol, V* oval, Ctl* ctl, bool fill) {
+  const int g = grid_of(rows * 32, 256, ctx.sms);
+  if (fill)
+    k_combine<V, IdxT, IdxO, J, true><<<g, 256, 0, ctx.stream>>>(s.ptr, s.base, static_cast<const IdxT*>(s.idx),
+                                                                static_cast<const V*>(s.val), rows, w, w_rows,
+                                                                w_cols, cnt, optr, ocol, oval, ctl);
+  else
+    k_combine<V, IdxT, IdxO, J, false><<<g, 256, 0, ctx.stream>>>(s.ptr, s.base, static_cast<const IdxT*>(s.idx),
+                                                                 static_cast<const V*>(s.val), rows, w, w_rows,
+                                                                 w_cols, cnt, optr, ocol, oval, ctl);
+  AB2_CUDA(cudaGetLastError());
+}
+
+template <class V, class IdxT, class IdxO>
+void combine_t(Ctx& ctx, const aires_b200_matrix& x, const void* w_in, uint64_t w_rows, uint64_t w_cols,
+               uint32_t w_location, aires_b200_output& out) {
+  const int64_t rows = static_cast<int64_t>(x.n_rows);
+  Staged s = stage_csr(ctx, x);
+  const V* w = static_cast<const V*>(w_in);
+  if (w_location == AIRES_B200_HOST) {
+    V* dw = static_cast<V*>(ctx.x_val.get(std::max<uint64_t>(w_rows * w_cols, 1) * sizeof(V)));
+    AB2_CUDA(cudaMemcpyAsync(dw, w_in, w_rows * w_cols * sizeof(V), cudaMemcpyHostToDevice, ctx.stream));
+    w = dw;
+  }
+  Ctl* ctl = ctx.ctl.as<Ctl>(1);
+  AB2_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx.stream));
+  int32_t* cnt = ctx.cnt.as<int32_t>(std::max<int64_t>(rows, 1));
+  int64_t* optr = ctx.cptr.as<int64_t>(rows + 1);
+  const int J = w_cols >= 256 ? 8 : static_cast<int>((w_cols + 31) / 32);
+  auto run = [&](bool fill, IdxO* ocol, V* oval) {
+    if (rows <= 0 || w_cols == 0) return;
+    switch (std::max(J, 1)) {
+      case 1: combine_launch<V, IdxT, IdxO, 1>(ctx, s, rows, w, w_rows, w_cols, cnt, optr, ocol, oval, ctl, fill); break;
+      case 2: combine_launch<V, IdxT, IdxO, 2>(ctx, s, rows, w, w_rows, w_cols, cnt, optr, ocol, oval, ctl, fill); break;
+      case 3:
+      case 4: combine_launch<V, IdxT, IdxO, 4>(ctx, s, rows, w, w_rows, w_cols, cnt, optr, ocol, oval, ctl, fill); break;
+      default: combine_launch<V, IdxT, IdxO, 8>(ctx, s, rows, w, w_rows, w_cols, cnt, optr, ocol, oval, ctl, fill); break;
+    }
+  };
+  int launches = 0;
+  if (rows > 0 && w_cols > 0) {
+    run(false, nullptr, nullptr);
+    launches++;
+    scan_counts(ctx, cnt, rows, optr, ctl, &launches);
+  } else {
+    AB2_CUDA(cudaMemsetAsync(optr, 0, (rows + 1) * 8, ctx.stream));
+  }
+  Ctl* h = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
+  AB2_CUDA(cudaMemcpyAsync(h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (h->bad_row) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "feature column outside the weight rows");
+  const uint64_t nnz = rows > 0 && w_cols > 0 ? h->nnz : 0;
+  IdxO* ocol = static_cast<IdxO*>(ctx.c_col.get(std::max<uint64_t>(nnz, 1) * sizeof(IdxO)));
+  V* oval = static_cast<V*>(ctx.c_val.get(std::max<uint64_t>(nnz, 1) * sizeof(V)));
+  if (nnz) {
+    run(true, ocol, oval);
+    launches++;
+  }
+  deliver<IdxO, V>(ctx, out, static_cast<uint64_t>(rows), w_cols, nnz, optr, ocol, oval);
+  ctx.launches = launches;
+}
+
+}  // namespace
+
+void normalize_adjacency(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
+  if (a.layout != AIRES_B200_CSR) fail(AIRES_B200_INVALID_ARGUMENT, "adjacency must be CSR");
+  if (a.n_rows != a.n_cols)
+    fail(1 + 13, std::to_string(a.n_rows) + "x" + std::to_string(a.n_cols) + " adjacency is not square");  // non_square
+  if ((a.idx_bytes != 4 && a.idx_bytes != 8) || (a.val_bytes != 4 && a.val_bytes != 8) ||
+      (out.idx_bytes != 4 && out.idx_bytes != 8) || (out.val_bytes != 4 && out.val_bytes != 8))
+    fail(AIRES_B200_INVALID_ARGUMENT, "index / value widths must be 4 or 8");
+  if (!out.alloc) fail(AIRES_B200_INVALID_ARGUMENT, "output allocator is null");
+#define AB2_NORM(IT, VI, IO, VO_)                                                      \
+  if (a.idx_bytes == sizeof(IT) && a.val_bytes == sizeof(VI) && out.idx_bytes == sizeof(IO) && \
+      out.val_bytes == sizeof(VO_))                                                    \
+    return normalize_t<IT, VI, IO, VO_>(ctx, a, out);
+  AB2_NORM(uint32_t, float, uint32_t, float)
+  AB2_NORM(uint32_t, double, uint32_t, float)
+  AB2_NORM(uint32_t, float, uint32_t, double)
+  AB2_NORM(uint32_t, double, uint32_t, double)
+  AB2_NORM(uint64_t, double, uint64_t, double)
+  AB2_NORM(uint64_t, float, uint64_t, float)
+  AB2_NORM(uint64_t, double, uint64_t, float)
+  AB2_NORM(uint64_t, float, uint64_t, double)
+#undef AB2_NORM
+  fail(AIRES_B200_INVALID_ARGUMENT, "output index width must equal the adjacency's");
+}
+
+void combine(Ctx& ctx, const aires_b200_matrix& x, const void* w, uint64_t w_rows, uint64_t w_cols,
+             uint32_t w_location, aires_b200_output& out) {
+  if (x.layout != AIRES_B200_CSR) fail(AIRES_B200_INVALID_ARGUMENT, "features must be CSR");
+  if (x.n_cols != w_rows)
+    fail(AIRES_B200_DIMENSION_MISMATCH, "feature width " + std::to_string(x.n_cols) + " does not match weight rows " +
+                                            std::to_string(w_rows));
+  if (x.val_bytes != out.val_bytes) fail(AIRES_B200_INVALID_ARGUMENT, "value widths of X, W and H must agree");
+  if (!out.alloc) fail(AIRES_B200_INVALID_ARGUMENT, "output allocator is null");
+#define AB2_COMB(V, IT, IO)                                                                     \
+  if (x.val_bytes == sizeof(V) && x.idx_bytes == sizeof(IT) && out.idx_bytes == sizeof(IO)) \
+    return combine_t<V, IT, IO>(ctx, x, w, w_rows, w_cols, w_location, out);
+  AB2_COMB(float, uint32_t, uint32_t)
+  AB2_COMB(double, uint32_t, uint32_t)
+  AB2_COMB(float, uint64_t, uint64_t)
+  AB2_COMB(double, uint64_t, uint64_t)
+  AB2_COMB(float, uint32_t, uint64_t)
+  AB2_COMB(double, uint64_t, uint32_t)
+  AB2_COMB(double, uint32_t, uint64_t)
+  AB2_COMB(float, uint64_t, uint32_t)
+#undef AB2_COMB
+  fail(AIRES_B200_INVALID_ARGUMENT, "index widths must be 4 or 8");
+}
+
+}  // namespace ab2

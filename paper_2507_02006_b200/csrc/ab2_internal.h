@@ -138,6 +138,11 @@ struct TilePass {
 int tile_symbolic(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TileSym& t);
 int tile_product(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TilePass& t);
 
+// GCN layer steps either side of A·X (ab2_gcn.cu, gcn.hpp:29-116).
+void normalize_adjacency(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out);
+void combine(Ctx& ctx, const aires_b200_matrix& x, const void* w, uint64_t w_rows, uint64_t w_cols,
+             uint32_t w_location, aires_b200_output& out);
+
 // Out-of-core run (ab2_pipeline.cu).
 void destroy_pipe_cache(void* p);
 void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b, const aires_b200_run_config& cfg,

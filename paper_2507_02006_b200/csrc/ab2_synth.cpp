@@ -307,4 +307,12 @@ int aires_b200_synth_features(uint64_t n, uint64_t dim, double sparsity_pct, uin
 
 const char* aires_b200_synth_last_error(void) { return tl_synth_error.c_str(); }
 
+// synth.hpp:81-86 (gen_weights): dense in_dim x out_dim, uniform01 - 0.5, row-major, same draws.
+int aires_b200_synth_weights(uint64_t in_dim, uint64_t out_dim, uint64_t seed, double* out) {
+  if (!out && in_dim * out_dim) return AIRES_B200_INVALID_ARGUMENT;
+  std::mt19937_64 rng(seed);
+  for (uint64_t i = 0; i < in_dim * out_dim; i++) out[i] = static_cast<double>(rng() >> 11) * 0x1.0p-53 - 0.5;
+  return AIRES_B200_OK;
+}
+
 }  // extern "C"

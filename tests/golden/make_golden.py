@@ -12,6 +12,8 @@ can pin the oracle restatement and the B200 kernels against the reference's own 
   robw.npz      : robw_partition cuts (partition.hpp:52-74) incl. row_too_large cases
   features.npz  : gen_features (synth.hpp:73-78) outputs for the seeds the benches use
   run_aires.npz : run_aires (scheduler.hpp:72-168) ledgers on single-segment budgets
+  gcn.npz       : normalize_adjacency (gcn.hpp:29-72) incl. graphs with existing diagonals and
+                  weighted edges, gen_weights (synth.hpp:81-86) and combine (gcn.hpp:90-116)
 """
 import os
 import sys
@@ -120,6 +122,44 @@ def run_aires_cases():
     np.savez_compressed(os.path.join(HERE, "run_aires.npz"), **out)
 
 
+def gcn_cases():
+    rng = np.random.default_rng(91)
+    out = {}
+    n_cases = 0
+    graphs = []
+    for n, d, seed in ((40, 0.1, 1), (300, 0.03, 7), (2, 0.5, 3)):
+        rc, g = po.gen_symmetric(n, d, seed)
+        assert rc == 0
+        graphs.append((n, g))
+    # weighted, with some diagonal entries present
+    n = 60
+    p, i, v = random_csr(rng, n, n, 0.1, 0.1, 2.0)
+    graphs.append((n, (p, i, np.abs(v))))
+    for n, (p, i, v) in graphs:
+        rc, (tp, ti, tv) = po.normalize_adjacency(n, p, i, v, use_ref=True)
+        assert rc == 0
+        k = f"n{n_cases}"
+        out[k + "_in_ptr"], out[k + "_in_idx"], out[k + "_in_val"] = p, i, v
+        out[k + "_out_ptr"], out[k + "_out_idx"], out[k + "_out_val"] = tp, ti, tv
+        out[k + "_n"] = np.array([n], np.uint64)
+        n_cases += 1
+    out["n_norm"] = np.array([n_cases])
+    n_comb = 0
+    for rows, cin, cout, d, seed in ((30, 20, 7, 0.3, 4), (50, 64, 40, 0.2, 5), (10, 5, 300, 0.5, 6)):
+        x = random_csr(rng, rows, cin, d, -1.0, 1.0)
+        w = po.gen_weights(cin, cout, seed, use_ref=True)
+        rc, (hp, hi, hv) = po.combine(rows, cin, *x, w, use_ref=True)
+        assert rc == 0
+        k = f"c{n_comb}"
+        out[k + "_x_ptr"], out[k + "_x_idx"], out[k + "_x_val"] = x
+        out[k + "_w"] = w
+        out[k + "_h_ptr"], out[k + "_h_idx"], out[k + "_h_val"] = hp, hi, hv
+        out[k + "_dims"] = np.array([rows, cin, cout, seed], np.uint64)
+        n_comb += 1
+    out["n_comb"] = np.array([n_comb])
+    np.savez_compressed(os.path.join(HERE, "gcn.npz"), **out)
+
+
 if __name__ == "__main__":
     if not po.ref_available():
         sys.exit("oracle/_ref/libaires_ref.so missing: run `make -C oracle ref` (needs /root/reference)")
@@ -127,6 +167,7 @@ if __name__ == "__main__":
     robw_cases()
     feature_cases()
     run_aires_cases()
+    gcn_cases()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

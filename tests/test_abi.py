@@ -96,3 +96,10 @@ def test_dropin_binaries_fail_loudly_without_a_device():
         pytest.skip("drop-in binary absent or a device is visible")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode != 0 and "no CUDA device" in (r.stdout + r.stderr)
+
+
+def test_synth_weights_is_reference_gen_weights():
+    g = np.load(os.path.join(ROOT, "tests", "golden", "gcn.npz"))
+    for c in range(int(g["n_comb"][0])):
+        rows, cin, cout, seed = (int(x) for x in g[f"c{c}_dims"])
+        assert np.array_equal(ab.gen_weights(cin, cout, seed).view(np.uint64), g[f"c{c}_w"].view(np.uint64))

@@ -13,7 +13,7 @@ REF = os.path.join(ROOT, "oracle", "_ref")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("unit", ["spgemm_test", "partition_test", "scheduler_test", "acceptance"])
+@pytest.mark.parametrize("unit", ["spgemm_test", "partition_test", "scheduler_test", "gcn_test", "acceptance"])
 def test_reference_suite_on_b200(unit):
     exe = os.path.join(REF, f"dropin_{unit}")
     if not os.path.exists(exe):

@@ -249,3 +249,74 @@ def test_wide_operand_column_tiles(mode, monkeypatch):
                                            inner=False)
             assert_structure_equal(c.row_ptr, c.col_idx, wp, wi)
             assert_close_fp32(c.values, wv, sv)
+
+
+def _gold_gcn():
+    import os
+    return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "gcn.npz"))
+
+
+def test_normalize_adjacency_matches_reference_goldens():
+    """gcn.hpp:29-72 on the device: bit-identical to the reference (inserted and existing self loops,
+    weighted edges, a 2-node graph)."""
+    g = _gold_gcn()
+    for c in range(int(g["n_norm"][0])):
+        k = f"n{c}"
+        n = int(g[k + "_n"][0])
+        a = ab.CsrMatrix(n, n, g[k + "_in_ptr"], g[k + "_in_idx"], g[k + "_in_val"])
+        t = ab.normalize_adjacency(a)
+        assert np.array_equal(t.row_ptr, g[k + "_out_ptr"]) and np.array_equal(t.col_idx, g[k + "_out_idx"])
+        assert bits_equal(t.values, g[k + "_out_val"])
+    # errors (gcn_test.cpp:65-80)
+    with pytest.raises(ab.AiresError) as e:
+        ab.normalize_adjacency(ab.CsrMatrix(2, 3, np.zeros(3, np.uint64), np.zeros(0, np.uint64), np.zeros(0)))
+    assert e.value.code == ab.errc.non_square
+    with pytest.raises(ab.AiresError) as e:
+        ab.normalize_adjacency(csr(2, 2, np.array([0, 1, 1], np.uint64), np.array([1], np.uint64), np.array([-1.0])))
+    assert e.value.code == ab.errc.negative_weight
+
+
+def test_combine_matches_reference_goldens():
+    """gcn.hpp:90-116 on the device: ReLU(X·W), non-positives dropped; fp64 bit-identical, fp32 1e-5."""
+    g = _gold_gcn()
+    for c in range(int(g["n_comb"][0])):
+        k = f"c{c}"
+        rows, cin, cout, seed = (int(x) for x in g[k + "_dims"])
+        x = ab.CsrMatrix(rows, cin, g[k + "_x_ptr"], g[k + "_x_idx"], g[k + "_x_val"])
+        h = ab.combine(x, g[k + "_w"])
+        assert np.array_equal(h.row_ptr, g[k + "_h_ptr"]) and np.array_equal(h.col_idx, g[k + "_h_idx"])
+        assert bits_equal(h.values, g[k + "_h_val"])
+        x32 = ab.CsrMatrix(rows, cin, g[k + "_x_ptr"], g[k + "_x_idx"].astype(np.uint32),
+                           g[k + "_x_val"].astype(np.float32))
+        h32 = ab.combine(x32, g[k + "_w"].astype(np.float32))
+        # fp32 may flip entries whose fp64 value is within rounding of zero; compare on the common set
+        ref = {(r, int(cc)): vv for r in range(rows) for cc, vv in
+               zip(g[k + "_h_idx"][g[k + "_h_ptr"][r]:g[k + "_h_ptr"][r + 1]],
+                   g[k + "_h_val"][g[k + "_h_ptr"][r]:g[k + "_h_ptr"][r + 1]])}
+        got = {(r, int(cc)): float(vv) for r in range(rows) for cc, vv in
+               zip(h32.col_idx[h32.row_ptr[r]:h32.row_ptr[r + 1]], h32.values[h32.row_ptr[r]:h32.row_ptr[r + 1]])}
+        for key in set(ref) ^ set(got):
+            assert abs(ref.get(key, 0.0) + got.get(key, 0.0)) < 1e-5
+        for key in set(ref) & set(got):
+            assert abs(ref[key] - got[key]) <= 1e-5 * max(1.0, abs(ref[key]))
+    with pytest.raises(ab.AiresError) as e:
+        ab.combine(ab.CsrMatrix(1, 3, np.array([0, 0], np.uint64), np.zeros(0, np.uint64), np.zeros(0)), np.ones((2, 2)))
+    assert e.value.code == ab.errc.dimension_mismatch
+
+
+def test_layer_forward_two_layers_match_oracle():
+    """gcn.hpp:125-132 chained twice on a power-law graph, every step on the device, against the
+    oracle's normalize -> row-wise A·H -> combine (fp64, bit-identical)."""
+    a, _ = ab.synth_graph(3000, 30000, degree_cap=300, normalize=False, idx_dtype=np.uint64)
+    x = ab.synth_features(3000, 64, 95.0, 3, idx_dtype=np.uint64)
+    w1, w2 = ab.gen_weights(64, 32, 4), ab.gen_weights(32, 8, 5)
+    h1 = ab.layer_forward(a, x, w1).h_next
+    h2 = ab.layer_forward(a, h1, w2).h_next
+    rc, (tp, ti, tv) = po.normalize_adjacency(3000, a.row_ptr, a.col_idx, a.values)
+    want = (x.row_ptr, x.col_idx, x.values)
+    for w in (w1, w2):
+        rc, c, _ = po.spgemm_rowwise(tp, ti, tv, 3000, 3000, 3000, w.shape[0], *want, nthreads=4)
+        rc, want = po.combine(3000, w.shape[0], *c, w)
+        assert rc == 0
+    assert np.array_equal(h2.row_ptr, want[0]) and np.array_equal(h2.col_idx, want[1])
+    assert bits_equal(h2.values, want[2])

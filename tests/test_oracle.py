@@ -170,7 +170,7 @@ def test_oracle_normalize_adjacency_matches_reference():
     assert np.array_equal(bits(got[2]), bits(want[2]))
 
 
-REF_UNITS = ["spgemm_test", "partition_test", "memory_model_test", "sparse_test", "serialize_test",
+REF_UNITS = ["spgemm_test", "partition_test", "memory_model_test", "sparse_test", "serialize_test", "gcn_test",
              "scheduler_test"]
 
 
