@@ -131,12 +131,18 @@ def run_b200(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # AB2_FORCE_DEVICE / AB2_DIST_BACKEND exist only to exercise the multi-rank flow on a one-GPU box
+    # (gloo, every rank on the same device); production runs use NCCL, one GPU per rank.
+    if os.environ.get("AB2_FORCE_DEVICE"):
+        local = int(os.environ["AB2_FORCE_DEVICE"])
+    backend = os.environ.get("AB2_DIST_BACKEND", "nccl")
     dist = None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     torch.cuda.set_device(local)
+    cdev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")  # collective tensors
     L = ab.lib()
     ab._check(L.aires_b200_set_device(local))
     dev = torch.device("cuda", local)
@@ -186,7 +192,8 @@ def run_b200(args, cfg):
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    offsets_t = torch.zeros(world, dtype=torch.int64, device=dev)
+    from paper_2507_02006_b200 import shard
+    offsets = np.zeros(world, dtype=np.int64)
     with ClockSampler(local) as clk:
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
@@ -197,9 +204,8 @@ def run_b200(args, cfg):
             for k in prof_keys:
                 prof_sum[k] += p[k]
             launches += L.aires_b200_last_launches()
-            if dist:  # global row_ptr offsets: all-gather of one int64 nnz(C) per rank
-                mine = torch.tensor([int(out.nnz)], dtype=torch.int64, device=dev)
-                dist.all_gather_into_tensor(offsets_t, mine)
+            if dist:  # global row_ptr offsets: all-gather of one int64 nnz(C) per rank (shard.py)
+                offsets, _ = shard.global_offsets(int(out.nnz), device=cdev)
         ev1.record(lib_stream)
         ev1.synchronize()
     torch.cuda.synchronize(dev)
@@ -209,10 +215,10 @@ def run_b200(args, cfg):
     ms = ms_rank
     tot_macs = macs
     if dist:
-        t = torch.tensor([ms_rank], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_rank], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        m = torch.tensor([macs], dtype=torch.int64, device=dev)
+        m = torch.tensor([macs], dtype=torch.int64, device=cdev)
         dist.all_reduce(m)
         tot_macs = int(m.item())
     gflops = 2.0 * tot_macs / (ms * 1e-3) / 1e9
@@ -292,7 +298,7 @@ def run_b200(args, cfg):
         if int(hout_s.nnz) != nnz_c:
             raise RuntimeError(f"run_aires nnz {int(hout_s.nnz)} != spgemm nnz {nnz_c}")
         if dist:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            t = torch.tensor([e_ms], dtype=torch.float64, device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         h2d = int(rrep.h2d_bytes)
@@ -313,6 +319,10 @@ def run_b200(args, cfg):
         tA.clear(); tX.clear(); outbuf.clear()
         torch.cuda.empty_cache()
         ooc = out_of_core_leg(args, dev, L, ab, torch)
+    gcn = None
+    if world == 1 and not args.skip_gcn:
+        torch.cuda.empty_cache()
+        gcn = gcn_leg(args, dev, L, ab, torch)
 
     if rank == 0:
         line = {
@@ -324,9 +334,10 @@ def run_b200(args, cfg):
                        "nnz_a_tilde": g.nnz(), "x_cols": x.n_cols, "nnz_x": x.nnz(), "nnz_c": nnz_c,
                        "macs": tot_macs, "max_degree": st["max_degree"], "mode": args.mode,
                        "parallelism": f"row-block shards x{world}" if world > 1 else "single GPU",
+                       "global_row_ptr_offsets": [int(o) for o in offsets] if world > 1 else None,
                        "l2": "inputs larger than L2 (A 0.9 GB, C 1.1 GB vs 126 MB L2); X is meant to stay L2-resident",
                        "latency_ms": round(ms, 4)},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "out_of_core": ooc,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "out_of_core": ooc, "gcn_2layer": gcn,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -421,6 +432,100 @@ def out_of_core_leg(args, dev, L, ab, torch):
     }
 
 
+class DevOut:
+    """aires_b200_output handing out grow-only device tensors (torch) -- results stay in HBM."""
+
+    def __init__(self, ab, torch, dev, idx_dtype, val_dtype):
+        self.ab, self.torch, self.dev = ab, torch, dev
+        self.idx_dtype, self.val_dtype, self.t = idx_dtype, val_dtype, {}
+        self.fn = ab._ALLOC_FN(self._alloc)
+        self.out = ab._Output(ab.DEVICE, 4, 4 if val_dtype == torch.float32 else 8, 0, self.fn, None, 0, 0, 0, 0)
+
+    def _alloc(self, user, rows, nnz, pp, pi, pv):
+        T = self.torch
+        if self.t.get("rows", -1) < rows:
+            self.t["ptr"] = T.empty(rows + 1, dtype=T.int64, device=self.dev)
+            self.t["rows"] = rows
+        if self.t.get("cap", -1) < nnz:
+            self.t["idx"] = T.empty(max(nnz, 1), dtype=self.idx_dtype, device=self.dev)
+            self.t["val"] = T.empty(max(nnz, 1), dtype=self.val_dtype, device=self.dev)
+            self.t["cap"] = nnz
+        pp[0], pi[0], pv[0] = self.t["ptr"].data_ptr(), self.t["idx"].data_ptr(), self.t["val"].data_ptr()
+        return 0
+
+    def matrix(self, n_cols):
+        ab = self.ab
+        o = self.out
+        return ab._Matrix(o.n_rows, n_cols, ab.CSR, ab.DEVICE, 4, o.val_bytes, self.t["ptr"].data_ptr(),
+                          self.t["idx"].data_ptr(), self.t["val"].data_ptr(), o.nnz)
+
+
+def gcn_leg(args, dev, L, ab, torch):
+    """cfg5 on one GPU: the 2-layer GCN forward (gcn.hpp:125-132 twice) on the ogbn-products shape,
+    everything device-resident: Ã = normalize(A); H1 = ReLU((Ã·X)·W1); H2 = ReLU((Ã·H1)·W2)."""
+    cfg = CONFIGS["cfg3"]
+    t0 = time.time()
+    a, st = ab.synth_graph(cfg["n"], cfg["nnz"], alpha=0.75, degree_cap=cfg["cap"], seed=1, relabel_seed=2,
+                           normalize=False, idx_dtype=np.uint32, val_dtype=np.float32)
+    x = ab.synth_features(cfg["n"], cfg["dim"], 99.0, 3, idx_dtype=np.uint32, val_dtype=np.float32)
+    w1 = torch.from_numpy(ab.gen_weights(cfg["dim"], 256, 4).astype(np.float32)).to(dev)
+    w2 = torch.from_numpy(ab.gen_weights(256, 47, 5).astype(np.float32)).to(dev)
+    log(f"[gcn] inputs in {time.time() - t0:.1f}s")
+    tA = [torch.from_numpy(a.row_ptr.view(np.int64)).to(dev), torch.from_numpy(a.col_idx.view(np.int32)).to(dev),
+          torch.from_numpy(a.values).to(dev)]
+    tX = [torch.from_numpy(x.row_ptr.view(np.int64)).to(dev), torch.from_numpy(x.col_idx.view(np.int32)).to(dev),
+          torch.from_numpy(x.values).to(dev)]
+    n = a.n_rows
+    am = ab._Matrix(n, n, ab.CSR, ab.DEVICE, 4, 4, tA[0].data_ptr(), tA[1].data_ptr(), tA[2].data_ptr(), a.nnz())
+    xm = ab._Matrix(n, x.n_cols, ab.CSR, ab.DEVICE, 4, 4, tX[0].data_ptr(), tX[1].data_ptr(), tX[2].data_ptr(), x.nnz())
+    o_t, o_c1, o_h1, o_c2, o_h2 = (DevOut(ab, torch, dev, torch.int32, torch.float32) for _ in range(5))
+    stream = torch.cuda.ExternalStream(L.aires_b200_stream(), device=dev)
+    stats = {}
+
+    def forward(record=None):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        ev[0].record(stream)
+        ab._check(L.aires_b200_normalize_adjacency(C.byref(am), C.byref(o_t.out)))
+        at = o_t.matrix(n)
+        ev[1].record(stream)
+        ab._check(L.aires_b200_spgemm(C.byref(at), C.byref(xm), ab.MODE_FP32, C.byref(o_c1.out)))
+        macs1 = int(o_c1.out.flops)
+        ev[2].record(stream)
+        ab._check(L.aires_b200_combine(C.byref(o_c1.matrix(x.n_cols)), C.c_void_p(w1.data_ptr()), w1.shape[0],
+                                       w1.shape[1], ab.DEVICE, C.byref(o_h1.out)))
+        ev[3].record(stream)
+        h1 = o_h1.matrix(w1.shape[1])
+        ab._check(L.aires_b200_spgemm(C.byref(at), C.byref(h1), ab.MODE_FP32, C.byref(o_c2.out)))
+        macs2 = int(o_c2.out.flops)
+        ev[4].record(stream)
+        ab._check(L.aires_b200_combine(C.byref(o_c2.matrix(w1.shape[1])), C.c_void_p(w2.data_ptr()), w2.shape[0],
+                                       w2.shape[1], ab.DEVICE, C.byref(o_h2.out)))
+        ev[5].record(stream)
+        ev[5].synchronize()
+        if record is not None:
+            names = ["normalize", "aggregate1", "combine1", "aggregate2", "combine2"]
+            for i, nm in enumerate(names):
+                record.setdefault(nm, []).append(ev[i].elapsed_time(ev[i + 1]))
+            record.setdefault("total", []).append(ev[0].elapsed_time(ev[5]))
+        return macs1, macs2
+
+    for _ in range(max(1, args.warmup)):
+        macs1, macs2 = forward()
+    rec = {}
+    for _ in range(args.steps):
+        forward(rec)
+    med = {k: round(float(np.median(v)), 3) for k, v in rec.items()}
+    comb_flops = 2 * (int(o_c1.out.nnz) * 256 + int(o_c2.out.nnz) * 47)
+    return {"workload": "cfg5 (1 GPU): 2-layer GCN forward on the ogbn-products shape, W1 100x256, W2 256x47 "
+                        "(gen_weights seeds 4, 5), all operands device-resident, fp32",
+            "ms": med, "nnz": {"a_tilde": int(o_t.out.nnz), "c1": int(o_c1.out.nnz), "h1": int(o_h1.out.nnz),
+                               "c2": int(o_c2.out.nnz), "h2": int(o_h2.out.nnz)},
+            "macs_aggregate": [macs1, macs2],
+            "gflops_aggregate": round(2.0 * (macs1 + macs2) / ((med["aggregate1"] + med["aggregate2"]) * 1e-3) / 1e9, 2),
+            "gflops_combine": round(comb_flops / ((med["combine1"] + med["combine2"]) * 1e-3) / 1e9, 2),
+            "layers_per_s": round(2.0 / (med["total"] * 1e-3), 2)}
+
+
 def sample_rows(n: int, count: int, seed: int = 11) -> np.ndarray:
     rng = np.random.default_rng(seed)
     return np.sort(rng.choice(n, size=min(count, n), replace=False)).astype(np.uint64)
@@ -507,6 +612,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-ooc", action="store_true", help="skip the cfg3 out-of-core leg")
+    ap.add_argument("--skip-gcn", action="store_true", help="skip the cfg5 2-layer GCN leg")
     ap.add_argument("--ooc-frac", type=float, default=0.25, help="cfg3 device budget / (B_A+B_X+B_C)")
     ap.add_argument("--ooc-buffers", type=int, default=3)
     args = ap.parse_args()
