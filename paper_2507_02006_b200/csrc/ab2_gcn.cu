@@ -119,13 +119,23 @@ __device__ __forceinline__ V mul_add(V acc, V a, V b) {
 }
 
 // FILL = false: per-row positive counts; FILL = true: writes the positives at optr[r].
-template <class V, class IdxT, class IdxO, int J, bool FILL>
+// SMEM: W is staged once per CTA in shared memory (every X entry reads a whole W row, so from
+// global memory the L1 datapath bound the kernel: 36 ms for the products-shaped layer 2).
+template <class V, class IdxT, class IdxO, int J, bool FILL, bool SMEM>
 __global__ void __launch_bounds__(256) k_combine(const uint64_t* __restrict__ xptr, uint64_t xbase,
                                                  const IdxT* __restrict__ xcol, const V* __restrict__ xval,
-                                                 int64_t rows, const V* __restrict__ w, int64_t w_rows, int64_t w_cols,
+                                                 int64_t rows, const V* __restrict__ wg, int64_t w_rows, int64_t w_cols,
                                                  int32_t* __restrict__ cnt, const int64_t* __restrict__ optr,
                                                  IdxO* __restrict__ ocol, V* __restrict__ oval, Ctl* __restrict__ ctl) {
   constexpr int TW = 32 * J;  // output columns per tile
+  extern __shared__ __align__(16) unsigned char smem_w[];
+  const V* __restrict__ w = wg;
+  if constexpr (SMEM) {
+    V* ws = reinterpret_cast<V*>(smem_w);
+    for (int64_t i = threadIdx.x; i < w_rows * w_cols; i += blockDim.x) ws[i] = wg[i];
+    __syncthreads();
+    w = ws;
+  }
   const int lane = lane_id();
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -136,18 +146,29 @@ __global__ void __launch_bounds__(256) k_combine(const uint64_t* __restrict__ xp
       V acc[J];
 #pragma unroll
       for (int j = 0; j < J; j++) acc[j] = V(0);
-      for (int64_t k = s; k < e; k++) {
-        const uint64_t in = static_cast<uint64_t>(xcol[k]);
-        if (in >= static_cast<uint64_t>(w_rows)) {
-          if (lane == 0) ctl->bad_row = 1;
-          continue;
+      // the row's entries are read 32 at a time (coalesced) and broadcast with SHFL, in order
+      for (int64_t k0 = s; k0 < e; k0 += 32) {
+        uint64_t lin = 0;
+        V lv = V(0);
+        if (k0 + lane < e) {
+          lin = static_cast<uint64_t>(xcol[k0 + lane]);
+          lv = xval[k0 + lane];
+          if (lin >= static_cast<uint64_t>(w_rows)) {
+            ctl->bad_row = 1;
+            lin = 0;
+            lv = V(0);
+          }
         }
-        const V v = xval[k];
-        const V* wr = w + in * w_cols + t0;
+        const int cnt_k = static_cast<int>(e - k0 < 32 ? e - k0 : 32);
+        for (int kk = 0; kk < cnt_k; kk++) {
+          const uint64_t in = __shfl_sync(kFull, lin, kk);
+          const V v = __shfl_sync(kFull, lv, kk);
+          const V* wr = w + in * w_cols + t0;
 #pragma unroll
-        for (int j = 0; j < J; j++) {
-          const int64_t c = lane + 32 * j;
-          if (t0 + c < w_cols) acc[j] = mul_add<V>(acc[j], v, __ldg(wr + c));
+          for (int j = 0; j < J; j++) {
+            const int64_t c = lane + 32 * j;
+            if (t0 + c < w_cols) acc[j] = mul_add<V>(acc[j], v, wr[c]);
+          }
         }
       }
 #pragma unroll
@@ -292,19 +313,36 @@ void normalize_t(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
   ctx.launches = launches;
 }
 
+template <class V, class IdxT, class IdxO, int J, bool FILL, bool SMEM>
+void combine_launch2(Ctx& ctx, const Staged& s, int64_t rows, const V* w, int64_t w_rows, int64_t w_cols, int32_t* cnt,
+                     int64_t* optr, IdxO* ocol, V* oval, Ctl* ctl) {
+  auto k = k_combine<V, IdxT, IdxO, J, FILL, SMEM>;
+  size_t smem = 0;
+  int grid = grid_of(rows * 32, 256, ctx.sms);
+  if constexpr (SMEM) {
+    smem = static_cast<size_t>(w_rows * w_cols) * sizeof(V);
+    AB2_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int nb = 0;
+    AB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 256, smem));
+    grid = std::max(1, std::min(grid, std::max(nb, 1) * ctx.sms));  // persistent: W staged once per CTA
+  }
+  k<<<grid, 256, smem, ctx.stream>>>(s.ptr, s.base, static_cast<const IdxT*>(s.idx), static_cast<const V*>(s.val),
+                                     rows, w, w_rows, w_cols, cnt, optr, ocol, oval, ctl);
+  AB2_CUDA(cudaGetLastError());
+}
+
 template <class V, class IdxT, class IdxO, int J>
 void combine_launch(Ctx& ctx, const Staged& s, int64_t rows, const V* w, int64_t w_rows, int64_t w_cols, int32_t* cnt,
                     int64_t* optr, IdxO* ocol, V* oval, Ctl* ctl, bool fill) {
-  const int g = grid_of(rows * 32, 256, ctx.sms);
-  if (fill)
-    k_combine<V, IdxT, IdxO, J, true><<<g, 256, 0, ctx.stream>>>(s.ptr, s.base, static_cast<const IdxT*>(s.idx),
-                                                                static_cast<const V*>(s.val), rows, w, w_rows,
-                                                                w_cols, cnt, optr, ocol, oval, ctl);
+  const bool smem = static_cast<size_t>(w_rows * w_cols) * sizeof(V) <= 200 * 1024 && env_int("AB2_COMBINE_SMEM", 1);
+  if (fill && smem)
+    combine_launch2<V, IdxT, IdxO, J, true, true>(ctx, s, rows, w, w_rows, w_cols, cnt, optr, ocol, oval, ctl);
+  else if (fill)
+    combine_launch2<V, IdxT, IdxO, J, true, false>(ctx, s, rows, w, w_rows, w_cols, cnt, optr, ocol, oval, ctl);
+  else if (smem)
+    combine_launch2<V, IdxT, IdxO, J, false, true>(ctx, s, rows, w, w_rows, w_cols, cnt, optr, ocol, oval, ctl);
   else
-    k_combine<V, IdxT, IdxO, J, false><<<g, 256, 0, ctx.stream>>>(s.ptr, s.base, static_cast<const IdxT*>(s.idx),
-                                                                 static_cast<const V*>(s.val), rows, w, w_rows,
-                                                                 w_cols, cnt, optr, ocol, oval, ctl);
-  AB2_CUDA(cudaGetLastError());
+    combine_launch2<V, IdxT, IdxO, J, false, false>(ctx, s, rows, w, w_rows, w_cols, cnt, optr, ocol, oval, ctl);
 }
 
 template <class V, class IdxT, class IdxO>
