@@ -20,6 +20,7 @@
  *   aires_b200_checksum      -> aires::checksum (FNV-1a of C)   serialize.hpp:50-59
  *   aires_b200_normalize_adjacency -> aires::normalize_adjacency gcn.hpp:29-72
  *   aires_b200_combine       -> aires::combine (ReLU(X*W))      gcn.hpp:90-116
+ *   aires_b200_layer_fused   -> aggregate + combine of layer_forward, fused  gcn.hpp:81-116
  *   aires_b200_last_error    -> the what() string of aires::error error.hpp:53-62
  *
  * Status codes: 0 = OK, otherwise 1 + (int)aires::errc (error.hpp:9-27), so
@@ -184,6 +185,12 @@ int aires_b200_normalize_adjacency(const aires_b200_matrix* a, aires_b200_output
    of X's value type at w_location; fp64 bit-identical to the reference, fp32 within tolerance. */
 int aires_b200_combine(const aires_b200_matrix* x, const void* w, uint64_t w_rows, uint64_t w_cols,
                        uint32_t w_location, aires_b200_output* out);
+
+/* H' = ReLU((Ã * H) * W) in one pass without materialising Ã*H (gcn.hpp:81-116 fused): the
+   aggregate and combine of layer_forward for a dense-ish H (fp32, u32 columns; H width <= 256,
+   W width <= 128).  Terms are re-associated: within the fp32 tolerance, not bit-exact. */
+int aires_b200_layer_fused(const aires_b200_matrix* a_tilde, const aires_b200_matrix* h, const void* w,
+                           uint64_t w_rows, uint64_t w_cols, uint32_t w_location, aires_b200_output* out);
 
 /* FNV-1a 64 of a CSR in the reference's canonical byte stream (serialize.hpp:50-59); host only.
    row_ptr may be absolute (it is rebased); 4-byte indices / values are widened to u64 / f64. */

@@ -138,6 +138,8 @@ def lib() -> C.CDLL:
     L.aires_b200_synth_last_error.restype = C.c_char_p
     L.aires_b200_normalize_adjacency.argtypes = [P(_Matrix), P(_Output)]
     L.aires_b200_combine.argtypes = [P(_Matrix), C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, P(_Output)]
+    L.aires_b200_layer_fused.argtypes = [P(_Matrix), P(_Matrix), C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32,
+                                         P(_Output)]
     L.aires_b200_synth_weights.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, P(C.c_double)]
     L.aires_b200_checksum.restype = C.c_uint64
     L.aires_b200_checksum.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, P(C.c_uint64), C.c_void_p, C.c_uint32,
@@ -509,6 +511,22 @@ def combine(x: CsrMatrix, w: np.ndarray) -> CsrMatrix:
     out = al.output()
     _check(L.aires_b200_combine(C.byref(xm), _np_view(wd), wd.shape[0], wd.shape[1], HOST, C.byref(out)))
     return CsrMatrix(x.n_rows, wd.shape[1], al.ptr, al.idx[: out.nnz], al.val[: out.nnz])
+
+
+def layer_fused(a_tilde: CsrMatrix, h: CsrMatrix, w: np.ndarray) -> CsrMatrix:
+    """ReLU((Ã·H)·W) in one device pass (fp32, dense-ish H): the aggregate + combine of layer_forward
+    without materialising Ã·H; within the fp32 tolerance of the unfused chain."""
+    L = lib()
+    am, ka = _matrix_from_np(a_tilde.n_rows, a_tilde.n_cols, CSR, a_tilde.row_ptr, a_tilde.col_idx.astype(np.uint32),
+                             a_tilde.values.astype(np.float32))
+    hm, kh = _matrix_from_np(h.n_rows, h.n_cols, CSR, h.row_ptr, h.col_idx.astype(np.uint32),
+                             h.values.astype(np.float32))
+    wd = np.ascontiguousarray(w, dtype=np.float32)
+    al = _HostAlloc(np.uint32, np.float32)
+    out = al.output()
+    _check(L.aires_b200_layer_fused(C.byref(am), C.byref(hm), _np_view(wd), wd.shape[0], wd.shape[1], HOST,
+                                    C.byref(out)))
+    return CsrMatrix(a_tilde.n_rows, wd.shape[1], al.ptr, al.idx[: out.nnz], al.val[: out.nnz])
 
 
 def gen_weights(in_dim: int, out_dim: int, seed: int) -> np.ndarray:

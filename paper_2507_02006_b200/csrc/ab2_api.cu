@@ -263,6 +263,15 @@ int aires_b200_combine(const aires_b200_matrix* x, const void* w, uint64_t w_row
   });
 }
 
+int aires_b200_layer_fused(const aires_b200_matrix* a_tilde, const aires_b200_matrix* h, const void* w,
+                           uint64_t w_rows, uint64_t w_cols, uint32_t w_location, aires_b200_output* out) {
+  return ab2::guarded([&] {
+    if (!a_tilde || !h || !out || (!w && w_rows * w_cols)) ab2::fail(AIRES_B200_INVALID_ARGUMENT, "null argument");
+    ab2::Ctx& ctx = ab2::ctx_for_thread();
+    ab2::layer_fused(ctx, *a_tilde, *h, w, w_rows, w_cols, w_location, *out);
+  });
+}
+
 void* aires_b200_stream(void) {
   void* s = nullptr;
   ab2::guarded([&] { s = static_cast<void*>(ab2::ctx_for_thread().stream); });

@@ -394,6 +394,181 @@ void combine_t(Ctx& ctx, const aires_b200_matrix& x, const void* w_in, uint64_t 
   ctx.launches = launches;
 }
 
+// ---- fused aggregate + combine for a dense-ish H (fp32) ---------------------
+// H' = ReLU((Ã·H)·W) without materialising Ã·H.  When H is dense enough (post-ReLU GCN features
+// are ~50% dense) its rows are gathered as dense fp32 rows: lane l accumulates the H columns
+// l + 32m in registers (no shared-memory scatter, no bank conflicts), then the row is multiplied
+// by W from shared memory (stored lane-major, Wt[m][j][l], conflict-free) and the 32 partial sums
+// per output chunk are reduce-scattered across the warp (31 SHFLs per 32 outputs).  fp32 only:
+// the terms are re-associated (within the stated tolerance); fp64 layers run unfused (exact).
+template <int M>
+__global__ void k_densify(const uint64_t* __restrict__ ptr, uint64_t base, const uint32_t* __restrict__ col,
+                          const float* __restrict__ val, int64_t K, int64_t hc, float* __restrict__ hd) {
+  const int lane = lane_id();
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t k = wid; k < K; k += nw) {
+    float* row = hd + k * (32 * M);
+#pragma unroll
+    for (int m = 0; m < M; m++) row[lane + 32 * m] = 0.f;
+    __syncwarp();
+    for (int64_t t = static_cast<int64_t>(ptr[k] - base) + lane; t < static_cast<int64_t>(ptr[k + 1] - base); t += 32)
+      if (col[t] < hc) row[col[t]] = val[t];
+  }
+}
+
+// Wt[(m * w_cols + j) * 32 + l] = W[(l + 32 m) * w_cols + j]  (zero past the rows of W)
+__global__ void k_w_lane_major(const float* __restrict__ w, int64_t w_rows, int64_t w_cols, int M,
+                               float* __restrict__ wt) {
+  const int64_t total = static_cast<int64_t>(M) * w_cols * 32;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t l = i % 32, j = (i / 32) % w_cols, m = i / (32 * w_cols);
+    const int64_t c = l + 32 * m;
+    wt[i] = c < w_rows ? w[c * w_cols + j] : 0.f;
+  }
+}
+
+// Reduce-scatter of 32 per-lane partials p[0..31]: afterwards lane l holds sum over lanes of p[l].
+__device__ __forceinline__ float reduce_scatter32(float (&p)[32]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool upper = (lane & h) != 0;
+#pragma unroll
+    for (int i = 0; i < h; i++) {
+      // keep the half of the values this lane will own; send the other half to the partner
+      const float send = upper ? p[i] : p[i + h];
+      const float keep = upper ? p[i + h] : p[i];
+      p[i] = keep + __shfl_xor_sync(kFull, send, h);
+    }
+  }
+  return p[0];
+}
+
+template <int M, int JC>
+__global__ void __launch_bounds__(256) k_agg_comb(const uint64_t* __restrict__ aptr, uint64_t abase,
+                                                  const uint32_t* __restrict__ acol, const float* __restrict__ aval,
+                                                  int64_t rows, int64_t K, const float* __restrict__ hd,
+                                                  const float* __restrict__ wt_g, int64_t w_cols,
+                                                  float* __restrict__ dense_out, int32_t* __restrict__ cnt) {
+  extern __shared__ __align__(16) float wt[];
+  for (int64_t i = threadIdx.x; i < static_cast<int64_t>(M) * w_cols * 32; i += blockDim.x) wt[i] = wt_g[i];
+  __syncthreads();
+  const int lane = lane_id();
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = wid; r < rows; r += nw) {
+    float acc[M];
+#pragma unroll
+    for (int m = 0; m < M; m++) acc[m] = 0.f;
+    const int64_t s = static_cast<int64_t>(aptr[r] - abase), e = static_cast<int64_t>(aptr[r + 1] - abase);
+    for (int64_t b = s; b < e; b += 32) {
+      uint32_t k = 0;
+      float a = 0.f;
+      if (b + lane < e) {
+        k = acol[b + lane];
+        a = aval[b + lane];
+        if (k >= K) a = 0.f, k = 0;
+      }
+      const int n = static_cast<int>(e - b < 32 ? e - b : 32);
+      int kk = 0;
+      for (; kk + 4 <= n; kk += 4) {  // four dense rows in flight
+        float x[4][M];
+        float av[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const uint32_t kq = __shfl_sync(kFull, k, kk + q);
+          av[q] = __shfl_sync(kFull, a, kk + q);
+          const float* row = hd + static_cast<int64_t>(kq) * (32 * M) + lane;
+#pragma unroll
+          for (int m = 0; m < M; m++) x[q][m] = __ldg(row + 32 * m);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+          for (int m = 0; m < M; m++) acc[m] = fmaf(av[q], x[q][m], acc[m]);
+      }
+      for (; kk < n; kk++) {
+        const uint32_t kq = __shfl_sync(kFull, k, kk);
+        const float aq = __shfl_sync(kFull, a, kk);
+        const float* row = hd + static_cast<int64_t>(kq) * (32 * M) + lane;
+#pragma unroll
+        for (int m = 0; m < M; m++) acc[m] = fmaf(aq, __ldg(row + 32 * m), acc[m]);
+      }
+    }
+    int32_t count = 0;
+#pragma unroll
+    for (int jc = 0; jc < JC; jc++) {
+      float p[32];
+#pragma unroll
+      for (int jj = 0; jj < 32; jj++) {
+        const int64_t j = jc * 32 + jj;
+        float v = 0.f;
+        if (j < w_cols) {
+#pragma unroll
+          for (int m = 0; m < M; m++) v = fmaf(acc[m], wt[(m * w_cols + j) * 32 + lane], v);
+        }
+        p[jj] = v;
+      }
+      const float o = reduce_scatter32(p);
+      const int64_t j = jc * 32 + lane;
+      const bool pos = j < w_cols && o > 0.f;
+      if (j < w_cols) dense_out[r * w_cols + j] = pos ? o : 0.f;
+      count += __popc(__ballot_sync(kFull, pos));
+    }
+    if (lane == 0) cnt[r] = count;
+  }
+}
+
+template <class IdxO>
+__global__ void k_compact_rows(const float* __restrict__ dense, int64_t rows, int64_t w_cols,
+                               const int64_t* __restrict__ optr, IdxO* __restrict__ ocol, float* __restrict__ oval) {
+  const int lane = lane_id();
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = wid; r < rows; r += nw) {
+    int64_t o = optr[r];
+    for (int64_t j0 = 0; j0 < w_cols; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const float v = j < w_cols ? dense[r * w_cols + j] : 0.f;
+      const unsigned m = __ballot_sync(kFull, v > 0.f);
+      if (v > 0.f) {
+        const int64_t d = o + __popc(m & ((1u << lane) - 1));
+        ocol[d] = static_cast<IdxO>(j);
+        oval[d] = v;
+      }
+      o += __popc(m);
+    }
+  }
+}
+
+template <int M, int JC>
+void agg_comb_launch(Ctx& ctx, const uint64_t* aptr, uint64_t abase, const uint32_t* acol, const float* aval,
+                     int64_t rows, int64_t K, const float* hd, const float* wt, int64_t w_cols, float* dense,
+                     int32_t* cnt) {
+  auto k = k_agg_comb<M, JC>;
+  const size_t smem = static_cast<size_t>(M) * w_cols * 32 * sizeof(float);
+  AB2_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int nb = 0;
+  AB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 256, smem));
+  if (nb < 1) fail(AIRES_B200_UNSUPPORTED_FORMAT, "weights too large for the fused layer");
+  const int grid = std::max(1, std::min(grid_of(rows * 32, 256, ctx.sms), nb * ctx.sms));
+  k<<<grid, 256, smem, ctx.stream>>>(aptr, abase, acol, aval, rows, K, hd, wt, w_cols, dense, cnt);
+  AB2_CUDA(cudaGetLastError());
+}
+
+template <int M>
+void agg_comb_m(Ctx& ctx, int jc, const uint64_t* aptr, uint64_t abase, const uint32_t* acol, const float* aval,
+                int64_t rows, int64_t K, const float* hd, const float* wt, int64_t w_cols, float* dense, int32_t* cnt) {
+  switch (jc) {
+    case 1: agg_comb_launch<M, 1>(ctx, aptr, abase, acol, aval, rows, K, hd, wt, w_cols, dense, cnt); break;
+    case 2: agg_comb_launch<M, 2>(ctx, aptr, abase, acol, aval, rows, K, hd, wt, w_cols, dense, cnt); break;
+    case 3: agg_comb_launch<M, 3>(ctx, aptr, abase, acol, aval, rows, K, hd, wt, w_cols, dense, cnt); break;
+    default: agg_comb_launch<M, 4>(ctx, aptr, abase, acol, aval, rows, K, hd, wt, w_cols, dense, cnt); break;
+  }
+}
+
 }  // namespace
 
 void normalize_adjacency(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
@@ -441,6 +616,103 @@ void combine(Ctx& ctx, const aires_b200_matrix& x, const void* w, uint64_t w_row
   AB2_COMB(float, uint64_t, uint32_t)
 #undef AB2_COMB
   fail(AIRES_B200_INVALID_ARGUMENT, "index widths must be 4 or 8");
+}
+
+}  // namespace ab2
+
+namespace ab2 {
+
+// H' = ReLU((Ã·H)·W), fp32, fused (dense-H path); Ã and H device or host CSR (u32 columns, f32).
+void layer_fused(Ctx& ctx, const aires_b200_matrix& at, const aires_b200_matrix& h, const void* w, uint64_t w_rows,
+                 uint64_t w_cols, uint32_t w_location, aires_b200_output& out) {
+  if (at.layout != AIRES_B200_CSR || h.layout != AIRES_B200_CSR)
+    fail(AIRES_B200_INVALID_ARGUMENT, "Ã and H must be CSR");
+  if (at.idx_bytes != 4 || at.val_bytes != 4 || h.idx_bytes != 4 || h.val_bytes != 4 || out.val_bytes != 4)
+    fail(AIRES_B200_INVALID_ARGUMENT, "the fused layer is fp32 with 4-byte column indices");
+  if (at.n_cols != h.n_rows || h.n_cols != w_rows)
+    fail(AIRES_B200_DIMENSION_MISMATCH, "Ã, H and W dimensions do not chain");
+  const int M = static_cast<int>((h.n_cols + 31) / 32);
+  const int JC = static_cast<int>((w_cols + 31) / 32);
+  if (M < 1 || M > 8 || JC < 1 || JC > 4)
+    fail(AIRES_B200_UNSUPPORTED_FORMAT, "fused layer supports H widths <= 256 and W widths <= 128");
+  if (!out.alloc) fail(AIRES_B200_INVALID_ARGUMENT, "output allocator is null");
+  const int64_t rows = static_cast<int64_t>(at.n_rows), K = static_cast<int64_t>(h.n_rows);
+  int launches = 0;
+  // H -> dense rows (32*M floats each)
+  const Staged hs = stage_csr(ctx, h);
+  float* hd = static_cast<float*>(ctx.xo_val.get(std::max<int64_t>(K, 1) * 32 * M * sizeof(float)));
+  switch (M) {
+#define AB2_DENS(MM) case MM: k_densify<MM><<<grid_of(K * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(hs.ptr, hs.base, static_cast<const uint32_t*>(hs.idx), static_cast<const float*>(hs.val), K, static_cast<int64_t>(h.n_cols), hd); break;
+    AB2_DENS(1) AB2_DENS(2) AB2_DENS(3) AB2_DENS(4) AB2_DENS(5) AB2_DENS(6) AB2_DENS(7) AB2_DENS(8)
+#undef AB2_DENS
+  }
+  launches++;
+  // W -> lane-major
+  const float* wsrc = static_cast<const float*>(w);
+  if (w_location == AIRES_B200_HOST) {
+    float* dw = static_cast<float*>(ctx.x_idx.get(std::max<uint64_t>(w_rows * w_cols, 1) * sizeof(float)));
+    AB2_CUDA(cudaMemcpyAsync(dw, w, w_rows * w_cols * sizeof(float), cudaMemcpyHostToDevice, ctx.stream));
+    wsrc = dw;
+  }
+  float* wt = static_cast<float*>(ctx.xo_desc.get(static_cast<size_t>(M) * w_cols * 32 * sizeof(float)));
+  k_w_lane_major<<<grid_of(static_cast<int64_t>(M) * w_cols * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(
+      wsrc, static_cast<int64_t>(w_rows), static_cast<int64_t>(w_cols), M, wt);
+  launches++;
+  // Ã rows (staged after H: the A buffers of the context)
+  const Staged as = stage_csr(ctx, at);
+  float* dense = static_cast<float*>(ctx.t_val.get(std::max<int64_t>(rows, 1) * w_cols * sizeof(float)));
+  int32_t* cnt = ctx.cnt.as<int32_t>(std::max<int64_t>(rows, 1));
+  int64_t* optr = ctx.cptr.as<int64_t>(rows + 1);
+  Ctl* ctl = ctx.ctl.as<Ctl>(1);
+  AB2_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx.stream));
+  AB2_CUDA(cudaEventRecord(ctx.ev[0], ctx.stream));
+  if (rows > 0) {
+    const auto* ac = static_cast<const uint32_t*>(as.idx);
+    const auto* av = static_cast<const float*>(as.val);
+    switch (M) {
+#define AB2_AC(MM) case MM: agg_comb_m<MM>(ctx, JC, as.ptr, as.base, ac, av, rows, K, hd, wt, static_cast<int64_t>(w_cols), dense, cnt); break;
+      AB2_AC(1) AB2_AC(2) AB2_AC(3) AB2_AC(4) AB2_AC(5) AB2_AC(6) AB2_AC(7) AB2_AC(8)
+#undef AB2_AC
+    }
+    launches++;
+  }
+  AB2_CUDA(cudaEventRecord(ctx.ev[1], ctx.stream));
+  scan_counts(ctx, cnt, rows, optr, ctl, &launches);
+  Ctl* hc = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
+  AB2_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  const uint64_t nnz = rows > 0 ? hc->nnz : 0;
+  void *optr_o = nullptr, *oidx = nullptr, *oval = nullptr;
+  const int rc = out.alloc(out.user, static_cast<uint64_t>(rows), nnz, &optr_o, &oidx, &oval);
+  if (rc != 0) fail(rc, "output allocator failed for " + std::to_string(nnz) + " nonzeros");
+  void* dcol = out.location == AIRES_B200_DEVICE ? oidx : ctx.c_col.get(std::max<uint64_t>(nnz, 1) * out.idx_bytes);
+  float* dval = out.location == AIRES_B200_DEVICE ? static_cast<float*>(oval)
+                                                  : static_cast<float*>(ctx.c_val.get(std::max<uint64_t>(nnz, 1) * 4));
+  if (rows > 0 && nnz > 0) {
+    if (out.idx_bytes == 4)
+      k_compact_rows<uint32_t><<<grid_of(rows * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(
+          dense, rows, static_cast<int64_t>(w_cols), optr, static_cast<uint32_t*>(dcol), dval);
+    else
+      k_compact_rows<uint64_t><<<grid_of(rows * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(
+          dense, rows, static_cast<int64_t>(w_cols), optr, static_cast<uint64_t*>(dcol), dval);
+    AB2_CUDA(cudaGetLastError());
+    launches++;
+  }
+  const cudaMemcpyKind kind = out.location == AIRES_B200_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  AB2_CUDA(cudaMemcpyAsync(optr_o, optr, (rows + 1) * 8, kind, ctx.stream));
+  if (out.location != AIRES_B200_DEVICE && nnz) {
+    AB2_CUDA(cudaMemcpyAsync(oidx, dcol, nnz * out.idx_bytes, kind, ctx.stream));
+    AB2_CUDA(cudaMemcpyAsync(oval, dval, nnz * 4, kind, ctx.stream));
+  }
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  float ms = 0;
+  AB2_CUDA(cudaEventElapsedTime(&ms, ctx.ev[0], ctx.ev[1]));
+  ctx.last_ms = ms;
+  ctx.launches = launches;
+  out.n_rows = static_cast<uint64_t>(rows);
+  out.n_cols = w_cols;
+  out.nnz = nnz;
+  out.flops = 0;
 }
 
 }  // namespace ab2

@@ -142,6 +142,8 @@ int tile_product(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TilePass
 void normalize_adjacency(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out);
 void combine(Ctx& ctx, const aires_b200_matrix& x, const void* w, uint64_t w_rows, uint64_t w_cols,
              uint32_t w_location, aires_b200_output& out);
+void layer_fused(Ctx& ctx, const aires_b200_matrix& at, const aires_b200_matrix& h, const void* w, uint64_t w_rows,
+                 uint64_t w_cols, uint32_t w_location, aires_b200_output& out);
 
 // Out-of-core run (ab2_pipeline.cu).
 void destroy_pipe_cache(void* p);

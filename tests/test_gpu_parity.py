@@ -320,3 +320,29 @@ def test_layer_forward_two_layers_match_oracle():
         assert rc == 0
     assert np.array_equal(h2.row_ptr, want[0]) and np.array_equal(h2.col_idx, want[1])
     assert bits_equal(h2.values, want[2])
+
+
+@pytest.mark.parametrize("hcols,wcols", [(256, 47), (100, 128), (64, 8), (33, 40)])
+def test_layer_fused_matches_unfused_chain(hcols, wcols):
+    """ReLU((Ã·H)·W) fused (dense-ish H gathered as dense rows) against the fp64 oracle chain
+    normalize -> row-wise A·H -> combine: values within 1e-5 relative to the cell's scale; entries
+    whose exact value is within rounding of zero may flip across the ReLU."""
+    a, _ = ab.synth_graph(4000, 40000, degree_cap=400, normalize=True, idx_dtype=np.uint64)
+    h = ab.synth_features(4000, hcols, 50.0, 7, idx_dtype=np.uint64)
+    w = ab.gen_weights(hcols, wcols, 9)
+    got = ab.layer_fused(a, h, w)
+    rc, c, _ = po.spgemm_rowwise(a.row_ptr, a.col_idx, a.values, 4000, 4000, 4000, hcols, h.row_ptr, h.col_idx,
+                                 h.values, nthreads=4)
+    rc, (wp, wi, wv) = po.combine(4000, hcols, *c, w)
+    # scale per output cell: sum_c |C[r,c]| * |W[c,j]|
+    rc, (sp, si, sv) = po.combine(4000, hcols, c[0], c[1], np.abs(c[2]), np.abs(w))
+    scale = {}
+    for r in range(4000):
+        for cc, vv in zip(si[sp[r]:sp[r + 1]], sv[sp[r]:sp[r + 1]]):
+            scale[(r, int(cc))] = vv
+    want = {(r, int(cc)): vv for r in range(4000) for cc, vv in zip(wi[wp[r]:wp[r + 1]], wv[wp[r]:wp[r + 1]])}
+    have = {(r, int(cc)): float(vv) for r in range(4000) for cc, vv in
+            zip(got.col_idx[got.row_ptr[r]:got.row_ptr[r + 1]], got.values[got.row_ptr[r]:got.row_ptr[r + 1]])}
+    for key in set(want) | set(have):
+        err = abs(want.get(key, 0.0) - have.get(key, 0.0))
+        assert err <= 1e-5 * max(scale.get(key, 0.0), 1e-30), (key, want.get(key), have.get(key), scale.get(key))
