@@ -311,11 +311,6 @@ __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, co
   const V tiny = p.tiny;
   const uint32_t copy_s = static_cast<uint32_t>(__cvta_generic_to_shared(EXACT ? acc : acc + gid * p.stride));
   uint32_t macs = 0;
-  auto col_of = [&](uint32_t c) -> uint32_t {
-    c &= kSlotColMask;
-    if constexpr (RANGE) c = (c >= c_lo && c < c_hi) ? c : trash;
-    return c;
-  };
   auto add = [&](uint32_t c, V a, V x) {
     if constexpr (XZ) {
       if constexpr (EXACT)
@@ -378,16 +373,19 @@ __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, co
         for (int u = 0; u < B; u++) {
           const bool real = col[u] != trash;
           macs += real;
-          uint32_t c = col[u];
-          if constexpr (RANGE) c = (c >= c_lo && c < c_hi) ? c : trash;
+          // (column-owner split: a column outside this warp's range is not touched at all, so no
+          // two warps ever share a cell -- not even a trash cell)
+          const uint32_t c = col[u];
+          const bool mine = real && (!RANGE || (c >= c_lo && c < c_hi));
           if constexpr (EXACT) {
 #pragma unroll
             for (int g = 0; g < G; g++) {
-              if (gid == g && real) add(c, aa[u], xv[u]);
+              if (gid == g && mine) add(c, aa[u], xv[u]);
               __syncwarp();
             }
           } else {
-            if (real) add(c, aa[u], xv[u]);
+            if (mine) add(c, aa[u], xv[u]);
+            __syncwarp();  // steps u and u+1 of one group may hit the same cell (different X rows)
           }
         }
         __syncwarp();
@@ -407,18 +405,25 @@ __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, co
           const bool real = col[u] != trash && !(col[u] & kSlotOvf);
           macs += real;
           for (uint32_t t = ent; t < tn; t += W) macs++;
+          auto mine = [&](uint32_t c) { return !RANGE || (c >= c_lo && c < c_hi); };
           if constexpr (EXACT) {
 #pragma unroll
             for (int g = 0; g < G; g++) {
               if (gid == g) {
-                if (real) add(col_of(col[u]), aa[u], xv[u]);
-                for (uint32_t t = ent; t < tn; t += W) add(col_of(xcol[mo + t]), aa[u], xval[mo + t]);
+                if (real && mine(col[u] & kSlotColMask)) add(col[u] & kSlotColMask, aa[u], xv[u]);
+                for (uint32_t t = ent; t < tn; t += W) {
+                  const uint32_t c = static_cast<uint32_t>(xcol[mo + t]);
+                  if (mine(c)) add(c, aa[u], xval[mo + t]);
+                }
               }
               __syncwarp();
             }
           } else {
-            if (real) add(col_of(col[u]), aa[u], xv[u]);
-            for (uint32_t t = ent; t < tn; t += W) add(col_of(xcol[mo + t]), aa[u], xval[mo + t]);
+            if (real && mine(col[u] & kSlotColMask)) add(col[u] & kSlotColMask, aa[u], xv[u]);
+            for (uint32_t t = ent; t < tn; t += W) {
+              const uint32_t c = static_cast<uint32_t>(xcol[mo + t]);
+              if (mine(c)) add(c, aa[u], xval[mo + t]);
+            }
             __syncwarp();
           }
         }
@@ -492,6 +497,7 @@ __device__ __forceinline__ uint32_t fold_count(V* acc, int stride, int copies, i
     acc[c] = v;
     cnt += __popc(__ballot_sync(kFull, !Sentinel<V>::is(v)));
   }
+  __syncwarp();
   return cnt;
 }
 
@@ -513,6 +519,7 @@ __device__ __forceinline__ void emit_copy0(V* acc, int n_cols, IdxT* __restrict_
     }
     n += __popc(b);
   }
+  __syncwarp();  // the next row's accumulation reads these cells from other lanes
 }
 
 // Warp-level bump allocation in the staging area.

@@ -165,6 +165,7 @@ __device__ __forceinline__ uint32_t walk5(const Num5Args<IdxT>& p, const IdxT* _
             if constexpr (XZ) zero |= ax[u] * xv == 0.f;
             smem_fma5(copy_s + xe[u].x, ax[u], xv);
           }
+          __syncwarp();  // consecutive steps of one group may hit the same cell
         }
         __syncwarp();
       }
