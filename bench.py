@@ -40,6 +40,10 @@ CONFIGS = {
                  n=232_965, nnz=114_000_000, dim=602, cap=20_000),
     "cfg3": dict(workload="cfg3: ogbn-products-shaped 2,449,029 nodes / 62M edges, X 100 @1%",
                  n=2_449_029, nnz=62_000_000, dim=100, cap=20_000),
+    # one of eight row-block shards of the PPI-scale graph (68M nodes / 1.5B edges, X 256 @1%):
+    # the per-GPU unit of the 8-GPU run, generated as its own power-law block
+    "cfg4shard": dict(workload="cfg4 shard: 1/8 of the PPI-scale graph (8.5M nodes / 187.5M edges, X 256 @1%), "
+                               "pinned-host streaming", n=8_500_000, nnz=187_500_000, dim=256, cap=50_000),
 }
 
 
@@ -319,6 +323,10 @@ def run_b200(args, cfg):
         tA.clear(); tX.clear(); outbuf.clear()
         torch.cuda.empty_cache()
         ooc = out_of_core_leg(args, dev, L, ab, torch)
+    ppi = None
+    if world == 1 and args.cfg4_shard:
+        torch.cuda.empty_cache()
+        ppi = out_of_core_leg(args, dev, L, ab, torch, "cfg4shard")
     gcn = None
     if world == 1 and not args.skip_gcn:
         torch.cuda.empty_cache()
@@ -337,7 +345,7 @@ def run_b200(args, cfg):
                        "global_row_ptr_offsets": [int(o) for o in offsets] if world > 1 else None,
                        "l2": "inputs larger than L2 (A 0.9 GB, C 1.1 GB vs 126 MB L2); X is meant to stay L2-resident",
                        "latency_ms": round(ms, 4)},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "out_of_core": ooc, "gcn_2layer": gcn,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "out_of_core": ooc, "gcn_2layer": gcn, "cfg4_shard": ppi,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -365,11 +373,11 @@ def link_bandwidth(dev, nbytes=512 << 20, reps=5):
     return out
 
 
-def out_of_core_leg(args, dev, L, ab, torch):
+def out_of_core_leg(args, dev, L, ab, torch, cfg_name="cfg3"):
     """cfg3 (ogbn-products-shaped) through aires_b200_run with the device budget capped to
     args.ooc_frac of B_A + B_X + B_C: A and X in pinned host memory, C drained to pinned host
     memory tile by tile.  Roofline = the host link (measured in this run)."""
-    cfg = CONFIGS["cfg3"]
+    cfg = CONFIGS[cfg_name]
     g, st, x = make_inputs(cfg, 0, 1)
     n, K = g.n_rows, x.n_rows
     hA = [torch.from_numpy(g.row_ptr.view(np.int64)).pin_memory(), torch.from_numpy(g.col_idx.view(np.int32)).pin_memory(),
@@ -630,6 +638,8 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-ooc", action="store_true", help="skip the cfg3 out-of-core leg")
     ap.add_argument("--skip-gcn", action="store_true", help="skip the cfg5 2-layer GCN leg")
+    ap.add_argument("--cfg4-shard", action="store_true", help="also run one 1/8 shard of the PPI-scale cfg4 "
+                    "out of core (slow input generation)")
     ap.add_argument("--ooc-frac", type=float, default=0.25, help="cfg3 device budget / (B_A+B_X+B_C)")
     ap.add_argument("--ooc-buffers", type=int, default=3)
     args = ap.parse_args()
