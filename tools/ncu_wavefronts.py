@@ -15,6 +15,8 @@ for b in out.split('"Kernel Name",')[1:]:
         continue
     rows = list(csv.reader(io.StringIO(b.split("\n", 1)[1])))
     h = rows[0]
+    if "L1 Wavefronts Shared" not in h:
+        continue
     col = {k: h.index(k) for k in ("Source", "Instructions Executed", "L1 Wavefronts Shared",
                                    "L1 Wavefronts Shared Ideal", "L2 Theoretical Sectors Global", "L1 Tag Requests Global")}
     agg = collections.defaultdict(lambda: [0, 0, 0, 0, 0])
