@@ -21,6 +21,8 @@
  *   aires_b200_normalize_adjacency -> aires::normalize_adjacency gcn.hpp:29-72
  *   aires_b200_combine       -> aires::combine (ReLU(X*W))      gcn.hpp:90-116
  *   aires_b200_layer_fused   -> aggregate + combine of layer_forward, fused  gcn.hpp:81-116
+ *   aires_b200_spgemm_segments -> read_segments + spgemm_block per segment  serialize.hpp:148-209,
+ *                               spgemm.hpp:134-139 (the storage leg: cuFile/GDS or pinned host)
  *   aires_b200_last_error    -> the what() string of aires::error error.hpp:53-62
  *
  * Status codes: 0 = OK, otherwise 1 + (int)aires::errc (error.hpp:9-27), so
@@ -176,6 +178,29 @@ typedef struct aires_b200_run_report {
 int aires_b200_run(const aires_b200_matrix* a, const aires_b200_matrix* b,
                    const aires_b200_run_config* cfg, aires_b200_output* c,
                    aires_b200_run_report* report);
+
+/* ---- storage leg: RoBW segments from the reference's segment container ------ */
+/* Called once per segment with the positioned fragment (CsrBlockResult, spgemm.hpp:47-52): local
+   row_ptr (end_row - start_row + 1 u64), col_idx (nnz u64), values (nnz, 4 or 8 bytes per the mode);
+   the pointers are valid during the call.  Return 0 to continue. */
+typedef int (*aires_b200_segment_fn)(void* user, uint64_t seg_index, uint64_t start_row, uint64_t end_row,
+                                     uint64_t nnz, const uint64_t* row_ptr, const void* col_idx,
+                                     const void* values, uint64_t flops);
+typedef struct aires_b200_storage_report {
+  uint64_t segments;
+  uint64_t bytes_read; /* file bytes moved to the device */
+  uint64_t flops;
+  uint64_t c_nnz;
+  uint32_t used_gds;   /* 1: cuFileRead into device memory (GPUDirect Storage); 0: pread + pinned H2D */
+  uint32_t reserved;
+  double read_ms;      /* host time spent reading (overlapped with the products) */
+  double total_ms;
+} aires_b200_storage_report;
+/* Streams the segments of `path` (serialize.hpp:148-209 format, ElementSizes {index_bytes,
+   value_bytes}) to the device and multiplies each against B (host or device, CSR or CSC). */
+int aires_b200_spgemm_segments(const char* path, uint32_t index_bytes, uint32_t value_bytes, uint64_t a_n_cols,
+                               const aires_b200_matrix* b, uint32_t mode, aires_b200_segment_fn cb, void* user,
+                               aires_b200_storage_report* report);
 
 /* ---- GCN layer steps either side of A·X ------------------ */
 /* Ã = D̂^-½ (A + I) D̂^-½, bit-identical to the reference (fp64 arithmetic; fp32 output is the

@@ -99,6 +99,8 @@ def ref() -> C.CDLL:
         L.ref_spgemm_rows_timed.argtypes = [U64P, U64P, F64P, C.c_uint64, C.c_uint64, U64P, C.c_uint64,
                                             C.c_uint64, C.c_uint64, U64P, U64P, F64P, C.c_int, U64P, U64P, U64P]
         L.ref_free.argtypes = [C.POINTER(AoCsr)]
+        L.ref_write_segments.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, U64P, U64P, F64P, C.c_uint64, C.c_uint64,
+                                         C.c_uint64]
         L.ref_gen_weights.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, F64P]
         L.ref_combine.argtypes = [C.c_uint64, C.c_uint64, U64P, U64P, F64P, F64P, C.c_uint64, C.c_uint64,
                                   C.POINTER(AoCsr)]
@@ -321,3 +323,9 @@ def combine(rows, x_cols, row_ptr, col_idx, values, w, use_ref=False):
     if rc:
         return rc, None
     return 0, _take(m, rows + 1, L.ref_free if use_ref else L.ao_free)
+
+
+def ref_write_segments(path, n_rows, n_cols, row_ptr, col_idx, values, m_a, I=8, V=8) -> int:
+    """The reference's robw_partition + write_segments to `path` (serialize.hpp:148-174)."""
+    rp, ci, va = _u64(row_ptr), _u64(col_idx), _f64(values)
+    return int(ref().ref_write_segments(path.encode(), n_rows, n_cols, _p64(rp), _p64(ci), _pf(va), m_a, I, V))

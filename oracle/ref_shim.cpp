@@ -9,6 +9,7 @@
 // Build recipe: oracle/Makefile (reference flags -std=c++20 -O3 -DNDEBUG, no -march,
 // -ffp-contract=off; proj/CMakeLists.txt:3,8-10).
 #include <atomic>
+#include <fstream>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -177,6 +178,20 @@ int ref_normalize_adjacency(uint64_t n, const uint64_t* row_ptr, const uint64_t*
   try {
     export_csr(normalize_adjacency(make_csr(n, n, row_ptr, col_idx, values)).a_tilde, out);
     return 0;
+  } catch (const error& e) {
+    return code_of(e);
+  }
+}
+
+// robw_partition + write_segments (partition.hpp:52-74, serialize.hpp:148-174) to a file.
+int ref_write_segments(const char* path, uint64_t n_rows, uint64_t n_cols, const uint64_t* row_ptr,
+                       const uint64_t* col_idx, const double* values, uint64_t m_a, uint64_t I, uint64_t V) {
+  try {
+    ElementSizes s{I, V};
+    std::vector<RobwSegment> segs = robw_partition(make_csr(n_rows, n_cols, row_ptr, col_idx, values), m_a, s);
+    std::ofstream out(path, std::ios::binary);
+    write_segments(out, segs, s);
+    return out ? 0 : 1 + static_cast<int>(errc::io_error);
   } catch (const error& e) {
     return code_of(e);
   }

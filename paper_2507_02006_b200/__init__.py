@@ -94,6 +94,15 @@ class _RunReport(C.Structure):
                 ("phase3_ms", C.c_double)]
 
 
+_SEG_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64),
+                      C.c_void_p, C.c_void_p, C.c_uint64)
+
+
+class _StorageReport(C.Structure):
+    _fields_ = [("segments", C.c_uint64), ("bytes_read", C.c_uint64), ("flops", C.c_uint64), ("c_nnz", C.c_uint64),
+                ("used_gds", C.c_uint32), ("reserved", C.c_uint32), ("read_ms", C.c_double), ("total_ms", C.c_double)]
+
+
 class _GraphSpec(C.Structure):
     _fields_ = [("n", C.c_uint64), ("target_nnz", C.c_uint64), ("alpha", C.c_double),
                 ("degree_cap", C.c_uint64), ("seed", C.c_uint64), ("relabel_seed", C.c_uint64),
@@ -140,6 +149,8 @@ def lib() -> C.CDLL:
     L.aires_b200_combine.argtypes = [P(_Matrix), C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32, P(_Output)]
     L.aires_b200_layer_fused.argtypes = [P(_Matrix), P(_Matrix), C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32,
                                          P(_Output)]
+    L.aires_b200_spgemm_segments.argtypes = [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint64, P(_Matrix), C.c_uint32,
+                                             _SEG_FN, C.c_void_p, P(_StorageReport)]
     L.aires_b200_synth_weights.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, P(C.c_double)]
     L.aires_b200_checksum.restype = C.c_uint64
     L.aires_b200_checksum.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, P(C.c_uint64), C.c_void_p, C.c_uint32,
@@ -511,6 +522,108 @@ def combine(x: CsrMatrix, w: np.ndarray) -> CsrMatrix:
     out = al.output()
     _check(L.aires_b200_combine(C.byref(xm), _np_view(wd), wd.shape[0], wd.shape[1], HOST, C.byref(out)))
     return CsrMatrix(x.n_rows, wd.shape[1], al.ptr, al.idx[: out.nnz], al.val[: out.nnz])
+
+
+# ---------------------------------------------------------------------------
+# containers (serialize.hpp:60-209) and the storage leg
+# ---------------------------------------------------------------------------
+
+def _put(arr, width: int) -> bytes:
+    a = np.asarray(arr)
+    if width == 8:
+        return np.ascontiguousarray(a, dtype="<u8").tobytes()
+    return np.ascontiguousarray(a, dtype="<u4").tobytes()
+
+
+def _put_val(arr, width: int) -> bytes:
+    a = np.asarray(arr, dtype=np.float64)
+    return (np.ascontiguousarray(a, dtype="<f8") if width == 8 else np.ascontiguousarray(a.astype(np.float32),
+                                                                                     dtype="<f4")).tobytes()
+
+
+def write_segments(path: str, segs: list, s: ElementSizes = ElementSizes()) -> None:
+    """serialize.hpp:148-174: per segment a length-prefixed little-endian record."""
+    with open(path, "wb") as f:
+        for seg in segs:
+            if s.index_bytes < 8:
+                lim = (1 << (8 * s.index_bytes)) - 1
+                if (seg.row_ptr_local.size and int(np.max(seg.row_ptr_local)) > lim) or \
+                        (seg.col_idx.size and int(np.max(seg.col_idx)) > lim):
+                    raise AiresError(1 + errc.capacity_exceeded, "index exceeds index width")
+            record = 32 + seg.row_ptr_local.shape[0] * s.index_bytes + seg.nnz() * (s.index_bytes + s.value_bytes)
+            f.write(_put([record, seg.seg_index, seg.start_row, seg.end_row, seg.nnz()], 8))
+            f.write(_put(seg.row_ptr_local, s.index_bytes))
+            f.write(_put(seg.col_idx, s.index_bytes))
+            f.write(_put_val(seg.values, s.value_bytes))
+
+
+def write_matrix(path: str, a: CsrMatrix) -> None:
+    """serialize.hpp:102-122: the ARSM container (all 64-bit little-endian)."""
+    with open(path, "wb") as f:
+        f.write(b"ARSM" + _put([1, a.n_rows, a.n_cols, a.nnz()], 8))
+        f.write(_put(a.row_ptr, 8) + _put(a.col_idx, 8) + _put_val(a.values, 8))
+
+
+def read_matrix(path: str) -> CsrMatrix:
+    """serialize.hpp:124-142."""
+    raw = np.fromfile(path, dtype=np.uint8)
+    if raw[:4].tobytes() != b"ARSM":
+        raise AiresError(1 + errc.parse_error, "bad matrix container magic")
+    ver, nr, nc, nnz = (int(v) for v in raw[4:36].view("<u8"))
+    if ver != 1:
+        raise AiresError(1 + errc.unsupported_format, f"matrix container version {ver}")
+    o = 36
+    rp = raw[o:o + 8 * (nr + 1)].view("<u8").copy(); o += 8 * (nr + 1)
+    ci = raw[o:o + 8 * nnz].view("<u8").copy(); o += 8 * nnz
+    va = raw[o:o + 8 * nnz].view("<f8").copy()
+    return CsrMatrix(nr, nc, rp, ci, va)
+
+
+def assemble_blocks(blocks: list, n_rows: int, n_cols: int) -> CsrMatrix:
+    """spgemm.hpp:155-181: consecutive fragments -> one CSR (throws on gaps / overlaps)."""
+    expect = 0
+    ptrs, cols, vals = [np.zeros(1, np.uint64)], [], []
+    base = 0
+    for b in sorted(blocks, key=lambda b: b.start_row):
+        if b.start_row != expect:
+            raise AiresError(1 + errc.non_adjacent_fragments, f"fragment starts at {b.start_row}, expected {expect}")
+        expect = b.end_row
+        rp = np.asarray(b.fragment.row_ptr, dtype=np.uint64)
+        ptrs.append(rp[1:] - rp[0] + np.uint64(base))
+        base += int(rp[-1] - rp[0])
+        cols.append(b.fragment.col_idx)
+        vals.append(b.fragment.values)
+    if expect != n_rows:
+        raise AiresError(1 + errc.non_adjacent_fragments, f"fragments cover {expect} of {n_rows} rows")
+    return CsrMatrix(n_rows, n_cols, np.concatenate(ptrs),
+                     np.concatenate(cols) if cols else np.zeros(0, np.uint64),
+                     np.concatenate(vals) if vals else np.zeros(0))
+
+
+def spgemm_segments_file(path: str, sizes: ElementSizes, a_n_cols: int, b, mode: int = MODE_AUTO) -> tuple:
+    """read_segments + spgemm_block per segment on the B200 (the storage leg): the records of a
+    segment container go from the file to device memory (cuFile/GDS, or pread + pinned H2D).
+    Returns (list of CsrBlockResult, report dict)."""
+    L = lib()
+    bm, keep = _operand_matrix(b)
+    blocks = []
+    vdt = np.float64 if (mode == MODE_FP64_EXACT or (mode == MODE_AUTO and sizes.value_bytes == 8)) else np.float32
+
+    def cb(user, seg_index, start_row, end_row, nnz, rp, ci, va, flops):
+        rows = end_row - start_row
+        ptr = np.ctypeslib.as_array(rp, shape=(rows + 1,)).copy()
+        idx = np.ctypeslib.as_array(C.cast(ci, C.POINTER(C.c_uint64)), shape=(max(nnz, 1),))[:nnz].copy()
+        vt = C.c_double if vdt == np.float64 else C.c_float
+        val = np.ctypeslib.as_array(C.cast(va, C.POINTER(vt)), shape=(max(nnz, 1),))[:nnz].copy()
+        blocks.append(CsrBlockResult(start_row, end_row, CsrMatrix(rows, b.n_cols, ptr, idx, val), flops))
+        return 0
+
+    fn = _SEG_FN(cb)
+    rep = _StorageReport()
+    _check(L.aires_b200_spgemm_segments(path.encode(), sizes.index_bytes, sizes.value_bytes, a_n_cols, C.byref(bm),
+                                        mode, fn, None, C.byref(rep)))
+    return blocks, {"segments": rep.segments, "bytes_read": rep.bytes_read, "flops": rep.flops, "c_nnz": rep.c_nnz,
+                    "used_gds": bool(rep.used_gds), "read_ms": rep.read_ms, "total_ms": rep.total_ms}
 
 
 def layer_fused(a_tilde: CsrMatrix, h: CsrMatrix, w: np.ndarray) -> CsrMatrix:

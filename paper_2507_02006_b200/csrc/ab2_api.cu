@@ -272,6 +272,16 @@ int aires_b200_layer_fused(const aires_b200_matrix* a_tilde, const aires_b200_ma
   });
 }
 
+int aires_b200_spgemm_segments(const char* path, uint32_t index_bytes, uint32_t value_bytes, uint64_t a_n_cols,
+                               const aires_b200_matrix* b, uint32_t mode, aires_b200_segment_fn cb, void* user,
+                               aires_b200_storage_report* report) {
+  return ab2::guarded([&] {
+    if (!path || !b || !report) ab2::fail(AIRES_B200_INVALID_ARGUMENT, "null argument");
+    ab2::Ctx& ctx = ab2::ctx_for_thread();
+    ab2::spgemm_segments(ctx, path, index_bytes, value_bytes, a_n_cols, *b, mode, cb, user, *report);
+  });
+}
+
 void* aires_b200_stream(void) {
   void* s = nullptr;
   ab2::guarded([&] { s = static_cast<void*>(ab2::ctx_for_thread().stream); });

@@ -145,6 +145,11 @@ void combine(Ctx& ctx, const aires_b200_matrix& x, const void* w, uint64_t w_row
 void layer_fused(Ctx& ctx, const aires_b200_matrix& at, const aires_b200_matrix& h, const void* w, uint64_t w_rows,
                  uint64_t w_cols, uint32_t w_location, aires_b200_output& out);
 
+// Storage leg (ab2_storage.cu).
+void spgemm_segments(Ctx& ctx, const char* path, uint32_t ib, uint32_t vb, uint64_t a_n_cols,
+                     const aires_b200_matrix& b, uint32_t mode, aires_b200_segment_fn cb, void* user,
+                     aires_b200_storage_report& rep);
+
 // Out-of-core run (ab2_pipeline.cu).
 void destroy_pipe_cache(void* p);
 void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b, const aires_b200_run_config& cfg,

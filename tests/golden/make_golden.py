@@ -12,6 +12,8 @@ can pin the oracle restatement and the B200 kernels against the reference's own 
   robw.npz      : robw_partition cuts (partition.hpp:52-74) incl. row_too_large cases
   features.npz  : gen_features (synth.hpp:73-78) outputs for the seeds the benches use
   run_aires.npz : run_aires (scheduler.hpp:72-168) ledgers on single-segment budgets
+  segments.npz  : the reference's robw_partition + write_segments byte streams (serialize.hpp:148-174)
+                  at ElementSizes {8,8} and {4,4}
   gcn.npz       : normalize_adjacency (gcn.hpp:29-72) incl. graphs with existing diagonals and
                   weighted edges, gen_weights (synth.hpp:81-86) and combine (gcn.hpp:90-116)
 """
@@ -160,6 +162,23 @@ def gcn_cases():
     np.savez_compressed(os.path.join(HERE, "gcn.npz"), **out)
 
 
+def segment_cases():
+    import tempfile
+    rng = np.random.default_rng(17)
+    out = {}
+    cases = [(50, 40, 0.2, 8, 8, 700), (80, 30, 0.15, 4, 4, 300)]
+    for c, (nr, nc, d, I, V, m_a) in enumerate(cases):
+        a = random_csr(rng, nr, nc, d, 0.1, 1.0)
+        with tempfile.NamedTemporaryFile(suffix=".seg") as f:
+            rc = po.ref_write_segments(f.name, nr, nc, *a, m_a, I, V)
+            assert rc == 0
+            out[f"s{c}_bytes"] = np.fromfile(f.name, dtype=np.uint8)
+        out[f"s{c}_a_ptr"], out[f"s{c}_a_idx"], out[f"s{c}_a_val"] = a
+        out[f"s{c}_args"] = np.array([nr, nc, I, V, m_a], np.uint64)
+    out["n_cases"] = np.array([len(cases)])
+    np.savez_compressed(os.path.join(HERE, "segments.npz"), **out)
+
+
 if __name__ == "__main__":
     if not po.ref_available():
         sys.exit("oracle/_ref/libaires_ref.so missing: run `make -C oracle ref` (needs /root/reference)")
@@ -168,6 +187,7 @@ if __name__ == "__main__":
     feature_cases()
     run_aires_cases()
     gcn_cases()
+    segment_cases()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -103,3 +103,44 @@ def test_synth_weights_is_reference_gen_weights():
     for c in range(int(g["n_comb"][0])):
         rows, cin, cout, seed = (int(x) for x in g[f"c{c}_dims"])
         assert np.array_equal(ab.gen_weights(cin, cout, seed).view(np.uint64), g[f"c{c}_w"].view(np.uint64))
+
+
+def _host_segments(ptr, idx, val, n_rows, m_a, I, V):
+    """robw_partition on the host for the CPU tier: the oracle's cuts + slice_rows (partition.hpp:33-74)."""
+    from oracle import pyoracle as po
+    rc, cuts, _ = po.robw_cuts(ptr, m_a, I, V)
+    assert rc == 0
+    segs = []
+    for j in range(len(cuts) - 1):
+        r0, r1 = int(cuts[j]), int(cuts[j + 1])
+        b0, b1 = int(ptr[r0]), int(ptr[r1])
+        segs.append(ab.RobwSegment(j, r0, r1, (np.asarray(ptr[r0:r1 + 1]) - b0).astype(np.uint64), idx[b0:b1],
+                                   val[b0:b1], ab.calc_mem(r1 - r0, b1 - b0, ab.ElementSizes(I, V))))
+    return segs
+
+
+def test_segment_container_bytes_match_reference(tmp_path):
+    """write_segments (serialize.hpp:148-174) restated: byte-identical to the reference's file at
+    ElementSizes {8,8} and {4,4}."""
+    g = np.load(os.path.join(ROOT, "tests", "golden", "segments.npz"))
+    for c in range(int(g["n_cases"][0])):
+        nr, nc, I, V, m_a = (int(x) for x in g[f"s{c}_args"])
+        segs = _host_segments(g[f"s{c}_a_ptr"], g[f"s{c}_a_idx"], g[f"s{c}_a_val"], nr, m_a, I, V)
+        path = str(tmp_path / f"s{c}.seg")
+        ab.write_segments(path, segs, ab.ElementSizes(I, V))
+        assert np.array_equal(np.fromfile(path, dtype=np.uint8), g[f"s{c}_bytes"])
+
+
+def test_matrix_container_round_trip(tmp_path):
+    """ARSM (serialize.hpp:102-142): write/read round trip, magic and version checks."""
+    g = np.load(os.path.join(ROOT, "tests", "golden", "spgemm.npz"))
+    a = ab.CsrMatrix(int(g["c0_dims"][0]), int(g["c0_dims"][1]), g["c0_a_ptr"], g["c0_a_idx"], g["c0_a_val"])
+    p = str(tmp_path / "a.arsm")
+    ab.write_matrix(p, a)
+    assert ab.read_matrix(p) == a
+    raw = np.fromfile(p, dtype=np.uint8)
+    raw[0] = ord("X")
+    raw.tofile(p)
+    with pytest.raises(ab.AiresError) as e:
+        ab.read_matrix(p)
+    assert e.value.code == ab.errc.parse_error

@@ -4,7 +4,7 @@
 NAME=$1; shift
 HERE=/root/repo/paper_2507_02006_b200/csrc
 OUT=/tmp/variant_$NAME; mkdir -p $OUT /root/repo/paper_2507_02006_b200/variants
-for f in ab2_api ab2_operand ab2_spgemm ab2_robw ab2_pipeline ab2_gcn; do
+for f in ab2_api ab2_operand ab2_spgemm ab2_robw ab2_pipeline ab2_gcn ab2_storage; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -I/root/repo/include -I$HERE \
     --expt-relaxed-constexpr "$@" -c -o $OUT/$f.o $HERE/$f.cu &
 done
