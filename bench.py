@@ -331,6 +331,10 @@ def run_b200(args, cfg):
     if world == 1 and not args.skip_gcn:
         torch.cuda.empty_cache()
         gcn = gcn_leg(args, dev, L, ab, torch)
+    elif world > 1 and not args.skip_gcn:
+        tA.clear(); tX.clear(); outbuf.clear()
+        torch.cuda.empty_cache()
+        gcn = gcn_leg_dist(args, dev, L, ab, torch, dist, rank, world, cdev)
 
     if rank == 0:
         line = {
@@ -466,6 +470,83 @@ class DevOut:
         o = self.out
         return ab._Matrix(o.n_rows, n_cols, ab.CSR, ab.DEVICE, 4, o.val_bytes, self.t["ptr"].data_ptr(),
                           self.t["idx"].data_ptr(), self.t["val"].data_ptr(), o.nnz)
+
+
+def gcn_leg_dist(args, dev, L, ab, torch, dist, rank, world, cdev):
+    """cfg5 across ranks (strong scaling): the same products-shaped graph on every rank, rank r owns a
+    work-balanced contiguous row block of Ã; layer 1 on the block, then the H1 blocks are all-gathered
+    over NCCL into the replicated H1 the next layer needs (shard.allgather_csr_torch), then the fused
+    layer 2 on the block.  Time = max over ranks (CUDA events)."""
+    from paper_2507_02006_b200 import shard
+    cfg = CONFIGS["cfg3"]
+    a, _ = ab.synth_graph(cfg["n"], cfg["nnz"], alpha=0.75, degree_cap=cfg["cap"], seed=1, relabel_seed=2,
+                          normalize=False, idx_dtype=np.uint32, val_dtype=np.float32)
+    x = ab.synth_features(cfg["n"], cfg["dim"], 99.0, 3, idx_dtype=np.uint32, val_dtype=np.float32)
+    w1 = torch.from_numpy(ab.gen_weights(cfg["dim"], 256, 4).astype(np.float32)).to(dev)
+    w2 = torch.from_numpy(ab.gen_weights(256, 47, 5).astype(np.float32)).to(dev)
+    n = a.n_rows
+    cuts = shard.row_shards(a.row_ptr, world)
+    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    tA = [torch.from_numpy(a.row_ptr.view(np.int64)).to(dev), torch.from_numpy(a.col_idx.view(np.int32)).to(dev),
+          torch.from_numpy(a.values).to(dev)]
+    tX = [torch.from_numpy(x.row_ptr.view(np.int64)).to(dev), torch.from_numpy(x.col_idx.view(np.int32)).to(dev),
+          torch.from_numpy(x.values).to(dev)]
+    am = ab._Matrix(n, n, ab.CSR, ab.DEVICE, 4, 4, tA[0].data_ptr(), tA[1].data_ptr(), tA[2].data_ptr(), a.nnz())
+    xm = ab._Matrix(n, x.n_cols, ab.CSR, ab.DEVICE, 4, 4, tX[0].data_ptr(), tX[1].data_ptr(), tX[2].data_ptr(), x.nnz())
+    o_t, o_c1, o_h1, o_h2 = (DevOut(ab, torch, dev, torch.int32, torch.float32) for _ in range(4))
+    stream = torch.cuda.ExternalStream(L.aires_b200_stream(), device=dev)
+    gathered = {}
+
+    def block(o, cols):  # rows [r0, r1) of a device CSR as a zero-copy view (absolute row pointers)
+        t = o.t
+        return ab._Matrix(r1 - r0, cols, ab.CSR, ab.DEVICE, 4, 4, t["ptr"].data_ptr() + 8 * r0, t["idx"].data_ptr(),
+                          t["val"].data_ptr(), o.out.nnz)
+
+    def forward(rec=None):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record(stream)
+        ab._check(L.aires_b200_normalize_adjacency(C.byref(am), C.byref(o_t.out)))
+        at_blk = block(o_t, n)
+        ab._check(L.aires_b200_spgemm(C.byref(at_blk), C.byref(xm), ab.MODE_FP32, C.byref(o_c1.out)))
+        ab._check(L.aires_b200_combine(C.byref(o_c1.matrix(x.n_cols)), C.c_void_p(w1.data_ptr()), w1.shape[0],
+                                       w1.shape[1], ab.DEVICE, C.byref(o_h1.out)))
+        ev[1].record(stream)
+        ev[1].synchronize()
+        t = o_h1.t
+        rows_h = int(o_h1.out.n_rows)
+        g_ptr, g_idx, g_val = shard.allgather_csr_torch(t["ptr"][: rows_h + 1], t["idx"], t["val"])
+        torch.cuda.synchronize(dev)
+        ev[2].record(stream)
+        gathered.update(ptr=g_ptr, idx=g_idx, val=g_val)
+        h1 = ab._Matrix(n, w1.shape[1], ab.CSR, ab.DEVICE, 4, 4, g_ptr.data_ptr(), g_idx.data_ptr(),
+                        g_val.data_ptr(), g_idx.numel())
+        ab._check(L.aires_b200_layer_fused(C.byref(at_blk), C.byref(h1), C.c_void_p(w2.data_ptr()), w2.shape[0],
+                                           w2.shape[1], ab.DEVICE, C.byref(o_h2.out)))
+        ev[3].record(stream)
+        ev[3].synchronize()
+        if rec is not None:
+            rec.setdefault("layer1", []).append(ev[0].elapsed_time(ev[1]))
+            rec.setdefault("layer2_fused", []).append(ev[2].elapsed_time(ev[3]))
+            rec.setdefault("h1_allgather", []).append(ev[1].elapsed_time(ev[2]))
+            rec.setdefault("total", []).append(ev[0].elapsed_time(ev[3]))
+
+    for _ in range(max(1, args.warmup)):
+        forward()
+    dist.barrier()
+    rec = {}
+    for _ in range(args.steps):
+        forward(rec)
+    med = {k: float(np.median(v)) for k, v in rec.items()}
+    tt = torch.tensor([med["total"], med["layer1"], med["layer2_fused"], med["h1_allgather"]], dtype=torch.float64,
+                      device=cdev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return {"workload": f"cfg5 across {world} ranks: 2-layer GCN forward on the ogbn-products shape, rows of Ã in "
+                        "work-balanced contiguous blocks, H1 all-gathered for layer 2, fp32",
+            "ms_max_over_ranks": {"total": round(float(tt[0]), 3), "layer1_incl_normalize": round(float(tt[1]), 3),
+                                  "layer2_fused": round(float(tt[2]), 3), "h1_allgather": round(float(tt[3]), 3)},
+            "collective": f"torch.distributed {dist.get_backend()} all_gather_into_tensor (sizes, then padded arrays)",
+            "rows_per_rank": [int(cuts[i + 1] - cuts[i]) for i in range(world)],
+            "h1_allgather_bytes": int(gathered["idx"].numel()) * 8 + 8 * (n + 1), "h2_nnz_rank0": int(o_h2.out.nnz)}
 
 
 def gcn_leg(args, dev, L, ab, torch):

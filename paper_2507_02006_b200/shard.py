@@ -94,3 +94,43 @@ def shard_rows(row_ptr: np.ndarray, col_idx: np.ndarray, values: np.ndarray, cut
     """Zero-copy row block of rank `rank`: (absolute row_ptr slice, col_idx, values, rows)."""
     r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
     return np.asarray(row_ptr)[r0:r1 + 1], col_idx, values, r1 - r0
+
+
+def allgather_csr_torch(ptr, idx, val, group=None):
+    """Device-side assembly of the replicated C (or H) for the next GCN layer: every rank passes its
+    row block as torch tensors (ptr int64 rows+1 rebased or absolute, idx, val); one all-gather of
+    the sizes, then one padded all-gather per array (NCCL: the tensors stay on the GPU; gloo: they
+    are staged through host memory).  Returns (ptr, idx, val) of the whole matrix on the input
+    tensors' device, blocks in rank order."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = ptr.device
+    cdev = dev if nccl else torch.device("cpu")
+    rows = ptr.numel() - 1
+    base = ptr[0]
+    nnz = int((ptr[-1] - base).item())
+    meta = torch.tensor([rows, nnz], dtype=torch.int64, device=cdev)
+    metas = torch.zeros(2 * world, dtype=torch.int64, device=cdev)
+    dist.all_gather_into_tensor(metas, meta, group=group)
+    metas = metas.view(world, 2).cpu()
+    mr, mn = int(metas[:, 0].max()), max(int(metas[:, 1].max()), 1)
+
+    def gather(t, length):
+        pad = torch.zeros(max(length, 1), dtype=t.dtype, device=cdev)
+        pad[: t.numel()] = t.to(cdev)
+        out = torch.empty(world * max(length, 1), dtype=t.dtype, device=cdev)
+        dist.all_gather_into_tensor(out, pad, group=group)
+        return out.view(world, max(length, 1))
+
+    counts = gather((ptr[1:] - ptr[:-1]).to(torch.int64), mr)
+    cols = gather(idx[int(base): int(base) + nnz], mn)
+    vals = gather(val[int(base): int(base) + nnz], mn)
+    parts_c = [counts[r, : int(metas[r, 0])] for r in range(world)]
+    g_cnt = torch.cat(parts_c).to(dev)
+    g_ptr = torch.zeros(g_cnt.numel() + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(g_cnt, 0, out=g_ptr[1:])
+    g_idx = torch.cat([cols[r, : int(metas[r, 1])] for r in range(world)]).to(dev)
+    g_val = torch.cat([vals[r, : int(metas[r, 1])] for r in range(world)]).to(dev)
+    return g_ptr, g_idx, g_val
