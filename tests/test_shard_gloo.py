@@ -53,9 +53,14 @@ def _worker(rank, world, port, q):
         g_rows = shard.global_row_ptr(lp, offs[rank])
         g_rp, g_col, g_val = shard.allgather_csr(lp, li, lv)
         rc, (wp, wi, wv), _ = po.spgemm_rowwise(*a, 57, 40, 40, 23, *x)
+        import torch
+        tp, ti, tv = shard.allgather_csr_torch(torch.from_numpy(lp.astype(np.int64)), torch.from_numpy(li.astype(np.int64)),
+                                               torch.from_numpy(lv))
         ok = (total == wi.shape[0] and np.array_equal(g_rp, wp) and np.array_equal(g_col.astype(np.uint64), wi)
               and np.array_equal(g_val.view(np.uint64), wv.view(np.uint64))
-              and np.array_equal(g_rows.astype(np.uint64), wp[cuts[rank]:cuts[rank + 1] + 1]))
+              and np.array_equal(g_rows.astype(np.uint64), wp[cuts[rank]:cuts[rank + 1] + 1])
+              and np.array_equal(tp.numpy().astype(np.uint64), wp) and np.array_equal(ti.numpy().astype(np.uint64), wi)
+              and np.array_equal(tv.numpy().view(np.uint64), wv.view(np.uint64)))
         q.put((rank, bool(ok)))
     finally:
         dist.destroy_process_group()
