@@ -346,3 +346,29 @@ def test_layer_fused_matches_unfused_chain(hcols, wcols):
     for key in set(want) | set(have):
         err = abs(want.get(key, 0.0) - have.get(key, 0.0))
         assert err <= 1e-5 * max(scale.get(key, 0.0), 1e-30), (key, want.get(key), have.get(key), scale.get(key))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("shape", ["cfg2", "cfg3"])
+def test_full_size_parity(shape):
+    """BASELINE configs at full size (Reddit- and ogbn-products-shaped): fp32 structure bit-exact and
+    values within 1e-5 of the fp64 oracle; fp64-exact checksum equal to the oracle's; MACs equal."""
+    import bench
+    cfg = bench.CONFIGS[shape]
+    g, st, x = bench.make_inputs(cfg, 0, 1)
+    gu = ab.CsrMatrix(g.n_rows, g.n_cols, g.row_ptr, g.col_idx.astype(np.uint64), g.values)
+    xu = ab.CsrMatrix(x.n_rows, x.n_cols, x.row_ptr, x.col_idx.astype(np.uint64), x.values)
+    rc, (wp, wi, wv), macs = po.spgemm_rowwise(gu.row_ptr, gu.col_idx, gu.values, g.n_rows, g.n_cols, x.n_rows,
+                                               x.n_cols, xu.row_ptr, xu.col_idx, xu.values, nthreads=16)
+    assert rc == 0
+    g32 = ab.CsrMatrix(g.n_rows, g.n_cols, g.row_ptr, g.col_idx, g.values.astype(np.float32))
+    x32 = ab.CsrMatrix(x.n_rows, x.n_cols, x.row_ptr, x.col_idx, x.values.astype(np.float32))
+    blk = ab.spgemm_block(g32.row_ptr, g32.col_idx, g32.values, g.n_rows, g.n_cols, x32)
+    c = blk.fragment
+    assert blk.flops == macs
+    assert np.array_equal(c.row_ptr, wp) and np.array_equal(c.col_idx.astype(np.uint64), wi)
+    err = np.abs(c.values.astype(np.float64) - wv) / np.abs(wv)
+    assert float(err.max()) <= 1e-5
+    c64 = ab.spgemm_full(gu, xu)  # fp64-exact
+    assert po.checksum(c64.n_rows, c64.n_cols, c64.row_ptr, c64.col_idx, c64.values) == \
+        po.checksum(g.n_rows, x.n_cols, wp, wi, wv)
