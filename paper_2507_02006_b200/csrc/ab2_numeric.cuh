@@ -56,7 +56,7 @@ struct Num3Args {
   int32_t stride;      // accumulator elements per copy (>= n_cols + 1, multiple of 32)
   int32_t copies;      // accumulator copies per warp
   int32_t warp_bytes;  // shared bytes per warp: copies*stride*sizeof(V) + stride marks + chunk table
-  int32_t pad0;
+  int32_t pad0;          // 1: rows with <= 32 terms take the register sort path (short_row)
   const int64_t* heavy;  // heavy rows (A-degree > heavy_deg)
   int64_t heavy_deg;
   uint32_t* cnt;         // per-row nnz
@@ -559,6 +559,114 @@ __device__ __forceinline__ unsigned long long out_offset(const P& p, int64_t r, 
   return stage.take(cnt, p.ctl, p.stage_block);
 }
 
+// Rows whose products fit one warp (<= 32 terms; degree <= 32): the terms are formed one per lane,
+// sorted by (column, order of arrival) with a bitonic network over shuffles, and each column's terms
+// are summed left to right from +0.0 -- dot_row_col's arithmetic (spgemm.hpp:21-42), so fp64 stays
+// bit-exact, and every column with a term is kept (structural zeros included).  No shared-memory
+// accumulator, no fold: for short rows (the ogbn-products shape averages ~26 terms per row) the
+// copies' fold was a third of the kernel.  Returns false (nothing done) when the row has more terms.
+template <class V>
+__device__ __forceinline__ V mul_rn(V a, V b) {
+  if constexpr (sizeof(V) == 8)
+    return __dmul_rn(a, b);
+  else
+    return __fmul_rn(a, b);
+}
+template <class V>
+__device__ __forceinline__ V add_rn(V a, V b) {
+  if constexpr (sizeof(V) == 8)
+    return __dadd_rn(a, b);
+  else
+    return __fadd_rn(a, b);
+}
+
+template <class V, class IdxT>
+__device__ __forceinline__ bool short_row(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac,
+                                          const V* __restrict__ av, uint32_t n, int64_t r, StageCursor& stage,
+                                          unsigned long long& my_nnz, unsigned long long& my_macs) {
+  const int lane = lane_id();
+  const uint64_t K = static_cast<uint64_t>(p.x.K);
+  int64_t xs = 0;
+  uint32_t len = 0;
+  V a = V(0);
+  if (static_cast<uint32_t>(lane) < n) {
+    const uint64_t k = static_cast<uint64_t>(ac[lane]);
+    a = av[lane];
+    if (k < K) {
+      xs = p.x.ptr[k];
+      len = static_cast<uint32_t>(p.x.ptr[k + 1] - xs);
+    }
+  }
+  const uint32_t incl = warp_incl_scan(len);
+  const uint32_t T = __shfl_sync(kFull, incl, 31);
+  if (T > 32) return false;
+  const uint32_t excl = incl - len;
+  // owner of term t = lane: the last entry j with excl_j <= t (it has len_j > 0 when t < T)
+  const uint32_t t = static_cast<uint32_t>(lane);
+  int j = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const int cand = j + step;
+    const uint32_t ec = __shfl_sync(kFull, excl, cand & 31);
+    if (cand < 32 && ec <= t) j = cand;
+  }
+  const int64_t xs_j = __shfl_sync(kFull, xs, j);
+  const uint32_t ex_j = __shfl_sync(kFull, excl, j);
+  const V a_j = __shfl_sync(kFull, a, j);
+  uint32_t key = 0xffffffffu;
+  V v = V(0);
+  if (t < T) {
+    const int64_t q = xs_j + static_cast<int64_t>(t - ex_j);
+    key = (static_cast<uint32_t>(p.x.col[q]) << 5) | t;
+    v = mul_rn<V>(a_j, p.x.val[q]);
+  }
+  // bitonic sort of the 32 (key, value) pairs, ascending
+#pragma unroll
+  for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      const uint32_t ok = __shfl_xor_sync(kFull, key, jj);
+      const V ov = __shfl_xor_sync(kFull, v, jj);
+      const bool keep_min = ((lane & kk) == 0) == ((lane & jj) == 0);
+      if (keep_min ? ok < key : ok > key) {
+        key = ok;
+        v = ov;
+      }
+    }
+  }
+  const bool real = key != 0xffffffffu;
+  const uint32_t col = key >> 5;
+  const uint32_t pcol = __shfl_up_sync(kFull, col, 1);
+  const bool head = real && (lane == 0 || pcol != col);
+  V sum = add_rn<V>(V(0), v);  // sum = 0.0; sum += term (a -0.0 term gives +0.0, as in the reference)
+  for (int d = 1; d < 32; d++) {
+    const uint32_t ncol = __shfl_down_sync(kFull, col, d);
+    const V nv = __shfl_down_sync(kFull, v, d);
+    const bool cont = head && lane + d < 32 && ncol == col;
+    if (!__any_sync(kFull, cont)) break;
+    if (cont) sum = add_rn<V>(sum, nv);
+  }
+  const unsigned hm = __ballot_sync(kFull, head);
+  const uint32_t cnt = __popc(hm);
+  const unsigned long long off = out_offset(p, r, cnt, stage);
+  if (off <= p.t_cap && off + cnt <= p.t_cap) {
+    if (head) {
+      const unsigned long long pos = off + __popc(hm & ((1u << lane) - 1));
+      p.tcol[pos] = static_cast<IdxT>(col);
+      p.tval[pos] = sum;
+    }
+  } else if (lane == 0) {
+    atomicMax(&p.ctl->bad_row, 1ull);
+  }
+  if (lane == 0) {
+    p.cnt[r] = cnt;
+    p.toff[r] = off;
+    my_nnz += cnt;
+    my_macs += T;
+  }
+  return true;
+}
+
 template <class V, class IdxT, int W, bool XZ>
 __global__ void __launch_bounds__(256, AB2_NUM_MINB) k_numeric3(Num3Args<V, IdxT> p) {
   constexpr bool EXACT = sizeof(V) == 8;
@@ -661,6 +769,7 @@ __global__ void __launch_bounds__(256, AB2_NUM_MINB) k_numeric3(Num3Args<V, IdxT
       const uint32_t n = static_cast<uint32_t>(e - s);
       const IdxT* ac = p.acol + s;
       const V* av = p.aval + s;
+      if (p.pad0 && n <= 32 && short_row<V, IdxT>(p, ac, av, n, r, stage, my_nnz, my_macs)) continue;
       bool zero = false;
       my_macs += walk_any<V, IdxT, W, EXACT, false, XZ>(p, ac, av, n, 0, 1, acc, warp_tab(warp), 0, 0, zero);
       if (__any_sync(kFull, zero)) slow_row<V, IdxT>(p, ac, av, n, acc, warp_mark(warp));
