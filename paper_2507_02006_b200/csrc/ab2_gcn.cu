@@ -84,14 +84,22 @@ __global__ void k_norm_fill(const uint64_t* __restrict__ ptr, uint64_t base, con
   }
 }
 
-// weighted degrees, summed left to right (gcn.hpp:61-64)
+// weighted degrees, summed left to right (gcn.hpp:61-64): one warp per row, the row read coalesced
+// 32 values at a time and folded into lane 0's running sum in order (exact for any weights).
 __global__ void k_norm_degree(const int64_t* __restrict__ optr, const double* __restrict__ oval, int64_t n,
                               double* __restrict__ deg) {
-  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n;
-       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int lane = lane_id();
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = wid; r < n; r += nw) {
+    const int64_t s = optr[r], e = optr[r + 1];
     double d = 0.0;
-    for (int64_t k = optr[r]; k < optr[r + 1]; k++) d = __dadd_rn(d, oval[k]);
-    deg[r] = d;
+    for (int64_t b = s; b < e; b += 32) {
+      const double v = b + lane < e ? oval[b + lane] : 0.0;
+      const int m = static_cast<int>(e - b < 32 ? e - b : 32);
+      for (int i = 0; i < m; i++) d = __dadd_rn(d, __shfl_sync(kFull, v, i));
+    }
+    if (lane == 0) deg[r] = d;
   }
 }
 
@@ -304,7 +312,7 @@ void normalize_t(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
   if (n > 0) {
     k_norm_fill<IdxT, VIn, IdxO><<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(s.ptr, s.base, col, val, n,
                                                                                        optr, ocol, oval);
-    k_norm_degree<<<grid_of(n, 128, ctx.sms), 128, 0, ctx.stream>>>(optr, oval, n, deg);
+    k_norm_degree<<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(optr, oval, n, deg);
     k_norm_scale<IdxO, VO><<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(optr, ocol, oval, deg, n, outv);
     AB2_CUDA(cudaGetLastError());
     launches += 3;
