@@ -289,7 +289,7 @@ __device__ __forceinline__ uint32_t walk_entries(const Num3Args<V, IdxT>& p, con
 }
 
 // Register-fed variant (default, AB2_NUM_SHFL=1).  The kernel is bound by the L1 / shared-memory
-// datapath (90% L1 throughput at cfg2, profiles/r01d); per warp step the variant above spends two
+// datapath (90% L1 throughput at cfg2, profiles/r01g); per warp step the variant above spends two
 // shared wavefronts on the chunk table (LDS.128) and, per chunk, one 32-sector gather of X row
 // lengths.  Here each lane keeps its own entry (slot base k*W, weight a) in registers and groups
 // fetch theirs with SHFL; slots are loaded whole (entries past the row's length hold the trash
