@@ -36,6 +36,9 @@
 #ifndef AB2_NUM_BATCH
 #define AB2_NUM_BATCH 8
 #endif
+#ifndef AB2_NUM_TAB
+#define AB2_NUM_TAB 1  // chunk entries through a per-warp shared table (1) or SHFL (0)
+#endif
 #ifndef AB2_NUM_MINB
 #define AB2_NUM_MINB 4
 #endif
@@ -297,8 +300,8 @@ __device__ __forceinline__ uint32_t walk_entries(const Num3Args<V, IdxT>& p, con
 template <class V, class IdxT, int W, bool EXACT, bool RANGE, bool XZ>
 __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac,
                                                   const V* __restrict__ av, uint32_t n, uint32_t chunk0,
-                                                  uint32_t chunk_stride, V* acc, uint32_t c_lo, uint32_t c_hi,
-                                                  bool& zero) {
+                                                  uint32_t chunk_stride, V* acc, ChunkPair* tab, uint32_t c_lo,
+                                                  uint32_t c_hi, bool& zero) {
   constexpr int G = 32 / W;
   constexpr int B = W < AB2_NUM_BATCH ? W : AB2_NUM_BATCH;  // group steps per batch (loads in flight)
   constexpr uint32_t VS = sizeof(V);
@@ -310,6 +313,7 @@ __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, co
   const V* __restrict__ xval = p.x.val;
   const V tiny = p.tiny;
   const uint32_t copy_s = static_cast<uint32_t>(__cvta_generic_to_shared(EXACT ? acc : acc + gid * p.stride));
+  const uint32_t tab_s = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
   uint32_t macs = 0;
   auto add = [&](uint32_t c, V a, V x) {
     if constexpr (XZ) {
@@ -343,6 +347,19 @@ __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, co
     k1 = k2;
     a1 = a2;
     load_ka(b + 2 * step, k2, a2);
+#if AB2_NUM_TAB
+    // the chunk's entries {k*W, a} go to a per-warp table once; each step then reads its group's
+    // entry with one broadcast LDS (1 wavefront) instead of two SHFLs (~2.6 wavefronts measured)
+    __syncwarp();
+    if constexpr (sizeof(V) == 4)
+      asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(tab_s + lane * 8u), "r"(kw), "r"(__float_as_uint(a))
+                   : "memory");
+    else
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(tab_s + lane * 16u), "r"(kw), "r"(0u),
+                   "r"(__double2loint(a)), "r"(__double2hiint(a))
+                   : "memory");
+    __syncwarp();
+#endif
     const uint32_t steps = (min(32u, n - b) + G - 1) / G;
 #pragma unroll 1
     for (uint32_t u0 = 0; u0 < steps; u0 += B) {
@@ -352,8 +369,24 @@ __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, co
 #pragma unroll
       for (int u = 0; u < B; u++) {
         const int src = static_cast<int>(((u0 + u) * G + gid) & 31u);
+#if AB2_NUM_TAB
+        uint32_t skw;
+        if constexpr (sizeof(V) == 4) {
+          uint32_t ab;
+          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(skw), "=r"(ab) : "r"(tab_s + src * 8u) : "memory");
+          aa[u] = __uint_as_float(ab);
+        } else {
+          uint32_t z, lo, hi;
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(skw), "=r"(z), "=r"(lo), "=r"(hi)
+                       : "r"(tab_s + src * 16u)
+                       : "memory");
+          aa[u] = __hiloint2double(hi, lo);
+        }
+#else
         const uint32_t skw = __shfl_sync(kFull, kw, src);
         aa[u] = __shfl_sync(kFull, a, src);
+#endif
         if constexpr (sizeof(V) == 4) {
           const uint2 e = __ldg(reinterpret_cast<const uint2*>(p.x.slots) + (skw + ent));
           col[u] = e.x;
@@ -436,6 +469,9 @@ __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, co
 #ifndef AB2_NUM_SHFL
 #define AB2_NUM_SHFL 1
 #endif
+#ifndef AB2_NUM_TAB
+#define AB2_NUM_TAB 1
+#endif
 
 template <class V, class IdxT, int W, bool EXACT, bool RANGE, bool XZ>
 __device__ __forceinline__ uint32_t walk_any(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac,
@@ -443,8 +479,7 @@ __device__ __forceinline__ uint32_t walk_any(const Num3Args<V, IdxT>& p, const I
                                              uint32_t chunk_stride, V* acc, ChunkPair* tab, uint32_t c_lo,
                                              uint32_t c_hi, bool& zero) {
 #if AB2_NUM_SHFL
-  (void)tab;
-  return walk_entries2<V, IdxT, W, EXACT, RANGE, XZ>(p, ac, av, n, chunk0, chunk_stride, acc, c_lo, c_hi, zero);
+  return walk_entries2<V, IdxT, W, EXACT, RANGE, XZ>(p, ac, av, n, chunk0, chunk_stride, acc, tab, c_lo, c_hi, zero);
 #else
   return walk_entries<V, IdxT, W, EXACT, RANGE, XZ>(p, ac, av, n, chunk0, chunk_stride, acc, tab, c_lo, c_hi, zero);
 #endif
