@@ -46,7 +46,7 @@ void launch_numeric_w(Ctx& ctx, const Num3Args<V, IdxT>& p, int threads, size_t 
 
 template <class V, class IdxT>
 int numeric_warps(const Num3Args<V, IdxT>& p) {
-  int nw = static_cast<int>(env_int("AB2_NUM_WARPS", 8));
+  int nw = static_cast<int>(env_int("AB2_NUM_WARPS", 4));
   return std::max(1, std::min<int>(nw, static_cast<int>((200 * 1024) / p.warp_bytes)));
 }
 
@@ -193,7 +193,7 @@ void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_
   if (x.K >= (int64_t(1) << 31) / 16) fail(AIRES_B200_CAPACITY_EXCEEDED, "inner dimension too large for slot indexing");
   Ctl* ctl = ctx.ctl.as<Ctl>(1);
   Ctl* h = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
-  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 4096);
+  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 1024);
   int64_t* heavy = ctx.sym_heavy.as<int64_t>(std::max<int64_t>(rows, 1));
   uint32_t* cnt = reinterpret_cast<uint32_t*>(ctx.cnt.as<int32_t>(std::max<int64_t>(rows, 1)));
   uint64_t* toff = reinterpret_cast<uint64_t*>(ctx.rflops.as<int64_t>(std::max<int64_t>(rows, 1)));
@@ -297,7 +297,7 @@ namespace {
 template <class V, class IdxT>
 int tile_product_t(Ctx& ctx, const XOperand& x, const TilePass& t) {
   if (t.rows <= 0) return 0;
-  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 4096);
+  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 1024);
   const int g = static_cast<int>(std::min<int64_t>((t.rows + 255) / 256, static_cast<int64_t>(ctx.sms) * 16));
   k_classify<<<g, 256, 0, ctx.stream>>>(t.aptr, t.rows, heavy_deg, t.heavy, t.ctl);
   AB2_CUDA(cudaGetLastError());
@@ -416,7 +416,7 @@ void wide_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires
   const int64_t T = (n_cols + tw - 1) / tw;
   const int64_t K = x.K;
   const uint32_t mode = x.mode;
-  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 4096);
+  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 1024);
   int64_t* heavy = ctx.sym_heavy.as<int64_t>(std::max<int64_t>(rows, 1));
   struct Tile {
     DevBuf ptr, col, val, cnt, toff, tcol, tval;
