@@ -23,7 +23,10 @@
 
 namespace ab2 {
 
-constexpr int kLightBatch = 4;   // light rows per ticket
+#ifndef AB2_LIGHT_BATCH
+#define AB2_LIGHT_BATCH 4
+#endif
+constexpr int kLightBatch = AB2_LIGHT_BATCH;  // light rows per ticket
 
 template <class V>
 struct Sentinel;
