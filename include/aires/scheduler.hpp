@@ -27,8 +27,8 @@
 
 namespace aires::b200 {
 
-inline RunResult run_aires_real(const CsrMatrix& a, const CscMatrix& b, const MemoryBudget& budget,
-                                const SimConfig& cfg, std::uint32_t n_buffers = 2) {
+inline RunResult run_real(const CsrMatrix& a, const CscMatrix& b, const MemoryBudget& budget, const SimConfig& cfg,
+                          std::uint32_t n_buffers, std::uint32_t strategy /* 1 AIRES, 2 MaxMemory */) {
   (void)cfg;  // cost-model parameters of the simulator; the real run measures instead
   if (a.n_cols != b.n_rows)
     fail(errc::dimension_mismatch,
@@ -42,14 +42,14 @@ inline RunResult run_aires_real(const CsrMatrix& a, const CscMatrix& b, const Me
   aires_b200_run_config rc{};
   rc.device_budget = budget.device_total;
   rc.mode = AIRES_B200_MODE_FP64_EXACT;
-  rc.c_aware = 1;
+  rc.c_aware = strategy;
   rc.n_buffers = n_buffers;
   aires_b200_run_report rep{};
   check(aires_b200_run(&am, &bm, &rc, &out, &rep));
   res.c.n_rows = a.n_rows;
   res.c.n_cols = b.n_cols;
   RunReport& r = res.report;
-  r.strategy = Strategy::aires;
+  r.strategy = strategy == 2 ? Strategy::maxmemory : Strategy::aires;
   r.budget_bytes = budget.device_total;
   r.phase1_s = rep.phase1_ms * 1e-3;
   r.phase2_s = rep.phase2_ms * 1e-3;
@@ -58,9 +58,23 @@ inline RunResult run_aires_real(const CsrMatrix& a, const CscMatrix& b, const Me
   r.ledger.h2d.bytes = rep.h2d_bytes;
   r.ledger.d2h.bytes = rep.d2h_bytes;
   r.ledger.peak_device_occupancy = rep.peak_device_bytes;
+  r.ledger.merge_bytes = rep.merge_bytes;
   r.c_checksum = checksum(res.c);
   r.segments = rep.segments;
   return res;
+}
+
+/// run_aires (scheduler.hpp:72-168) as the real out-of-core pipeline.
+inline RunResult run_aires_real(const CsrMatrix& a, const CscMatrix& b, const MemoryBudget& budget,
+                                const SimConfig& cfg, std::uint32_t n_buffers = 2) {
+  return run_real(a, b, budget, cfg, n_buffers, 1);
+}
+
+/// run_maxmemory (scheduler.hpp:174-293) for real: fixed byte tiles, split rows' fragments returned
+/// to the host and re-sent with the next tile.
+inline RunResult run_maxmemory_real(const CsrMatrix& a, const CscMatrix& b, const MemoryBudget& budget,
+                                    const SimConfig& cfg, std::uint32_t n_buffers = 2) {
+  return run_real(a, b, budget, cfg, n_buffers, 2);
 }
 
 }  // namespace aires::b200

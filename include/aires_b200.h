@@ -156,7 +156,9 @@ int aires_b200_robw_cuts(const uint64_t* row_ptr, uint64_t n_rows, uint64_t m_a,
 typedef struct aires_b200_run_config {
   uint64_t device_budget; /* bytes the run may hold on the device at once (0 = no cap) */
   uint32_t mode;          /* AIRES_B200_MODE_* */
-  uint32_t c_aware;       /* 1: tiles sized by A + C bytes (default); 0: RoBW by A only */
+  uint32_t c_aware;       /* 1: tiles sized by A + C bytes (default); 0: RoBW by A only;
+                             2: the MaxMemory baseline (fixed byte tiles, split rows' fragments
+                                returned to the host and re-sent, scheduler.hpp:174-293) */
   uint32_t n_buffers;     /* tile ring depth (default 2) */
   uint32_t reserved;
 } aires_b200_run_config;
@@ -172,6 +174,7 @@ typedef struct aires_b200_run_report {
   double phase1_ms;  /* operand upload + symbolic sizing + cut */
   double phase2_ms;  /* tile streaming */
   double phase3_ms;  /* final drain / assembly */
+  uint64_t merge_bytes; /* MaxMemory: fragment bytes re-sent after the host stitch (IoLedger::merge_bytes) */
 } aires_b200_run_report;
 
 /* A in host memory (CSR); B host or device; C written through c->alloc (host). */

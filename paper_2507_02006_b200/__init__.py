@@ -91,7 +91,7 @@ class _RunReport(C.Structure):
     _fields_ = [("segments", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("flops", C.c_uint64), ("c_nnz", C.c_uint64), ("peak_device_bytes", C.c_uint64),
                 ("total_ms", C.c_double), ("phase1_ms", C.c_double), ("phase2_ms", C.c_double),
-                ("phase3_ms", C.c_double)]
+                ("phase3_ms", C.c_double), ("merge_bytes", C.c_uint64)]
 
 
 _SEG_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64),
@@ -461,6 +461,17 @@ class RunResult:
     trace: list
 
 
+def run_maxmemory(a: CsrMatrix, b, budget: MemoryBudget, cfg=None, mode: int = MODE_AUTO, n_buffers: int = 2,
+                  with_checksum: bool = True) -> RunResult:
+    """scheduler.hpp:174-293 on the B200: the MaxMemory baseline -- the A element stream cut at fixed
+    byte boundaries (maxmemory_partition, partition.hpp:140-169), the fragment of every split row
+    returned to the host and re-sent with the next tile (merge_partial, :176-197).  Same result as
+    run_aires; the ledger shows the extra link traffic (merge_bytes)."""
+    res = run_aires(a, b, budget, cfg, mode, c_aware=2, n_buffers=n_buffers, with_checksum=with_checksum)
+    res.report.strategy = "maxmemory"
+    return res
+
+
 def run_aires(a: CsrMatrix, b, budget: MemoryBudget, cfg=None, mode: int = MODE_AUTO, c_aware: bool = True,
               n_buffers: int = 2, with_checksum: bool = True) -> RunResult:
     """scheduler.hpp:72-168 as a real three-phase tile pipeline on the B200 (ab2_pipeline.cu).
@@ -482,7 +493,7 @@ def run_aires(a: CsrMatrix, b, budget: MemoryBudget, cfg=None, mode: int = MODE_
         am.val_bytes = keep_a[2].dtype.itemsize
     al = _HostAlloc(keep_a[1].dtype, vdt)
     out = al.output()
-    cfgc = _RunConfig(int(budget.device_total), mode, int(bool(c_aware)), int(n_buffers), 0)
+    cfgc = _RunConfig(int(budget.device_total), mode, 2 if c_aware == 2 else int(bool(c_aware)), int(n_buffers), 0)
     rep = _RunReport()
     _check(L.aires_b200_run(C.byref(am), C.byref(bm), C.byref(cfgc), C.byref(out), C.byref(rep)))
     c = CsrMatrix(a.n_rows, b.n_cols, al.ptr, al.idx[: out.nnz], al.val[: out.nnz])
@@ -491,6 +502,7 @@ def run_aires(a: CsrMatrix, b, budget: MemoryBudget, cfg=None, mode: int = MODE_
                   flops=int(rep.flops))
     r.ledger.h2d.bytes, r.ledger.d2h.bytes = int(rep.h2d_bytes), int(rep.d2h_bytes)
     r.ledger.peak_device_occupancy = int(rep.peak_device_bytes)
+    r.ledger.merge_bytes = int(rep.merge_bytes)
     if with_checksum:
         r.c_checksum = checksum(c)
     return RunResult(c, r, [])

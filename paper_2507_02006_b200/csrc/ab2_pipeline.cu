@@ -231,7 +231,8 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   // Uncapped runs keep A's column indices resident and stream them right after X (X first: its
   // build synchronises the host once and must not queue behind A on the link).
   const uint64_t a_col_bytes = (pend - p0) * ib;
-  const bool early_cols = cfg.device_budget == 0 && env_int("AB2_RUN_RESIDENT_COLS", 1) != 0 && n > 0;
+  const bool maxmem = cfg.c_aware == 2;  // the MaxMemory baseline (scheduler.hpp:174-293)
+  const bool early_cols = !maxmem && cfg.device_budget == 0 && env_int("AB2_RUN_RESIDENT_COLS", 1) != 0 && n > 0;
   char* d_acol_full = nullptr;
   std::vector<uint64_t> early_cuts;
   std::vector<cudaEvent_t> early_ev;
@@ -282,7 +283,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   // A's column indices stay resident after the sizing pass when they take at most half of the
   // budget left (then Phase II streams only A's values): one column pass over the link instead of two
   const bool cols_resident =
-      early_cols || (env_int("AB2_RUN_RESIDENT_COLS", 1) != 0 && budget - fixed >= 2 * a_col_bytes + 4096);
+      early_cols || (!maxmem && env_int("AB2_RUN_RESIDENT_COLS", 1) != 0 && budget - fixed >= 2 * a_col_bytes + 4096);
   if (cols_resident && !d_acol_full) d_acol_full = static_cast<char*>(arena.get(a_col_bytes));
   const uint64_t fixed2 = fixed + (cols_resident && !early_cols ? std::max<uint64_t>(a_col_bytes, 256) : 0);
   const uint64_t slot_budget = (budget - fixed2) / nbuf;
@@ -446,11 +447,64 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
     const uint64_t want = std::max<uint64_t>(env_int("AB2_RUN_TILES", 16), 1);
     tile_budget = std::min<uint64_t>(slot_budget, std::max<uint64_t>(p2_bytes / want, 64ull << 20));
   }
+  // MaxMemory (partition.hpp:140-169): the element stream is cut at fixed byte boundaries, rows split
+  // mid-way; tile j ships its raw bytes plus the fragment of the row cut by the previous tile, which
+  // came back to the host (D2H) and is stitched on in front (merge_partial, partition.hpp:176-197).
+  struct MmTile {
+    uint64_t q_frag, q0, q1;  // entries [q_frag, q0) re-sent fragment, [q0, q1) raw bytes
+    uint64_t r0, r1;          // complete rows multiplied in this tile
+  };
+  std::vector<MmTile> mm;
+  // The reference reserves C statically from its Eq. 5 estimate (~1e-4 of the real C on GCN
+  // shapes, so it cannot run them); here the baseline gets the generous version: the slot is split
+  // between A bytes and output bytes in the proportion of the whole product (known from the sizing
+  // pass), and the tile is halved until every tile's fragment + raw bytes + output block fits.
+  auto mm_build = [&](uint64_t te) {
+    mm.clear();
+    uint64_t cursor = 0, frag = p0;
+    for (uint64_t e0 = p0; e0 < pend; e0 += te) {
+      const uint64_t e1 = std::min(e0 + te, pend);
+      MmTile t{frag, e0, e1, cursor, cursor};
+      while (t.r1 < n && a.ptr[t.r1 + 1] <= e1) t.r1++;
+      cursor = t.r1;
+      frag = cursor < n ? a.ptr[cursor] : pend;  // start of the row cut at e1 (a row longer than a
+                                                  // tile is re-sent from its start, partition.hpp:110-114)
+      mm.push_back(t);
+    }
+    while (cursor < n) {  // trailing empty rows
+      mm.push_back(MmTile{pend, pend, pend, cursor, n});
+      cursor = n;
+    }
+  };
+  if (maxmem) {
+    const double a_share = static_cast<double>((pend - p0) * (ib + vb)) /
+                           std::max<double>(1.0, static_cast<double>((pend - p0) * (ib + vb) + nnz * (ib + vb)));
+    uint64_t te = std::max<uint64_t>(static_cast<uint64_t>(slot_budget * a_share * 0.9) / (ib + vb), 1);
+    for (;;) {
+      mm_build(te);
+      bool fits = true;
+      for (const MmTile& t : mm)
+        fits = fits && carve_bytes(t.r1 - t.r0, t.q1 - t.q_frag, true, cp[t.r1] - cp[t.r0]) <= slot_budget + 4096;
+      if (fits || te == 1) break;
+      te = std::max<uint64_t>(te / 2, 1);
+    }
+  }
   std::vector<uint64_t> cuts;
-  if (!greedy_cuts(a.ptr, cfg.c_aware ? cp : nullptr, n, row_bytes, a_tile_bytes, ib + vb,
-                   cfg.c_aware ? tile_budget : slot_budget - slot_budget / 16, cuts, &bad))
+  if (maxmem) {
+    cuts.assign(1, 0);
+    for (const MmTile& t : mm) cuts.push_back(t.r1);
+  } else if (!greedy_cuts(a.ptr, cfg.c_aware ? cp : nullptr, n, row_bytes, a_tile_bytes, ib + vb,
+                          cfg.c_aware ? tile_budget : slot_budget - slot_budget / 16, cuts, &bad))
     fail(AIRES_B200_ROW_TOO_LARGE, "row " + std::to_string(bad) + " does not fit a ring slot of " +
                                        std::to_string(slot_budget) + " bytes");
+  if (maxmem) {
+    for (size_t j = 0; j < mm.size(); j++) {
+      const MmTile& t = mm[j];
+      if (carve_bytes(t.r1 - t.r0, t.q1 - t.q_frag, true, cp[t.r1] - cp[t.r0]) > slot_budget + 4096)
+        fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY,
+             "MaxMemory tile " + std::to_string(j) + " (fragment + raw bytes + output block) does not fit a slot");
+    }
+  }
   if (!cfg.c_aware) {
     for (size_t j = 0; j + 1 < cuts.size(); j++) {
       const uint64_t r0 = cuts[j], r1 = cuts[j + 1];
@@ -465,7 +519,8 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   if (cfg.device_budget == 0) {  // resize the ring to the largest tile
     uint64_t need = 0;
     for (uint64_t j = 0; j < n_tiles; j++)
-      need = std::max(need, carve_bytes(cuts[j + 1] - cuts[j], a.ptr[cuts[j + 1]] - a.ptr[cuts[j]], true,
+      need = std::max(need, carve_bytes(cuts[j + 1] - cuts[j],
+                                        maxmem ? mm[j].q1 - mm[j].q_frag : a.ptr[cuts[j + 1]] - a.ptr[cuts[j]], true,
                                         cp[cuts[j + 1]] - cp[cuts[j]]));
     if (need > slot_cap) {
       slot_cap = need;
@@ -475,6 +530,19 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   Ctl* d_tctl = static_cast<Ctl*>(arena.get(sizeof(Ctl) * std::max<uint64_t>(n_tiles, 1)));
   AB2_CUDA(cudaMemsetAsync(d_tctl, 0, sizeof(Ctl) * std::max<uint64_t>(n_tiles, 1), cs));
   AB2_CUDA(cudaEventRecord(t_p1, cs));
+
+  // MaxMemory's host merge buffer (pinned): the trailing fragment of tile j, re-sent with tile j+1
+  void* merge_col = nullptr;
+  void* merge_val = nullptr;
+  cudaEvent_t frag_back = st.make();
+  HostBuf merge_buf;
+  if (maxmem) {
+    uint64_t maxfrag = 1;
+    for (const MmTile& m : mm) maxfrag = std::max(maxfrag, m.q0 - m.q_frag);
+    char* mb = static_cast<char*>(merge_buf.get(maxfrag * (ib + vb) + 256));
+    merge_col = mb;
+    merge_val = mb + ((maxfrag * ib + 127) & ~uint64_t(127));
+  }
 
   // ---------------- Phase II ----------------
   mark("tiles cut");
@@ -489,6 +557,66 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
     if (j >= nbuf) AB2_CUDA(cudaStreamWaitEvent(st.h2d, slot[s].computed, 0));
     // its C space is free once tile j-nbuf was drained
     if (j >= nbuf) AB2_CUDA(cudaStreamWaitEvent(st.h2d, slot[s].drained, 0));
+    if (maxmem) {
+      // fragment (from the host merge buffer, filled by tile j-1's D2H) + raw tile (from A)
+      const MmTile& m = mm[j];
+      carve(s, r1 - r0, m.q1 - m.q_frag, true, c1 - c0);
+      if (j > 0) AB2_CUDA(cudaStreamWaitEvent(st.h2d, frag_back, 0));
+      const uint64_t nf = m.q0 - m.q_frag, nr = m.q1 - m.q0;
+      if (nf) {
+        AB2_CUDA(cudaMemcpyAsync(slot[s].acol, merge_col, nf * ib, cudaMemcpyHostToDevice, st.h2d));
+        AB2_CUDA(cudaMemcpyAsync(slot[s].aval, merge_val, nf * vb, cudaMemcpyHostToDevice, st.h2d));
+      }
+      if (nr) {
+        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(slot[s].acol) + nf * ib, static_cast<const char*>(a.idx) + m.q0 * ib,
+                                 nr * ib, cudaMemcpyHostToDevice, st.h2d));
+        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(slot[s].aval) + nf * vb, static_cast<const char*>(a.val) + m.q0 * vb,
+                                 nr * vb, cudaMemcpyHostToDevice, st.h2d));
+      }
+      rep.h2d_bytes += (nf + nr) * (ib + vb);
+      rep.merge_bytes += nf * (ib + vb);
+      AB2_CUDA(cudaEventRecord(slot[s].loaded, st.h2d));
+      AB2_CUDA(cudaStreamWaitEvent(cs, slot[s].loaded, 0));
+      // the trailing fragment goes back to the host once this tile is on the device
+      const uint64_t fb = j + 1 < mm.size() ? mm[j + 1].q_frag : pend;
+      const uint64_t tail = m.q1 > fb ? m.q1 - fb : 0;
+      AB2_CUDA(cudaStreamWaitEvent(st.d2h, slot[s].loaded, 0));
+      if (tail) {
+        AB2_CUDA(cudaMemcpyAsync(merge_col, static_cast<char*>(slot[s].acol) + (fb - m.q_frag) * ib, tail * ib,
+                                 cudaMemcpyDeviceToHost, st.d2h));
+        AB2_CUDA(cudaMemcpyAsync(merge_val, static_cast<char*>(slot[s].aval) + (fb - m.q_frag) * vb, tail * vb,
+                                 cudaMemcpyDeviceToHost, st.d2h));
+        rep.d2h_bytes += tail * (ib + vb);
+      }
+      AB2_CUDA(cudaEventRecord(frag_back, st.d2h));
+      TilePass t{};
+      t.aptr = d_aptr + r0;
+      t.abase = m.q_frag;
+      t.acol = slot[s].acol;
+      t.aval = slot[s].aval;
+      t.rows = static_cast<int64_t>(r1 - r0);
+      t.cpos = d_cptr + r0;
+      t.cbase = static_cast<int64_t>(c0);
+      t.ccol = slot[s].ccol;
+      t.cval = slot[s].cval;
+      t.c_cap = c1 - c0;
+      t.heavy = slot[s].heavy;
+      t.cnt = slot[s].cnt;
+      t.toff = slot[s].toff;
+      t.ctl = d_tctl + j;
+      ctx.launches += tile_product(ctx, *x, ib, t);
+      AB2_CUDA(cudaEventRecord(slot[s].computed, cs));
+      AB2_CUDA(cudaStreamWaitEvent(st.d2h, slot[s].computed, 0));
+      if (c1 > c0) {
+        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oidx) + c0 * ib, slot[s].ccol, (c1 - c0) * ib,
+                                 cudaMemcpyDeviceToHost, st.d2h));
+        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oval) + c0 * vb, slot[s].cval, (c1 - c0) * vb,
+                                 cudaMemcpyDeviceToHost, st.d2h));
+      }
+      rep.d2h_bytes += (c1 - c0) * (ib + vb);
+      AB2_CUDA(cudaEventRecord(slot[s].drained, st.d2h));
+      continue;
+    }
     carve(s, r1 - r0, q1 - q0, true, c1 - c0);
     if (cols_resident) slot[s].acol = d_acol_full + (q0 - p0) * ib;
     if (q1 > q0) {

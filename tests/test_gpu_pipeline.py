@@ -136,3 +136,19 @@ def test_storage_leg_segments_file(tmp_path, sizes, mode):
         # plus the input rounding (2^-24 relative per operand)
         assert np.max(np.abs(c.values - wv) / np.abs(wv)) < 1e-5 + 2 * 2.0 ** -24
     print("storage leg used GDS:", rep["used_gds"])
+
+
+@pytest.mark.parametrize("frac", [0.5, 0.25])
+def test_maxmemory_baseline_same_result_more_traffic(frac):
+    """run_maxmemory (scheduler.hpp:174-293) on the device: fixed byte tiles that split rows, each
+    split row's fragment returned to the host and re-sent.  Bit-identical C to run_aires (fp64) and
+    the oracle; its ledger carries the fragment round trips (merge_bytes > 0 when rows are split)."""
+    g, x = _graph(20_000, 300_000, 128)
+    wp, wi, wv, macs = _oracle(g, x)
+    a_b, c_b = _bytes(g, x, (wp, wi))
+    budget = ab.MemoryBudget(int(3e6 + frac * (a_b + c_b)))
+    mm = ab.run_maxmemory(g, x, budget)
+    ar = ab.run_aires(g, x, budget)
+    assert mm.report.c_checksum == ar.report.c_checksum == po.checksum(g.n_rows, x.n_cols, wp, wi, wv)
+    assert mm.report.segments >= 2 and mm.report.ledger.merge_bytes > 0
+    assert mm.report.ledger.h2d.bytes > 0 and mm.report.strategy == "maxmemory"
