@@ -42,6 +42,9 @@
 #ifndef AB2_NUM_MINB
 #define AB2_NUM_MINB 4
 #endif
+#ifndef AB2_NUM_MAXT
+#define AB2_NUM_MAXT 256
+#endif
 
 #include "ab2_kernels.cuh"
 
@@ -703,7 +706,7 @@ __device__ __forceinline__ bool short_row(const Num3Args<V, IdxT>& p, const IdxT
 }
 
 template <class V, class IdxT, int W, bool XZ>
-__global__ void __launch_bounds__(256, AB2_NUM_MINB) k_numeric3(Num3Args<V, IdxT> p) {
+__global__ void __launch_bounds__(AB2_NUM_MAXT, AB2_NUM_MINB) k_numeric3(Num3Args<V, IdxT> p) {
   constexpr bool EXACT = sizeof(V) == 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned long long s_ticket;

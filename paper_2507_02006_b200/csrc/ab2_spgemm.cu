@@ -46,7 +46,7 @@ void launch_numeric_w(Ctx& ctx, const Num3Args<V, IdxT>& p, int threads, size_t 
 
 template <class V, class IdxT>
 int numeric_warps(const Num3Args<V, IdxT>& p) {
-  int nw = static_cast<int>(env_int("AB2_NUM_WARPS", 4));
+  int nw = std::min<int>(static_cast<int>(env_int("AB2_NUM_WARPS", 4)), AB2_NUM_MAXT / 32);
   return std::max(1, std::min<int>(nw, static_cast<int>((200 * 1024) / p.warp_bytes)));
 }
 
