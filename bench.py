@@ -226,6 +226,10 @@ def run_b200(args, cfg):
         dist.all_reduce(m)
         tot_macs = int(m.item())
     gflops = 2.0 * tot_macs / (ms * 1e-3) / 1e9
+    c_ptr_check = c_idx_check = None
+    if not args.skip_e2e and rank == 0 and world == 1:  # the device product, to check the host-API run against
+        c_ptr_check = outbuf["ptr"][: n + 1].cpu().numpy().view(np.uint64)
+        c_idx_check = outbuf["idx"][:nnz_c].cpu().numpy()
 
     # roofline of the dominant kernel (numeric) and of the whole step
     peak, peak_src = peaks()
@@ -261,9 +265,12 @@ def run_b200(args, cfg):
                          g.nnz())
         hxm = ab._Matrix(K, x.n_cols, ab.CSR, ab.HOST, 4, vb, hX[0].data_ptr(), hX[1].data_ptr(),
                          hX[2].data_ptr(), x.nnz())
+        # streamed output hands the allocator an upper bound of nnz(C) (include/aires_b200.h):
+        # min(rows * n_cols, nnz(A) * longest X row); the pinned result buffers cover it
+        c_bound = min(n * x.n_cols, g.nnz() * int(np.diff(x.row_ptr.astype(np.int64)).max(initial=1)))
         hout = {"ptr": torch.empty(n + 1, dtype=torch.int64).pin_memory(),
-                "idx": torch.empty(max(nnz_c, 1), dtype=torch.int32).pin_memory(),
-                "val": torch.empty(max(nnz_c, 1), dtype=vdt_t).pin_memory()}
+                "idx": torch.empty(max(nnz_c, c_bound, 1), dtype=torch.int32).pin_memory(),
+                "val": torch.empty(max(nnz_c, c_bound, 1), dtype=vdt_t).pin_memory()}
 
         def host_alloc(user, rows, nnz, pp, pi, pv):
             if nnz > hout["idx"].numel():
@@ -278,16 +285,23 @@ def run_b200(args, cfg):
             ab._check(L.aires_b200_spgemm(C.byref(ham), C.byref(hxm), mode, C.byref(hout_s)))
 
         # the public entry point for host-resident operands is the out-of-core run (run_aires,
-        # aires_b200_run): uncapped, it keeps A's columns resident after the sizing pass and cuts
-        # ~8 tiles so H2D of A, the product and the D2H of C overlap on the two copy engines
+        # aires_b200_run), uncapped.  Streamed output (the headline): no sizing pass, ~16 row
+        # blocks, C drains on copy engine 1 while A still crosses on copy engine 0.  Exact protocol
+        # (beside it): sizing pass over A's columns first, exact allocation, then the tiles.
         rrep = ab._RunReport()
-        rcfg = ab._RunConfig(0, mode, 1, 3, 0)
+        rcfg = ab._RunConfig(0, mode, 1, 0, ab.RUN_STREAM_OUT)
+        xrep = ab._RunReport()
+        xcfg = ab._RunConfig(0, mode, 1, 3, 0)
 
         def rstep():
             ab._check(L.aires_b200_run(C.byref(ham), C.byref(hxm), C.byref(rcfg), C.byref(hout_s), C.byref(rrep)))
 
+        def xstep():
+            ab._check(L.aires_b200_run(C.byref(ham), C.byref(hxm), C.byref(xcfg), C.byref(hout_s), C.byref(xrep)))
+
         for _ in range(max(1, args.warmup)):
             estep()
+            xstep()
             rstep()
         if dist:
             dist.barrier()
@@ -297,10 +311,25 @@ def run_b200(args, cfg):
         s_ms = (time.perf_counter() - t0) * 1e3 / args.steps
         t0 = time.perf_counter()
         for _ in range(args.steps):
+            xstep()
+        x_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        if int(hout_s.nnz) != nnz_c:
+            raise RuntimeError(f"run_aires (exact) nnz {int(hout_s.nnz)} != spgemm nnz {nnz_c}")
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
             rstep()
         e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
         if int(hout_s.nnz) != nnz_c:
-            raise RuntimeError(f"run_aires nnz {int(hout_s.nnz)} != spgemm nnz {nnz_c}")
+            raise RuntimeError(f"run_aires (streamed) nnz {int(hout_s.nnz)} != spgemm nnz {nnz_c}")
+        if rank == 0 and world == 1:
+            # the streamed result against the device product (structure bit-exact, values 1e-5)
+            hp = hout["ptr"].numpy().view(np.uint64)
+            if not np.array_equal(hp, c_ptr_check):
+                raise RuntimeError("streamed run row_ptr differs from the device product")
+            if not np.array_equal(hout["idx"][:nnz_c].numpy(), c_idx_check):
+                raise RuntimeError("streamed run col_idx differs from the device product")
+        link = link_bandwidth(dev)
+        e2e_duplex_ms = max(int(rrep.h2d_bytes) / link["h2d"], int(rrep.d2h_bytes) / link["d2h"]) / 1e6
         if dist:
             t = torch.tensor([e_ms], dtype=torch.float64, device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -309,8 +338,16 @@ def run_b200(args, cfg):
         d2h = int(rrep.d2h_bytes)
         e2e = {"value": round(2.0 * tot_macs / (e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(e_ms, 3),
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "api": "aires_b200_run (run_aires), pinned host A/X/C (u64 ptr, u32 idx, fp32 val), wall clock",
+               "api": "aires_b200_run (run_aires, streamed output), pinned host A/X/C (u64 ptr, u32 idx, fp32 val), "
+                      "wall clock",
                "segments": int(rrep.segments), "device_ms": round(rrep.total_ms, 3),
+               "roofline": {"bound": "host-link (full duplex)", "link_gbs": {k: round(v, 2) for k, v in link.items()},
+                            "t_roof_ms": round(e2e_duplex_ms, 3), "frac": round(e2e_duplex_ms / e_ms, 4),
+                            "basis": "max(H2D bytes / measured pinned H2D GB/s, D2H bytes / measured D2H GB/s)"},
+               "exact_protocol": {"api": "aires_b200_run without streamed output (sizing pass over A's columns, "
+                                         "exact allocation, then the tiles)",
+                                  "ms_per_step": round(x_ms, 3), "value": round(2.0 * tot_macs / (x_ms * 1e-3) / 1e9, 3),
+                                  "device_ms": round(xrep.total_ms, 3), "segments": int(xrep.segments)},
                "spgemm_call": {"api": "aires_b200_spgemm with host buffers (one-shot H2D, product, D2H)",
                                "ms_per_step": round(s_ms, 3),
                                "value": round(2.0 * tot_macs / (s_ms * 1e-3) / 1e9, 3)}}

@@ -159,9 +159,16 @@ typedef struct aires_b200_run_config {
   uint32_t c_aware;       /* 1: tiles sized by A + C bytes (default); 0: RoBW by A only;
                              2: the MaxMemory baseline (fixed byte tiles, split rows' fragments
                                 returned to the host and re-sent, scheduler.hpp:174-293) */
-  uint32_t n_buffers;     /* tile ring depth (default 2) */
-  uint32_t reserved;
+  uint32_t n_buffers;     /* tile ring depth (default 2; 3 for streamed output) */
+  uint32_t flags;         /* AIRES_B200_RUN_* bits (0 = the reference's exact-allocation protocol) */
 } aires_b200_run_config;
+
+/* Streamed output (uncapped runs, device_budget 0): no sizing pass before the product.  c->alloc
+ * receives an UPPER BOUND of nnz(C) (min(rows * n_cols, nnz(A) * longest X row)) before the first
+ * tile, C is drained tile by tile while A is still crossing the link, and c->nnz reports the exact
+ * count (the arrays hold the exact CSR in their first c->nnz entries).  Ignored for capped and
+ * MaxMemory runs and for operands wider than the dense accumulator (exact protocol). */
+#define AIRES_B200_RUN_STREAM_OUT 1u
 
 typedef struct aires_b200_run_report {
   uint64_t segments;

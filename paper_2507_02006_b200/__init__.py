@@ -84,7 +84,7 @@ class _Output(C.Structure):
 
 class _RunConfig(C.Structure):
     _fields_ = [("device_budget", C.c_uint64), ("mode", C.c_uint32), ("c_aware", C.c_uint32),
-                ("n_buffers", C.c_uint32), ("reserved", C.c_uint32)]
+                ("n_buffers", C.c_uint32), ("flags", C.c_uint32)]
 
 
 class _RunReport(C.Structure):
@@ -472,15 +472,20 @@ def run_maxmemory(a: CsrMatrix, b, budget: MemoryBudget, cfg=None, mode: int = M
     return res
 
 
+RUN_STREAM_OUT = 1  # aires_b200_run_config.flags: streamed output (include/aires_b200.h)
+
+
 def run_aires(a: CsrMatrix, b, budget: MemoryBudget, cfg=None, mode: int = MODE_AUTO, c_aware: bool = True,
-              n_buffers: int = 2, with_checksum: bool = True) -> RunResult:
+              n_buffers: int = 2, with_checksum: bool = True, stream_out: bool = False) -> RunResult:
     """scheduler.hpp:72-168 as a real three-phase tile pipeline on the B200 (ab2_pipeline.cu).
 
     A stays in host memory and streams through a ring of device slots sized by A + C bytes;
     C drains tile by tile straight into the result arrays.  ``budget.device_total`` caps the
     device bytes the run may hold (0: free memory).  ``cfg`` (SimConfig) only parameterises
     the reference's simulator and is accepted for signature compatibility.  Raises AiresError
-    (insufficient_device_memory / row_too_large) instead of truncating (proj/README.md:58-60)."""
+    (insufficient_device_memory / row_too_large) instead of truncating (proj/README.md:58-60).
+    ``stream_out`` (uncapped runs): no sizing pass before the product -- the result arrays are
+    allocated at an upper bound of nnz(C) and C drains while A is still uploading; same C."""
     del cfg
     L = lib()
     am, keep_a = _matrix_from_np(a.n_rows, a.n_cols, CSR, a.row_ptr, a.col_idx, a.values)
@@ -493,7 +498,8 @@ def run_aires(a: CsrMatrix, b, budget: MemoryBudget, cfg=None, mode: int = MODE_
         am.val_bytes = keep_a[2].dtype.itemsize
     al = _HostAlloc(keep_a[1].dtype, vdt)
     out = al.output()
-    cfgc = _RunConfig(int(budget.device_total), mode, 2 if c_aware == 2 else int(bool(c_aware)), int(n_buffers), 0)
+    cfgc = _RunConfig(int(budget.device_total), mode, 2 if c_aware == 2 else int(bool(c_aware)),
+                      0 if stream_out and n_buffers == 2 else int(n_buffers), RUN_STREAM_OUT if stream_out else 0)
     rep = _RunReport()
     _check(L.aires_b200_run(C.byref(am), C.byref(bm), C.byref(cfgc), C.byref(out), C.byref(rep)))
     c = CsrMatrix(a.n_rows, b.n_cols, al.ptr, al.idx[: out.nnz], al.val[: out.nnz])

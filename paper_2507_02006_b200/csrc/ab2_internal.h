@@ -21,6 +21,23 @@ struct DevBuf {
     return static_cast<T*>(get(n * sizeof(T)));
   }
   void release();
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;  // owns its allocation: containers move it, never copy it
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), cap(o.cap) {
+    o.p = nullptr;
+    o.cap = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      cap = o.cap;
+      o.p = nullptr;
+      o.cap = 0;
+    }
+    return *this;
+  }
   ~DevBuf() { release(); }
 };
 
@@ -30,6 +47,9 @@ struct HostBuf {
   size_t cap = 0;
   void* get(size_t bytes);
   void release();
+  HostBuf() = default;
+  HostBuf(const HostBuf&) = delete;
+  HostBuf& operator=(const HostBuf&) = delete;
   ~HostBuf() { release(); }
 };
 
@@ -134,9 +154,33 @@ struct TilePass {
   uint64_t* toff;   // rows scratch
   Ctl* ctl;         // zeroed; bad_row != 0 afterwards means a count/capacity failure
 };
-// Both return the number of kernels launched.
+// A tile whose C row counts are not known in advance (streamed-output runs): product into a
+// staging area, scan of the row counts -> local C row offsets, placement into a contiguous C block.
+struct TileStaged {
+  const uint64_t* aptr;
+  uint64_t abase;
+  const void* acol;
+  const void* aval;
+  int64_t rows;
+  uint64_t a_nnz;    // A entries of the tile (staging bound)
+  void* tcol;        // staging, staged_capacity() entries
+  void* tval;
+  uint64_t t_cap;
+  int64_t* cptr;     // rows+1 local C row offsets (out)
+  void* ccol;        // C block, >= c_bound() entries
+  void* cval;
+  int64_t* heavy;    // rows scratch
+  uint32_t* cnt;     // rows scratch
+  uint64_t* toff;    // rows scratch
+  int64_t* part;     // scan partials, (rows + 2047) / 2048
+  Ctl* ctl;          // zeroed; afterwards nnz = tile nnz, flops = MACs, bad_row != 0 = staging overflow
+};
+uint64_t c_bound(const XOperand& x, uint64_t rows, uint64_t a_nnz);  // nnz(C) upper bound of a tile
+uint64_t staged_capacity(Ctx& ctx, const XOperand& x, uint64_t rows, uint64_t a_nnz);
+// All return the number of kernels launched.
 int tile_symbolic(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TileSym& t);
 int tile_product(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TilePass& t);
+int tile_product_staged(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TileStaged& t);
 
 // GCN layer steps either side of A·X (ab2_gcn.cu, gcn.hpp:29-116).
 void normalize_adjacency(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out);

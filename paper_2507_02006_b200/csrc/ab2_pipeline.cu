@@ -161,6 +161,219 @@ double ms_between(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
+// Global C row offsets of a streamed tile: local offsets + the nnz of every earlier tile (a device
+// running total, so the compute stream needs nothing from the host); the last block carries the
+// total on to the next tile.
+// The tile's {nnz, MACs, bad_row} also go straight to pinned host memory (UVA-mapped), so the host
+// learns them without a copy queued behind the D2H of C on the copy engine.
+__global__ void k_tile_ptr(const int64_t* __restrict__ in, int64_t n, const Ctl* __restrict__ ctl,
+                           unsigned long long* __restrict__ base, uint64_t* __restrict__ out,
+                           volatile unsigned long long* host) {
+  const unsigned long long b = base[0];
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<uint64_t>(in[i]) + b;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    base[1] = b + ctl->nnz;
+    host[0] = ctl->nnz;
+    host[1] = ctl->flops;
+    host[2] = ctl->bad_row;
+    __threadfence_system();
+  }
+}
+
+// Streamed-output run (AIRES_B200_RUN_STREAM_OUT, uncapped): no sizing pass before the product.
+// The caller's allocator receives an upper bound of nnz(C) up front (min(rows * n_cols, nnz(A) *
+// longest X row)); A is cut into ~AB2_STREAM_TILES row blocks of equal nnz and every tile goes
+// H2D (copy engine 0) -> product into staging + scan + placement (compute stream) -> D2H of its
+// exact C block to the running offset (copy engine 1).  The host learns tile j's nnz (one pinned
+// Ctl readback) while tile j+1 is already queued, so the D2H of C overlaps the H2D of A from the
+// first tile on -- with exact sizing first, D2H cannot start before every column of A has crossed
+// the link (the run's Phase I).  Same results as the exact run; out.nnz is the exact count.
+void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b, uint32_t mode, uint32_t nbuf,
+                aires_b200_output& out, aires_b200_run_report& rep, Streams& st, Arena& arena, Pinned& pin) {
+  const uint32_t ib = a.idx_bytes, vb = mode == AIRES_B200_MODE_FP32 ? 4 : 8;
+  const uint64_t n = a.n_rows;
+  const uint64_t p0 = a.ptr[0], pend = a.ptr[n];
+  cudaStream_t cs = ctx.stream;
+  cudaEvent_t t_begin = st.make_timed(), t_p1 = st.make_timed(), t_p2 = st.make_timed(), t_end = st.make_timed();
+  AB2_CUDA(cudaEventRecord(t_begin, cs));
+  AB2_CUDA(cudaStreamWaitEvent(st.h2d, t_begin, 0));
+  auto x = make_operand(ctx, b, mode, /*temp=*/true, kPlanSlots);
+  if (b.location == AIRES_B200_HOST)
+    rep.h2d_bytes += (b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols) * 8 + 8 +
+                     static_cast<uint64_t>(x->nnz) * (b.idx_bytes + b.val_bytes);
+  uint64_t* d_aptr = static_cast<uint64_t*>(arena.get((n + 1) * 8));
+  AB2_CUDA(cudaMemcpyAsync(d_aptr, a.ptr, (n + 1) * 8, cudaMemcpyHostToDevice, st.h2d));
+  rep.h2d_bytes += (n + 1) * 8;
+  // row blocks of ~equal A nnz, the first one a quarter of the others (the D2H of C starts sooner)
+  const uint64_t T = static_cast<uint64_t>(std::max<int64_t>(1, env_int("AB2_STREAM_TILES", 16)));
+  std::vector<uint64_t> cuts{0};
+  const double unit = static_cast<double>(pend - p0) / (static_cast<double>(T) - 0.75);
+  for (uint64_t i = 1; i < T; i++) {
+    const uint64_t target = p0 + static_cast<uint64_t>(unit * (static_cast<double>(i) - 0.75));
+    const uint64_t r = static_cast<uint64_t>(std::lower_bound(a.ptr, a.ptr + n + 1, target) - a.ptr);
+    if (r > cuts.back() && r < n) cuts.push_back(r);
+  }
+  if (n > 0) cuts.push_back(n);
+  const uint64_t n_tiles = cuts.size() - 1;
+  uint64_t max_rows = 1, max_annz = 1, max_cb = 1, max_stage = 1;
+  for (uint64_t j = 0; j < n_tiles; j++) {
+    const uint64_t rows = cuts[j + 1] - cuts[j], an = a.ptr[cuts[j + 1]] - a.ptr[cuts[j]];
+    max_rows = std::max(max_rows, rows);
+    max_annz = std::max(max_annz, an);
+    max_cb = std::max(max_cb, c_bound(*x, rows, an));
+    max_stage = std::max(max_stage, staged_capacity(ctx, *x, rows, an));
+  }
+  // the caller's allocator: an upper bound of nnz(C); the exact count is reported in out.nnz
+  const uint64_t bound = c_bound(*x, n, pend - p0);
+  void *optr = nullptr, *oidx = nullptr, *oval = nullptr;
+  int rc = out.alloc(out.user, n, bound, &optr, &oidx, &oval);
+  if (rc != 0) fail(rc, "output allocator failed for a bound of " + std::to_string(bound) + " nonzeros");
+  pin.ensure(optr, (n + 1) * 8);
+  pin.ensure(oidx, bound * ib);
+  pin.ensure(oval, bound * vb);
+  struct Slot {
+    void *acol, *aval, *tcol, *tval, *ccol, *cval;
+    int64_t *cptr, *heavy, *part;
+    uint64_t* optr;
+    uint32_t* cnt;
+    uint64_t* toff;
+    cudaEvent_t loaded, computed, drained;
+  };
+  // AB2_TRACE=1: per-tile device timeline (loaded / computed / drained, ms from the start) on stderr
+  const bool trace = env_int("AB2_TRACE", 0) != 0;
+  std::vector<cudaEvent_t> tl;
+  if (trace)
+    for (uint64_t j = 0; j < 3 * n_tiles; j++) tl.push_back(st.make_timed());
+  std::vector<Slot> slot(nbuf);
+  for (auto& s : slot) {
+    s.acol = arena.get(max_annz * ib);
+    s.aval = arena.get(max_annz * vb);
+    s.tcol = arena.get(max_stage * ib);
+    s.tval = arena.get(max_stage * vb);
+    s.ccol = arena.get(max_cb * ib);
+    s.cval = arena.get(max_cb * vb);
+    s.cptr = static_cast<int64_t*>(arena.get((max_rows + 1) * 8));
+    s.optr = static_cast<uint64_t*>(arena.get((max_rows + 1) * 8));
+    s.heavy = static_cast<int64_t*>(arena.get(max_rows * 8));
+    s.part = static_cast<int64_t*>(arena.get(((max_rows + kScanTile - 1) / kScanTile + 1) * 8));
+    s.cnt = static_cast<uint32_t*>(arena.get(max_rows * 4));
+    s.toff = static_cast<uint64_t*>(arena.get(max_rows * 8));
+    s.loaded = st.make();
+    s.computed = st.make();
+    s.drained = st.make();
+  }
+  Ctl* d_ctl = static_cast<Ctl*>(arena.get(sizeof(Ctl) * std::max<uint64_t>(n_tiles, 1)));
+  auto* h_rep = static_cast<unsigned long long*>(ctx.h_ctl.get(24 * std::max<uint64_t>(n_tiles, 1)));
+  AB2_CUDA(cudaMemsetAsync(d_ctl, 0, sizeof(Ctl) * std::max<uint64_t>(n_tiles, 1), cs));
+  auto* d_base = static_cast<unsigned long long*>(arena.get(8 * (n_tiles + 1)));
+  AB2_CUDA(cudaMemsetAsync(d_base, 0, 8 * (n_tiles + 1), cs));
+  cudaEvent_t e_ptr = st.make();
+  AB2_CUDA(cudaEventRecord(e_ptr, st.h2d));
+  AB2_CUDA(cudaStreamWaitEvent(cs, e_ptr, 0));
+  AB2_CUDA(cudaEventRecord(t_p1, cs));
+  cudaEvent_t e_zero = st.make();
+  AB2_CUDA(cudaEventRecord(e_zero, cs));
+  AB2_CUDA(cudaStreamWaitEvent(st.h2d, e_zero, 0));
+  AB2_CUDA(cudaStreamWaitEvent(st.d2h, e_zero, 0));
+
+  uint64_t running = 0, flops = 0;
+  auto drain = [&](uint64_t j) {
+    Slot& s = slot[j % nbuf];
+    AB2_CUDA(cudaEventSynchronize(s.computed));
+    const volatile unsigned long long* c = h_rep + 3 * j;
+    if (c[2]) fail(AIRES_B200_CAPACITY_EXCEEDED, "tile staging overflow");
+    const uint64_t r0 = cuts[j], rows = cuts[j + 1] - r0, nz = c[0];
+    if (running + nz > bound) fail(AIRES_B200_CAPACITY_EXCEEDED, "C exceeds its bound");
+    flops += c[1];
+    AB2_CUDA(cudaStreamWaitEvent(st.d2h, s.computed, 0));  // (already complete: the host waited on it)
+    AB2_CUDA(cudaMemcpyAsync(static_cast<uint64_t*>(optr) + r0, s.optr, (rows + 1) * 8, cudaMemcpyDeviceToHost, st.d2h));
+    if (nz) {
+      AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oidx) + running * ib, s.ccol, nz * ib, cudaMemcpyDeviceToHost, st.d2h));
+      AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oval) + running * vb, s.cval, nz * vb, cudaMemcpyDeviceToHost, st.d2h));
+    }
+    rep.d2h_bytes += (rows + 1) * 8 + nz * (ib + vb);
+    AB2_CUDA(cudaEventRecord(s.drained, st.d2h));
+    if (trace) AB2_CUDA(cudaEventRecord(tl[3 * j + 2], st.d2h));
+    running += nz;
+  };
+  for (uint64_t j = 0; j < n_tiles; j++) {
+    Slot& s = slot[j % nbuf];
+    const uint64_t r0 = cuts[j], r1 = cuts[j + 1];
+    const uint64_t q0 = a.ptr[r0], q1 = a.ptr[r1];
+    if (j >= nbuf) AB2_CUDA(cudaStreamWaitEvent(st.h2d, s.drained, 0));
+    if (q1 > q0) {
+      AB2_CUDA(cudaMemcpyAsync(s.acol, static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib,
+                               cudaMemcpyHostToDevice, st.h2d));
+      AB2_CUDA(cudaMemcpyAsync(s.aval, static_cast<const char*>(a.val) + q0 * vb, (q1 - q0) * vb,
+                               cudaMemcpyHostToDevice, st.h2d));
+    }
+    rep.h2d_bytes += (q1 - q0) * (ib + vb);
+    AB2_CUDA(cudaEventRecord(s.loaded, st.h2d));
+    if (trace) AB2_CUDA(cudaEventRecord(tl[3 * j], st.h2d));
+    AB2_CUDA(cudaStreamWaitEvent(cs, s.loaded, 0));
+    if (j >= nbuf) AB2_CUDA(cudaStreamWaitEvent(cs, s.drained, 0));  // staging / C block of tile j-nbuf
+    TileStaged t{};
+    t.aptr = d_aptr + r0;
+    t.abase = q0;
+    t.acol = s.acol;
+    t.aval = s.aval;
+    t.rows = static_cast<int64_t>(r1 - r0);
+    t.a_nnz = q1 - q0;
+    t.tcol = s.tcol;
+    t.tval = s.tval;
+    t.t_cap = staged_capacity(ctx, *x, r1 - r0, q1 - q0);
+    t.cptr = s.cptr;
+    t.ccol = s.ccol;
+    t.cval = s.cval;
+    t.heavy = s.heavy;
+    t.cnt = s.cnt;
+    t.toff = s.toff;
+    t.part = s.part;
+    t.ctl = d_ctl + j;
+    ctx.launches += tile_product_staged(ctx, *x, ib, t);
+    {
+      const int g = static_cast<int>(std::min<uint64_t>((r1 - r0 + 256) / 256, static_cast<uint64_t>(ctx.sms) * 4));
+      k_tile_ptr<<<g, 256, 0, cs>>>(s.cptr, static_cast<int64_t>(r1 - r0 + 1), d_ctl + j, d_base + j, s.optr,
+                                    h_rep + 3 * j);
+      AB2_CUDA(cudaGetLastError());
+      ctx.launches++;
+    }
+    AB2_CUDA(cudaEventRecord(s.computed, cs));
+    if (trace) AB2_CUDA(cudaEventRecord(tl[3 * j + 1], cs));
+    if (j >= 1) drain(j - 1);
+  }
+  AB2_CUDA(cudaEventRecord(t_p2, cs));
+  if (n_tiles) drain(n_tiles - 1);
+  if (n == 0) static_cast<uint64_t*>(optr)[0] = 0;
+  cudaEvent_t e_d2h = st.make();
+  AB2_CUDA(cudaEventRecord(e_d2h, st.d2h));
+  AB2_CUDA(cudaStreamWaitEvent(cs, e_d2h, 0));
+  AB2_CUDA(cudaEventRecord(t_end, cs));
+  AB2_CUDA(cudaStreamSynchronize(cs));
+  if (trace) {
+    std::fprintf(stderr, "[ab2 stream] phase1 (X, A row_ptr) %.3f ms\n", ms_between(t_begin, t_p1));
+    for (uint64_t j = 0; j < n_tiles; j++)
+      std::fprintf(stderr, "[ab2 stream] tile %3llu  loaded %8.3f  computed %8.3f  drained %8.3f ms\n",
+                   static_cast<unsigned long long>(j), ms_between(t_begin, tl[3 * j]),
+                   ms_between(t_begin, tl[3 * j + 1]), ms_between(t_begin, tl[3 * j + 2]));
+  }
+  rep.segments = n_tiles;
+  rep.flops = flops;
+  rep.c_nnz = running;
+  rep.peak_device_bytes = arena.used + x->bytes;
+  rep.phase1_ms = ms_between(t_begin, t_p1);
+  rep.phase2_ms = ms_between(t_p1, t_p2);
+  rep.phase3_ms = ms_between(t_p2, t_end);
+  rep.total_ms = ms_between(t_begin, t_end);
+  ctx.last_ms = rep.total_ms;
+  out.n_rows = n;
+  out.n_cols = static_cast<uint64_t>(x->n_cols);
+  out.nnz = running;
+  out.flops = flops;
+}
+
 }  // namespace
 
 void destroy_pipe_cache(void* p) { delete static_cast<PipeCacheImpl*>(p); }
@@ -206,6 +419,11 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   pin.ensure(a.ptr, (n + 1) * 8);
   pin.ensure(static_cast<const char*>(a.idx) + p0 * ib, (pend - p0) * ib);
   pin.ensure(static_cast<const char*>(a.val) + p0 * vb, (pend - p0) * vb);
+  if ((cfg.flags & AIRES_B200_RUN_STREAM_OUT) && cfg.device_budget == 0 && cfg.c_aware != 2 &&
+      static_cast<int64_t>(b.n_cols) <= wide_threshold(mode)) {
+    run_stream(ctx, a, b, mode, cfg.n_buffers ? nbuf : 3, out, rep, st, arena, pin);
+    return;
+  }
 
   // ---------------- Phase I ----------------
   mark("pinned checks done");

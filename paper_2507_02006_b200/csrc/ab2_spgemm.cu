@@ -546,6 +546,55 @@ void wide_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires
 
 }  // namespace
 
+namespace {
+template <class V, class IdxT>
+int tile_product_staged_t(Ctx& ctx, const XOperand& x, const TileStaged& t) {
+  if (t.rows <= 0) return 0;
+  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 1024);
+  const int g = static_cast<int>(std::min<int64_t>((t.rows + 255) / 256, static_cast<int64_t>(ctx.sms) * 16));
+  k_classify<<<g, 256, 0, ctx.stream>>>(t.aptr, t.rows, heavy_deg, t.heavy, t.ctl);
+  AB2_CUDA(cudaGetLastError());
+  Num3Args<V, IdxT> np = make_num3<V, IdxT>(x, t.aptr, t.abase, static_cast<const IdxT*>(t.acol),
+                                            static_cast<const V*>(t.aval), t.rows, t.heavy, heavy_deg, t.cnt,
+                                            t.toff, t.ctl);
+  np.tcol = static_cast<IdxT*>(t.tcol);
+  np.tval = static_cast<V*>(t.tval);
+  np.t_cap = t.t_cap;
+  launch_product<V, IdxT>(ctx, np, x);
+  const int64_t nb = (t.rows + kScanTile - 1) / kScanTile;
+  const int32_t* cin = reinterpret_cast<const int32_t*>(t.cnt);
+  k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(cin, t.rows, t.part);
+  k_scan_part<<<1, 1024, 0, ctx.stream>>>(t.part, nb, t.ctl);
+  k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(cin, t.rows, t.part, t.cptr);
+  k_place<V, IdxT><<<ctx.sms * 8, 256, 0, ctx.stream>>>(t.cnt, t.toff, t.cptr, np.tcol, np.tval, t.rows,
+                                                        static_cast<IdxT*>(t.ccol), static_cast<V*>(t.cval));
+  AB2_CUDA(cudaGetLastError());
+  return 6;
+}
+}  // namespace
+
+uint64_t c_bound(const XOperand& x, uint64_t rows, uint64_t a_nnz) {
+  const uint64_t maxlen = static_cast<uint64_t>(std::max<int64_t>(x.max_row_len, 1));
+  return std::min<uint64_t>(rows * static_cast<uint64_t>(x.n_cols), a_nnz * maxlen);
+}
+
+// Staging entries of one product pass over `rows` rows: the nnz bound + 1/7 (each warp's bump
+// reservation wastes less than one row out of >= 8 rows' worth) + one reservation block per
+// resident warp (the same sizing as run_product).
+uint64_t staged_capacity(Ctx& ctx, const XOperand& x, uint64_t rows, uint64_t a_nnz) {
+  const uint64_t bound = c_bound(x, rows, a_nnz);
+  const uint64_t stride = static_cast<uint64_t>((x.n_cols + 1 + 31) & ~int64_t(31));
+  const uint64_t block = std::max<uint64_t>(4096, 8 * stride);
+  return bound + bound / 7 + (static_cast<uint64_t>(ctx.sms) * 64 + 1) * block;
+}
+
+int tile_product_staged(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TileStaged& t) {
+  const bool f32 = x.mode == AIRES_B200_MODE_FP32;
+  if (idx_bytes == 4)
+    return f32 ? tile_product_staged_t<float, uint32_t>(ctx, x, t) : tile_product_staged_t<double, uint32_t>(ctx, x, t);
+  return f32 ? tile_product_staged_t<float, uint64_t>(ctx, x, t) : tile_product_staged_t<double, uint64_t>(ctx, x, t);
+}
+
 int tile_product(Ctx& ctx, const XOperand& x, uint32_t idx_bytes, const TilePass& t) {
   const bool f32 = x.mode == AIRES_B200_MODE_FP32;
   if (idx_bytes == 4) return f32 ? tile_product_t<float, uint32_t>(ctx, x, t) : tile_product_t<double, uint32_t>(ctx, x, t);

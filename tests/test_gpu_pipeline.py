@@ -152,3 +152,71 @@ def test_maxmemory_baseline_same_result_more_traffic(frac):
     assert mm.report.c_checksum == ar.report.c_checksum == po.checksum(g.n_rows, x.n_cols, wp, wi, wv)
     assert mm.report.segments >= 2 and mm.report.ledger.merge_bytes > 0
     assert mm.report.ledger.h2d.bytes > 0 and mm.report.strategy == "maxmemory"
+
+
+# ---- streamed output (AIRES_B200_RUN_STREAM_OUT): no sizing pass, C drained while A uploads ----
+
+@pytest.mark.parametrize("tiles", ["1", "5", "16", "300"])
+def test_stream_out_fp64_bit_exact(tiles, monkeypatch):
+    monkeypatch.setenv("AB2_STREAM_TILES", tiles)
+    g, x = _graph(20_000, 300_000, 128, seed=8)
+    wp, wi, wv, macs = _oracle(g, x)
+    res = ab.run_aires(g, x, ab.MemoryBudget(0), stream_out=True)
+    assert 1 <= res.report.segments <= int(tiles)
+    if int(tiles) > 1:
+        assert res.report.segments >= 2
+    assert res.report.c_checksum == po.checksum(g.n_rows, x.n_cols, wp, wi, wv)
+    assert res.report.flops == macs
+    assert np.array_equal(res.c.row_ptr, wp) and np.array_equal(res.c.col_idx, wi)
+    # every byte crosses the link once: A (ptr, col, val) and X up, C (ptr, col, val) down
+    base = 8 * (g.n_rows + 1) + 16 * g.nnz() + 8 * (x.n_rows + 1) + 16 * x.nnz()
+    assert res.report.ledger.h2d.bytes == base
+    assert res.report.ledger.d2h.bytes >= 8 * (g.n_rows + 1) + 16 * wi.shape[0]
+
+
+@pytest.mark.parametrize("n_buffers", [2, 3, 4])
+def test_stream_out_fp32_matches_exact_protocol(n_buffers, monkeypatch):
+    monkeypatch.setenv("AB2_STREAM_TILES", "12")
+    g, x = _graph(30_000, 400_000, 100, seed=4)
+    g32 = ab.CsrMatrix(g.n_rows, g.n_cols, g.row_ptr, g.col_idx.astype(np.uint32), g.values.astype(np.float32))
+    x32 = ab.CsrMatrix(x.n_rows, x.n_cols, x.row_ptr, x.col_idx.astype(np.uint32), x.values.astype(np.float32))
+    exact = ab.run_aires(g32, x32, ab.MemoryBudget(0), with_checksum=False)
+    res = ab.run_aires(g32, x32, ab.MemoryBudget(0), n_buffers=n_buffers, with_checksum=False, stream_out=True)
+    assert res.report.segments >= 4
+    assert np.array_equal(res.c.row_ptr, exact.c.row_ptr)
+    assert np.array_equal(res.c.col_idx, exact.c.col_idx)
+    np.testing.assert_allclose(res.c.values, exact.c.values, rtol=2e-6)
+    assert res.report.flops == exact.report.flops
+
+
+def test_stream_out_edge_shapes():
+    # empty rows at both ends, an all-empty A, and zero rows
+    g, x = _graph(4_000, 40_000, 64, seed=9)
+    lens = np.diff(g.row_ptr.astype(np.int64))
+    row_of = np.repeat(np.arange(g.n_rows), lens)
+    keep = (row_of >= 100) & (row_of < g.n_rows - 100)
+    lens[:100] = 0
+    lens[-100:] = 0
+    ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    g2 = ab.CsrMatrix(g.n_rows, g.n_cols, ptr, g.col_idx[keep], g.values[keep])
+    wp, wi, wv, _ = _oracle(g2, x)
+    res = ab.run_aires(g2, x, ab.MemoryBudget(0), stream_out=True)
+    assert np.array_equal(res.c.row_ptr, wp) and np.array_equal(res.c.col_idx, wi)
+    assert res.report.c_checksum == po.checksum(g2.n_rows, x.n_cols, wp, wi, wv)
+    empty = ab.CsrMatrix(g.n_rows, g.n_cols, np.zeros(g.n_rows + 1, np.uint64), np.zeros(0, np.uint64),
+                         np.zeros(0, np.float64))
+    res = ab.run_aires(empty, x, ab.MemoryBudget(0), stream_out=True)
+    assert res.c.nnz() == 0 and not res.c.row_ptr.any()
+    none = ab.CsrMatrix(0, g.n_cols, np.zeros(1, np.uint64), np.zeros(0, np.uint64), np.zeros(0, np.float64))
+    res = ab.run_aires(none, x, ab.MemoryBudget(0), stream_out=True)
+    assert res.c.nnz() == 0 and res.c.row_ptr.shape[0] == 1
+
+
+def test_stream_out_ignored_when_capped():
+    # a capped budget keeps the exact protocol (C-aware tiles need the sizing pass)
+    g, x = _graph(20_000, 300_000, 128)
+    wp, wi, wv, _ = _oracle(g, x)
+    a_b, c_b = _bytes(g, x, (wp, wi))
+    res = ab.run_aires(g, x, ab.MemoryBudget(int(3e6 + 0.25 * (a_b + c_b))), stream_out=True)
+    assert res.report.segments >= 2
+    assert res.report.c_checksum == po.checksum(g.n_rows, x.n_cols, wp, wi, wv)

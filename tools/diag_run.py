@@ -1,5 +1,5 @@
 """Where the wall time of an aires_b200_run goes (cfg inputs, pinned host buffers).
-usage: python tools/diag_run.py [cfg2] [budget_MB]"""
+usage: python tools/diag_run.py [cfg2] [budget_MB] [stream]  (stream: AIRES_B200_RUN_STREAM_OUT)"""
 import ctypes as C
 import os
 import sys
@@ -38,12 +38,14 @@ def alloc(user, rows, nnz, pp, pi, pv):
 afn = ab._ALLOC_FN(alloc)
 out = ab._Output(ab.HOST, 4, 4, 0, afn, None, 0, 0, 0, 0)
 budget = int(float(sys.argv[2]) * 1e6) if len(sys.argv) > 2 else 0
+flags = ab.RUN_STREAM_OUT if "stream" in sys.argv[3:] else 0
+nbuf = int(os.environ.get("NBUF", "0" if flags else "3"))
 for it in range(4):
     rep = ab._RunReport()
     if it == 3:
         os.environ["AB2_TRACE"] = "1"
     t0 = time.perf_counter()
-    ab._check(L.aires_b200_run(C.byref(am), C.byref(xm), C.byref(ab._RunConfig(budget, ab.MODE_FP32, 1, 3, 0)),
+    ab._check(L.aires_b200_run(C.byref(am), C.byref(xm), C.byref(ab._RunConfig(budget, ab.MODE_FP32, 1, nbuf, flags)),
                                C.byref(out), C.byref(rep)))
     print(f"run {it}: wall {(time.perf_counter() - t0) * 1e3:.2f} ms device {rep.total_ms:.2f} ms "
           f"p1 {rep.phase1_ms:.2f} p2 {rep.phase2_ms:.2f} p3 {rep.phase3_ms:.2f} segs {rep.segments} "
