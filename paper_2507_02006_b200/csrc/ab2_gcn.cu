@@ -8,13 +8,16 @@
 //   K8 combine (gcn.hpp:90-116): H' = ReLU(X · W), X sparse CSR, W dense row-major; entries <= 0
 //      after the activation are dropped (re-sparsified CSR).  One warp per row, lanes over output
 //      columns (tiles of 256), terms added in ascending k with separate multiply and add: fp64 is
-//      bit-identical to the reference; fp32 is within tolerance.  Two passes (count, fill) around a
-//      scan give the exact CSR.
+//      bit-identical to the reference; fp32 is within tolerance.  One-tile widths (<= 256 output
+//      columns) run one pass: positives go to a bump-allocated staging area with per-row counts,
+//      then scan + K_place give the exact CSR (the product is computed once; the extra bytes are
+//      one streaming copy of the output).  Wider W: two passes (count, fill) around a scan.
 #include <algorithm>
 #include <cmath>
 
 #include "ab2_internal.h"
 #include "ab2_kernels.cuh"
+#include "ab2_numeric.cuh"
 
 namespace ab2 {
 
@@ -129,12 +132,16 @@ __device__ __forceinline__ V mul_add(V acc, V a, V b) {
 // FILL = false: per-row positive counts; FILL = true: writes the positives at optr[r].
 // SMEM: W is staged once per CTA in shared memory (every X entry reads a whole W row, so from
 // global memory the L1 datapath bound the kernel: 36 ms for the products-shaped layer 2).
-template <class V, class IdxT, class IdxO, int J, bool FILL, bool SMEM>
+// STAGE (w_cols <= 32 * J): one pass; the row's positives go to a warp's bump reservation in the
+// staging area (ocol/oval, capacity t_cap), cnt[r] / toff[r] record where (K_place finishes).
+template <class V, class IdxT, class IdxO, int J, bool FILL, bool SMEM, bool STAGE = false>
 __global__ void __launch_bounds__(256) k_combine(const uint64_t* __restrict__ xptr, uint64_t xbase,
                                                  const IdxT* __restrict__ xcol, const V* __restrict__ xval,
                                                  int64_t rows, const V* __restrict__ wg, int64_t w_rows, int64_t w_cols,
                                                  int32_t* __restrict__ cnt, const int64_t* __restrict__ optr,
-                                                 IdxO* __restrict__ ocol, V* __restrict__ oval, Ctl* __restrict__ ctl) {
+                                                 IdxO* __restrict__ ocol, V* __restrict__ oval, Ctl* __restrict__ ctl,
+                                                 uint64_t* __restrict__ toff = nullptr, uint64_t t_cap = 0) {
+  StageCursor stage;
   constexpr int TW = 32 * J;  // output columns per tile
   extern __shared__ __align__(16) unsigned char smem_w[];
   const V* __restrict__ w = wg;
@@ -179,6 +186,34 @@ __global__ void __launch_bounds__(256) k_combine(const uint64_t* __restrict__ xp
           }
         }
       }
+      if constexpr (STAGE) {
+        unsigned m[J];
+        uint32_t total = 0;
+#pragma unroll
+        for (int j = 0; j < J; j++) {
+          m[j] = __ballot_sync(kFull, t0 + lane + 32 * j < w_cols && acc[j] > V(0));
+          total += __popc(m[j]);
+        }
+        const unsigned long long off = stage.take(total, ctl, 4096);
+        if (off + total <= t_cap) {
+#pragma unroll
+          for (int j = 0; j < J; j++) {
+            if (m[j] >> lane & 1u) {
+              const unsigned long long dst = off + written + __popc(m[j] & ((1u << lane) - 1));
+              ocol[dst] = static_cast<IdxO>(t0 + lane + 32 * j);
+              oval[dst] = acc[j];
+            }
+            written += __popc(m[j]);
+          }
+        } else if (lane == 0) {
+          ctl->bad_row = 2;  // staging overflow (the host sized it for the dense bound)
+        }
+        if (lane == 0) {
+          cnt[r] = static_cast<int32_t>(total);
+          toff[r] = off;
+        }
+        continue;
+      }
 #pragma unroll
       for (int j = 0; j < J; j++) {
         const int64_t c = t0 + lane + 32 * j;
@@ -194,7 +229,7 @@ __global__ void __launch_bounds__(256) k_combine(const uint64_t* __restrict__ xp
         written += __popc(m);
       }
     }
-    if constexpr (!FILL) {
+    if constexpr (!FILL && !STAGE) {
       if (lane == 0) cnt[r] = static_cast<int32_t>(written);
     }
   }
@@ -321,10 +356,10 @@ void normalize_t(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
   ctx.launches = launches;
 }
 
-template <class V, class IdxT, class IdxO, int J, bool FILL, bool SMEM>
+template <class V, class IdxT, class IdxO, int J, bool FILL, bool SMEM, bool STAGE = false>
 void combine_launch2(Ctx& ctx, const Staged& s, int64_t rows, const V* w, int64_t w_rows, int64_t w_cols, int32_t* cnt,
-                     int64_t* optr, IdxO* ocol, V* oval, Ctl* ctl) {
-  auto k = k_combine<V, IdxT, IdxO, J, FILL, SMEM>;
+                     int64_t* optr, IdxO* ocol, V* oval, Ctl* ctl, uint64_t* toff = nullptr, uint64_t t_cap = 0) {
+  auto k = k_combine<V, IdxT, IdxO, J, FILL, SMEM, STAGE>;
   size_t smem = 0;
   int grid = grid_of(rows * 32, 256, ctx.sms);
   if constexpr (SMEM) {
@@ -335,8 +370,135 @@ void combine_launch2(Ctx& ctx, const Staged& s, int64_t rows, const V* w, int64_
     grid = std::max(1, std::min(grid, std::max(nb, 1) * ctx.sms));  // persistent: W staged once per CTA
   }
   k<<<grid, 256, smem, ctx.stream>>>(s.ptr, s.base, static_cast<const IdxT*>(s.idx), static_cast<const V*>(s.val),
-                                     rows, w, w_rows, w_cols, cnt, optr, ocol, oval, ctl);
+                                     rows, w, w_rows, w_cols, cnt, optr, ocol, oval, ctl, toff, t_cap);
   AB2_CUDA(cudaGetLastError());
+}
+
+// fp32, 96 <= w_cols <= 256, W in shared memory: each lane owns 4 consecutive output columns per
+// 128-column group (one LDS.128 of the zero-padded W row per group and X entry, FFMA -- fp32 mode
+// is within tolerance, not bit-exact), so an X entry costs 2 SHFL + H LDS.128 + 4H FFMA instead of
+// 8 LDS + 8 FMUL + 8 FADD + 8 bounds checks.  Padded columns hold W = 0, so they are never
+// positive and drop out with the ReLU.  Output in ascending columns: group-major, then lane
+// (warp scan of the per-lane positive counts), then the lane's 4 columns.  One pass into staging.
+template <class IdxT, class IdxO, int H>
+__global__ void __launch_bounds__(512) k_combine_v4(const uint64_t* __restrict__ xptr, uint64_t xbase,
+                                                    const IdxT* __restrict__ xcol, const float* __restrict__ xval,
+                                                    int64_t rows, const float* __restrict__ wg, int64_t w_rows,
+                                                    int64_t w_cols, int32_t* __restrict__ cnt,
+                                                    IdxO* __restrict__ ocol, float* __restrict__ oval,
+                                                    Ctl* __restrict__ ctl, uint64_t* __restrict__ toff, uint64_t t_cap) {
+  constexpr int P = 128 * H;  // padded row length
+  extern __shared__ __align__(16) unsigned char smem_w[];
+  float* ws = reinterpret_cast<float*>(smem_w);
+  for (int64_t i = threadIdx.x; i < w_rows * P; i += blockDim.x) {
+    const int64_t rr = i / P, c = i % P;
+    ws[i] = c < w_cols ? wg[rr * w_cols + c] : 0.f;
+  }
+  __syncthreads();
+  const float4* __restrict__ w4 = reinterpret_cast<const float4*>(ws);
+  StageCursor stage;
+  const int lane = lane_id();
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = wid; r < rows; r += nw) {
+    const int64_t s = static_cast<int64_t>(xptr[r] - xbase), e = static_cast<int64_t>(xptr[r + 1] - xbase);
+    float4 acc[H];
+#pragma unroll
+    for (int h = 0; h < H; h++) acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t k0 = s; k0 < e; k0 += 32) {
+      uint32_t lin = 0;
+      float lv = 0.f;
+      if (k0 + lane < e) {
+        const uint64_t c = static_cast<uint64_t>(xcol[k0 + lane]);
+        lv = xval[k0 + lane];
+        if (c >= static_cast<uint64_t>(w_rows)) {
+          ctl->bad_row = 1;
+          lv = 0.f;
+        } else {
+          lin = static_cast<uint32_t>(c);
+        }
+      }
+      const int n = static_cast<int>(e - k0 < 32 ? e - k0 : 32);
+      for (int kk = 0; kk < n; kk++) {
+        const uint32_t in = __shfl_sync(kFull, lin, kk);
+        const float v = __shfl_sync(kFull, lv, kk);
+        const float4* wr = w4 + in * (P / 4) + lane;
+#pragma unroll
+        for (int h = 0; h < H; h++) {
+          const float4 q = wr[32 * h];
+          acc[h].x = fmaf(v, q.x, acc[h].x);
+          acc[h].y = fmaf(v, q.y, acc[h].y);
+          acc[h].z = fmaf(v, q.z, acc[h].z);
+          acc[h].w = fmaf(v, q.w, acc[h].w);
+        }
+      }
+    }
+    uint32_t c_h[H], ex_h[H], total = 0;
+#pragma unroll
+    for (int h = 0; h < H; h++) {
+      c_h[h] = (acc[h].x > 0.f) + (acc[h].y > 0.f) + (acc[h].z > 0.f) + (acc[h].w > 0.f);
+      const uint32_t incl = warp_incl_scan(c_h[h]);
+      ex_h[h] = total + incl - c_h[h];
+      total += __shfl_sync(kFull, incl, 31);
+    }
+    const unsigned long long off = stage.take(total, ctl, 4096);
+    if (off + total <= t_cap) {
+#pragma unroll
+      for (int h = 0; h < H; h++) {
+        unsigned long long pos = off + ex_h[h];
+        const uint32_t c0 = static_cast<uint32_t>(128 * h + 4 * lane);
+        const float vv[4] = {acc[h].x, acc[h].y, acc[h].z, acc[h].w};
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          if (vv[q] > 0.f) {
+            ocol[pos] = static_cast<IdxO>(c0 + q);
+            oval[pos] = vv[q];
+            pos++;
+          }
+      }
+    } else if (lane == 0) {
+      ctl->bad_row = 2;
+    }
+    if (lane == 0) {
+      cnt[r] = static_cast<int32_t>(total);
+      toff[r] = off;
+    }
+  }
+}
+
+// Staging entries of the one-pass combine: the dense bound + 1/15 (a 4096-entry reservation wastes
+// less than one <= 256-entry row) + one reservation per warp of the largest grid.
+uint64_t combine_stage_cap(Ctx& ctx, int64_t rows, int64_t w_cols) {
+  const uint64_t dense = static_cast<uint64_t>(rows) * static_cast<uint64_t>(w_cols);
+  return dense + dense / 15 + (static_cast<uint64_t>(ctx.sms) * 32 * 8 + 1) * 4096;
+}
+
+template <class V, class IdxT, class IdxO, int J>
+void combine_stage(Ctx& ctx, const Staged& s, int64_t rows, const V* w, int64_t w_rows, int64_t w_cols, int32_t* cnt,
+                   IdxO* tcol, V* tval, uint64_t* toff, uint64_t t_cap, Ctl* ctl) {
+  if constexpr (sizeof(V) == 4) {
+    const int H = w_cols > 128 ? 2 : 1;
+    const size_t smem4 = static_cast<size_t>(w_rows) * 128 * H * 4;
+    if (w_cols >= 96 && w_cols <= 256 && smem4 <= 200 * 1024 && env_int("AB2_COMBINE_V4", 1)) {
+      auto k = H == 2 ? k_combine_v4<IdxT, IdxO, 2> : k_combine_v4<IdxT, IdxO, 1>;
+      AB2_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem4)));
+      int nb = 0;
+      AB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 512, smem4));
+      const int grid = std::max(1, std::min(grid_of(rows * 32, 512, ctx.sms), std::max(nb, 1) * ctx.sms));
+      k<<<grid, 512, smem4, ctx.stream>>>(s.ptr, s.base, static_cast<const IdxT*>(s.idx),
+                                          static_cast<const float*>(s.val), rows, w, w_rows, w_cols, cnt, tcol, tval,
+                                          ctl, toff, t_cap);
+      AB2_CUDA(cudaGetLastError());
+      return;
+    }
+  }
+  const bool smem = static_cast<size_t>(w_rows * w_cols) * sizeof(V) <= 200 * 1024 && env_int("AB2_COMBINE_SMEM", 1);
+  if (smem)
+    combine_launch2<V, IdxT, IdxO, J, false, true, true>(ctx, s, rows, w, w_rows, w_cols, cnt, nullptr, tcol, tval, ctl,
+                                                          toff, t_cap);
+  else
+    combine_launch2<V, IdxT, IdxO, J, false, false, true>(ctx, s, rows, w, w_rows, w_cols, cnt, nullptr, tcol, tval,
+                                                           ctl, toff, t_cap);
 }
 
 template <class V, class IdxT, class IdxO, int J>
@@ -380,6 +542,41 @@ void combine_t(Ctx& ctx, const aires_b200_matrix& x, const void* w_in, uint64_t 
     }
   };
   int launches = 0;
+  // one pass when the output fits one column tile and its dense-bound staging fits in memory
+  const uint64_t t_cap = combine_stage_cap(ctx, rows, static_cast<int64_t>(w_cols));
+  const bool one_pass = rows > 0 && w_cols > 0 && static_cast<int64_t>(w_cols) <= 32 * std::max(J, 1) &&
+                        t_cap * (sizeof(IdxO) + sizeof(V)) <= (uint64_t(48) << 30) && env_int("AB2_COMBINE_ONE_PASS", 1);
+  if (one_pass) {
+    IdxO* tcol = static_cast<IdxO*>(ctx.t_col.get(t_cap * sizeof(IdxO)));
+    V* tval = static_cast<V*>(ctx.t_val.get(t_cap * sizeof(V)));
+    uint64_t* toff = static_cast<uint64_t*>(ctx.rflops.get(static_cast<size_t>(rows) * 8));
+    switch (std::max(J, 1)) {
+      case 1: combine_stage<V, IdxT, IdxO, 1>(ctx, s, rows, w, w_rows, w_cols, cnt, tcol, tval, toff, t_cap, ctl); break;
+      case 2: combine_stage<V, IdxT, IdxO, 2>(ctx, s, rows, w, w_rows, w_cols, cnt, tcol, tval, toff, t_cap, ctl); break;
+      case 3:
+      case 4: combine_stage<V, IdxT, IdxO, 4>(ctx, s, rows, w, w_rows, w_cols, cnt, tcol, tval, toff, t_cap, ctl); break;
+      default: combine_stage<V, IdxT, IdxO, 8>(ctx, s, rows, w, w_rows, w_cols, cnt, tcol, tval, toff, t_cap, ctl); break;
+    }
+    launches++;
+    scan_counts(ctx, cnt, rows, optr, ctl, &launches);
+    Ctl* h = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
+    AB2_CUDA(cudaMemcpyAsync(h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
+    AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (h->bad_row == 1) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "feature column outside the weight rows");
+    if (h->bad_row) fail(AIRES_B200_CAPACITY_EXCEEDED, "combine staging overflow");
+    const uint64_t nnz = h->nnz;
+    IdxO* ocol = static_cast<IdxO*>(ctx.c_col.get(std::max<uint64_t>(nnz, 1) * sizeof(IdxO)));
+    V* oval = static_cast<V*>(ctx.c_val.get(std::max<uint64_t>(nnz, 1) * sizeof(V)));
+    if (nnz) {
+      k_place<V, IdxO><<<ctx.sms * 8, 256, 0, ctx.stream>>>(reinterpret_cast<const uint32_t*>(cnt), toff, optr, tcol,
+                                                           tval, rows, ocol, oval);
+      AB2_CUDA(cudaGetLastError());
+      launches++;
+    }
+    deliver<IdxO, V>(ctx, out, static_cast<uint64_t>(rows), w_cols, nnz, optr, ocol, oval);
+    ctx.launches = launches;
+    return;
+  }
   if (rows > 0 && w_cols > 0) {
     run(false, nullptr, nullptr);
     launches++;

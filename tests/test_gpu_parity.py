@@ -348,6 +348,35 @@ def test_layer_fused_matches_unfused_chain(hcols, wcols):
         assert err <= 1e-5 * max(scale.get(key, 0.0), 1e-30), (key, want.get(key), have.get(key), scale.get(key))
 
 
+@pytest.mark.parametrize("cin,cout,path", [(100, 256, "v4"), (64, 130, "v4"), (40, 100, "v4"), (30, 96, "v4"),
+                                           (100, 256, "scalar"), (64, 130, "two-pass"), (20, 300, "auto")])
+def test_combine_fp32_kernels_match_oracle(cin, cout, path, monkeypatch):
+    """fp32 combine through each kernel path (LDS.128 one-pass for 96..256 output columns, the scalar
+    one-pass, the two-pass count/fill) against the fp64 oracle: values within 1e-5 of the cell's
+    scale sum |X|·|W|; only entries within that rounding of zero may flip across the ReLU."""
+    if path == "scalar":
+        monkeypatch.setenv("AB2_COMBINE_V4", "0")
+    if path == "two-pass":
+        monkeypatch.setenv("AB2_COMBINE_ONE_PASS", "0")
+    rows = 5000
+    x = ab.synth_features(rows, cin, 80.0, 11, idx_dtype=np.uint64)
+    w = ab.gen_weights(cin, cout, 12)
+    x32 = ab.CsrMatrix(rows, cin, x.row_ptr, x.col_idx.astype(np.uint32), x.values.astype(np.float32))
+    got = ab.combine(x32, w.astype(np.float32))
+    rc, (wp, wi, wv) = po.combine(rows, cin, x.row_ptr, x.col_idx, x.values, w)
+    assert rc == 0
+    rc, (sp, si, sv) = po.combine(rows, cin, x.row_ptr, x.col_idx, np.abs(x.values), np.abs(w))
+    dense = lambda p, i, v: {(r, int(c)): float(vv) for r in range(rows)  # noqa: E731
+                             for c, vv in zip(i[p[r]:p[r + 1]], v[p[r]:p[r + 1]])}
+    want, have, scale = dense(wp, wi, wv), dense(got.row_ptr, got.col_idx, got.values), dense(sp, si, sv)
+    assert len(have) > 0.3 * len(want)
+    for key in set(want) | set(have):
+        err = abs(want.get(key, 0.0) - have.get(key, 0.0))
+        assert err <= 1e-5 * max(scale.get(key, 0.0), 1e-30), (key, want.get(key), have.get(key))
+    for r in range(0, rows, 97):  # ascending columns per row
+        assert np.all(np.diff(got.col_idx[got.row_ptr[r]:got.row_ptr[r + 1]].astype(np.int64)) > 0)
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("shape", ["cfg2", "cfg3"])
 def test_full_size_parity(shape):

@@ -1,3 +1,5 @@
+"""Pinned cudaMemcpy GB/s vs host / device start offsets (the DMA alignment penalty of writing C tiles at
+arbitrary CSR offsets).  usage: python tools/link_align.py"""
 import torch
 n = 64 << 20
 dev = torch.device("cuda:0")
