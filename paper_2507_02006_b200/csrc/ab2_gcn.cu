@@ -64,6 +64,11 @@ __global__ void k_norm_fill(const uint64_t* __restrict__ ptr, uint64_t base, con
   for (int64_t r = wid; r < n; r += nw) {
     const int64_t s = static_cast<int64_t>(ptr[r] - base), e = static_cast<int64_t>(ptr[r + 1] - base);
     int64_t lo = s, hi = e;
+    if (e - s <= 32) {  // short row: one coalesced load and a ballot instead of a dependent search
+      const bool below = s + lane < e && static_cast<int64_t>(col[s + lane]) < r;
+      lo = s + __popc(__ballot_sync(kFull, below));
+      hi = lo;
+    }
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
       if (static_cast<int64_t>(col[mid]) < r)
@@ -87,25 +92,56 @@ __global__ void k_norm_fill(const uint64_t* __restrict__ ptr, uint64_t base, con
   }
 }
 
-// weighted degrees, summed left to right (gcn.hpp:61-64): one warp per row, the row read coalesced
-// 32 values at a time and folded into lane 0's running sum in order (exact for any weights).
+// Rows of Â are short on GCN graphs (~26 entries on the products shape) with a power-law tail:
+// the degree sum takes one thread per row (a warp's 32 rows stream through L1 together, each
+// thread's loads run ahead of its arithmetic), and rows longer than kNormHeavy are handed to the
+// whole warp (coalesced 32-entry loads).  A warp per row left most lanes idle and issued the
+// per-row overhead 32 times (1.2 ms for the products-shaped Â); a thread per row alone serialised
+// the hub rows (0.94 ms); both together 0.73 ms.
+constexpr int64_t kNormHeavy = 256;
+
+// weighted degrees, summed left to right (gcn.hpp:61-64), exact for any weights.
 __global__ void k_norm_degree(const int64_t* __restrict__ optr, const double* __restrict__ oval, int64_t n,
                               double* __restrict__ deg) {
   const int lane = lane_id();
-  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t r = wid; r < n; r += nw) {
-    const int64_t s = optr[r], e = optr[r + 1];
-    double d = 0.0;
-    for (int64_t b = s; b < e; b += 32) {
-      const double v = b + lane < e ? oval[b + lane] : 0.0;
-      const int m = static_cast<int>(e - b < 32 ? e - b : 32);
-      for (int i = 0; i < m; i++) d = __dadd_rn(d, __shfl_sync(kFull, v, i));
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t base = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) & ~int64_t(31); base < n;
+       base += stride) {
+    const int64_t r = base + lane;
+    int64_t s = 0, e = 0;
+    if (r < n) {
+      s = optr[r];
+      e = optr[r + 1];
     }
-    if (lane == 0) deg[r] = d;
+    const bool heavy = e - s > kNormHeavy;
+    if (r < n && !heavy) {
+      double d = 0.0;
+      int64_t k = s;
+      for (; k + 4 <= e; k += 4) {
+        const double v0 = oval[k], v1 = oval[k + 1], v2 = oval[k + 2], v3 = oval[k + 3];
+        d = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(d, v0), v1), v2), v3);
+      }
+      for (; k < e; k++) d = __dadd_rn(d, oval[k]);
+      deg[r] = d;
+    }
+    for (unsigned hm = __ballot_sync(kFull, heavy); hm; hm &= hm - 1) {
+      const int h = __ffs(hm) - 1;
+      const int64_t hs = __shfl_sync(kFull, s, h), he = __shfl_sync(kFull, e, h);
+      double d = 0.0;
+      double v = hs + lane < he ? oval[hs + lane] : 0.0;
+      for (int64_t b = hs; b < he; b += 32) {
+        const double nv = b + 32 + lane < he ? oval[b + 32 + lane] : 0.0;  // next chunk in flight
+        const int m = static_cast<int>(he - b < 32 ? he - b : 32);
+        for (int i = 0; i < m; i++) d = __dadd_rn(d, __shfl_sync(kFull, v, i));
+        v = nv;
+      }
+      if (lane == h) deg[r] = d;
+    }
   }
 }
 
+// v / sqrt(d_i * d_j): one IEEE multiply, sqrt and divide.  One warp per row (a thread per row
+// measured 1.40 ms vs 1.21 ms here: the gathers of deg[col] then run 32 rows apart).
 template <class IdxO, class VO>
 __global__ void k_norm_scale(const int64_t* __restrict__ optr, const IdxO* __restrict__ ocol,
                              const double* __restrict__ oval, const double* __restrict__ deg, int64_t n,
@@ -347,7 +383,7 @@ void normalize_t(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
   if (n > 0) {
     k_norm_fill<IdxT, VIn, IdxO><<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(s.ptr, s.base, col, val, n,
                                                                                        optr, ocol, oval);
-    k_norm_degree<<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(optr, oval, n, deg);
+    k_norm_degree<<<grid_of(n, 256, ctx.sms), 256, 0, ctx.stream>>>(optr, oval, n, deg);
     k_norm_scale<IdxO, VO><<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(optr, ocol, oval, deg, n, outv);
     AB2_CUDA(cudaGetLastError());
     launches += 3;
