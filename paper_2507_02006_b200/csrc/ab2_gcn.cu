@@ -810,6 +810,185 @@ void agg_comb_m(Ctx& ctx, int jc, const uint64_t* aptr, uint64_t abase, const ui
   }
 }
 
+// ---- reassociated layer: ReLU(Ã·(H·W)) when W narrows the features -----------------------------
+// (Ã·H)·W = Ã·(H·W) exactly in real arithmetic; in fp32 the terms are summed in another order,
+// within the stated tolerance (the cell's scale sum |Ã||H||W| bounds both orders' rounding).  The
+// point is the gather: the aggregation reads one row of its right operand per Ã entry, 4·h_cols
+// bytes for H (1 KB at the products shape: 64 GB of gathers for layer 2, the bound of k_agg_comb)
+// but only 4·w_cols for T = H·W (188 B).  T costs one pass over H's rows with W in shared memory.
+
+// W packed for LDS.128: wt4[(j * M4 + m4) * 32 + l] = {W[l + 32 (4 m4 + q)][j], q = 0..3} (zero past W).
+__global__ void k_w_lane_major4(const float* __restrict__ w, int64_t w_rows, int64_t w_cols, int M4,
+                                float4* __restrict__ wt4) {
+  const int64_t total = static_cast<int64_t>(M4) * w_cols * 32;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t l = i % 32, m4 = (i / 32) % M4, j = i / (32 * M4);
+    float q[4];
+    for (int k = 0; k < 4; k++) {
+      const int64_t c = l + 32 * (4 * m4 + k);
+      q[k] = c < w_rows ? w[c * w_cols + j] : 0.f;
+    }
+    wt4[i] = make_float4(q[0], q[1], q[2], q[3]);
+  }
+}
+
+// T[r, :w_cols] = H[r, :] · W, one warp per H row: the sparse row is scattered into a per-warp
+// shared row (lane l then holds columns l + 32 m), multiplied by W from shared memory (LDS.128 of
+// four W rows per output column), and the 32-lane partials are reduce-scattered (lane l gets
+// output column 32 jc + l).  T rows are tp floats apart (w_cols rounded to 8: whole sectors).
+template <int M4, int JC>
+__global__ void __launch_bounds__(256) k_hw(const uint64_t* __restrict__ hptr, uint64_t hbase,
+                                            const uint32_t* __restrict__ hcol, const float* __restrict__ hval,
+                                            int64_t K, int64_t h_cols, const float4* __restrict__ wt4_g,
+                                            int64_t w_cols, int64_t tp, float* __restrict__ t, Ctl* __restrict__ ctl) {
+  // Bound by the shared-memory reads of W (L1 95% at cfg5, 4.5 ms).  Measured slower: two H rows per
+  // warp step sharing the W loads (113 registers, 5.8 ms); a register-tiled GEMM over dense 56/64-row
+  // tiles of H scattered into shared memory (5.3-6.7 ms: the scatter's global-load latency, with one
+  // or two CTAs per SM, stalls the FFMAs)
+  extern __shared__ __align__(16) float4 sm4[];
+  const int64_t nwt = static_cast<int64_t>(M4) * w_cols * 32;
+  for (int64_t i = threadIdx.x; i < nwt; i += blockDim.x) sm4[i] = wt4_g[i];
+  __syncthreads();
+  const int lane = lane_id(), warp = warp_id();
+  float* row = reinterpret_cast<float*>(sm4 + nwt) + warp * (128 * M4);
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = wid; r < K; r += nw) {
+#pragma unroll
+    for (int m = 0; m < 4 * M4; m++) row[lane + 32 * m] = 0.f;
+    __syncwarp();
+    const int64_t s = static_cast<int64_t>(hptr[r] - hbase), e = static_cast<int64_t>(hptr[r + 1] - hbase);
+    for (int64_t k = s + lane; k < e; k += 32) {
+      const uint32_t c = hcol[k];
+      if (c < static_cast<uint64_t>(h_cols))
+        row[c] = hval[k];
+      else
+        ctl->bad_row = 1;
+    }
+    __syncwarp();
+    float4 a4[M4];
+#pragma unroll
+    for (int m4 = 0; m4 < M4; m4++)
+      a4[m4] = make_float4(row[lane + 32 * (4 * m4)], row[lane + 32 * (4 * m4 + 1)], row[lane + 32 * (4 * m4 + 2)],
+                           row[lane + 32 * (4 * m4 + 3)]);
+    __syncwarp();
+#pragma unroll
+    for (int jc = 0; jc < JC; jc++) {
+      float p[32];
+#pragma unroll
+      for (int jj = 0; jj < 32; jj++) {
+        const int64_t j = jc * 32 + jj;
+        float v = 0.f;
+        if (j < w_cols) {
+#pragma unroll
+          for (int m4 = 0; m4 < M4; m4++) {
+            const float4 q = sm4[(j * M4 + m4) * 32 + lane];
+            v = fmaf(a4[m4].x, q.x, v);
+            v = fmaf(a4[m4].y, q.y, v);
+            v = fmaf(a4[m4].z, q.z, v);
+            v = fmaf(a4[m4].w, q.w, v);
+          }
+        }
+        p[jj] = v;
+      }
+      const float o = reduce_scatter32(p);
+      const int64_t j = jc * 32 + lane;
+      if (j < w_cols) t[r * tp + j] = o;
+    }
+  }
+}
+
+// out[r, j] = ReLU(sum_k Ã[r, k] T[k, j]) as a dense row + the row's positive count (then scan +
+// k_compact_rows, as for k_agg_comb).  One warp per Ã row, lane l owns columns l + 32 jc; eight T rows
+// in flight per step.
+template <int JC>
+__global__ void __launch_bounds__(256) k_agg_t(const uint64_t* __restrict__ aptr, uint64_t abase,
+                                               const uint32_t* __restrict__ acol, const float* __restrict__ aval,
+                                               int64_t rows, int64_t K, const float* __restrict__ t, int64_t tp,
+                                               int64_t w_cols, float* __restrict__ dense_out,
+                                               int32_t* __restrict__ cnt) {
+  const int lane = lane_id();
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  bool mine[JC];
+#pragma unroll
+  for (int jc = 0; jc < JC; jc++) mine[jc] = jc * 32 + lane < w_cols;
+  for (int64_t r = wid; r < rows; r += nw) {
+    float acc[JC];
+#pragma unroll
+    for (int jc = 0; jc < JC; jc++) acc[jc] = 0.f;
+    const int64_t s = static_cast<int64_t>(aptr[r] - abase), e = static_cast<int64_t>(aptr[r + 1] - abase);
+    for (int64_t b = s; b < e; b += 32) {
+      uint32_t k = 0;
+      float a = 0.f;
+      if (b + lane < e) {
+        k = acol[b + lane];
+        a = aval[b + lane];
+        if (k >= K) a = 0.f, k = 0;
+      }
+      const int n = static_cast<int>(e - b < 32 ? e - b : 32);
+      int kk = 0;
+      for (; kk + 8 <= n; kk += 8) {
+        float x[8][JC], av[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const uint32_t kq = __shfl_sync(kFull, k, kk + q);
+          av[q] = __shfl_sync(kFull, a, kk + q);
+          const float* tr = t + static_cast<int64_t>(kq) * tp + lane;
+#pragma unroll
+          for (int jc = 0; jc < JC; jc++) x[q][jc] = mine[jc] ? __ldg(tr + 32 * jc) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+#pragma unroll
+          for (int jc = 0; jc < JC; jc++) acc[jc] = fmaf(av[q], x[q][jc], acc[jc]);
+      }
+      for (; kk < n; kk++) {
+        const uint32_t kq = __shfl_sync(kFull, k, kk);
+        const float aq = __shfl_sync(kFull, a, kk);
+        const float* tr = t + static_cast<int64_t>(kq) * tp + lane;
+#pragma unroll
+        for (int jc = 0; jc < JC; jc++)
+          if (mine[jc]) acc[jc] = fmaf(aq, __ldg(tr + 32 * jc), acc[jc]);
+      }
+    }
+    int32_t count = 0;
+#pragma unroll
+    for (int jc = 0; jc < JC; jc++) {
+      const bool pos = mine[jc] && acc[jc] > 0.f;
+      if (mine[jc]) dense_out[r * w_cols + jc * 32 + lane] = pos ? acc[jc] : 0.f;
+      count += __popc(__ballot_sync(kFull, pos));
+    }
+    if (lane == 0) cnt[r] = count;
+  }
+}
+
+template <int M4, int JC>
+void hw_launch(Ctx& ctx, const Staged& hs, int64_t K, int64_t h_cols, const float4* wt4, int64_t w_cols, int64_t tp,
+               float* t, Ctl* ctl) {
+  const size_t smem = static_cast<size_t>(M4) * w_cols * 32 * 16 + 8 * 128 * M4 * 4;
+  auto k1 = k_hw<M4, JC>;
+  AB2_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int nb = 0;
+  AB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k1, 256, smem));
+  if (K > 0)
+    k1<<<std::max(1, std::min(grid_of(K * 32, 256, ctx.sms), std::max(nb, 1) * ctx.sms)), 256, smem, ctx.stream>>>(
+        hs.ptr, hs.base, static_cast<const uint32_t*>(hs.idx), static_cast<const float*>(hs.val), K, h_cols, wt4,
+        w_cols, tp, t, ctl);
+  AB2_CUDA(cudaGetLastError());
+}
+
+template <int JC>
+void agg_t_launch(Ctx& ctx, const Staged& as, int64_t rows, int64_t K, const float* t, int64_t tp, int64_t w_cols,
+                  float* dense, int32_t* cnt) {
+  if (rows > 0)
+    k_agg_t<JC><<<grid_of(rows * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(
+        as.ptr, as.base, static_cast<const uint32_t*>(as.idx), static_cast<const float*>(as.val), rows, K, t, tp,
+        w_cols, dense, cnt);
+  AB2_CUDA(cudaGetLastError());
+}
+
 }  // namespace
 
 void normalize_adjacency(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
@@ -864,6 +1043,49 @@ void combine(Ctx& ctx, const aires_b200_matrix& x, const void* w, uint64_t w_row
 namespace ab2 {
 
 // H' = ReLU((Ã·H)·W), fp32, fused (dense-H path); Ã and H device or host CSR (u32 columns, f32).
+// Scan of the positive counts, the caller's allocation, compaction of the dense ReLU rows and the
+// copies out (both fused-layer forms).
+static void finish_fused(Ctx& ctx, aires_b200_output& out, int64_t rows, uint64_t w_cols, const float* dense, int32_t* cnt,
+                  Ctl* ctl, int launches) {
+  int64_t* optr = ctx.cptr.as<int64_t>(rows + 1);
+  scan_counts(ctx, cnt, rows, optr, ctl, &launches);
+  Ctl* hc = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
+  AB2_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  const uint64_t nnz = rows > 0 ? hc->nnz : 0;
+  void *optr_o = nullptr, *oidx = nullptr, *oval = nullptr;
+  const int rc = out.alloc(out.user, static_cast<uint64_t>(rows), nnz, &optr_o, &oidx, &oval);
+  if (rc != 0) fail(rc, "output allocator failed for " + std::to_string(nnz) + " nonzeros");
+  void* dcol = out.location == AIRES_B200_DEVICE ? oidx : ctx.c_col.get(std::max<uint64_t>(nnz, 1) * out.idx_bytes);
+  float* dval = out.location == AIRES_B200_DEVICE ? static_cast<float*>(oval)
+                                                  : static_cast<float*>(ctx.c_val.get(std::max<uint64_t>(nnz, 1) * 4));
+  if (rows > 0 && nnz > 0) {
+    if (out.idx_bytes == 4)
+      k_compact_rows<uint32_t><<<grid_of(rows * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(
+          dense, rows, static_cast<int64_t>(w_cols), optr, static_cast<uint32_t*>(dcol), dval);
+    else
+      k_compact_rows<uint64_t><<<grid_of(rows * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(
+          dense, rows, static_cast<int64_t>(w_cols), optr, static_cast<uint64_t*>(dcol), dval);
+    AB2_CUDA(cudaGetLastError());
+    launches++;
+  }
+  const cudaMemcpyKind kind = out.location == AIRES_B200_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  AB2_CUDA(cudaMemcpyAsync(optr_o, optr, (rows + 1) * 8, kind, ctx.stream));
+  if (out.location != AIRES_B200_DEVICE && nnz) {
+    AB2_CUDA(cudaMemcpyAsync(oidx, dcol, nnz * out.idx_bytes, kind, ctx.stream));
+    AB2_CUDA(cudaMemcpyAsync(oval, dval, nnz * 4, kind, ctx.stream));
+  }
+  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+  float ms = 0;
+  AB2_CUDA(cudaEventElapsedTime(&ms, ctx.ev[0], ctx.ev[1]));
+  ctx.last_ms = ms;
+  ctx.launches = launches;
+  out.n_rows = static_cast<uint64_t>(rows);
+  out.n_cols = w_cols;
+  out.nnz = nnz;
+  out.flops = 0;
+}
+
 void layer_fused(Ctx& ctx, const aires_b200_matrix& at, const aires_b200_matrix& h, const void* w, uint64_t w_rows,
                  uint64_t w_cols, uint32_t w_location, aires_b200_output& out) {
   if (at.layout != AIRES_B200_CSR || h.layout != AIRES_B200_CSR)
@@ -879,6 +1101,49 @@ void layer_fused(Ctx& ctx, const aires_b200_matrix& at, const aires_b200_matrix&
   if (!out.alloc) fail(AIRES_B200_INVALID_ARGUMENT, "output allocator is null");
   const int64_t rows = static_cast<int64_t>(at.n_rows), K = static_cast<int64_t>(h.n_rows);
   int launches = 0;
+  // W narrower than H: aggregate T = H·W instead of H (see k_hw / k_agg_t)
+  if (w_cols < h.n_cols && env_int("AB2_FUSED_REASSOC", 1) != 0) {
+    const int M4 = (M + 3) / 4;
+    const size_t smem = static_cast<size_t>(M4) * w_cols * 32 * 16 + 8 * 128 * M4 * 4;
+    if (smem <= 200 * 1024) {
+      const Staged hs = stage_csr(ctx, h);
+      const float* wsrc = static_cast<const float*>(w);
+      if (w_location == AIRES_B200_HOST) {
+        float* dw = static_cast<float*>(ctx.x_idx.get(std::max<uint64_t>(w_rows * w_cols, 1) * sizeof(float)));
+        AB2_CUDA(cudaMemcpyAsync(dw, w, w_rows * w_cols * sizeof(float), cudaMemcpyHostToDevice, ctx.stream));
+        wsrc = dw;
+      }
+      float4* wt4 = static_cast<float4*>(ctx.xo_desc.get(static_cast<size_t>(M4) * w_cols * 32 * sizeof(float4)));
+      k_w_lane_major4<<<grid_of(static_cast<int64_t>(M4) * w_cols * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(
+          wsrc, static_cast<int64_t>(w_rows), static_cast<int64_t>(w_cols), M4, wt4);
+      const int64_t tp = (static_cast<int64_t>(w_cols) + 7) & ~int64_t(7);
+      float* t = static_cast<float*>(ctx.xo_val.get(std::max<int64_t>(K, 1) * tp * sizeof(float)));
+      float* dense = static_cast<float*>(ctx.t_val.get(std::max<int64_t>(rows, 1) * w_cols * sizeof(float)));
+      int32_t* cnt = ctx.cnt.as<int32_t>(std::max<int64_t>(rows, 1));
+      Ctl* ctl = ctx.ctl.as<Ctl>(1);
+      AB2_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx.stream));
+      AB2_CUDA(cudaEventRecord(ctx.ev[0], ctx.stream));
+      const int64_t hc = static_cast<int64_t>(h.n_cols), wc = static_cast<int64_t>(w_cols);
+      // T = H·W is enqueued before Ã is staged: both stagings use the context's A buffers
+      switch (M4 * 8 + JC) {
+#define AB2_RA(A, B) case A * 8 + B: hw_launch<A, B>(ctx, hs, K, hc, wt4, wc, tp, t, ctl); break;
+        AB2_RA(1, 1) AB2_RA(1, 2) AB2_RA(1, 3) AB2_RA(1, 4) AB2_RA(2, 1) AB2_RA(2, 2) AB2_RA(2, 3) AB2_RA(2, 4)
+#undef AB2_RA
+        default: fail(AIRES_B200_UNSUPPORTED_FORMAT, "fused layer shape");
+      }
+      const Staged as = stage_csr(ctx, at);
+      switch (JC) {
+        case 1: agg_t_launch<1>(ctx, as, rows, K, t, tp, wc, dense, cnt); break;
+        case 2: agg_t_launch<2>(ctx, as, rows, K, t, tp, wc, dense, cnt); break;
+        case 3: agg_t_launch<3>(ctx, as, rows, K, t, tp, wc, dense, cnt); break;
+        default: agg_t_launch<4>(ctx, as, rows, K, t, tp, wc, dense, cnt); break;
+      }
+      launches += 3;
+      AB2_CUDA(cudaEventRecord(ctx.ev[1], ctx.stream));
+      finish_fused(ctx, out, rows, w_cols, dense, cnt, ctl, launches);
+      return;
+    }
+  }
   // H -> dense rows (32*M floats each)
   const Staged hs = stage_csr(ctx, h);
   float* hd = static_cast<float*>(ctx.xo_val.get(std::max<int64_t>(K, 1) * 32 * M * sizeof(float)));
@@ -918,42 +1183,7 @@ void layer_fused(Ctx& ctx, const aires_b200_matrix& at, const aires_b200_matrix&
     launches++;
   }
   AB2_CUDA(cudaEventRecord(ctx.ev[1], ctx.stream));
-  scan_counts(ctx, cnt, rows, optr, ctl, &launches);
-  Ctl* hc = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
-  AB2_CUDA(cudaMemcpyAsync(hc, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx.stream));
-  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
-  const uint64_t nnz = rows > 0 ? hc->nnz : 0;
-  void *optr_o = nullptr, *oidx = nullptr, *oval = nullptr;
-  const int rc = out.alloc(out.user, static_cast<uint64_t>(rows), nnz, &optr_o, &oidx, &oval);
-  if (rc != 0) fail(rc, "output allocator failed for " + std::to_string(nnz) + " nonzeros");
-  void* dcol = out.location == AIRES_B200_DEVICE ? oidx : ctx.c_col.get(std::max<uint64_t>(nnz, 1) * out.idx_bytes);
-  float* dval = out.location == AIRES_B200_DEVICE ? static_cast<float*>(oval)
-                                                  : static_cast<float*>(ctx.c_val.get(std::max<uint64_t>(nnz, 1) * 4));
-  if (rows > 0 && nnz > 0) {
-    if (out.idx_bytes == 4)
-      k_compact_rows<uint32_t><<<grid_of(rows * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(
-          dense, rows, static_cast<int64_t>(w_cols), optr, static_cast<uint32_t*>(dcol), dval);
-    else
-      k_compact_rows<uint64_t><<<grid_of(rows * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(
-          dense, rows, static_cast<int64_t>(w_cols), optr, static_cast<uint64_t*>(dcol), dval);
-    AB2_CUDA(cudaGetLastError());
-    launches++;
-  }
-  const cudaMemcpyKind kind = out.location == AIRES_B200_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  AB2_CUDA(cudaMemcpyAsync(optr_o, optr, (rows + 1) * 8, kind, ctx.stream));
-  if (out.location != AIRES_B200_DEVICE && nnz) {
-    AB2_CUDA(cudaMemcpyAsync(oidx, dcol, nnz * out.idx_bytes, kind, ctx.stream));
-    AB2_CUDA(cudaMemcpyAsync(oval, dval, nnz * 4, kind, ctx.stream));
-  }
-  AB2_CUDA(cudaStreamSynchronize(ctx.stream));
-  float ms = 0;
-  AB2_CUDA(cudaEventElapsedTime(&ms, ctx.ev[0], ctx.ev[1]));
-  ctx.last_ms = ms;
-  ctx.launches = launches;
-  out.n_rows = static_cast<uint64_t>(rows);
-  out.n_cols = w_cols;
-  out.nnz = nnz;
-  out.flops = 0;
+  finish_fused(ctx, out, rows, w_cols, dense, cnt, ctl, launches);
 }
 
 }  // namespace ab2
