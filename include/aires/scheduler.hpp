@@ -28,7 +28,8 @@
 namespace aires::b200 {
 
 inline RunResult run_real(const CsrMatrix& a, const CscMatrix& b, const MemoryBudget& budget, const SimConfig& cfg,
-                          std::uint32_t n_buffers, std::uint32_t strategy /* 1 AIRES, 2 MaxMemory */) {
+                          std::uint32_t n_buffers, std::uint32_t strategy /* 1 AIRES, 2 MaxMemory */,
+                          bool stream_out = false) {
   (void)cfg;  // cost-model parameters of the simulator; the real run measures instead
   if (a.n_cols != b.n_rows)
     fail(errc::dimension_mismatch,
@@ -44,8 +45,11 @@ inline RunResult run_real(const CsrMatrix& a, const CscMatrix& b, const MemoryBu
   rc.mode = AIRES_B200_MODE_FP64_EXACT;
   rc.c_aware = strategy;
   rc.n_buffers = n_buffers;
+  rc.flags = stream_out ? AIRES_B200_RUN_STREAM_OUT : 0u;
   aires_b200_run_report rep{};
   check(aires_b200_run(&am, &bm, &rc, &out, &rep));
+  res.c.col_idx.resize(out.nnz);  // streamed output: the vectors were sized to the nnz bound
+  res.c.values.resize(out.nnz);
   res.c.n_rows = a.n_rows;
   res.c.n_cols = b.n_cols;
   RunReport& r = res.report;
@@ -64,10 +68,13 @@ inline RunResult run_real(const CsrMatrix& a, const CscMatrix& b, const MemoryBu
   return res;
 }
 
-/// run_aires (scheduler.hpp:72-168) as the real out-of-core pipeline.
+/// run_aires (scheduler.hpp:72-168) as the real out-of-core pipeline.  stream_out (uncapped budgets,
+/// device_total 0): no sizing pass, C drained while A uploads (AIRES_B200_RUN_STREAM_OUT); the result
+/// vectors are first sized to an upper bound of nnz(C) (value-initialised by std::vector), then
+/// trimmed -- the gain is on the device side, so it pays for large products.
 inline RunResult run_aires_real(const CsrMatrix& a, const CscMatrix& b, const MemoryBudget& budget,
-                                const SimConfig& cfg, std::uint32_t n_buffers = 2) {
-  return run_real(a, b, budget, cfg, n_buffers, 1);
+                                const SimConfig& cfg, std::uint32_t n_buffers = 2, bool stream_out = false) {
+  return run_real(a, b, budget, cfg, n_buffers, 1, stream_out);
 }
 
 /// run_maxmemory (scheduler.hpp:174-293) for real: fixed byte tiles, split rows' fragments returned

@@ -21,6 +21,9 @@
 //   Phase III (assemble / drain / store, scheduler.hpp:142-166)
 //     nothing to assemble: every tile's C already sits at its final offsets; sync and report.
 //
+// Streamed output (AIRES_B200_RUN_STREAM_OUT, uncapped runs only): run_stream below skips the sizing
+// pass -- the allocator gets an upper bound of nnz(C) and C drains tile by tile from the first tile on.
+//
 // Host memory: A and C host buffers that are not page-locked are registered for the call
 // (cudaHostRegister) so every copy is an async DMA; GPUDirect Storage is not used on this path
 // (the operands arrive in host memory through the API).

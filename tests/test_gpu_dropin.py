@@ -1,7 +1,9 @@
 """The reference's OWN unit tests (spgemm_test.cpp, partition_test.cpp, scheduler_test.cpp) and its
 release gate (acceptance.cpp), unmodified, compiled against the drop-in headers of include/aires/
 (hot path on the B200, everything else the reference's) and linked to libaires_b200.so.  Built by
-`make -C oracle dropin` where /root/reference exists (the binaries travel with the repo copy)."""
+`make -C oracle dropin` where /root/reference exists (the binaries travel with the repo copy).
+`real_test` (oracle/dropin_real_test.cpp) is ours: the real out-of-core run behind the same headers
+(exact and streamed output, capped budgets, MaxMemory) against the in-core product, bit-exact."""
 import os
 import subprocess
 
@@ -13,7 +15,8 @@ REF = os.path.join(ROOT, "oracle", "_ref")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("unit", ["spgemm_test", "partition_test", "scheduler_test", "gcn_test", "acceptance"])
+@pytest.mark.parametrize("unit", ["spgemm_test", "partition_test", "scheduler_test", "gcn_test", "acceptance",
+                                  "real_test"])
 def test_reference_suite_on_b200(unit):
     exe = os.path.join(REF, f"dropin_{unit}")
     if not os.path.exists(exe):
