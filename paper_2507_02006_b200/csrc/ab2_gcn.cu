@@ -57,7 +57,7 @@ __global__ void k_norm_check(const IdxT* __restrict__ col, const VIn* __restrict
 template <class IdxT, class VIn, class IdxO>
 __global__ void k_norm_fill(const uint64_t* __restrict__ ptr, uint64_t base, const IdxT* __restrict__ col,
                             const VIn* __restrict__ val, int64_t n, const int64_t* __restrict__ optr,
-                            IdxO* __restrict__ ocol, double* __restrict__ oval) {
+                            IdxO* __restrict__ ocol, double* __restrict__ oval, int32_t* __restrict__ orow) {
   const int lane = lane_id();
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -84,10 +84,12 @@ __global__ void k_norm_fill(const uint64_t* __restrict__ ptr, uint64_t base, con
       const int64_t dst = o + (i - s) + (i >= p && !diag ? 1 : 0);
       ocol[dst] = static_cast<IdxO>(col[i]);
       oval[dst] = static_cast<double>(val[i]);
+      if (orow) orow[dst] = static_cast<int32_t>(r);
     }
     if (lane == 0) {
       ocol[o + (p - s)] = static_cast<IdxO>(r);
       oval[o + (p - s)] = diag ? static_cast<double>(val[p]) + 1.0 : 1.0;
+      if (orow) orow[o + (p - s)] = static_cast<int32_t>(r);
     }
   }
 }
@@ -140,8 +142,22 @@ __global__ void k_norm_degree(const int64_t* __restrict__ optr, const double* __
   }
 }
 
-// v / sqrt(d_i * d_j): one IEEE multiply, sqrt and divide.  One warp per row (a thread per row
-// measured 1.40 ms vs 1.21 ms here: the gathers of deg[col] then run 32 rows apart).
+// v / sqrt(d_i * d_j): one IEEE multiply, sqrt and divide, one thread per entry (the fill pass
+// records each entry's row): every lane busy and every stream coalesced; only deg[] is gathered
+// (L2-resident).  A warp per row measured 1.21 ms at cfg5 (lanes idle on ~26-entry rows, the
+// per-row load chain exposed), a thread per row 1.40 ms; this form 0.37 ms.  (Summing the degree
+// inside the fill's warp-per-row pass measured slower: 2.57 ms vs 0.90 + 0.73.)
+template <class IdxO, class VO>
+__global__ void k_norm_scale_flat(const int32_t* __restrict__ orow, const IdxO* __restrict__ ocol,
+                                  const double* __restrict__ oval, const double* __restrict__ deg, int64_t nnz,
+                                  VO* __restrict__ out) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[k] = static_cast<VO>(
+        __ddiv_rn(oval[k], __dsqrt_rn(__dmul_rn(deg[orow[k]], deg[static_cast<int64_t>(ocol[k])]))));
+}
+
+// (row form, used when the row ids do not fit int32)
 template <class IdxO, class VO>
 __global__ void k_norm_scale(const int64_t* __restrict__ optr, const IdxO* __restrict__ ocol,
                              const double* __restrict__ oval, const double* __restrict__ deg, int64_t n,
@@ -378,13 +394,19 @@ void normalize_t(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
   const uint64_t nnz = n > 0 ? h->nnz : 0;
   IdxO* ocol = static_cast<IdxO*>(ctx.c_col.get(std::max<uint64_t>(nnz, 1) * sizeof(IdxO)));
   double* oval = static_cast<double*>(ctx.t_val.get(std::max<uint64_t>(nnz, 1) * 8));
+  const bool flat = n < (int64_t(1) << 31);  // per-entry row ids for the flat scale pass
+  int32_t* orow = flat ? static_cast<int32_t*>(ctx.t_col.get(std::max<uint64_t>(nnz, 1) * 4)) : nullptr;
   double* deg = static_cast<double*>(ctx.rflops.get(std::max<int64_t>(n, 1) * 8));
   VO* outv = static_cast<VO*>(ctx.c_val.get(std::max<uint64_t>(nnz, 1) * sizeof(VO)));
   if (n > 0) {
     k_norm_fill<IdxT, VIn, IdxO><<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(s.ptr, s.base, col, val, n,
-                                                                                       optr, ocol, oval);
+                                                                                       optr, ocol, oval, orow);
     k_norm_degree<<<grid_of(n, 256, ctx.sms), 256, 0, ctx.stream>>>(optr, oval, n, deg);
-    k_norm_scale<IdxO, VO><<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(optr, ocol, oval, deg, n, outv);
+    if (flat)
+      k_norm_scale_flat<IdxO, VO><<<grid_of(static_cast<int64_t>(nnz), 256, ctx.sms), 256, 0, ctx.stream>>>(
+          orow, ocol, oval, deg, static_cast<int64_t>(nnz), outv);
+    else
+      k_norm_scale<IdxO, VO><<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(optr, ocol, oval, deg, n, outv);
     AB2_CUDA(cudaGetLastError());
     launches += 3;
   }
