@@ -2,18 +2,24 @@
 """bench.py -- A·X SpGEMM (AIRES hot path) on B200: latency, GFLOP/s and roofline fraction.
 
 Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE JSON line on
-rank 0.  N>1 runs under torchrun, one rank per GPU (NCCL); every rank owns one contiguous
-row block (weak scaling: each rank's block is a cfg-shaped Ã_r over its own slice of the
-replicated X) and the only collective is the all-gather of per-rank nnz(C) that forms the
-global row_ptr offsets.
+rank 0.  N>1 runs under torchrun, one rank per GPU (NCCL).  Every rank builds the SAME graph
+(deterministic seeds) and owns one contiguous row block of it, cut on the prefix sum of per-row
+MACs (shard.row_shards); X is replicated; the only collective is the all-gather of per-rank
+nnz(C) that forms the global row_ptr offsets.  Total work is fixed as N grows
+("scaling": "strong"); at N=1 the block is the whole matrix.
 
-Workload at N=1: BASELINE.json configs[1] (Reddit-shaped, 232,965 nodes, 114 M edges, X 602
-wide at 1 %, fully HBM-resident), synthetic (BASELINE.md §4 seeds: graph 1, relabel 2, X 3).
-A "step" is one full A·X through the C ABI (aires_b200_spgemm) with device-resident A and X
-(device C): X layout build, classify, symbolic, scan, nnz readback + exact allocation,
-numeric.  `e2e` is the same call with pinned HOST buffers (H2D of A and X and D2H of C
-inside the timed region).  `--impl reference` times the reference's own CPU spgemm_block
-(oracle/_ref, built from /root/reference) on a row sample with all host threads.
+Workload: BASELINE.json configs[1] (Reddit-shaped, 232,965 nodes, 114 M edges, X 602 wide at 1 %,
+fully HBM-resident), synthetic (seeds graph 1, relabel 2, X 3).  A "step" is one full A·X through
+the C ABI (aires_b200_spgemm) with device-resident A and X (device C): X layout build, classify,
+product, scan, nnz readback + exact allocation, placement.  `e2e` is the same product through
+the public out-of-core entry point (aires_b200_run, run_aires) with pinned HOST buffers, H2D of
+A/X and D2H of C inside the timed region.  Every figure is checked against a resident product
+or the reference (`checked` keys), outside the timed regions.
+
+`--impl reference` times the reference's own CPU spgemm_block (oracle/_ref, compiled from
+/root/reference) on a row sample with all host threads, on inputs built by the oracle's
+restatement of the generator (oracle/aires_oracle.c ao_synth_graph, byte-identical to the
+library's, tests/test_oracle.py) -- no libaires_b200.so is loaded in that arm.
 """
 from __future__ import annotations
 
@@ -25,6 +31,7 @@ import subprocess
 import sys
 import threading
 import time
+from types import SimpleNamespace
 
 import numpy as np
 
@@ -32,6 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "A·X SpGEMM latency (ms) and GFLOP/s; % of HBM/host-link roofline at 1/2/4/8 B200"
+SEEDS = {"graph": 1, "relabel": 2, "x": 3, "alpha": 0.75}
 
 CONFIGS = {
     "cfg1": dict(workload="cfg1: power-law 100K nodes / 1M edges, X 100Kx512 @1%",
@@ -106,31 +114,188 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def make_inputs(cfg: dict, rank: int, world: int):
-    """Rank r: Ã_r (seed 1+r) over node block r; X (seed 3) covering all world*n rows."""
+# ---------------------------------------------------------------------------------------------
+# inputs
+# ---------------------------------------------------------------------------------------------
+
+def make_inputs(cfg: dict):
+    """b200 arm: the library's seeded generator (same graph on every rank)."""
     import paper_2507_02006_b200 as ab
-    n = cfg["n"]
     t0 = time.time()
-    g, st = ab.synth_graph(n, cfg["nnz"], alpha=0.75, degree_cap=cfg["cap"], seed=1 + rank, relabel_seed=2,
-                           idx_dtype=np.uint32, val_dtype=np.float64)
-    x = ab.synth_features(n * world, cfg["dim"], 99.0, 3, idx_dtype=np.uint32, val_dtype=np.float64)
-    if world > 1:  # Ã_r's columns address X rows [r*n, (r+1)*n)
-        g.col_idx = g.col_idx + np.uint32(rank * n)
-        g.n_cols = n * world
-    log(f"[rank {rank}] inputs: A {g.n_rows}x{g.n_cols} nnz {g.nnz()} (edges {st['nnz_a']}, max deg "
-        f"{st['max_degree']}), X {x.n_rows}x{x.n_cols} nnz {x.nnz()} in {time.time() - t0:.1f}s")
+    g, st = ab.synth_graph(cfg["n"], cfg["nnz"], alpha=SEEDS["alpha"], degree_cap=cfg["cap"], seed=SEEDS["graph"],
+                           relabel_seed=SEEDS["relabel"], idx_dtype=np.uint32, val_dtype=np.float64)
+    x = ab.synth_features(cfg["n"], cfg["dim"], 99.0, SEEDS["x"], idx_dtype=np.uint32, val_dtype=np.float64)
+    log(f"inputs: A {g.n_rows}x{g.n_cols} nnz {g.nnz()} (edges {st['nnz_a']}, max deg {st['max_degree']}), "
+        f"X {x.n_rows}x{x.n_cols} nnz {x.nnz()} in {time.time() - t0:.1f}s")
     return g, st, x
 
 
+def make_inputs_ref(cfg: dict):
+    """reference arm: the oracle's restatement of the same generator (byte-identical arrays,
+    tests/test_oracle.py::test_synth_graph_restatement) -- libaires_b200.so is never loaded."""
+    from oracle import pyoracle as po
+    t0 = time.time()
+    (p, i, v), st = po.synth_graph(cfg["n"], cfg["nnz"], SEEDS["alpha"], cfg["cap"], SEEDS["graph"], SEEDS["relabel"])
+    rc, (xp, xi, xv) = po.gen_features(cfg["n"], cfg["dim"], 99.0, SEEDS["x"])
+    if rc:
+        raise RuntimeError(f"gen_features failed ({rc})")
+    g = SimpleNamespace(n_rows=cfg["n"], n_cols=cfg["n"], row_ptr=p, col_idx=i, values=v, nnz=lambda: int(p[-1]))
+    x = SimpleNamespace(n_rows=cfg["n"], n_cols=cfg["dim"], row_ptr=xp, col_idx=xi, values=xv, nnz=lambda: int(xp[-1]))
+    log(f"inputs (oracle generator): A nnz {g.nnz()}, X nnz {x.nnz()} in {time.time() - t0:.1f}s")
+    return g, st, x
+
+
+def config_of(cfg: dict, st: dict, g, x) -> dict:
+    """The workload, identical in both arms (computed from the inputs only)."""
+    b_a = 8 * (g.n_rows + 1) + 8 * g.nnz()
+    return {"workload": cfg["workload"], "nodes": int(g.n_rows), "edges": int(st["nnz_a"]),
+            "nnz_a_tilde": int(g.nnz()), "x_cols": int(x.n_cols), "nnz_x": int(x.nnz()),
+            "max_degree": int(st["max_degree"]), "seeds": dict(SEEDS),
+            "l2": f"inputs larger than L2 between steps (A {b_a / 1e9:.2f} GB + C vs the 126 MB L2); X stays "
+                  "L2-resident by design"}
+
+
+def row_macs(g, x) -> np.ndarray:
+    """MACs per row of A·X: the X row lengths gathered over A's columns (the work the shards balance)."""
+    xlen = np.diff(np.asarray(x.row_ptr, dtype=np.int64))
+    cs = np.concatenate([[0], np.cumsum(xlen[np.asarray(g.col_idx, dtype=np.int64)])])
+    rp = np.asarray(g.row_ptr, dtype=np.int64)
+    return cs[rp[1:]] - cs[rp[:-1]]
+
+
+def block_of(g, r0: int, r1: int):
+    """Rows [r0, r1) of g as a rebased CSR (host copies)."""
+    rp = np.asarray(g.row_ptr, dtype=np.uint64)
+    p0, p1 = int(rp[r0]), int(rp[r1])
+    return SimpleNamespace(n_rows=r1 - r0, n_cols=g.n_cols, row_ptr=rp[r0:r1 + 1] - np.uint64(p0),
+                           col_idx=g.col_idx[p0:p1], values=g.values[p0:p1], nnz=lambda: p1 - p0)
+
+
 def algorithmic_bytes(n_rows, nnz_a, k_rows, nnz_x, nnz_c, vb=4):
-    """BASELINE.md §5: Σ_{A,X,C} 8(rows+1) + (4+vb)·nnz (int64 ptr, int32 idx, fp32/fp64 val)."""
+    """SURVEY.md §8(d): Σ_{A,X,C} 8(rows+1) + (4+vb)·nnz (int64 ptr, int32 idx, fp32/fp64 val)."""
     return (8 * (n_rows + 1) + (4 + vb) * nnz_a) + (8 * (k_rows + 1) + (4 + vb) * nnz_x) + \
         (8 * (n_rows + 1) + (4 + vb) * nnz_c)
+
+
+def compare(ptr, idx, val, ref_ptr, ref_idx, ref_val, rtol=1e-5) -> dict:
+    """Structure bit-exact + values within rtol (relative; the synthetic operands are positive so no
+    cell cancels) -- the north_star parity rule, applied to two B200 results or B200 vs oracle."""
+    ptr = np.asarray(ptr).view(np.uint64) if np.asarray(ptr).dtype == np.int64 else np.asarray(ptr, np.uint64)
+    rptr = np.asarray(ref_ptr).view(np.uint64) if np.asarray(ref_ptr).dtype == np.int64 else np.asarray(ref_ptr,
+                                                                                                          np.uint64)
+    s_ok = bool(np.array_equal(ptr, rptr)) and bool(np.array_equal(np.asarray(idx, np.int64),
+                                                                   np.asarray(ref_idx, np.int64)))
+    err = 0.0
+    if s_ok and len(val):
+        a = np.asarray(val, np.float64)
+        b = np.asarray(ref_val, np.float64)
+        err = float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-30)))
+    return {"structure_equal": s_ok, "max_rel_err": err, "rtol": rtol, "checked": bool(s_ok and err <= rtol)}
+
+
+# ---------------------------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------------------------
+
+class DeviceProduct:
+    """One device-resident A·X through aires_b200_spgemm (the step), grow-only device output."""
+
+    def __init__(self, ab, torch, dev, blk, x, mode):
+        self.ab, self.torch, self.dev, self.mode = ab, torch, dev, mode
+        vb = 8 if mode == ab.MODE_FP64_EXACT else 4
+        vnp = np.float64 if vb == 8 else np.float32
+        self.vt = torch.float64 if vb == 8 else torch.float32
+        self.vb = vb
+        self.tA = [torch.from_numpy(np.ascontiguousarray(blk.row_ptr).view(np.int64)).to(dev),
+                   torch.from_numpy(np.ascontiguousarray(blk.col_idx, np.uint32).view(np.int32)).to(dev),
+                   torch.from_numpy(np.ascontiguousarray(blk.values, vnp)).to(dev)]
+        self.tX = [torch.from_numpy(np.ascontiguousarray(x.row_ptr).view(np.int64)).to(dev),
+                   torch.from_numpy(np.ascontiguousarray(x.col_idx, np.uint32).view(np.int32)).to(dev),
+                   torch.from_numpy(np.ascontiguousarray(x.values, vnp)).to(dev)]
+        self.am = ab._Matrix(blk.n_rows, blk.n_cols, ab.CSR, ab.DEVICE, 4, vb, self.tA[0].data_ptr(),
+                             self.tA[1].data_ptr(), self.tA[2].data_ptr(), blk.nnz())
+        self.xm = ab._Matrix(x.n_rows, x.n_cols, ab.CSR, ab.DEVICE, 4, vb, self.tX[0].data_ptr(),
+                             self.tX[1].data_ptr(), self.tX[2].data_ptr(), x.nnz())
+        self.buf = {}
+        self.fn = ab._ALLOC_FN(self._alloc)
+        self.out = ab._Output(ab.DEVICE, 4, vb, 0, self.fn, None, 0, 0, 0, 0)
+
+    def _alloc(self, user, rows, nnz, pp, pi, pv):
+        T = self.torch
+        if self.buf.get("cap", -1) < nnz or self.buf.get("rows", -1) < rows:
+            self.buf = {"ptr": T.empty(rows + 1, dtype=T.int64, device=self.dev),
+                        "idx": T.empty(max(nnz, 1), dtype=T.int32, device=self.dev),
+                        "val": T.empty(max(nnz, 1), dtype=self.vt, device=self.dev), "cap": nnz, "rows": rows}
+        pp[0], pi[0], pv[0] = self.buf["ptr"].data_ptr(), self.buf["idx"].data_ptr(), self.buf["val"].data_ptr()
+        return 0
+
+    def step(self):
+        self.ab._check(self.ab.lib().aires_b200_spgemm(C.byref(self.am), C.byref(self.xm), self.mode,
+                                                       C.byref(self.out)))
+
+    def result_host(self):
+        n, z = int(self.out.n_rows), int(self.out.nnz)
+        return (self.buf["ptr"][: n + 1].cpu().numpy(), self.buf["idx"][:z].cpu().numpy(),
+                self.buf["val"][:z].cpu().numpy())
+
+    def free(self):
+        self.tA.clear()
+        self.tX.clear()
+        self.buf = {}
+
+
+def time_steps(L, ab, torch, dev, fn, steps, warmup, dist=None, prof=True):
+    """warmup untimed steps, then `steps` timed on the library's stream with CUDA events, bracketed by
+    a barrier + synchronize on both sides; returns (ms per step on this rank, per-kernel ms, launches)."""
+    lib_stream = torch.cuda.ExternalStream(L.aires_b200_stream(), device=dev)
+    for _ in range(warmup):
+        fn()
+    keys = ["classify", "symbolic", "scan", "numeric", "x_prep"]
+    psum = {k: 0.0 for k in keys}
+    launches = 0
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(lib_stream)
+    for _ in range(steps):
+        fn()
+        if prof:
+            p = ab.last_profile()
+            for k in keys:
+                psum[k] += p[k]
+        launches += L.aires_b200_last_launches()
+    ev1.record(lib_stream)
+    ev1.synchronize()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    return ev0.elapsed_time(ev1) / steps, {k: v / steps for k, v in psum.items()}, launches
+
+
+def max_over_ranks(v: float, dist, cdev):
+    if not dist:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=cdev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(v: int, dist, cdev):
+    if not dist:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.int64, device=cdev)
+    dist.all_reduce(t)
+    return int(t.item())
 
 
 def run_b200(args, cfg):
     import torch
     import paper_2507_02006_b200 as ab
+    from paper_2507_02006_b200 import shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -146,248 +311,101 @@ def run_b200(args, cfg):
         torch.cuda.set_device(local)
         dist.init_process_group(backend)
     torch.cuda.set_device(local)
-    cdev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")  # collective tensors
+    cdev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
     L = ab.lib()
     ab._check(L.aires_b200_set_device(local))
     dev = torch.device("cuda", local)
-    mode = ab.MODE_FP64_EXACT if args.mode == "fp64" else ab.MODE_FP32
-    vdt_np = np.float64 if mode == ab.MODE_FP64_EXACT else np.float32
-    vdt_t = torch.float64 if mode == ab.MODE_FP64_EXACT else torch.float32
-    vb = 8 if mode == ab.MODE_FP64_EXACT else 4
 
-    g, st, x = make_inputs(cfg, rank, world)
+    g, st, x = make_inputs(cfg)
     n, K = g.n_rows, x.n_rows
-    # device-resident inputs (u64 ptr, u32 idx, fp32/fp64 values)
-    tA = [torch.from_numpy(g.row_ptr.view(np.int64)).to(dev), torch.from_numpy(g.col_idx.view(np.int32)).to(dev),
-          torch.from_numpy(g.values.astype(vdt_np)).to(dev)]
-    tX = [torch.from_numpy(x.row_ptr.view(np.int64)).to(dev), torch.from_numpy(x.col_idx.view(np.int32)).to(dev),
-          torch.from_numpy(x.values.astype(vdt_np)).to(dev)]
-    am = ab._Matrix(n, g.n_cols, ab.CSR, ab.DEVICE, 4, vb, tA[0].data_ptr(), tA[1].data_ptr(), tA[2].data_ptr(),
-                    g.nnz())
-    xm = ab._Matrix(K, x.n_cols, ab.CSR, ab.DEVICE, 4, vb, tX[0].data_ptr(), tX[1].data_ptr(), tX[2].data_ptr(),
-                    x.nnz())
+    cuts = shard.row_shards(g.row_ptr, world, work=row_macs(g, x)) if world > 1 else np.array([0, n])
+    r0, r1 = int(cuts[rank]), int(cuts[rank + 1])
+    blk = block_of(g, r0, r1) if world > 1 else g
 
-    # device output: grow-only buffers handed out by the allocator
-    outbuf = {}
-
-    def dev_alloc(user, rows, nnz, pp, pi, pv):
-        if outbuf.get("cap", -1) < nnz:
-            outbuf["ptr"] = torch.empty(rows + 1, dtype=torch.int64, device=dev)
-            outbuf["idx"] = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
-            outbuf["val"] = torch.empty(max(nnz, 1), dtype=vdt_t, device=dev)
-            outbuf["cap"] = nnz
-        pp[0], pi[0], pv[0] = outbuf["ptr"].data_ptr(), outbuf["idx"].data_ptr(), outbuf["val"].data_ptr()
-        return 0
-
-    afn = ab._ALLOC_FN(dev_alloc)
-    out = ab._Output(ab.DEVICE, 4, vb, 0, afn, None, 0, 0, 0, 0)
-
-    def step():
-        ab._check(L.aires_b200_spgemm(C.byref(am), C.byref(xm), mode, C.byref(out)))
-
-    lib_stream = torch.cuda.ExternalStream(L.aires_b200_stream(), device=dev)
-    for _ in range(args.warmup):
-        step()
-    nnz_c, macs = int(out.nnz), int(out.flops)
-    prof_keys = ["classify", "symbolic", "scan", "numeric", "x_prep"]
-    prof_sum = {k: 0.0 for k in prof_keys}
-    launches = 0
-    torch.cuda.synchronize(dev)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    from paper_2507_02006_b200 import shard
-    offsets = np.zeros(world, dtype=np.int64)
+    # ---- the step: device-resident fp32 product of this rank's block --------------------------
+    prod = DeviceProduct(ab, torch, dev, blk, x, ab.MODE_FP32)
     with ClockSampler(local) as clk:
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(lib_stream)
-        for _ in range(args.steps):
-            step()
-            p = ab.last_profile()
-            for k in prof_keys:
-                prof_sum[k] += p[k]
-            launches += L.aires_b200_last_launches()
-            if dist:  # global row_ptr offsets: all-gather of one int64 nnz(C) per rank (shard.py)
-                offsets, _ = shard.global_offsets(int(out.nnz), device=cdev)
-        ev1.record(lib_stream)
-        ev1.synchronize()
-    torch.cuda.synchronize(dev)
-    if dist:
-        dist.barrier()
-    ms_rank = ev0.elapsed_time(ev1) / args.steps
-    ms = ms_rank
-    tot_macs = macs
-    if dist:
-        t = torch.tensor([ms_rank], dtype=torch.float64, device=cdev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        m = torch.tensor([macs], dtype=torch.int64, device=cdev)
-        dist.all_reduce(m)
-        tot_macs = int(m.item())
+        ms_rank, kern, launches = time_steps(L, ab, torch, dev, prod.step, args.steps, args.warmup, dist)
+    ms = max_over_ranks(ms_rank, dist, cdev)
+    nnz_c, macs = int(prod.out.nnz), int(prod.out.flops)
+    tot_macs = sum_over_ranks(macs, dist, cdev)
+    offsets, tot_nnz = (shard.global_offsets(nnz_c, device=cdev) if dist else (np.zeros(1, np.int64), nnz_c))
     gflops = 2.0 * tot_macs / (ms * 1e-3) / 1e9
-    c_ptr_check = c_idx_check = None
-    if not args.skip_e2e and rank == 0 and world == 1:  # the device product, to check the host-API run against
-        c_ptr_check = outbuf["ptr"][: n + 1].cpu().numpy().view(np.uint64)
-        c_idx_check = outbuf["idx"][:nnz_c].cpu().numpy()
+    res32 = prod.result_host()
 
-    # roofline of the dominant kernel (numeric) and of the whole step
     peak, peak_src = peaks()
-    b_alg = algorithmic_bytes(n, g.nnz(), K, x.nnz(), nnz_c, vb)
-    num_ms = prof_sum["numeric"] / args.steps
-    sym_ms = prof_sum["symbolic"] / args.steps
+    b_alg = algorithmic_bytes(blk.n_rows, blk.nnz(), K, x.nnz(), nnz_c, 4)
+    num_ms = kern["numeric"]
     ach = b_alg / (num_ms * 1e-3) / 1e9
     traffic = None
     try:  # DRAM bytes of the dominant kernel from the committed ncu --set full capture (cfg2 fp32)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
-        if cfg is CONFIGS["cfg2"] and vb == 4 and "k_numeric3" in tj:
-            traffic = tj["k_numeric3"]["dram_bytes"]
+        if cfg is CONFIGS["cfg2"] and world == 1 and "k_numeric" in tj:
+            traffic = tj["k_numeric"]["dram_bytes"] if tj["k_numeric"].get("kernel") else None
     except Exception:
         traffic = None
     roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
             "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write, one launch)",
-            "kernel": "k_numeric3_f32" if vb == 4 else "k_numeric3_f64",
-            "kernel_ms": round(num_ms, 4), "bytes_per_launch": b_alg, "peak_source": peak_src,
-            "step_frac": round(b_alg / (ms * 1e-3) / 1e9 / peak, 4),
-            "kernel_ms_breakdown": {k: round(v / args.steps, 4) for k, v in prof_sum.items()}}
+            "kernel": "k_numeric (fp32 product pass)", "kernel_ms": round(num_ms, 4), "bytes_per_launch": b_alg,
+            "bytes_basis": "8(rows+1)+8nnz over A block, X and C block (int64 ptr, int32 idx, fp32 val)",
+            "peak_source": peak_src, "step_frac": round(b_alg / (ms_rank * 1e-3) / 1e9 / peak, 4),
+            "kernel_ms_breakdown": {("place" if k == "symbolic" else k): round(v, 4) for k, v in kern.items()}}
+    prod.free()
+    torch.cuda.empty_cache()
 
-    # e2e: same call, pinned host buffers, H2D + D2H inside the timed region
+    # ---- fp64-exact leg: the drop-in's arithmetic and the reference's precision ---------------
+    fp64 = None
+    res64 = None
+    if world == 1 and not args.skip_fp64:
+        p64 = DeviceProduct(ab, torch, dev, blk, x, ab.MODE_FP64_EXACT)
+        ms64, k64, _ = time_steps(L, ab, torch, dev, p64.step, max(3, args.steps // 2), args.warmup)
+        res64 = p64.result_host()
+        b64 = algorithmic_bytes(blk.n_rows, blk.nnz(), K, x.nnz(), int(p64.out.nnz), 8)
+        fp64 = {"mode": "FP64_EXACT (no FMA, ascending k: bit-identical to spgemm_block)", "ms_per_step": round(ms64, 4),
+                "gflops": round(2.0 * int(p64.out.flops) / (ms64 * 1e-3) / 1e9, 3),
+                "kernel_ms": round(k64["numeric"], 4),
+                "roofline": {"bound": "hbm", "bytes_per_launch": b64, "bytes_basis": "8(rows+1)+12nnz (fp64 values)",
+                             "achieved": round(b64 / (k64["numeric"] * 1e-3) / 1e9, 1), "peak": peak,
+                             "frac": round(b64 / (k64["numeric"] * 1e-3) / 1e9 / peak, 4)},
+                "structure_equal_fp32": bool(np.array_equal(res64[0], res32[0]) and np.array_equal(res64[1], res32[1])),
+                "nnz_c": int(p64.out.nnz), "macs": int(p64.out.flops)}
+        p64.free()
+        torch.cuda.empty_cache()
+
+    # ---- e2e: the public out-of-core entry point with pinned host buffers ---------------------
     e2e = None
     if not args.skip_e2e:
-        hA = [torch.from_numpy(g.row_ptr.view(np.int64)).pin_memory(),
-              torch.from_numpy(g.col_idx.view(np.int32)).pin_memory(),
-              torch.from_numpy(g.values.astype(vdt_np)).pin_memory()]
-        hX = [torch.from_numpy(x.row_ptr.view(np.int64)).pin_memory(),
-              torch.from_numpy(x.col_idx.view(np.int32)).pin_memory(),
-              torch.from_numpy(x.values.astype(vdt_np)).pin_memory()]
-        ham = ab._Matrix(n, g.n_cols, ab.CSR, ab.HOST, 4, vb, hA[0].data_ptr(), hA[1].data_ptr(), hA[2].data_ptr(),
-                         g.nnz())
-        hxm = ab._Matrix(K, x.n_cols, ab.CSR, ab.HOST, 4, vb, hX[0].data_ptr(), hX[1].data_ptr(),
-                         hX[2].data_ptr(), x.nnz())
-        # streamed output hands the allocator an upper bound of nnz(C) (include/aires_b200.h):
-        # min(rows * n_cols, nnz(A) * longest X row); the pinned result buffers cover it
-        c_bound = min(n * x.n_cols, g.nnz() * int(np.diff(x.row_ptr.astype(np.int64)).max(initial=1)))
-        hout = {"ptr": torch.empty(n + 1, dtype=torch.int64).pin_memory(),
-                "idx": torch.empty(max(nnz_c, c_bound, 1), dtype=torch.int32).pin_memory(),
-                "val": torch.empty(max(nnz_c, c_bound, 1), dtype=vdt_t).pin_memory()}
+        e2e = e2e_leg(args, dev, L, ab, torch, blk, x, res32, tot_macs, dist, cdev)
 
-        def host_alloc(user, rows, nnz, pp, pi, pv):
-            if nnz > hout["idx"].numel():
-                return 9
-            pp[0], pi[0], pv[0] = hout["ptr"].data_ptr(), hout["idx"].data_ptr(), hout["val"].data_ptr()
-            return 0
-
-        hfn = ab._ALLOC_FN(host_alloc)
-        hout_s = ab._Output(ab.HOST, 4, vb, 0, hfn, None, 0, 0, 0, 0)
-
-        def estep():
-            ab._check(L.aires_b200_spgemm(C.byref(ham), C.byref(hxm), mode, C.byref(hout_s)))
-
-        # the public entry point for host-resident operands is the out-of-core run (run_aires,
-        # aires_b200_run), uncapped.  Streamed output (the headline): no sizing pass, ~16 row
-        # blocks, C drains on copy engine 1 while A still crosses on copy engine 0.  Exact protocol
-        # (beside it): sizing pass over A's columns first, exact allocation, then the tiles.
-        rrep = ab._RunReport()
-        rcfg = ab._RunConfig(0, mode, 1, 0, ab.RUN_STREAM_OUT)
-        xrep = ab._RunReport()
-        xcfg = ab._RunConfig(0, mode, 1, 3, 0)
-
-        def rstep():
-            ab._check(L.aires_b200_run(C.byref(ham), C.byref(hxm), C.byref(rcfg), C.byref(hout_s), C.byref(rrep)))
-
-        def xstep():
-            ab._check(L.aires_b200_run(C.byref(ham), C.byref(hxm), C.byref(xcfg), C.byref(hout_s), C.byref(xrep)))
-
-        for _ in range(max(1, args.warmup)):
-            estep()
-            xstep()
-            rstep()
-        if dist:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            estep()
-        s_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            xstep()
-        x_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-        if int(hout_s.nnz) != nnz_c:
-            raise RuntimeError(f"run_aires (exact) nnz {int(hout_s.nnz)} != spgemm nnz {nnz_c}")
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            rstep()
-        e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-        if int(hout_s.nnz) != nnz_c:
-            raise RuntimeError(f"run_aires (streamed) nnz {int(hout_s.nnz)} != spgemm nnz {nnz_c}")
-        if rank == 0 and world == 1:
-            # the streamed result against the device product (structure bit-exact, values 1e-5)
-            hp = hout["ptr"].numpy().view(np.uint64)
-            if not np.array_equal(hp, c_ptr_check):
-                raise RuntimeError("streamed run row_ptr differs from the device product")
-            if not np.array_equal(hout["idx"][:nnz_c].numpy(), c_idx_check):
-                raise RuntimeError("streamed run col_idx differs from the device product")
-        link = link_bandwidth(dev)
-        e2e_duplex_ms = max(int(rrep.h2d_bytes) / link["h2d"], int(rrep.d2h_bytes) / link["d2h"]) / 1e6
-        if dist:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=cdev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        h2d = int(rrep.h2d_bytes)
-        d2h = int(rrep.d2h_bytes)
-        e2e = {"value": round(2.0 * tot_macs / (e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s", "ms_per_step": round(e_ms, 3),
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "api": "aires_b200_run (run_aires, streamed output), pinned host A/X/C (u64 ptr, u32 idx, fp32 val), "
-                      "wall clock",
-               "segments": int(rrep.segments), "device_ms": round(rrep.total_ms, 3),
-               "roofline": {"bound": "host-link (full duplex)", "link_gbs": {k: round(v, 2) for k, v in link.items()},
-                            "t_roof_ms": round(e2e_duplex_ms, 3), "frac": round(e2e_duplex_ms / e_ms, 4),
-                            "basis": "max(H2D bytes / measured pinned H2D GB/s, D2H bytes / measured D2H GB/s)"},
-               "exact_protocol": {"api": "aires_b200_run without streamed output (sizing pass over A's columns, "
-                                         "exact allocation, then the tiles)",
-                                  "ms_per_step": round(x_ms, 3), "value": round(2.0 * tot_macs / (x_ms * 1e-3) / 1e9, 3),
-                                  "device_ms": round(xrep.total_ms, 3), "segments": int(xrep.segments)},
-               "spgemm_call": {"api": "aires_b200_spgemm with host buffers (one-shot H2D, product, D2H)",
-                               "ms_per_step": round(s_ms, 3),
-                               "value": round(2.0 * tot_macs / (s_ms * 1e-3) / 1e9, 3)}}
-
+    # ---- CPU baseline (rank 0): the reference on a row sample, its rows checked against ours ----
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
-        cpu = cpu_baseline(g, x, args.cpu_seconds)
+        cpu = cpu_baseline(g, x, args.cpu_seconds, res32, res64)
+
     ooc = None
-    if world == 1 and not args.skip_ooc:
-        tA.clear(); tX.clear(); outbuf.clear()
-        torch.cuda.empty_cache()
-        ooc = out_of_core_leg(args, dev, L, ab, torch)
-    ppi = None
-    if world == 1 and args.cfg4_shard:
-        torch.cuda.empty_cache()
-        ppi = out_of_core_leg(args, dev, L, ab, torch, "cfg4shard")
+    if not args.skip_ooc:
+        ooc = out_of_core_legs(args, dev, L, ab, torch, g if world == 1 else None, x, res32, rank, world, dist, cdev)
     gcn = None
     if world == 1 and not args.skip_gcn:
-        torch.cuda.empty_cache()
         gcn = gcn_leg(args, dev, L, ab, torch)
     elif world > 1 and not args.skip_gcn:
-        tA.clear(); tX.clear(); outbuf.clear()
-        torch.cuda.empty_cache()
         gcn = gcn_leg_dist(args, dev, L, ab, torch, dist, rank, world, cdev)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if vb == 4 else "f64",
-            "data": "synthetic (Chung-Lu power-law Ã, gen_features X; seeds graph 1+rank, relabel 2, X 3)",
-            "config": {"workload": cfg["workload"], "nodes_per_gpu": n, "edges_per_gpu": st["nnz_a"],
-                       "nnz_a_tilde": g.nnz(), "x_cols": x.n_cols, "nnz_x": x.nnz(), "nnz_c": nnz_c,
-                       "macs": tot_macs, "max_degree": st["max_degree"], "mode": args.mode,
-                       "parallelism": f"row-block shards x{world}" if world > 1 else "single GPU",
-                       "global_row_ptr_offsets": [int(o) for o in offsets] if world > 1 else None,
-                       "l2": "inputs larger than L2 (A 0.9 GB, C 1.1 GB vs 126 MB L2); X is meant to stay L2-resident",
-                       "latency_ms": round(ms, 4)},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "out_of_core": ooc, "gcn_2layer": gcn, "cfg4_shard": ppi,
-            "clocks": clk.summary(),
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (Chung-Lu power-law Ã, gen_features X; seeds graph 1, relabel 2, X 3)",
+            "config": config_of(cfg, st, g, x),
+            "parallelism": (f"row-block shards x{world} (MAC-balanced, X replicated, nnz(C) offsets all-gathered)"
+                            if world > 1 else "single GPU"),
+            "result": {"nnz_c": tot_nnz, "macs": tot_macs, "latency_ms": round(ms, 4),
+                       "rows_per_rank": [int(cuts[i + 1] - cuts[i]) for i in range(world)],
+                       "global_row_ptr_offsets": [int(o) for o in offsets] if world > 1 else None},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "fp64_exact": fp64, "gpu_launches": launches,
+            "out_of_core": ooc, "gcn_2layer": gcn, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -414,88 +432,213 @@ def link_bandwidth(dev, nbytes=512 << 20, reps=5):
     return out
 
 
-def out_of_core_leg(args, dev, L, ab, torch, cfg_name="cfg3"):
-    """cfg3 (ogbn-products-shaped) through aires_b200_run with the device budget capped to
-    args.ooc_frac of B_A + B_X + B_C: A and X in pinned host memory, C drained to pinned host
-    memory tile by tile.  Roofline = the host link (measured in this run)."""
-    cfg = CONFIGS[cfg_name]
-    g, st, x = make_inputs(cfg, 0, 1)
-    n, K = g.n_rows, x.n_rows
-    hA = [torch.from_numpy(g.row_ptr.view(np.int64)).pin_memory(), torch.from_numpy(g.col_idx.view(np.int32)).pin_memory(),
-          torch.from_numpy(g.values.astype(np.float32)).pin_memory()]
-    hX = [torch.from_numpy(x.row_ptr.view(np.int64)).pin_memory(), torch.from_numpy(x.col_idx.view(np.int32)).pin_memory(),
-          torch.from_numpy(x.values.astype(np.float32)).pin_memory()]
-    am = ab._Matrix(n, g.n_cols, ab.CSR, ab.HOST, 4, 4, hA[0].data_ptr(), hA[1].data_ptr(), hA[2].data_ptr(), g.nnz())
-    xm = ab._Matrix(K, x.n_cols, ab.CSR, ab.HOST, 4, 4, hX[0].data_ptr(), hX[1].data_ptr(), hX[2].data_ptr(), x.nnz())
-    hout = {}
+class HostOperands:
+    """Pinned host copies of an A block (u64 ptr, u32 idx, fp32 val) and of X, plus a pinned output
+    sized for `cap` nonzeros (or grown on demand) -- the buffers aires_b200_run sees."""
 
-    def alloc(user, rows, nnz, pp, pi, pv):
-        if hout.get("cap", -1) < nnz:
-            hout["ptr"] = torch.empty(rows + 1, dtype=torch.int64).pin_memory()
-            hout["idx"] = torch.empty(max(nnz, 1), dtype=torch.int32).pin_memory()
-            hout["val"] = torch.empty(max(nnz, 1), dtype=torch.float32).pin_memory()
-            hout["cap"] = nnz
-        pp[0], pi[0], pv[0] = hout["ptr"].data_ptr(), hout["idx"].data_ptr(), hout["val"].data_ptr()
+    def __init__(self, ab, torch, a, x, cap=0):
+        self.ab, self.torch = ab, torch
+        self.hA = [torch.from_numpy(np.ascontiguousarray(a.row_ptr, np.uint64).view(np.int64)).pin_memory(),
+                   torch.from_numpy(np.ascontiguousarray(a.col_idx, np.uint32).view(np.int32)).pin_memory(),
+                   torch.from_numpy(np.ascontiguousarray(a.values, np.float32)).pin_memory()]
+        self.hX = [torch.from_numpy(np.ascontiguousarray(x.row_ptr, np.uint64).view(np.int64)).pin_memory(),
+                   torch.from_numpy(np.ascontiguousarray(x.col_idx, np.uint32).view(np.int32)).pin_memory(),
+                   torch.from_numpy(np.ascontiguousarray(x.values, np.float32)).pin_memory()]
+        self.am = ab._Matrix(a.n_rows, a.n_cols, ab.CSR, ab.HOST, 4, 4, self.hA[0].data_ptr(), self.hA[1].data_ptr(),
+                             self.hA[2].data_ptr(), a.nnz())
+        self.xm = ab._Matrix(x.n_rows, x.n_cols, ab.CSR, ab.HOST, 4, 4, self.hX[0].data_ptr(), self.hX[1].data_ptr(),
+                             self.hX[2].data_ptr(), x.nnz())
+        self.rows = a.n_rows
+        self.out_t = {}
+        if cap:
+            self._grow(a.n_rows, cap)
+        self.fn = ab._ALLOC_FN(self._alloc)
+        self.out = ab._Output(ab.HOST, 4, 4, 0, self.fn, None, 0, 0, 0, 0)
+
+    def _grow(self, rows, nnz):
+        T = self.torch
+        self.out_t = {"ptr": T.empty(rows + 1, dtype=T.int64).pin_memory(),
+                      "idx": T.empty(max(nnz, 1), dtype=T.int32).pin_memory(),
+                      "val": T.empty(max(nnz, 1), dtype=T.float32).pin_memory(), "cap": nnz}
+
+    def _alloc(self, user, rows, nnz, pp, pi, pv):
+        if self.out_t.get("cap", -1) < nnz:
+            self._grow(rows, nnz)
+        pp[0], pi[0], pv[0] = (self.out_t["ptr"].data_ptr(), self.out_t["idx"].data_ptr(),
+                               self.out_t["val"].data_ptr())
         return 0
 
-    afn = ab._ALLOC_FN(alloc)
-    out = ab._Output(ab.HOST, 4, 4, 0, afn, None, 0, 0, 0, 0)
-    rep = ab._RunReport()
-    # size the budget from a first unconstrained run (C bytes are only known after it)
-    ab._check(L.aires_b200_run(C.byref(am), C.byref(xm), C.byref(ab._RunConfig(0, ab.MODE_FP32, 1, 2, 0)),
-                               C.byref(out), C.byref(rep)))
-    nnz_c, macs = int(out.nnz), int(out.flops)
-    b_a = 8 * (n + 1) + 8 * g.nnz()
-    b_x = 8 * (K + 1) + 8 * x.nnz()
-    b_c = 8 * (n + 1) + 8 * nnz_c
-    budget = int(args.ooc_frac * (b_a + b_x + b_c))
-    rc = ab._RunConfig(budget, ab.MODE_FP32, 1, args.ooc_buffers, 0)
+    def run(self, budget=0, c_aware=1, n_buffers=0, flags=0):
+        ab = self.ab
+        rep = ab._RunReport()
+        cfg = ab._RunConfig(int(budget), ab.MODE_FP32, c_aware, n_buffers, flags)
+        ab._check(ab.lib().aires_b200_run(C.byref(self.am), C.byref(self.xm), C.byref(cfg), C.byref(self.out),
+                                          C.byref(rep)))
+        return rep
+
+    def result(self):
+        z = int(self.out.nnz)
+        return (self.out_t["ptr"][: self.rows + 1].numpy(), self.out_t["idx"][:z].numpy(),
+                self.out_t["val"][:z].numpy())
+
+
+def e2e_leg(args, dev, L, ab, torch, blk, x, res32, tot_macs, dist, cdev):
+    """run_aires (aires_b200_run) with pinned host A/X/C, uncapped: streamed output (the headline:
+    no sizing pass, C drains while A still crosses) and, beside it, the exact-allocation protocol
+    and the one-shot aires_b200_spgemm call with host buffers.  Wall clock per step (host time =
+    device time: the calls synchronize); every result checked against the resident product."""
+    c_bound = min(blk.n_rows * x.n_cols, blk.nnz() * int(np.diff(np.asarray(x.row_ptr, np.int64)).max(initial=1)))
+    h = HostOperands(ab, torch, blk, x, cap=max(c_bound, 1))
+
+    def spgemm_host():
+        ab._check(L.aires_b200_spgemm(C.byref(h.am), C.byref(h.xm), ab.MODE_FP32, C.byref(h.out)))
+
     for _ in range(max(1, args.warmup)):
-        ab._check(L.aires_b200_run(C.byref(am), C.byref(xm), C.byref(rc), C.byref(out), C.byref(rep)))
-    dev_ms, wall_ms, segs, launches = [], [], 0, 0
+        spgemm_host()
+        h.run(n_buffers=3)
+        h.run(flags=ab.RUN_STREAM_OUT)
+
+    def wall(fn):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        r = None
+        for _ in range(args.steps):
+            r = fn()
+        return (time.perf_counter() - t0) * 1e3 / args.steps, r
+
+    s_ms, _ = wall(spgemm_host)
+    chk_s = compare(*h.result(), *res32)
+    x_ms, xrep = wall(lambda: h.run(n_buffers=3))
+    chk_x = compare(*h.result(), *res32)
+    e_ms, rrep = wall(lambda: h.run(flags=ab.RUN_STREAM_OUT))
+    chk_e = compare(*h.result(), *res32)
+    link = link_bandwidth(dev)
+    b_a = 8 * (blk.n_rows + 1) + 8 * blk.nnz()
+    b_x = 8 * (x.n_rows + 1) + 8 * x.nnz()
+    b_c = 8 * (blk.n_rows + 1) + 8 * int(h.out.nnz)
+    t_alg = max((b_a + b_x) / link["h2d"], b_c / link["d2h"]) / 1e6
+    e_ms_max = max_over_ranks(e_ms, dist, cdev)
+    per_rank_frac = t_alg / e_ms
+    h2d, d2h = int(rrep.h2d_bytes), int(rrep.d2h_bytes)
+    return {"value": round(2.0 * tot_macs / (e_ms_max * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+            "ms_per_step": round(e_ms_max, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "api": "aires_b200_run (run_aires, streamed output), pinned host A/X/C (u64 ptr, u32 idx, fp32 val), "
+                   "wall clock", "segments": int(rrep.segments), "device_ms": round(rrep.total_ms, 3),
+            "checked": chk_e["checked"], "check": chk_e,
+            "roofline": {"bound": "host-link (full duplex, algorithmic bytes)",
+                         "link_gbs": {k: round(v, 2) for k, v in link.items()}, "t_roof_ms": round(t_alg, 3),
+                         "frac": round(per_rank_frac, 4),
+                         "frac_max_over_ranks": round(t_alg / e_ms_max, 4) if dist else None,
+                         "basis": "max((B_A+B_X)/measured pinned H2D, B_C/measured pinned D2H); B = 8(rows+1)+8nnz",
+                         "bytes_moved_over_algorithmic": round((h2d + d2h) / (b_a + b_x + b_c), 4)},
+            "exact_protocol": {"api": "aires_b200_run without streamed output (sizing pass over A's columns, "
+                                      "exact allocation, then the tiles)", "ms_per_step": round(x_ms, 3),
+                               "value": round(2.0 * tot_macs / (x_ms * 1e-3) / 1e9, 3),
+                               "device_ms": round(xrep.total_ms, 3), "segments": int(xrep.segments),
+                               "checked": chk_x["checked"]},
+            "spgemm_call": {"api": "aires_b200_spgemm with host buffers (one-shot H2D, product, D2H)",
+                            "ms_per_step": round(s_ms, 3), "value": round(2.0 * tot_macs / (s_ms * 1e-3) / 1e9, 3),
+                            "checked": chk_s["checked"]}}
+
+
+def ooc_one(args, dev, ab, torch, g, x, frac, label, ref=None, maxmemory=False, link=None):
+    """One capped out-of-core run: budget = frac x (B_A + B_X + B_C) at device widths; timed by the
+    run's own CUDA events (first H2D to last D2H), median of steps; the result is compared with the
+    resident product (ref) outside the timed region."""
+    h = HostOperands(ab, torch, g, x)
+    rep0 = h.run(budget=0, c_aware=1, n_buffers=2)  # sizes C (nnz is only known after one run)
+    nnz_c, macs = int(rep0.c_nnz), int(rep0.flops)
+    b_a = 8 * (g.n_rows + 1) + 8 * g.nnz()
+    b_x = 8 * (x.n_rows + 1) + 8 * x.nnz()
+    b_c = 8 * (g.n_rows + 1) + 8 * nnz_c
+    budget = int(frac * (b_a + b_x + b_c))
+    for _ in range(max(1, args.warmup)):
+        rep = h.run(budget=budget, c_aware=1, n_buffers=args.ooc_buffers)
+    dev_ms, wall_ms, launches = [], [], 0
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        ab._check(L.aires_b200_run(C.byref(am), C.byref(xm), C.byref(rc), C.byref(out), C.byref(rep)))
+        rep = h.run(budget=budget, c_aware=1, n_buffers=args.ooc_buffers)
         wall_ms.append((time.perf_counter() - t0) * 1e3)
         dev_ms.append(rep.total_ms)
-        segs = int(rep.segments)
-        launches += L.aires_b200_last_launches()
-    h2d_b, d2h_b = int(rep.h2d_bytes), int(rep.d2h_bytes)
-    # the paper's baseline on the same budget: MaxMemory (fixed byte tiles, split rows' fragments
-    # returned to the host and re-sent; scheduler.hpp:174-293), same ring and streams
-    mm = None
-    try:
-        rcm = ab._RunConfig(budget, ab.MODE_FP32, 2, args.ooc_buffers, 0)
-        repm = ab._RunReport()
-        ab._check(L.aires_b200_run(C.byref(am), C.byref(xm), C.byref(rcm), C.byref(out), C.byref(repm)))
-        mms = []
-        for _ in range(max(1, args.steps // 2)):
-            ab._check(L.aires_b200_run(C.byref(am), C.byref(xm), C.byref(rcm), C.byref(out), C.byref(repm)))
-            mms.append(repm.total_ms)
-        mm = {"ms": round(float(np.median(mms)), 3), "segments": int(repm.segments), "h2d_bytes": int(repm.h2d_bytes),
-              "d2h_bytes": int(repm.d2h_bytes), "merge_bytes": int(repm.merge_bytes),
-              "aires_speedup": round(float(np.median(mms)) / float(np.median(dev_ms)), 3)}
-    except Exception as e:  # the baseline may not fit where AIRES does (the paper's point)
-        mm = {"failed": str(e)[:200]}
-    bw = link_bandwidth(dev)
+        launches += ab.lib().aires_b200_last_launches()
+    chk = compare(*h.result(), *ref) if ref is not None else {"checked": None}
+    if ref is not None:
+        chk["nnz_equal"] = int(h.out.nnz) == len(ref[1])
+    bw = link or link_bandwidth(dev)
     ms = float(np.median(dev_ms))
-    t_roof = (b_a + b_x + b_c) / (bw["h2d"] * 1e9) * 1e3
-    t_duplex = max(h2d_b / (bw["h2d"] * 1e9), d2h_b / (bw["d2h"] * 1e9)) * 1e3
-    return {
-        "workload": cfg["workload"] + f", device budget {args.ooc_frac:.3g} x (B_A+B_X+B_C) = {budget / 1e6:.1f} MB",
-        "metric": "A·X latency (ms) and GFLOP/s, out-of-core", "ms": round(ms, 3),
-        "gflops": round(2.0 * macs / (ms * 1e-3) / 1e9, 3), "wall_ms": round(float(np.median(wall_ms)), 3),
-        "segments": segs, "n_buffers": args.ooc_buffers, "nnz_a": g.nnz(), "nnz_x": x.nnz(), "nnz_c": nnz_c,
-        "macs": macs, "h2d_bytes": h2d_b, "d2h_bytes": d2h_b, "gpu_launches_per_run": launches // args.steps,
-        "phase_ms": {"phase1": round(rep.phase1_ms, 3), "phase2": round(rep.phase2_ms, 3),
-                     "phase3": round(rep.phase3_ms, 3)},
-        "roofline": {"bound": "host-link", "achieved": round((b_a + b_x + b_c) / (ms * 1e-3) / 1e9, 2),
-                     "peak": round(bw["h2d"], 2), "unit": "GB/s", "frac": round(t_roof / ms, 4),
-                     "frac_full_duplex": round(t_duplex / ms, 4), "link_gbs": {k: round(v, 2) for k, v in bw.items()},
-                     "basis": "(B_A+B_X+B_C) / measured pinned H2D GB/s; full duplex: max(H2D bytes/H2D, D2H bytes/D2H)"},
-        "storage": "pinned host memory (GPUDirect Storage not used: operands arrive through the host API)",
-        "maxmemory_baseline": mm,
-    }
+    h2d_b, d2h_b = int(rep.h2d_bytes), int(rep.d2h_bytes)
+    t_literal = (b_a + b_x + b_c) / (bw["h2d"] * 1e9) * 1e3
+    t_duplex_alg = max((b_a + b_x) / (bw["h2d"] * 1e9), b_c / (bw["d2h"] * 1e9)) * 1e3
+    out = {"label": label, "budget_frac": frac, "budget_bytes": budget, "ms": round(ms, 3),
+           "gflops": round(2.0 * macs / (ms * 1e-3) / 1e9, 3), "wall_ms": round(float(np.median(wall_ms)), 3),
+           "segments": int(rep.segments), "n_buffers": args.ooc_buffers, "nnz_c": nnz_c, "macs": macs,
+           "h2d_bytes": h2d_b, "d2h_bytes": d2h_b, "algorithmic_bytes": {"A": b_a, "X": b_x, "C": b_c},
+           "h2d_over_algorithmic": round(h2d_b / (b_a + b_x), 4),
+           "gpu_launches_per_run": launches // max(1, args.steps),
+           "phase_ms": {"phase1": round(rep.phase1_ms, 3), "phase2": round(rep.phase2_ms, 3),
+                        "phase3": round(rep.phase3_ms, 3)},
+           "roofline": {"bound": "host-link", "frac": round(t_duplex_alg / ms, 4),
+                        "basis": "full duplex, algorithmic bytes: max((B_A+B_X)/H2D, B_C/D2H), measured pinned "
+                                 "GB/s; B = 8(rows+1)+8nnz",
+                        "t_roof_ms": round(t_duplex_alg, 3),
+                        "frac_literal": round(t_literal / ms, 4),
+                        "literal_basis": "(B_A+B_X+B_C)/H2D (north_star wording; charges C's D2H to H2D)",
+                        "link_gbs": {k: round(v, 2) for k, v in bw.items()}},
+           "checked": chk["checked"], "check": chk}
+    if maxmemory:
+        try:
+            mms = []
+            h.run(budget=budget, c_aware=2, n_buffers=args.ooc_buffers)
+            for _ in range(max(1, args.steps // 2)):
+                repm = h.run(budget=budget, c_aware=2, n_buffers=args.ooc_buffers)
+                mms.append(repm.total_ms)
+            chm = compare(*h.result(), *ref) if ref is not None else {"checked": None}
+            out["maxmemory_baseline"] = {"ms": round(float(np.median(mms)), 3), "segments": int(repm.segments),
+                                         "h2d_bytes": int(repm.h2d_bytes), "d2h_bytes": int(repm.d2h_bytes),
+                                         "merge_bytes": int(repm.merge_bytes),
+                                         "aires_speedup": round(float(np.median(mms)) / ms, 3),
+                                         "checked": chm["checked"]}
+        except Exception as e:  # the baseline may not fit where AIRES does (the paper's point)
+            out["maxmemory_baseline"] = {"failed": str(e)[:200]}
+    return out
+
+
+def resident_reference(ab, torch, dev, g, x):
+    p = DeviceProduct(ab, torch, dev, g, x, ab.MODE_FP32)
+    p.step()
+    r = p.result_host()
+    p.free()
+    torch.cuda.empty_cache()
+    return r
+
+
+def out_of_core_legs(args, dev, L, ab, torch, g2, x2, res2, rank, world, dist, cdev):
+    """cfg3 (ogbn-products shape) capped at {0.5, 0.25, 0.125} x (B_A+B_X+B_C) -- the Table III-style
+    sweep -- with the MaxMemory baseline beside the 25% run, plus the Reddit shape
+    (cfg2) capped at 25%: A and X in pinned host memory, C drained tile by tile.  Every run is
+    checked against the resident product.  N>1: each rank runs its MAC-balanced cfg3 row block."""
+    from paper_2507_02006_b200 import shard
+    torch.cuda.empty_cache()
+    link = link_bandwidth(dev)
+    g3, st3, x3 = make_inputs(CONFIGS["cfg3"])
+    if world > 1:
+        cuts = shard.row_shards(g3.row_ptr, world, work=row_macs(g3, x3))
+        g3 = block_of(g3, int(cuts[rank]), int(cuts[rank + 1]))
+    ref3 = resident_reference(ab, torch, dev, g3, x3)
+    fracs = [float(f) for f in args.ooc_fracs.split(",")] if world == 1 else [0.25]
+    runs = [ooc_one(args, dev, ab, torch, g3, x3, f, f"cfg3 @{f:g}", ref3, maxmemory=(f == 0.25), link=link)
+            for f in fracs]
+    if g2 is not None and not args.skip_ooc_reddit:
+        runs.append(ooc_one(args, dev, ab, torch, g2, x2, 0.25, "cfg2 (Reddit shape) @0.25", res2, link=link))
+    out = {"metric": "A·X latency (ms) and GFLOP/s, out-of-core (device budget capped)",
+           "workload": CONFIGS["cfg3"]["workload"] + "; and " + CONFIGS["cfg2"]["workload"].split(",")[0],
+           "storage": "pinned host memory (GPUDirect Storage not used: operands arrive through the host API)",
+           "runs": runs, "checked": all(r["checked"] for r in runs)}
+    if world > 1:
+        out["ms_max_over_ranks"] = max_over_ranks(runs[0]["ms"], dist, cdev)
+        out["per_rank_link_frac"] = runs[0]["roofline"]["frac"]
+    return out
 
 
 class DevOut:
@@ -623,7 +766,6 @@ def gcn_leg(args, dev, L, ab, torch):
     xm = ab._Matrix(n, x.n_cols, ab.CSR, ab.DEVICE, 4, 4, tX[0].data_ptr(), tX[1].data_ptr(), tX[2].data_ptr(), x.nnz())
     o_t, o_c1, o_h1, o_c2, o_h2 = (DevOut(ab, torch, dev, torch.int32, torch.float32) for _ in range(5))
     stream = torch.cuda.ExternalStream(L.aires_b200_stream(), device=dev)
-    stats = {}
 
     def forward(record=None, fused=True):
         """layer 2 (H1 ~50% dense) runs the fused dense-H aggregate+combine unless fused=False"""
@@ -686,78 +828,110 @@ def gcn_leg(args, dev, L, ab, torch):
             "layers_per_s": round(2.0 / (med["total"] * 1e-3), 2)}
 
 
+# ---------------------------------------------------------------------------------------------
+# the reference's CPU path
+# ---------------------------------------------------------------------------------------------
+
 def sample_rows(n: int, count: int, seed: int = 11) -> np.ndarray:
     rng = np.random.default_rng(seed)
     return np.sort(rng.choice(n, size=min(count, n), replace=False)).astype(np.uint64)
 
 
-def ref_sample_run(g, x, seconds: float, threads: int):
-    """Reference spgemm_block (oracle/_ref) on a random row sample sized to ~`seconds` of work.
-    Returns (gflops, sample description, kind, rows, secs)."""
+def ref_sample_run(g, x, seconds: float, threads: int, seed: int = 11):
+    """Reference spgemm_block (oracle/_ref, unmodified headers) on a random row sample sized to ~`seconds`
+    of work, all `threads` host threads.  Returns dict(gflops, rows, kind, secs, macs, nnz, hash)."""
     from oracle import pyoracle as po
-    a_ptr, a_idx, a_val = g.row_ptr, g.col_idx.astype(np.uint64), g.values.astype(np.float64)
-    cp, ri, cv = po.csr_to_csc(x.n_rows, x.n_cols, x.row_ptr, x.col_idx.astype(np.uint64), x.values)
+    a_ptr, a_idx, a_val = g.row_ptr, np.asarray(g.col_idx, np.uint64), np.asarray(g.values, np.float64)
+    cp, ri, cv = po.csr_to_csc(x.n_rows, x.n_cols, x.row_ptr, np.asarray(x.col_idx, np.uint64), x.values)
     kind = "reference" if po.ref_available() else "port"
     if kind == "reference":
         def run(rows):
-            s, macs, z, _ = po.ref_rows_timed(a_ptr, a_idx, a_val, g.n_cols, rows, cp, ri, cv, x.n_rows, x.n_cols,
-                                              threads)
-            return s, macs
+            return po.ref_rows_timed(a_ptr, a_idx, a_val, g.n_cols, rows, cp, ri, cv, x.n_rows, x.n_cols, threads)
     else:  # oracle port of spgemm_block (inner product), one thread
         def run(rows):
             t0 = time.perf_counter()
-            macs = 0
+            macs = z = 0
             for r in rows:
-                rc, _, m = po.spgemm_inner(a_ptr[r:r + 2], a_idx, a_val, 1, g.n_cols, x.n_rows, x.n_cols, cp, ri, cv)
+                rc, c, m = po.spgemm_inner(a_ptr[r:r + 2], a_idx, a_val, 1, g.n_cols, x.n_rows, x.n_cols, cp, ri, cv)
                 macs += m
-            return time.perf_counter() - t0, macs
+                z += len(c[1])
+            return time.perf_counter() - t0, macs, z, None
     probe = sample_rows(g.n_rows, max(threads * 4, 16), seed=5)
-    s, _ = run(probe)
+    s, _, _, _ = run(probe)
     per_row = s / len(probe)
     count = int(max(threads * 4, min(g.n_rows, seconds / max(per_row, 1e-9))))
-    rows = sample_rows(g.n_rows, count)
-    s, macs = run(rows)
-    return 2.0 * macs / s / 1e9, rows, kind, s
+    rows = sample_rows(g.n_rows, count, seed)
+    s, macs, z, h = run(rows)
+    return {"gflops": 2.0 * macs / s / 1e9, "rows": rows, "kind": kind, "secs": s, "macs": macs, "nnz": z, "hash": h}
 
 
-def cpu_baseline(g, x, seconds: float):
+def cpu_baseline(g, x, seconds: float, res32, res64):
+    """The reference on a row sample of the same Ã·X (reported baseline), and its live rows checked
+    against the B200 results: nnz per sampled row vs the fp32 product, and the FNV row hash (row id,
+    columns, fp64 value bits) vs the FP64_EXACT product -- bit-identical rows."""
+    from oracle import pyoracle as po
     threads = len(os.sched_getaffinity(0))
     try:
-        gf, rows, kind, s = ref_sample_run(g, x, seconds, threads)
+        r = ref_sample_run(g, x, seconds, threads)
     except Exception as e:  # baseline is reported, never fatal
         return {"value": None, "unit": "GFLOP/s", "cores": threads, "kind": "reference", "sample": f"failed: {e}"}
-    return {"value": round(gf, 6), "unit": "GFLOP/s", "cores": threads if kind == "reference" else 1, "kind": kind,
-            "sample": f"{len(rows)} uniformly sampled rows of the same Ã·X ({s:.1f} s), reference spgemm_block "
-                      f"(inner product, spgemm.hpp:60-132) unmodified, -O3 no -march; GFLOP/s = 2*MACs/t"}
+    rows = r["rows"].astype(np.int64)
+    p32 = res32[0].astype(np.int64)
+    nnz_gpu = int(np.sum(p32[rows + 1] - p32[rows]))
+    check = {"rows": len(rows), "nnz_ref": int(r["nnz"]), "nnz_b200_fp32": nnz_gpu, "nnz_equal": nnz_gpu == int(r["nnz"])}
+    if res64 is not None and r["hash"] is not None:
+        h64 = po.rows_hash(res64[0].view(np.uint64), res64[1].astype(np.uint64), res64[2], r["rows"])
+        check["hash_equal_fp64_exact"] = h64 == int(r["hash"])
+        check["checked"] = bool(check["nnz_equal"] and check["hash_equal_fp64_exact"])
+    else:
+        check["checked"] = check["nnz_equal"]
+    return {"value": round(r["gflops"], 6), "unit": "GFLOP/s", "cores": threads if r["kind"] == "reference" else 1,
+            "kind": r["kind"],
+            "sample": f"{len(rows)} uniformly sampled rows of the same Ã·X ({r['secs']:.1f} s), reference spgemm_block "
+                      f"(inner product, spgemm.hpp:60-132) unmodified, -O3 no -march; GFLOP/s = 2*MACs/t",
+            "reference_rows_vs_b200": check}
 
 
 def run_reference(args, cfg):
-    """--impl reference: the reference's own CPU spgemm_block on the host cores (rank 0 only)."""
+    """--impl reference: the reference's own CPU spgemm_block on the host cores (rank 0 only), on
+    inputs from the oracle's generator restatement (libaires_b200.so is never loaded here)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
-    g, st, x = make_inputs(cfg, 0, 1)
+    g, st, x = make_inputs_ref(cfg)
     per_step = max(2.0, args.cpu_seconds / max(1, args.steps + args.warmup))
-    vals = []
-    kind = "reference"
-    rows_total = 0
+    vals, rows_total, kind, hashes = [], 0, "reference", []
     for i in range(args.warmup + args.steps):
-        gf, rows, kind, s = ref_sample_run(g, x, per_step, threads)
+        r = ref_sample_run(g, x, per_step, threads, seed=11 + i)
+        kind = r["kind"]
         if i >= args.warmup:
-            vals.append(gf)
-            rows_total += len(rows)
+            vals.append(r["gflops"])
+            rows_total += len(r["rows"])
+            hashes.append(r["hash"])
     v = float(np.median(vals))
-    line = {"metric": METRIC, "value": round(v, 6), "unit": "GFLOP/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    line = {"metric": METRIC, "value": round(v, 6), "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (same seeds as the b200 arm)",
-            "config": {"workload": cfg["workload"], "nodes": g.n_rows, "edges": st["nnz_a"], "x_cols": x.n_cols},
-            "impl": "reference",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Chung-Lu power-law Ã, gen_features X; seeds graph 1, relabel 2, X 3)",
+            "config": config_of(cfg, st, g, x), "impl": "reference",
+            "parallelism": f"host threads x{threads} (reference spgemm_block over sampled rows)",
+            "native_libraries_in_repo": sorted({os.path.relpath(p, ROOT) for p in _loaded_libs()
+                                                if os.path.realpath(p).startswith(os.path.realpath(ROOT))}),
             "cpu_baseline": {"value": round(v, 6), "unit": "GFLOP/s", "kind": kind,
                              "cores": threads if kind == "reference" else 1,
                              "sample": f"{rows_total} sampled rows over {args.steps} steps (~{per_step:.0f} s each)"},
             "e2e": {"value": round(v, 6), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _loaded_libs():
+    try:
+        with open("/proc/self/maps") as f:
+            return [ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")]
+    except Exception:
+        return []
 
 
 def main():
@@ -767,15 +941,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
-    ap.add_argument("--mode", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
-    ap.add_argument("--skip-ooc", action="store_true", help="skip the cfg3 out-of-core leg")
+    ap.add_argument("--skip-fp64", action="store_true")
+    ap.add_argument("--skip-ooc", action="store_true", help="skip the out-of-core legs")
+    ap.add_argument("--skip-ooc-reddit", action="store_true", help="skip the capped Reddit-shape run")
     ap.add_argument("--skip-gcn", action="store_true", help="skip the cfg5 2-layer GCN leg")
-    ap.add_argument("--cfg4-shard", action="store_true", help="also run one 1/8 shard of the PPI-scale cfg4 "
-                    "out of core (slow input generation)")
-    ap.add_argument("--ooc-frac", type=float, default=0.25, help="cfg3 device budget / (B_A+B_X+B_C)")
+    ap.add_argument("--ooc-fracs", default="0.5,0.25", help="cfg3 device budgets / (B_A+B_X+B_C)")
     ap.add_argument("--ooc-buffers", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -529,3 +529,275 @@ int ao_combine(uint64_t rows, uint64_t x_cols, const uint64_t* row_ptr, const ui
   free(acc);
   return AO_OK;
 }
+
+/* ---- benchmark inputs for the reference arm (bench.py --impl reference) ----------------------
+ * A restatement of the B200 library's Chung-Lu generator (paper_2507_02006_b200/csrc/ab2_synth.cpp,
+ * aires_b200_synth_graph; BASELINE.md §4 / SURVEY.md §8(d) "Synthetic inputs"), so the reference
+ * arm builds the identical Ã without loading libaires_b200.so.  Same arithmetic, draw for draw:
+ * splitmix64 hashes of the pair index, the continuous power law on [0, n) with density
+ * (x + i0)^-alpha, i0 bisected on a log scale so the heaviest node's expected degree is the cap,
+ * the std::mt19937_64 Fisher-Yates relabel, up to four sampling rounds rescaling the pair count,
+ * and normalize_adjacency's (gcn.hpp:29-72) D^-1/2 (A+I) D^-1/2 values.  Rows are sorted and
+ * de-duplicated, so the multi-threaded counting pass is deterministic.  Pinned byte for byte
+ * against aires_b200_synth_graph by tests/test_oracle.py::test_synth_graph_restatement. */
+static uint64_t sg_splitmix(uint64_t x) {
+  uint64_t z = x + 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+static double sg_u01(uint64_t h) { return (double)(h >> 11) * 0x1.0p-53; }
+
+typedef struct {
+  double alpha, i0, a1, lo, hi;
+  uint64_t n;
+} sg_plaw;
+
+static sg_plaw sg_plaw_make(uint64_t n, double alpha, double i0) {
+  sg_plaw p;
+  p.alpha = alpha;
+  p.i0 = i0;
+  p.n = n;
+  p.a1 = 1.0 - alpha;
+  p.lo = pow(i0, p.a1);
+  p.hi = pow((double)n + i0, p.a1);
+  return p;
+}
+static uint64_t sg_plaw_sample(const sg_plaw* p, double u) {
+  double t = p->lo + u * (p->hi - p->lo);
+  double x = pow(t, 1.0 / p->a1) - p->i0;
+  if (!(x >= 0)) x = 0;
+  uint64_t i = (uint64_t)x;
+  return i >= p->n ? p->n - 1 : i;
+}
+static double sg_plaw_mass(const sg_plaw* p, double a, double b) {
+  return (pow(b + p->i0, p->a1) - pow(a + p->i0, p->a1)) / (p->hi - p->lo);
+}
+static double sg_top(uint64_t n, double alpha, double pairs, double i0) {
+  sg_plaw p = sg_plaw_make(n, alpha, i0);
+  return 2.0 * pairs * sg_plaw_mass(&p, 0.0, 1.0);
+}
+static double sg_solve_i0(uint64_t n, double alpha, double pairs, double cap) {
+  if (sg_top(n, alpha, pairs, 1e-9) <= cap) return 1e-9;
+  double lo = 1e-9, hi = (double)n;
+  for (int it = 0; it < 200; it++) {
+    double mid = sqrt(lo * hi);
+    if (sg_top(n, alpha, pairs, mid) > cap)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return hi;
+}
+
+typedef struct {
+  const sg_plaw* pl;
+  const uint32_t* perm;
+  uint64_t seed, p0, p1, r0, r1;
+  uint32_t* deg;      /* atomic adds */
+  uint64_t* cur;      /* atomic cursors */
+  uint32_t* raw;
+  const uint64_t* off;
+  uint64_t* cnt;
+  int phase;
+} sg_job;
+
+static void sg_pair(const sg_job* j, uint64_t p, uint32_t* u, uint32_t* v) {
+  uint64_t h1 = sg_splitmix(j->seed * 0x100000001b3ULL + 2 * p);
+  uint64_t h2 = sg_splitmix(j->seed * 0x100000001b3ULL + 2 * p + 1);
+  uint64_t a = sg_plaw_sample(j->pl, sg_u01(h1)), b = sg_plaw_sample(j->pl, sg_u01(h2));
+  *u = j->perm ? j->perm[a] : (uint32_t)a;
+  *v = j->perm ? j->perm[b] : (uint32_t)b;
+}
+
+static int cmp_u32(const void* a, const void* b) {
+  uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+static void* sg_run(void* arg) {
+  sg_job* j = (sg_job*)arg;
+  if (j->phase == 0) {
+    for (uint64_t p = j->p0; p < j->p1; p++) {
+      uint32_t u, v;
+      sg_pair(j, p, &u, &v);
+      if (u == v) continue;
+      __atomic_fetch_add(&j->deg[u], 1u, __ATOMIC_RELAXED);
+      __atomic_fetch_add(&j->deg[v], 1u, __ATOMIC_RELAXED);
+    }
+  } else if (j->phase == 1) {
+    for (uint64_t p = j->p0; p < j->p1; p++) {
+      uint32_t u, v;
+      sg_pair(j, p, &u, &v);
+      if (u == v) continue;
+      j->raw[__atomic_fetch_add(&j->cur[u], 1ull, __ATOMIC_RELAXED)] = v;
+      j->raw[__atomic_fetch_add(&j->cur[v], 1ull, __ATOMIC_RELAXED)] = u;
+    }
+  } else {
+    for (uint64_t r = j->r0; r < j->r1; r++) { /* sort + unique per row */
+      uint32_t* s = j->raw + j->off[r];
+      uint64_t m = j->off[r + 1] - j->off[r], w = 0;
+      qsort(s, m, sizeof(uint32_t), cmp_u32);
+      for (uint64_t i = 0; i < m; i++)
+        if (w == 0 || s[i] != s[w - 1]) s[w++] = s[i];
+      j->cnt[r + 1] = w;
+    }
+  }
+  return NULL;
+}
+
+static void sg_parallel(sg_job* proto, int phase, uint64_t n_items, int threads) {
+  if (threads < 1) threads = 1;
+  if (n_items < 4096) threads = 1;
+  sg_job* jobs = (sg_job*)xcalloc((size_t)threads, sizeof(sg_job));
+  pthread_t* th = (pthread_t*)xcalloc((size_t)threads, sizeof(pthread_t));
+  for (int t = 0; t < threads; t++) {
+    jobs[t] = *proto;
+    jobs[t].phase = phase;
+    uint64_t a = n_items * (uint64_t)t / (uint64_t)threads, b = n_items * (uint64_t)(t + 1) / (uint64_t)threads;
+    jobs[t].p0 = jobs[t].r0 = a;
+    jobs[t].p1 = jobs[t].r1 = b;
+    if (threads == 1)
+      sg_run(&jobs[t]);
+    else
+      pthread_create(&th[t], NULL, sg_run, &jobs[t]);
+  }
+  if (threads > 1)
+    for (int t = 0; t < threads; t++) pthread_join(th[t], NULL);
+  free(jobs);
+  free(th);
+}
+
+/* One sampling round: M pairs -> symmetric, loop-free, duplicate-free CSR (ptr n+1, col u32). */
+static void sg_build(uint64_t n, uint64_t M, const sg_plaw* pl, const uint32_t* perm, uint64_t seed,
+                     int threads, uint64_t** ptr_out, uint32_t** col_out) {
+  sg_job j;
+  memset(&j, 0, sizeof j);
+  j.pl = pl;
+  j.perm = perm;
+  j.seed = seed;
+  j.deg = (uint32_t*)xcalloc(n, sizeof(uint32_t));
+  sg_parallel(&j, 0, M, threads);
+  uint64_t* off = (uint64_t*)xcalloc(n + 1, sizeof(uint64_t));
+  for (uint64_t i = 0; i < n; i++) off[i + 1] = off[i] + j.deg[i];
+  free(j.deg);
+  j.deg = NULL;
+  j.raw = (uint32_t*)xmalloc(off[n] * sizeof(uint32_t));
+  j.cur = (uint64_t*)xmalloc(n * sizeof(uint64_t));
+  memcpy(j.cur, off, n * sizeof(uint64_t));
+  sg_parallel(&j, 1, M, threads);
+  free(j.cur);
+  j.off = off;
+  j.cnt = (uint64_t*)xcalloc(n + 1, sizeof(uint64_t));
+  sg_parallel(&j, 2, n, threads);
+  uint64_t* ptr = j.cnt; /* cnt[r+1] -> prefix */
+  for (uint64_t i = 0; i < n; i++) ptr[i + 1] += ptr[i];
+  uint32_t* col = (uint32_t*)xmalloc((ptr[n] ? ptr[n] : 1) * sizeof(uint32_t));
+  for (uint64_t r = 0; r < n; r++) memcpy(col + ptr[r], j.raw + off[r], (ptr[r + 1] - ptr[r]) * sizeof(uint32_t));
+  free(j.raw);
+  free(off);
+  *ptr_out = ptr;
+  *col_out = col;
+}
+
+int ao_synth_graph(uint64_t n, uint64_t target_nnz, double alpha, uint64_t degree_cap, uint64_t seed,
+                   uint64_t relabel_seed, int relabel, int normalize, int threads, ao_csr* out, double* stats) {
+  if (n == 0 || n >= (1ull << 32) || !(alpha > 0.0 && alpha < 1.0)) return AO_INDEX_OUT_OF_RANGE;
+  if (threads < 1) threads = 1;
+  uint32_t* perm = NULL;
+  if (relabel) {
+    perm = (uint32_t*)xmalloc(n * sizeof(uint32_t));
+    for (uint64_t i = 0; i < n; i++) perm[i] = (uint32_t)i;
+    mt64* rng = (mt64*)xmalloc(sizeof(mt64));
+    mt64_seed(rng, relabel_seed);
+    for (uint64_t i = n - 1; i > 0; i--) {
+      uint64_t k = mt64_next(rng) % (i + 1);
+      uint32_t t = perm[i];
+      perm[i] = perm[k];
+      perm[k] = t;
+    }
+    free(rng);
+  }
+  double pairs = (double)target_nnz / 2.0;
+  if (pairs < 1.0) pairs = 1.0;
+  double cap = degree_cap ? (double)degree_cap : (double)n;
+  uint64_t* gp = NULL;
+  uint32_t* gc = NULL;
+  int rounds = 0;
+  double i0 = 0;
+  for (; rounds < 4; rounds++) {
+    i0 = sg_solve_i0(n, alpha, pairs, cap);
+    sg_plaw pl = sg_plaw_make(n, alpha, i0);
+    free(gp);
+    free(gc);
+    sg_build(n, (uint64_t)pairs, &pl, perm, seed, threads, &gp, &gc);
+    double got = (double)gp[n];
+    if (target_nnz == 0 || got <= 0) break;
+    double ratio = (double)target_nnz / got;
+    if (fabs(ratio - 1.0) < 0.005) break;
+    pairs *= ratio * (ratio > 1 ? 1.02 : 1.0);
+  }
+  free(perm);
+  const uint64_t nnz_a = gp[n];
+  uint64_t maxdeg = 0;
+  for (uint64_t r = 0; r < n; r++)
+    if (gp[r + 1] - gp[r] > maxdeg) maxdeg = gp[r + 1] - gp[r];
+  const uint64_t nnz = normalize ? nnz_a + n : nnz_a;
+  out->n_rows = n;
+  out->n_cols = n;
+  out->nnz = nnz;
+  out->ptr = (uint64_t*)xmalloc((n + 1) * sizeof(uint64_t));
+  out->idx = (uint64_t*)xmalloc(nnz * sizeof(uint64_t));
+  out->val = (double*)xmalloc(nnz * sizeof(double));
+  out->ptr[0] = 0;
+  for (uint64_t r = 0; r < n; r++) out->ptr[r + 1] = out->ptr[r] + (gp[r + 1] - gp[r]) + (normalize ? 1 : 0);
+  /* gcn.hpp:29-72 with unit weights and no loops: d_i = deg_i + 1, diagonal in column order */
+  for (uint64_t r = 0; r < n; r++) {
+    uint64_t w = out->ptr[r];
+    const double dr = (double)(gp[r + 1] - gp[r] + 1);
+    int placed = !normalize;
+    for (uint64_t k = gp[r]; k <= gp[r + 1]; k++) {
+      uint64_t c = k < gp[r + 1] ? gc[k] : UINT64_MAX;
+      if (!placed && c > r) {
+        out->idx[w] = r;
+        out->val[w++] = 1.0 / sqrt(dr * dr);
+        placed = 1;
+      }
+      if (k == gp[r + 1]) break;
+      out->idx[w] = c;
+      out->val[w++] = normalize ? 1.0 / sqrt(dr * (double)(gp[c + 1] - gp[c] + 1)) : 1.0;
+    }
+  }
+  if (stats) {
+    stats[0] = (double)nnz_a;
+    stats[1] = (double)maxdeg;
+    stats[2] = (double)nnz_a / (double)n;
+    stats[3] = (double)(rounds + 1);
+    stats[4] = 0.0;
+    stats[5] = i0;
+    stats[6] = stats[7] = 0.0;
+  }
+  free(gp);
+  free(gc);
+  return AO_OK;
+}
+
+/* Sum over rows[] of FNV-1a 64 (serialize.hpp:22-48) of (row id, col_idx..., value bits...) --
+ * the row hash oracle/ref_shim.cpp:ref_spgemm_rows_timed reports for the reference's sampled rows,
+ * computed here over any CSR (e.g. the B200 product read back) for the same rows. */
+uint64_t ao_rows_hash(const uint64_t* row_ptr, const uint64_t* col_idx, const double* values,
+                      const uint64_t* rows, uint64_t n_sample) {
+  uint64_t tot = 0;
+  for (uint64_t i = 0; i < n_sample; i++) {
+    uint64_t r = rows[i], h = 0xcbf29ce484222325ULL;
+    h = fnv_u64(h, r);
+    for (uint64_t p = row_ptr[r]; p < row_ptr[r + 1]; p++) h = fnv_u64(h, col_idx[p]);
+    for (uint64_t p = row_ptr[r]; p < row_ptr[r + 1]; p++) {
+      uint64_t b;
+      memcpy(&b, &values[p], 8);
+      h = fnv_u64(h, b);
+    }
+    tot += h;
+  }
+  return tot;
+}

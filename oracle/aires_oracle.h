@@ -118,6 +118,17 @@ int ao_gen_weights(uint64_t in_dim, uint64_t out_dim, uint64_t seed, double* out
 int ao_combine(uint64_t rows, uint64_t x_cols, const uint64_t* row_ptr, const uint64_t* col_idx,
                const double* values, const double* w, uint64_t w_rows, uint64_t w_cols, ao_csr* out);
 
+/* Benchmark inputs for the reference arm: restatement of aires_b200_synth_graph
+ * (paper_2507_02006_b200/csrc/ab2_synth.cpp), byte-identical output at API widths (u64/f64).
+ * stats (8 doubles, may be NULL): nnz(A) before self-loops, max degree, mean degree, rounds, 0, i0. */
+int ao_synth_graph(uint64_t n, uint64_t target_nnz, double alpha, uint64_t degree_cap, uint64_t seed,
+                   uint64_t relabel_seed, int relabel, int normalize, int threads, ao_csr* out, double* stats);
+
+/* Sum over rows[] of FNV-1a 64 of (row id, columns, value bits): the row hash the reference arm's
+ * ref_spgemm_rows_timed (oracle/ref_shim.cpp) reports for its sampled rows. */
+uint64_t ao_rows_hash(const uint64_t* row_ptr, const uint64_t* col_idx, const double* values,
+                      const uint64_t* rows, uint64_t n_sample);
+
 #ifdef __cplusplus
 }
 #endif

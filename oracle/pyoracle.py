@@ -63,6 +63,10 @@ def oracle() -> C.CDLL:
         L.ao_gen_weights.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, F64P]
         L.ao_combine.argtypes = [C.c_uint64, C.c_uint64, U64P, U64P, F64P, F64P, C.c_uint64, C.c_uint64,
                                  C.POINTER(AoCsr)]
+        L.ao_synth_graph.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64, C.c_uint64, C.c_uint64,
+                                     C.c_int, C.c_int, C.c_int, C.POINTER(AoCsr), C.POINTER(C.c_double)]
+        L.ao_rows_hash.restype = C.c_uint64
+        L.ao_rows_hash.argtypes = [U64P, U64P, F64P, U64P, C.c_uint64]
         _oracle = L
     return _oracle
 
@@ -329,3 +333,27 @@ def ref_write_segments(path, n_rows, n_cols, row_ptr, col_idx, values, m_a, I=8,
     """The reference's robw_partition + write_segments to `path` (serialize.hpp:148-174)."""
     rp, ci, va = _u64(row_ptr), _u64(col_idx), _f64(values)
     return int(ref().ref_write_segments(path.encode(), n_rows, n_cols, _p64(rp), _p64(ci), _pf(va), m_a, I, V))
+
+
+def synth_graph(n, target_nnz, alpha=0.75, degree_cap=20000, seed=1, relabel_seed=2, relabel=True, normalize=True,
+                threads=0):
+    """Restatement of the B200 library's Chung-Lu generator (reference-arm inputs, no libaires_b200.so).
+    Returns ((ptr, idx, val) at u64/u64/f64, stats dict) -- the same arrays and stats keys as
+    paper_2507_02006_b200.synth_graph."""
+    L = oracle()
+    m = AoCsr()
+    st = (C.c_double * 8)()
+    th = threads if threads > 0 else len(os.sched_getaffinity(0))
+    rc = L.ao_synth_graph(n, target_nnz, alpha, degree_cap, seed, relabel_seed, int(relabel), int(normalize), th,
+                          C.byref(m), st)
+    if rc:
+        raise RuntimeError(f"ao_synth_graph failed ({rc})")
+    arrs = _take(m, n + 1, L.ao_free)
+    stats = dict(nnz_a=int(st[0]), max_degree=int(st[1]), mean_degree=st[2], rounds=int(st[3]), i0=st[5])
+    return arrs, stats
+
+
+def rows_hash(row_ptr, col_idx, values, rows) -> int:
+    """Sum of per-row FNV-1a 64 over `rows` (matches ref_rows_timed's hash for the same rows)."""
+    rp, ci, va, rs = _u64(row_ptr), _u64(col_idx), _f64(values), _u64(rows)
+    return int(oracle().ao_rows_hash(_p64(rp), _p64(ci), _pf(va), _p64(rs), rs.shape[0]))

@@ -183,3 +183,37 @@ def test_reference_unit_suite_passes(unit):
         pytest.skip("reference unit binaries not built (no /root/reference)")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("args", [(20_000, 200_000, 0.75, 2_000, 1, 2, True, True),
+                                  (5_000, 40_000, 0.6, 500, 7, 3, False, True),
+                                  (30_000, 300_000, 0.9, 3_000, 2, 5, True, False),
+                                  (100_000, 1_000_000, 0.75, 20_000, 1, 2, True, True)])
+def test_synth_graph_restatement(args):
+    """The reference arm's input generator (ao_synth_graph) is byte-identical to the B200 library's
+    aires_b200_synth_graph, so `bench.py --impl reference` multiplies the same Ã without loading
+    libaires_b200.so (host code only: no GPU needed)."""
+    import paper_2507_02006_b200 as ab
+    n, nnz, alpha, cap, seed, rseed, relabel, norm = args
+    g, st = ab.synth_graph(n, nnz, alpha=alpha, degree_cap=cap, seed=seed, relabel_seed=rseed, relabel=relabel,
+                           normalize=norm, idx_dtype=np.uint64, val_dtype=np.float64)
+    (p, i, v), st2 = po.synth_graph(n, nnz, alpha, cap, seed, rseed, relabel, norm)
+    assert np.array_equal(g.row_ptr, p) and np.array_equal(g.col_idx, i)
+    assert np.array_equal(bits(g.values), bits(v))
+    assert all(st[k] == st2[k] for k in ("nnz_a", "max_degree", "rounds", "i0"))
+
+
+def test_rows_hash_matches_reference_sampled_rows():
+    """ao_rows_hash over a CSR product equals the hash ref_spgemm_rows_timed reports for the same rows,
+    so the reference's live sampled rows can be compared with any product read back (bench.py)."""
+    if not po.ref_available():
+        pytest.skip("oracle/_ref not built")
+    (ap, ai, av), _ = po.synth_graph(3_000, 30_000, 0.75, 300, 1, 2, True, True)
+    rc, (xp, xi, xv) = po.gen_features(3_000, 64, 90.0, 3)
+    assert rc == 0
+    rc, (cp_, ci_, cv_), macs = po.spgemm_rowwise(ap, ai, av, 3_000, 3_000, 3_000, 64, xp, xi, xv)
+    rows = np.sort(np.random.default_rng(0).choice(3_000, 200, replace=False)).astype(np.uint64)
+    cp, ri, cv = po.csr_to_csc(3_000, 64, xp, xi, xv)
+    _, m, z, h = po.ref_rows_timed(ap, ai, av, 3_000, rows, cp, ri, cv, 3_000, 64, 2)
+    assert h == po.rows_hash(cp_, ci_, cv_, rows)
+    assert z == int(sum(int(cp_[r + 1] - cp_[r]) for r in rows))
