@@ -36,14 +36,16 @@
 #ifndef AB2_NUM_BATCH
 #define AB2_NUM_BATCH 8
 #endif
-#ifndef AB2_NUM_TAB
-#define AB2_NUM_TAB 1  // chunk entries through a per-warp shared table (1) or SHFL (0)
-#endif
+// resident CTAs per SM the register budget is sized for: 128 threads x 6 CTAs -> 80 registers
+// for the fp32 16-entry-slot walk and the fp64 walks (two load buffers in flight), 64 otherwise
 #ifndef AB2_NUM_MINB
-#define AB2_NUM_MINB 4
+#define AB2_NUM_MINB 8
+#endif
+#ifndef AB2_NUM_MINB_WIDE
+#define AB2_NUM_MINB_WIDE 6
 #endif
 #ifndef AB2_NUM_MAXT
-#define AB2_NUM_MAXT 256
+#define AB2_NUM_MAXT 128
 #endif
 
 #include "ab2_kernels.cuh"
@@ -79,34 +81,7 @@ struct Num3Args {
   int64_t cbase;
 };
 
-template <class V>
-__device__ __forceinline__ typename SlotOf<V>::type load_slot(const typename SlotOf<V>::type* __restrict__ slots,
-                                                              uint32_t i) {
-  using S = typename SlotOf<V>::type;
-  S s;
-  if constexpr (sizeof(S) == 8) {
-    const uint2 v = __ldg(reinterpret_cast<const uint2*>(slots) + i);
-    s.col = v.x;
-    s.val = __uint_as_float(v.y);
-  } else {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(slots) + i);
-    s.col = v.x;
-    s.pad = v.y;
-    s.val = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(v.w) << 32) | v.z));
-  }
-  return s;
-}
-
-// ---- the group-strided walk over a contiguous range of A entries -----------
-// Entries [0, n) of ac/av in chunks of 32 (one coalesced load each); chunk c is handled iff
-// c == chunk0 (mod chunk_stride), which lets a CTA's warps interleave over one heavy row.
-// Columns outside [c_lo, c_hi) go to the trash column (the fp64 column-owner split).
-//
-// Zero products (which need the explicit-mark path) are detected per chunk, not per step:
-// a product can only round to zero if |a| * min|x| < 2^-148 (fp32) / 2^-1073 (fp64), or if
-// X stores an exact zero (operand flag XZ: then every product is checked).  MACs come from
-// the per-row length array, one gather per A entry.
-// Per-warp chunk table entry in shared memory: {slot index k*W, row length, a bits}.
+// Per-warp chunk table in shared memory (32 entries of up to 16 bytes: {slot index k*W, a}).
 using ChunkPair = uint4;
 
 // Shared-memory read-modify-write at a 32-bit shared address.
@@ -132,176 +107,19 @@ __device__ __forceinline__ void smem_acc(uint32_t addr, V a, V x) {
     smem_fma(addr, a, x);
 }
 
-// ---- the group-strided walk over a contiguous range of A entries -----------
+// ---- the group-strided walk over a contiguous range of A entries (W-lane slot groups) --------
 // Entries [0, n) of ac/av in chunks of 32 (one coalesced load each); chunk c is handled iff
 // c == chunk0 (mod chunk_stride), which lets a CTA's warps interleave over one heavy row.
-// Columns outside [c_lo, c_hi) go to the trash column (the fp64 column-owner split).
+// Columns outside [c_lo, c_hi) are skipped (the fp64 column-owner split).  The chunk's entries
+// {k*W, a} go to a per-warp shared table once; each step reads its group's entry with one
+// broadcast LDS.  Slots are loaded whole (entries past the row's length hold the trash column
+// and are skipped without touching shared memory); MACs are counted from the real entries.
 //
 // Zero products (which need the explicit-mark path) are detected per chunk, not per step:
 // a product can only round to zero if |a| * min|x| < 2^-148 (fp32) / 2^-1073 (fp64), or if
-// X stores an exact zero (operand flag XZ: then every product is checked).  MACs come from
-// the per-row length array, one gather per A entry.
+// X stores an exact zero (operand flag XZ: then every product is checked).
 template <class V, class IdxT, int W, bool EXACT, bool RANGE, bool XZ>
-__device__ __forceinline__ uint32_t walk_entries(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac,
-                                                 const V* __restrict__ av, uint32_t n, uint32_t chunk0,
-                                                 uint32_t chunk_stride, V* acc, ChunkPair* tab, uint32_t c_lo,
-                                                 uint32_t c_hi, bool& zero) {
-  constexpr int G = 32 / W;
-  constexpr int B = W < AB2_NUM_BATCH ? W : AB2_NUM_BATCH;  // group steps per batch (loads in flight)
-  constexpr uint32_t VS = sizeof(V);
-  const int lane = lane_id(), gid = lane / W, ent = lane % W;
-  const int mlane = gid * W + (W - 1);  // the group's marker lane
-  const uint32_t K = static_cast<uint32_t>(p.x.K);
-  const uint32_t trash = static_cast<uint32_t>(p.x.n_cols);
-  const int32_t* __restrict__ xcol = p.x.col;
-  const V* __restrict__ xval = p.x.val;
-  const uint16_t* __restrict__ xlen = p.xlen;
-  const V tiny = p.tiny;
-  const uint32_t copy_s = static_cast<uint32_t>(__cvta_generic_to_shared(EXACT ? acc : acc + gid * p.stride));
-  const uint32_t tab_s = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
-  uint32_t macs = 0;
-  auto col_of = [&](uint32_t c) -> uint32_t {
-    c &= kSlotColMask;
-    if constexpr (RANGE) c = (c >= c_lo && c < c_hi) ? c : trash;
-    return c;
-  };
-  auto add = [&](uint32_t c, V a, V x) {
-    if constexpr (XZ) {
-      if constexpr (EXACT)
-        zero |= __dmul_rn(a, x) == 0.0;
-      else
-        zero |= a * x == 0.f;
-    }
-    smem_acc<V>(copy_s + c * VS, a, x);
-  };
-  // Two-deep prefetch: the (k, a) loads of chunk c+2 (HBM stream) and the X row-length gather of
-  // chunk c+1 are in flight while chunk c runs (without it the A load and the length gather were
-  // ~25% of the stall samples, profiles/r01a).
-  const uint32_t step = chunk_stride * 32;
-  auto load_ka = [&](uint32_t bb, uint32_t& k, V& a) {
-    const uint32_t i = bb + lane;
-    k = K;  // dummy row
-    a = V(1);
-    if (i < n) {
-      const uint64_t kk = static_cast<uint64_t>(ac[i]);
-      k = kk < K ? static_cast<uint32_t>(kk) : K;
-      a = av[i];
-    }
-  };
-  uint32_t k1, k2;
-  V a1, a2;
-  load_ka(chunk0 * 32, k1, a1);
-  uint32_t len1 = xlen[k1];
-  load_ka(chunk0 * 32 + step, k2, a2);
-  for (uint32_t b = chunk0 * 32; b < n; b += step) {
-    const uint32_t k = k1, len = len1;
-    const V a = a1;
-    if (b + lane < n) zero |= !(fabs(a) >= tiny);  // zero, tiny, or NaN weight: take the explicit path
-    len1 = xlen[k2];
-    k1 = k2;
-    a1 = a2;
-    load_ka(b + 2 * step, k2, a2);
-    macs += len;
-    __syncwarp();
-    if constexpr (sizeof(V) == 4)
-      tab[lane] = make_uint4(k * W, len, __float_as_uint(a), 0u);
-    else
-      tab[lane] = make_uint4(k * W, len, __double2loint(a), __double2hiint(a));
-    __syncwarp();
-    const uint32_t steps = (min(32u, n - b) + G - 1) / G;
-#pragma unroll 1
-    for (uint32_t u0 = 0; u0 < steps; u0 += B) {
-      constexpr uint32_t kNone = 0x7fffffffu;  // lane past the row's length: no slot entry
-      uint32_t col[B];
-      V xv[B], aa[B];
-      uint32_t any = 0;
-#pragma unroll
-      for (int u = 0; u < B; u++) {
-        uint4 t;
-        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(t.x), "=r"(t.y), "=r"(t.z), "=r"(t.w)
-                     : "r"(tab_s + ((u0 + u) * G + gid) * 16u));
-        if constexpr (sizeof(V) == 4)
-          aa[u] = __uint_as_float(t.z);
-        else
-          aa[u] = __hiloint2double(t.w, t.z);
-        col[u] = kNone;
-        xv[u] = V(0);
-        // only the sectors holding the row's entries are fetched (a marker sits at W-1 < len)
-        if (static_cast<uint32_t>(ent) < t.y) {
-          if constexpr (sizeof(V) == 4) {
-            const uint2 e = __ldg(reinterpret_cast<const uint2*>(p.x.slots) + (t.x + ent));
-            col[u] = e.x;
-            xv[u] = __uint_as_float(e.y);
-          } else {
-            const uint4 e = __ldg(reinterpret_cast<const uint4*>(p.x.slots) + (t.x + ent));
-            col[u] = e.x;
-            xv[u] = __hiloint2double(e.w, e.z);
-            if (e.x & kSlotOvf) xv[u] = __longlong_as_double(static_cast<long long>(e.y));
-          }
-        }
-        any |= col[u];
-      }
-      if (!__any_sync(kFull, (any & kSlotOvf) != 0)) {
-        // fast path: no marker in the batch; lanes past a row's length touch nothing
-#pragma unroll
-        for (int u = 0; u < B; u++) {
-          uint32_t c = col[u];
-          if constexpr (RANGE) c = (c >= c_lo && c < c_hi) ? c : trash;
-          if constexpr (EXACT) {
-#pragma unroll
-            for (int g = 0; g < G; g++) {
-              if (gid == g && col[u] != kNone) add(c, aa[u], xv[u]);
-              __syncwarp();
-            }
-          } else {
-            if (col[u] != kNone) add(c, aa[u], xv[u]);
-          }
-        }
-        __syncwarp();
-      } else {
-#pragma unroll
-        for (int u = 0; u < B; u++) {
-          // marker lane: col = kSlotOvf | tail<<16 | trash; the tail offset rides in the value
-          // bits (fp32: 1.0f + offset ulps) or the pad word (fp64, stashed in xv above)
-          uint32_t moff;
-          if constexpr (sizeof(V) == 4)
-            moff = __float_as_uint(xv[u]) - kOneBits;
-          else
-            moff = static_cast<uint32_t>(__double_as_longlong(xv[u]));
-          const uint32_t mc = __shfl_sync(kFull, col[u], mlane);
-          const uint32_t mo = __shfl_sync(kFull, moff, mlane);
-          const uint32_t tn = (mc & kSlotOvf) ? (mc >> 16) & kMaxTail : 0;
-          const bool real = col[u] != kNone && !(col[u] & kSlotOvf);
-          if constexpr (EXACT) {
-#pragma unroll
-            for (int g = 0; g < G; g++) {
-              if (gid == g) {
-                if (real) add(col_of(col[u]), aa[u], xv[u]);
-                for (uint32_t t = ent; t < tn; t += W) add(col_of(xcol[mo + t]), aa[u], xval[mo + t]);
-              }
-              __syncwarp();
-            }
-          } else {
-            if (real) add(col_of(col[u]), aa[u], xv[u]);
-            for (uint32_t t = ent; t < tn; t += W) add(col_of(xcol[mo + t]), aa[u], xval[mo + t]);
-            __syncwarp();
-          }
-        }
-      }
-    }
-  }
-  return macs;
-}
-
-// Register-fed variant (default, AB2_NUM_SHFL=1).  The kernel is bound by the L1 / shared-memory
-// datapath (90% L1 throughput at cfg2, profiles/r01g); per warp step the variant above spends two
-// shared wavefronts on the chunk table (LDS.128) and, per chunk, one 32-sector gather of X row
-// lengths.  Here each lane keeps its own entry (slot base k*W, weight a) in registers and groups
-// fetch theirs with SHFL; slots are loaded whole (entries past the row's length hold the trash
-// column, skipped without touching shared memory) and MACs are counted from the real entries.
-template <class V, class IdxT, int W, bool EXACT, bool RANGE, bool XZ>
-__device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac,
+__device__ __forceinline__ uint32_t walk_slots(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac,
                                                   const V* __restrict__ av, uint32_t n, uint32_t chunk0,
                                                   uint32_t chunk_stride, V* acc, ChunkPair* tab, uint32_t c_lo,
                                                   uint32_t c_hi, bool& zero) {
@@ -350,9 +168,7 @@ __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, co
     k1 = k2;
     a1 = a2;
     load_ka(b + 2 * step, k2, a2);
-#if AB2_NUM_TAB
-    // the chunk's entries {k*W, a} go to a per-warp table once; each step then reads its group's
-    // entry with one broadcast LDS (1 wavefront) instead of two SHFLs (~2.6 wavefronts measured)
+    // one broadcast LDS per step (1 wavefront) instead of two SHFLs (~2.6 wavefronts measured)
     __syncwarp();
     if constexpr (sizeof(V) == 4)
       asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(tab_s + lane * 8u), "r"(kw), "r"(__float_as_uint(a))
@@ -362,7 +178,6 @@ __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, co
                    "r"(__double2loint(a)), "r"(__double2hiint(a))
                    : "memory");
     __syncwarp();
-#endif
     const uint32_t steps = (min(32u, n - b) + G - 1) / G;
 #pragma unroll 1
     for (uint32_t u0 = 0; u0 < steps; u0 += B) {
@@ -372,7 +187,6 @@ __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, co
 #pragma unroll
       for (int u = 0; u < B; u++) {
         const int src = static_cast<int>(((u0 + u) * G + gid) & 31u);
-#if AB2_NUM_TAB
         uint32_t skw;
         if constexpr (sizeof(V) == 4) {
           uint32_t ab;
@@ -386,10 +200,6 @@ __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, co
                        : "memory");
           aa[u] = __hiloint2double(hi, lo);
         }
-#else
-        const uint32_t skw = __shfl_sync(kFull, kw, src);
-        aa[u] = __shfl_sync(kFull, a, src);
-#endif
         if constexpr (sizeof(V) == 4) {
           const uint2 e = __ldg(reinterpret_cast<const uint2*>(p.x.slots) + (skw + ent));
           col[u] = e.x;
@@ -469,35 +279,159 @@ __device__ __forceinline__ uint32_t walk_entries2(const Num3Args<V, IdxT>& p, co
   return macs;
 }
 
-#ifndef AB2_NUM_SHFL
-#define AB2_NUM_SHFL 1
-#endif
-#ifndef AB2_NUM_TAB
-#define AB2_NUM_TAB 1
-#endif
-
-template <class V, class IdxT, int W, bool EXACT, bool RANGE, bool XZ>
-__device__ __forceinline__ uint32_t walk_any(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac,
-                                             const V* __restrict__ av, uint32_t n, uint32_t chunk0,
-                                             uint32_t chunk_stride, V* acc, ChunkPair* tab, uint32_t c_lo,
-                                             uint32_t c_hi, bool& zero) {
-#if AB2_NUM_SHFL
-  return walk_entries2<V, IdxT, W, EXACT, RANGE, XZ>(p, ac, av, n, chunk0, chunk_stride, acc, tab, c_lo, c_hi, zero);
-#else
-  return walk_entries<V, IdxT, W, EXACT, RANGE, XZ>(p, ac, av, n, chunk0, chunk_stride, acc, tab, c_lo, c_hi, zero);
-#endif
+// ---- fp32 walk over 16-entry slots: two 16-lane groups, column-interleaved copies -----------
+// Group g takes A entries 2u+g (step u) of a 32-entry chunk and adds the X row's slot entries into
+// its copy of the accumulator; the two copies are interleaved per column (cell 2c + g), so group g
+// only touches banks of parity g -- the two groups never conflict and a group's conflicts come
+// from its own X row alone (simulated: 1.69 vs 2.03 wavefronts per RMW with copies side by side);
+// the fold reads a column's two copies with one LDS.64.  The chunk's {k*16} and {a} go to two
+// small tables laid out so that a group reads four steps' entries with one LDS.128, and the slot
+// loads of the next eight steps are in flight while the current eight are added (two register
+// buffers; the next chunk's table is written while the current one is consumed).
+template <class IdxT, bool XZ>
+__device__ __forceinline__ uint32_t walk_pair(const Num3Args<float, IdxT>& p, const IdxT* __restrict__ ac,
+                                              const float* __restrict__ av, uint32_t n, uint32_t chunk0,
+                                              uint32_t chunk_stride, float* acc, ChunkPair* tab, bool& zero) {
+  const int lane = lane_id(), gid = lane >> 4, ent = lane & 15;
+  const uint32_t K = static_cast<uint32_t>(p.x.K);
+  const uint32_t trash = static_cast<uint32_t>(p.x.n_cols);
+  const uint2* __restrict__ sl = reinterpret_cast<const uint2*>(p.x.slots) + ent;  // this lane's entry of a slot
+  auto slot_at = [&](uint32_t kw) {  // sl + kw in one IMAD.WIDE.U32
+    const uint2* q;
+    asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(q) : "r"(kw), "l"(sl));
+    return q;
+  };
+  const float tiny = p.tiny;
+  const uint32_t copy_s = static_cast<uint32_t>(__cvta_generic_to_shared(acc)) + gid * 4u;
+  // table buffer t: kw words at tk(t) + 4*pos, a words at tk(t) + 144 + 4*pos, pos(j) = (j & 1) * 20 + (j >> 1)
+  const uint32_t tab_s = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
+  const uint32_t my_pos = (lane & 1) * 20u + (lane >> 1);
+  const uint32_t grp_pos = gid * 20u;
+  uint32_t macs = 0;
+  const uint32_t step = chunk_stride * 32;
+  uint64_t kr = K;  // raw (k, a) of the next chunk to stage
+  float ar = 1.f;
+  auto load_ka = [&](uint32_t bb) {
+    const uint32_t i = bb + lane;
+    kr = K;  // dummy row: an all-trash slot
+    ar = 1.f;
+    if (i < n) {
+      kr = static_cast<uint64_t>(ac[i]);
+      ar = av[i];
+    }
+  };
+  auto stage = [&](uint32_t b, uint32_t t) {
+    const uint32_t kw = (kr < K ? static_cast<uint32_t>(kr) : K) * 16u;
+    if (b + lane < n) zero |= !(fabsf(ar) >= tiny);  // zero, tiny, or NaN weight: take the explicit path
+    const uint32_t tk = tab_s + t * 288u + my_pos * 4u;
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(tk), "r"(kw) : "memory");
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(tk + 144u), "f"(ar) : "memory");
+  };
+  // slot loads of steps 8h .. 8h+7 of the chunk in table t (steps past the chunk: the dummy row)
+  auto issue = [&](uint32_t t, uint32_t h, uint2 (&e)[8]) {
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+      uint32_t k0, k1, k2, k3;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(k0), "=r"(k1), "=r"(k2), "=r"(k3)
+                   : "r"(tab_s + t * 288u + (grp_pos + 8u * h + 4u * q) * 4u)
+                   : "memory");
+      e[4 * q + 0] = __ldg(slot_at(k0));
+      e[4 * q + 1] = __ldg(slot_at(k1));
+      e[4 * q + 2] = __ldg(slot_at(k2));
+      e[4 * q + 3] = __ldg(slot_at(k3));
+    }
+  };
+  auto consume = [&](uint32_t t, uint32_t h, const uint2 (&e)[8]) {
+    float aa[8];
+#pragma unroll
+    for (int q = 0; q < 2; q++)
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(aa[4 * q]), "=f"(aa[4 * q + 1]), "=f"(aa[4 * q + 2]), "=f"(aa[4 * q + 3])
+                   : "r"(tab_s + t * 288u + 144u + (grp_pos + 8u * h + 4u * q) * 4u)
+                   : "memory");
+    uint32_t any = 0;
+#pragma unroll
+    for (int u = 0; u < 8; u++) any |= e[u].x;
+    if (!__any_sync(kFull, (any & kSlotOvf) != 0u)) {
+      // Steps u and u+1 of one group may hit the same cell (different X rows): the RMWs are
+      // volatile shared accesses of one converged warp, issued and performed in program order.
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const uint32_t c = e[u].x;
+        const bool real = c != trash;
+        if (real) {
+          if constexpr (XZ) zero |= aa[u] * __uint_as_float(e[u].y) == 0.f;
+          smem_fma(copy_s + (c << 3), aa[u], __uint_as_float(e[u].y));
+        }
+        macs += real;
+      }
+      __syncwarp();
+      return;
+    }
+    // a row longer than 16: entry 15 is col = kSlotOvf | tail << 16 | trash with the tail's CSR
+    // offset in the value bits (1.0f + offset ulps); the group adds the tail after the entry
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int ml = (gid << 4) | 15;
+      const uint32_t mc = __shfl_sync(kFull, e[u].x, ml);
+      const uint32_t mo = __shfl_sync(kFull, e[u].y - kOneBits, ml);
+      const uint32_t tn = (mc & kSlotOvf) ? (mc >> 16) & kMaxTail : 0u;
+      const uint32_t c = e[u].x;
+      if (c != trash && !(c & kSlotOvf)) {
+        smem_fma(copy_s + (c << 3), aa[u], __uint_as_float(e[u].y));
+        if constexpr (XZ) zero |= aa[u] * __uint_as_float(e[u].y) == 0.f;
+        macs++;
+      }
+      for (uint32_t t2 = ent; t2 < tn; t2 += 16) {
+        const float x = p.x.val[mo + t2];
+        smem_fma(copy_s + (static_cast<uint32_t>(p.x.col[mo + t2]) << 3), aa[u], x);
+        if constexpr (XZ) zero |= aa[u] * x == 0.f;
+        macs++;
+      }
+      __syncwarp();
+    }
+  };
+  uint32_t b = chunk0 * 32;
+  if (b >= n) return 0;
+  load_ka(b);
+  stage(b, 0);
+  load_ka(b + step);
+  uint2 e0[8], e1[8];
+  __syncwarp();
+  issue(0, 0, e0);
+  for (uint32_t t = 0;; t ^= 1u) {
+    const bool two = n - b > 16;  // the chunk has steps 8..15
+    if (two) issue(t, 1, e1);
+    consume(t, 0, e0);
+    const uint32_t bn = b + step;
+    if (bn < n) {
+      stage(bn, t ^ 1u);
+      load_ka(bn + step);
+      __syncwarp();
+      issue(t ^ 1u, 0, e0);
+    }
+    if (two) consume(t, 1, e1);
+    b = bn;
+    if (b >= n) break;
+    __syncwarp();  // table t is free again
+  }
+  return macs;
 }
 
 // Explicit-mark slow path (rows with a zero product): one k at a time in ascending order,
 // +0.0 start, byte marks; leaves copy 0 holding values for marked cells and the marker
 // everywhere else (other copies reset), so the common fold / emit path applies.
-template <class V, class IdxT>
+template <class V, class IdxT, int CS = 1>
 __device__ void slow_row(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac, const V* __restrict__ av,
                          uint32_t n, V* acc, unsigned char* mark) {
+  // (CS: cell stride of copy 0 -- 2 for the column-interleaved copies of walk_pair)
   const int lane = lane_id();
   const int n_cols = p.x.n_cols;
-  for (int c = lane; c < p.stride * p.copies; c += 32) acc[c] = c < n_cols ? V(0) : Sentinel<V>::value();
+  for (int c = lane; c < p.stride * p.copies; c += 32) acc[c] = Sentinel<V>::value();
   for (int c = lane; c < p.stride; c += 32) mark[c] = 0;
+  __syncwarp();
+  for (int c = lane; c < n_cols; c += 32) acc[c * CS] = V(0);
   __syncwarp();
   for (uint32_t i = 0; i < n; i++) {
     const uint64_t k = static_cast<uint64_t>(ac[i]);
@@ -506,15 +440,15 @@ __device__ void slow_row(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac
     for (int64_t t = p.x.ptr[k] + lane; t < p.x.ptr[k + 1]; t += 32) {
       const int c = p.x.col[t];
       if constexpr (sizeof(V) == 8)
-        acc[c] = __dadd_rn(acc[c], __dmul_rn(a, p.x.val[t]));
+        acc[c * CS] = __dadd_rn(acc[c * CS], __dmul_rn(a, p.x.val[t]));
       else
-        acc[c] = __fadd_rn(acc[c], __fmul_rn(a, p.x.val[t]));
+        acc[c * CS] = __fadd_rn(acc[c * CS], __fmul_rn(a, p.x.val[t]));
       mark[c] = 1;
     }
     __syncwarp();
   }
   for (int c = lane; c < n_cols; c += 32)
-    if (!mark[c]) acc[c] = Sentinel<V>::value();
+    if (!mark[c]) acc[c * CS] = Sentinel<V>::value();
   __syncwarp();
 }
 
@@ -579,6 +513,13 @@ struct StageCursor {
     cur += cnt;
     return o;
   }
+  // room for up to `most` entries at the cursor (a new block if needed); commit() keeps `cnt`
+  __device__ __forceinline__ unsigned long long reserve(uint32_t most, Ctl* ctl, uint32_t block) {
+    const unsigned long long o = take(most, ctl, block);
+    cur = o;
+    return o;
+  }
+  __device__ __forceinline__ void commit(uint32_t cnt) { cur += cnt; }
 };
 
 // Output offset of row r: the exact CSR position when the row counts are known in advance
@@ -595,6 +536,67 @@ __device__ __forceinline__ unsigned long long out_offset(const P& p, int64_t r, 
     return static_cast<unsigned long long>(o);
   }
   return stage.take(cnt, p.ctl, p.stage_block);
+}
+
+// Fold + count + emit in one pass over the accumulator: the copies are summed into the output
+// cells (all copies reset on the way), the row's entries are written in ascending column order,
+// and the count comes out at the end.  The position is fixed before the count is known: the
+// exact CSR offset in direct mode (a count that disagrees flags ctl->bad_row = 2), else room for
+// a full row (n_cols entries) at the warp's staging cursor, of which the row keeps its count.
+// Writes past the capacity are dropped and flag ctl->bad_row = 1.  Returns the count.
+template <class V, int CS, class P>
+__device__ __forceinline__ uint32_t fold_emit(const P& p, V* acc, int copies, int64_t r, StageCursor& stage,
+                                              unsigned long long& off) {
+  // CS = 2: two column-interleaved fp32 copies (cell 2c + g), read and reset with one LDS.64 /
+  // STS.64 per column; CS = 1: `copies` copies of `stride` cells each
+  const int lane = lane_id();
+  const int n_cols = p.x.n_cols, stride = p.stride;
+  unsigned long long cap;
+  if (p.cpos != nullptr) {
+    off = static_cast<unsigned long long>(p.cpos[r] - p.cbase);
+    cap = static_cast<unsigned long long>(p.cpos[r + 1] - p.cpos[r]);
+  } else {
+    off = stage.reserve(static_cast<uint32_t>(n_cols), p.ctl, p.stage_block);
+    cap = static_cast<unsigned long long>(n_cols);
+  }
+  const bool ok = off <= p.t_cap && off + cap <= p.t_cap;
+  uint32_t cnt = 0;
+  for (int c0 = 0; c0 < stride; c0 += 32) {
+    const int c = c0 + lane;
+    V v;
+    if constexpr (CS == 2) {
+      const uint32_t a2 = static_cast<uint32_t>(__cvta_generic_to_shared(acc + 2 * c));
+      float x0, x1;
+      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x0), "=f"(x1) : "r"(a2) : "memory");
+      const uint32_t s = 0x80000000u;
+      asm volatile("st.shared.v2.u32 [%0], {%1, %1};" ::"r"(a2), "r"(s) : "memory");
+      v = x0 + x1;  // -0.0 is the identity for every operand but +0.0 (stays +0.0)
+    } else {
+      v = acc[c];
+      for (int g = 1; g < copies; g++) {
+        v += acc[g * stride + c];
+        acc[g * stride + c] = Sentinel<V>::value();
+      }
+      acc[c] = Sentinel<V>::value();
+    }
+    if (c >= n_cols) v = Sentinel<V>::value();  // trash column / padding
+    const bool t = !Sentinel<V>::is(v);
+    const unsigned b = __ballot_sync(kFull, t);
+    const uint32_t pos = cnt + __popc(b & ((1u << lane) - 1));
+    if (t && ok && pos < cap) {
+      p.tcol[off + pos] = static_cast<decltype(+p.tcol[0])>(c);
+      p.tval[off + pos] = v;
+    }
+    cnt += __popc(b);
+  }
+  __syncwarp();  // the next row's accumulation reads these cells from other lanes
+  if (p.cpos != nullptr) {
+    if (cnt != cap && lane == 0) atomicMax(&p.ctl->bad_row, 2ull);
+  } else {
+    stage.commit(cnt);
+  }
+  if (!ok && lane == 0) atomicMax(&p.ctl->bad_row, 1ull);
+  return cnt;
 }
 
 // Rows whose products fit one warp (<= 32 terms; degree <= 32): the terms are formed one per lane,
@@ -705,13 +707,28 @@ __device__ __forceinline__ bool short_row(const Num3Args<V, IdxT>& p, const IdxT
   return true;
 }
 
+// fp32 over 16-entry slots: walk_pair (two column-interleaved copies); otherwise W-lane groups.
+template <class V, class IdxT, int W>
+constexpr bool kPairWalk = sizeof(V) == 4 && W == 16;
+
 template <class V, class IdxT, int W, bool XZ>
-__global__ void __launch_bounds__(AB2_NUM_MAXT, AB2_NUM_MINB) k_numeric3(Num3Args<V, IdxT> p) {
+__device__ __forceinline__ uint32_t walk(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac,
+                                         const V* __restrict__ av, uint32_t n, uint32_t chunk0, uint32_t chunk_stride,
+                                         V* acc, ChunkPair* tab, bool& zero) {
+  if constexpr (kPairWalk<V, IdxT, W>)
+    return walk_pair<IdxT, XZ>(p, ac, av, n, chunk0, chunk_stride, acc, tab, zero);
+  else
+    return walk_slots<V, IdxT, W, sizeof(V) == 8, false, XZ>(p, ac, av, n, chunk0, chunk_stride, acc, tab, 0, 0, zero);
+}
+
+template <class V, class IdxT, int W, bool XZ>
+__global__ void __launch_bounds__(AB2_NUM_MAXT, (sizeof(V) == 8 || W == 16) ? AB2_NUM_MINB_WIDE : AB2_NUM_MINB)
+    k_numeric3(Num3Args<V, IdxT> p) {
   constexpr bool EXACT = sizeof(V) == 8;
+  constexpr int CS = kPairWalk<V, IdxT, W> ? 2 : 1;  // cell stride of a warp's copies (walk_pair)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned long long s_ticket;
   __shared__ int s_zero;
-  __shared__ uint32_t s_cnt[32];
   const int lane = lane_id(), warp = warp_id(), nw = blockDim.x >> 5;
   const int n_cols = p.x.n_cols;
   const int acc_elems = p.stride * p.copies;
@@ -750,15 +767,15 @@ __global__ void __launch_bounds__(AB2_NUM_MAXT, AB2_NUM_MINB) k_numeric3(Num3Arg
       const uint32_t span = ((n_cols + nw - 1) / nw + 31) & ~31;
       const uint32_t c_lo = min(warp * span, static_cast<uint32_t>(n_cols));
       const uint32_t c_hi = min(c_lo + span, static_cast<uint32_t>(n_cols));
-      const uint32_t m = walk_any<V, IdxT, W, true, true, XZ>(p, ac, av, n, 0, 1, warp_acc(0), warp_tab(warp), c_lo, c_hi, zero);
+      const uint32_t m = walk_slots<V, IdxT, W, true, true, XZ>(p, ac, av, n, 0, 1, warp_acc(0), warp_tab(warp), c_lo, c_hi, zero);
       if (warp == 0) my_macs += m;
     } else {
-      my_macs += walk_any<V, IdxT, W, false, false, XZ>(p, ac, av, n, warp, nw, warp_acc(warp), warp_tab(warp), 0, 0, zero);
+      my_macs += walk<V, IdxT, W, XZ>(p, ac, av, n, warp, nw, warp_acc(warp), warp_tab(warp), zero);
     }
     if (zero) s_zero = 1;
     __syncthreads();
     if (s_zero) {
-      if (warp == 0) slow_row<V, IdxT>(p, ac, av, n, warp_acc(0), warp_mark(0));
+      if (warp == 0) slow_row<V, IdxT, CS>(p, ac, av, n, warp_acc(0), warp_mark(0));
       if (!EXACT && warp != 0)
         for (int i = lane; i < acc_elems; i += 32) warp_acc(warp)[i] = Sentinel<V>::value();
     } else if constexpr (!EXACT) {
@@ -767,23 +784,17 @@ __global__ void __launch_bounds__(AB2_NUM_MAXT, AB2_NUM_MINB) k_numeric3(Num3Arg
         V v = Sentinel<V>::value();
         for (int w = 0; w < nw; w++)
           for (int g = 0; g < p.copies; g++) {
-            V* q = warp_acc(w) + g * p.stride + c;
+            V* q = warp_acc(w) + (CS == 2 ? 2 * c + g : g * p.stride + c);
             v += *q;
             *q = Sentinel<V>::value();
           }
-        warp_acc(0)[c] = v;
+        warp_acc(0)[CS * c] = v;
       }
     }
     __syncthreads();
     if (warp == 0) {
-      const uint32_t cnt = fold_count<V>(warp_acc(0), p.stride, 1, n_cols);
-      const unsigned long long off = out_offset(p, r, cnt, stage);
-      if (off <= p.t_cap && off + cnt <= p.t_cap) {
-        emit_copy0<V, IdxT>(warp_acc(0), n_cols, p.tcol + off, p.tval + off);
-      } else {
-        fold_count<V>(warp_acc(0), p.stride, 1, 0);  // reset
-        if (lane == 0) atomicMax(&p.ctl->bad_row, 1ull);
-      }
+      unsigned long long off;
+      const uint32_t cnt = fold_emit<V, CS>(p, warp_acc(0), CS, r, stage, off);
       if (lane == 0) {
         p.cnt[r] = cnt;
         p.toff[r] = off;
@@ -809,16 +820,10 @@ __global__ void __launch_bounds__(AB2_NUM_MAXT, AB2_NUM_MINB) k_numeric3(Num3Arg
       const V* av = p.aval + s;
       if (p.pad0 && n <= 32 && short_row<V, IdxT>(p, ac, av, n, r, stage, my_nnz, my_macs)) continue;
       bool zero = false;
-      my_macs += walk_any<V, IdxT, W, EXACT, false, XZ>(p, ac, av, n, 0, 1, acc, warp_tab(warp), 0, 0, zero);
-      if (__any_sync(kFull, zero)) slow_row<V, IdxT>(p, ac, av, n, acc, warp_mark(warp));
-      const uint32_t cnt = fold_count<V>(acc, p.stride, EXACT ? 1 : p.copies, n_cols);
-      const unsigned long long off = out_offset(p, r, cnt, stage);
-      if (off <= p.t_cap && off + cnt <= p.t_cap) {
-        emit_copy0<V, IdxT>(acc, n_cols, p.tcol + off, p.tval + off);
-      } else {
-        fold_count<V>(acc, p.stride, 1, 0);  // reset
-        if (lane == 0) atomicMax(&p.ctl->bad_row, 1ull);
-      }
+      my_macs += walk<V, IdxT, W, XZ>(p, ac, av, n, 0, 1, acc, warp_tab(warp), zero);
+      if (__any_sync(kFull, zero)) slow_row<V, IdxT, CS>(p, ac, av, n, acc, warp_mark(warp));
+      unsigned long long off;
+      const uint32_t cnt = fold_emit<V, CS>(p, acc, EXACT ? 1 : p.copies, r, stage, off);
       if (lane == 0) {
         p.cnt[r] = cnt;
         p.toff[r] = off;
@@ -829,25 +834,6 @@ __global__ void __launch_bounds__(AB2_NUM_MAXT, AB2_NUM_MINB) k_numeric3(Num3Arg
   my_macs = warp_sum(my_macs);
   if (lane == 0 && my_nnz) atomicAdd(&p.ctl->nnz, my_nnz);
   if (lane == 0 && my_macs) atomicAdd(&p.ctl->flops, my_macs);
-  (void)s_cnt;
-}
-
-// MACs of the product: sum over A entries of the X row length (spgemm.hpp:51 `flops`).
-template <class IdxT>
-__global__ void __launch_bounds__(256) k_count_macs(const uint64_t* __restrict__ aptr, uint64_t abase,
-                                                    const IdxT* __restrict__ acol, int64_t rows,
-                                                    const int64_t* __restrict__ xptr, int64_t K,
-                                                    Ctl* __restrict__ ctl) {
-  __shared__ int64_t tmp[32];
-  const uint64_t s = aptr[0] - abase, e = aptr[rows] - abase;
-  int64_t m = 0;
-  for (uint64_t i = s + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < e;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t k = static_cast<uint64_t>(acol[i]);
-    if (k < static_cast<uint64_t>(K)) m += xptr[k + 1] - xptr[k];
-  }
-  m = block_sum<int64_t>(m, tmp);
-  if (threadIdx.x == 0 && m) atomicAdd(&ctl->flops, static_cast<unsigned long long>(m));
 }
 
 // K_place: staging -> exact CSR offsets.  One warp per row, 16-byte vector copies when the

@@ -151,10 +151,11 @@ Num3Args<V, IdxT> make_num3(const XOperand& x, const uint64_t* aptr, uint64_t ab
   np.x.slots = static_cast<const typename SlotOf<V>::type*>(x.slots);
   np.x.cslots = static_cast<const uint16_t*>(x.cslots);
   np.stride = static_cast<int32_t>((x.n_cols + 1 + 31) & ~int64_t(31));
+  // fp32: one accumulator copy per lane group (two 16-lane groups over 16-entry slots)
   np.copies = sizeof(V) == 8 ? 1 : 32 / x.W;
   np.warp_bytes = static_cast<int32_t>(
       ((static_cast<size_t>(np.copies) * np.stride * sizeof(V) + np.stride + 15) & ~size_t(15)) +
-      32 * sizeof(ChunkPair));
+      36 * sizeof(ChunkPair));  // chunk tables (walk_pair: two 288-byte buffers)
   np.heavy = heavy;
   np.heavy_deg = heavy_deg;
   np.cnt = cnt;

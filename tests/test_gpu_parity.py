@@ -384,7 +384,7 @@ def test_full_size_parity(shape):
     values within 1e-5 of the fp64 oracle; fp64-exact checksum equal to the oracle's; MACs equal."""
     import bench
     cfg = bench.CONFIGS[shape]
-    g, st, x = bench.make_inputs(cfg, 0, 1)
+    g, st, x = bench.make_inputs(cfg)
     gu = ab.CsrMatrix(g.n_rows, g.n_cols, g.row_ptr, g.col_idx.astype(np.uint64), g.values)
     xu = ab.CsrMatrix(x.n_rows, x.n_cols, x.row_ptr, x.col_idx.astype(np.uint64), x.values)
     rc, (wp, wi, wv), macs = po.spgemm_rowwise(gu.row_ptr, gu.col_idx, gu.values, g.n_rows, g.n_cols, x.n_rows,
