@@ -115,6 +115,7 @@ enum OperandPlan : uint32_t {
   kPlanSlots = 1,   // W-slot groups (k_numeric3)
   kPlanCSlots = 2,  // 16-wide column-only slots (symbolic pass over slots)
   kPlanStep = 4,    // padded step-list slots (k_numeric5, fp32 only)
+  kPlanLean = 8,    // with kPlanStep (fp32): drop the plain CSR once the step list is built (tight budgets)
   kPlanAuto = 0     // the in-core default for the mode (AB2_NUMERIC selects the fp32 kernel)
 };
 // Widest X handled by the dense accumulator (wider operands run in column tiles).

@@ -167,6 +167,9 @@ struct SymArgs {
   int64_t* num_heavy;
   int64_t heavy_flops;
   Ctl* ctl;
+  const uint2* xdesc;  // W == -1: the fp32 step list (ab2_numeric5.cuh) instead of the plain CSR
+  const uint2* xent;
+  int32_t w5;
 };
 
 __device__ __forceinline__ int count_flags(uint32_t* f, int words, int start, int stride) {
@@ -226,10 +229,31 @@ __device__ __forceinline__ uint32_t sym_walk_plain(const SymArgs& p, const IdxT*
   return f;
 }
 
+// Lane-per-A-entry over the fp32 step list (W == -1; tight budgets keep no plain CSR): the X row's
+// descriptor {slot start, nslot | len << 16}, then its len entries {col * 4, value bits}.
+template <class IdxT>
+__device__ __forceinline__ uint32_t sym_walk_steps(const SymArgs& p, const IdxT* __restrict__ ac, uint32_t n,
+                                                   uint32_t first, uint32_t stride, unsigned char* flags) {
+  const uint64_t K = static_cast<uint64_t>(p.K);
+  uint32_t f = 0;
+  for (uint32_t i = first; i < n; i += stride) {
+    const uint64_t k = static_cast<uint64_t>(ac[i]);
+    if (k >= K) continue;
+    const uint2 d = __ldg(p.xdesc + k);
+    const uint32_t len = d.y >> 16;
+    const uint2* e = p.xent + static_cast<uint64_t>(d.x) * p.w5;
+    f += len;
+    for (uint32_t t = 0; t < len; t++) flags[__ldg(e + t).x >> 2] = 1;
+  }
+  return f;
+}
+
 template <class IdxT, int W>
 __device__ __forceinline__ uint32_t sym_any(const SymArgs& p, const IdxT* __restrict__ ac, uint32_t n, uint32_t first,
                                             uint32_t stride, unsigned char* flags) {
-  if constexpr (W == 0)
+  if constexpr (W == -1)
+    return sym_walk_steps<IdxT>(p, ac, n, first, stride, flags);
+  else if constexpr (W == 0)
     return sym_walk_plain<IdxT>(p, ac, n, first, stride, flags);
   else
     return sym_walk<IdxT, W>(p, ac, n, first, stride, flags);

@@ -516,6 +516,17 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
     x->prep_launches += x->K > 0 ? 5 : 2;
   }
   x->prep_launches += (b.layout == AIRES_B200_CSR ? 1 : 6) + 2;
+  if ((plan & kPlanLean) && (plan & kPlanStep) && x->xdesc && !x->slots && !x->cslots && temp) {
+    // tight budgets: the step list is the only layout the product and the sizing kernels read, so
+    // the plain CSR (the build's input) is released rather than held through the run
+    AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+    const size_t csr = ctx.xo_ptr.cap + ctx.xo_col.cap + ctx.xo_val.cap;
+    ctx.xo_ptr.release();
+    ctx.xo_col.release();
+    ctx.xo_val.release();
+    x->ptr = x->col = x->val = nullptr;
+    x->bytes = x->bytes > csr ? x->bytes - csr : 0;
+  }
   if (!temp) AB2_CUDA(cudaStreamSynchronize(ctx.stream));
   return x;
 }

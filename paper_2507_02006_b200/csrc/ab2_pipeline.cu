@@ -58,15 +58,36 @@ struct Pinned {
   }
 };
 
+// Routes the kernels a helper launches on ctx.stream to another stream for a scope.
+struct StreamSwap {
+  Ctx& ctx;
+  cudaStream_t saved;
+  StreamSwap(Ctx& c, cudaStream_t s) : ctx(c), saved(c.stream) { c.stream = s; }
+  ~StreamSwap() { ctx.stream = saved; }
+};
+
+// Waits for every stream of a run before its host buffers can go away: a run that throws midway
+// (an allocation failure, an overflow found at a drain) still has copies into / out of the caller's
+// arrays and registered memory queued, and the Pinned registrations are dropped right after.
+struct SyncGuard {
+  cudaStream_t s[4];
+  ~SyncGuard() {
+    for (cudaStream_t q : s)
+      if (q) cudaStreamSynchronize(q);
+    cudaGetLastError();
+  }
+};
+
 // Streams, events and device buffers of the pipeline, cached per (thread, device) context so
 // repeated runs pay no cudaMalloc / stream creation on the host path.
 struct PipeCacheImpl {
-  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr, aux = nullptr;  // aux: sizing (capped streamed run), fragments (MaxMemory)
   std::vector<cudaEvent_t> ev, tev;  // disable-timing / timing
   std::vector<DevBuf> bufs;
   PipeCacheImpl() {
     AB2_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
     AB2_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    AB2_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
     bufs.resize(32);
   }
   ~PipeCacheImpl() {
@@ -74,14 +95,15 @@ struct PipeCacheImpl {
     for (auto e : tev) cudaEventDestroy(e);
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
+    if (aux) cudaStreamDestroy(aux);
   }
 };
 
 struct Streams {
   PipeCacheImpl& c;
-  cudaStream_t h2d, d2h;
+  cudaStream_t h2d, d2h, aux;
   size_t ne = 0, nt = 0;
-  explicit Streams(PipeCacheImpl& pc) : c(pc), h2d(pc.h2d), d2h(pc.d2h) {}
+  explicit Streams(PipeCacheImpl& pc) : c(pc), h2d(pc.h2d), d2h(pc.d2h), aux(pc.aux) {}
   cudaEvent_t make() {
     if (ne == c.ev.size()) {
       cudaEvent_t e;
@@ -377,6 +399,349 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
   out.flops = flops;
 }
 
+// C row pointers of a part of a tile: local offsets (cptr_local[i] - sub) + the running total; the
+// part's product status (ctl->bad_row) is folded into the run's flag.
+__global__ void k_part_ptr(const int64_t* __restrict__ in, int64_t n, int64_t sub, uint64_t add,
+                           uint64_t* __restrict__ out, const Ctl* __restrict__ ctl, unsigned long long* bad) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<uint64_t>(in[i] - sub) + add;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && ctl->bad_row) atomicMax(bad, ctl->bad_row);
+}
+
+// Capped streamed run: the report of a sized tile, written by the device into pinned host memory.
+constexpr int kMaxParts = 30;
+struct TileReport {
+  unsigned long long nnz, flops, n_parts, bad;
+  long long split[kMaxParts + 1];  // part boundaries (local rows), split[0] = 0
+  long long base[kMaxParts + 1];   // cptr_local at each boundary
+};
+
+// One thread: the tile's nnz / MACs and its parts -- greedy maximal row ranges whose C entries fit
+// the slot's C region (cap entries).  A row that does not fit on its own, or more than kMaxParts
+// parts, sets bad.
+__global__ void k_tile_report(const Ctl* __restrict__ ctl, const int64_t* __restrict__ cptr, int64_t rows,
+                              uint64_t cap, volatile TileReport* rep) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  rep->nnz = ctl->nnz;
+  rep->flops = ctl->flops;
+  unsigned long long bad = ctl->bad_row ? 1ull : 0ull;
+  int parts = 0;
+  int64_t p = 0;
+  rep->split[0] = 0;
+  rep->base[0] = 0;
+  while (p < rows && !bad) {
+    int64_t lo = p, hi = rows;  // largest q with cptr[q] - cptr[p] <= cap
+    while (lo < hi) {
+      const int64_t mid = lo + (hi - lo + 1) / 2;
+      if (static_cast<uint64_t>(cptr[mid] - cptr[p]) <= cap)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    if (lo == p || parts == kMaxParts) {
+      bad = 2;
+      break;
+    }
+    parts++;
+    rep->split[parts] = lo;
+    rep->base[parts] = cptr[lo];
+    p = lo;
+  }
+  rep->n_parts = static_cast<unsigned long long>(parts);
+  rep->bad = bad;
+  __threadfence_system();
+}
+
+// Capped streamed run (AIRES_B200_RUN_STREAM_OUT with a device budget): A crosses the link once.
+// The exact protocol sizes C before the first byte of it is placed -- a sizing pass over A's
+// column indices, then the tiles, so A's columns cross the link twice whenever the budget cannot
+// hold them (cfg3 at 25%: 1.45x the algorithmic H2D bytes).  Here each tile is sized on the device
+// right after its upload, from the columns already in its slot: classify + symbolic -> row counts
+// -> scan -> exact local offsets -> k_tile_report (parts that fit the slot's C region, straight
+// into pinned host memory).  The host reads the report of tile j while tile j+1 uploads and sizes,
+// then queues tile j's product in direct mode (rows written at their exact offsets, no staging)
+// part by part, each part's row_ptr rebased to the running total and drained to its final host
+// position.  Tiles are cut by A bytes with C bytes estimated from the ratio observed so far (the
+// first tile a quarter slot); an estimate that is off only costs an extra part (a D2H round trip
+// inside the tile), never a re-upload.  Slot layout: [A cols | A vals | per-row scratch | C region].
+void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b, uint32_t mode,
+                       uint32_t nbuf, uint64_t budget, aires_b200_output& out, aires_b200_run_report& rep,
+                       Streams& st, Arena& arena, Pinned& pin) {
+  const uint32_t ib = a.idx_bytes, vb = mode == AIRES_B200_MODE_FP32 ? 4 : 8;
+  const uint64_t n = a.n_rows;
+  const uint64_t p0 = a.ptr[0], pend = a.ptr[n];
+  cudaStream_t cs = ctx.stream;
+  cudaEvent_t t_begin = st.make_timed(), t_p1 = st.make_timed(), t_p2 = st.make_timed(), t_end = st.make_timed();
+  AB2_CUDA(cudaEventRecord(t_begin, cs));
+  AB2_CUDA(cudaStreamWaitEvent(st.h2d, t_begin, 0));
+  // X: W-slots (k_numeric3) when a 16-wide slot array takes <= 1/8 of the budget, else the lean
+  // step list (fp32); 16-wide column slots for the sizing kernel when rows average >= 4 entries
+  const uint64_t xk = b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols;
+  const uint64_t xnnz = b.location == AIRES_B200_HOST ? b.ptr[xk] - b.ptr[0] : b.span;
+  // (the step list alone: the sizing kernel walks it too, so the plain CSR is released after the build)
+  uint32_t plan = mode == AIRES_B200_MODE_FP32 && (xk + 1) * 16 * 8 * 8 > budget ? kPlanStep | kPlanLean : kPlanSlots;
+  if (!(plan & kPlanLean) && xk > 0 && xnnz >= 4 * xk && xk * kCSlotW * 2 * 16 <= budget) plan |= kPlanCSlots;
+  auto x = make_operand(ctx, b, mode, /*temp=*/true, plan);
+  uint64_t x_dev = x->bytes;
+  if (b.location == AIRES_B200_HOST) {
+    const uint64_t raw = ctx.x_ptr.cap + ctx.x_idx.cap + ctx.x_val.cap;
+    x_dev = x_dev > raw ? x_dev - raw : 0;
+    rep.h2d_bytes += xk * 8 + 8 + static_cast<uint64_t>(x->nnz) * (b.idx_bytes + b.val_bytes);
+  }
+  Ctl* d_ctl = static_cast<Ctl*>(arena.get(sizeof(Ctl) * nbuf * (kMaxParts + 1)));
+  auto* d_bad = static_cast<unsigned long long*>(arena.get(8));  // max of every part's ctl->bad_row
+  AB2_CUDA(cudaMemsetAsync(d_bad, 0, 8, cs));
+  const uint64_t fixed = x_dev + arena.used + (64 << 10);
+  if (budget <= fixed)
+    fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY, "device budget " + std::to_string(budget) +
+                                                    " does not cover the resident operand and row arrays (" +
+                                                    std::to_string(fixed) + " bytes)");
+  const uint64_t slot_bytes = ((budget - fixed) / nbuf) & ~uint64_t(255);
+  std::vector<char*> slot_mem(nbuf);
+  for (uint32_t s = 0; s < nbuf; s++) slot_mem[s] = static_cast<char*>(arena.get(slot_bytes));
+  auto* h_rep = static_cast<TileReport*>(ctx.h_ctl.get(sizeof(TileReport) * nbuf));
+  // the caller's allocator: an upper bound of nnz(C); the exact count is reported in out.nnz
+  const uint64_t bound = c_bound(*x, n, pend - p0);
+  void *optr = nullptr, *oidx = nullptr, *oval = nullptr;
+  int rc = out.alloc(out.user, n, bound, &optr, &oidx, &oval);
+  if (rc != 0) fail(rc, "output allocator failed for a bound of " + std::to_string(bound) + " nonzeros");
+  pin.ensure(optr, (n + 1) * 8);
+  pin.ensure(oidx, bound * ib);
+  pin.ensure(oval, bound * vb);
+  AB2_CUDA(cudaEventRecord(t_p1, cs));
+
+  auto r256 = [](uint64_t v) { return (v + 255) & ~uint64_t(255); };
+  struct Tile {
+    uint64_t r0, r1, q0, q1;
+    uint32_t slot;
+    uint64_t* aptr;  // the tile's A row pointers (absolute), uploaded with its columns and values
+    char *acol, *aval, *ccol, *cval;
+    int64_t *heavy, *cptr, *rflops;
+    uint64_t* toff;
+    uint64_t* optr;
+    int32_t* cnt;
+    uint64_t c_cap;
+    cudaEvent_t sized;
+    cudaEvent_t tl_loaded = nullptr, tl_computed = nullptr, tl_drained = nullptr;  // AB2_TRACE
+    uint64_t parts = 0;
+  };
+  // AB2_TRACE=1: per-tile device timeline (loaded / sized / last part computed / drained) on stderr
+  const bool trace = env_int("AB2_TRACE", 0) != 0;
+  std::vector<cudaEvent_t> slot_free(nbuf, nullptr);
+  // C entries per A entry, observed; the first tile assumes the mean X row length
+  double rho = std::max(0.05, std::min(static_cast<double>(x->n_cols),
+                                       static_cast<double>(x->nnz) / static_cast<double>(std::max<int64_t>(x->K, 1))));
+  uint64_t seen_a = 0, seen_c = 0, cursor = 0, running = 0, flops = 0, parts_total = 0;
+  auto bytes_of = [&](uint64_t r0, uint64_t r1, double ratio) {
+    const uint64_t an = a.ptr[r1] - a.ptr[r0];
+    return static_cast<double>(r256(an * ib) + r256(an * vb)) + static_cast<double>(r256((r1 - r0 + 1) * 8)) * 6 +
+           static_cast<double>(r256((r1 - r0 + 1) * 4)) + ratio * 1.1 * static_cast<double>(an) * (ib + vb) + 1024.0;
+  };
+  std::vector<Tile> tiles;
+  auto launch_tile = [&]() {
+    Tile t{};
+    t.slot = static_cast<uint32_t>(tiles.size() % nbuf);
+    t.r0 = cursor;
+    const double cap_bytes = tiles.empty() ? static_cast<double>(slot_bytes) / 4 : static_cast<double>(slot_bytes);
+    uint64_t lo = cursor + 1, hi = n;  // largest r1 whose estimated bytes fit
+    if (bytes_of(cursor, cursor + 1, 0.0) + static_cast<double>(x->n_cols) * (ib + vb) > static_cast<double>(slot_bytes))
+      fail(AIRES_B200_ROW_TOO_LARGE, "row " + std::to_string(cursor) + " does not fit a ring slot of " +
+                                         std::to_string(slot_bytes) + " bytes");
+    while (lo < hi) {
+      const uint64_t mid = lo + (hi - lo + 1) / 2;
+      if (bytes_of(cursor, mid, rho) <= cap_bytes)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    t.r1 = lo;
+    t.q0 = a.ptr[t.r0];
+    t.q1 = a.ptr[t.r1];
+    const uint64_t rows = t.r1 - t.r0, an = t.q1 - t.q0;
+    char* m = slot_mem[t.slot];
+    auto take = [&](uint64_t bytes) {
+      char* q = m;
+      m += r256(bytes);
+      return q;
+    };
+    t.aptr = reinterpret_cast<uint64_t*>(take((rows + 1) * 8));
+    t.acol = take(std::max<uint64_t>(an, 1) * ib);
+    t.aval = take(std::max<uint64_t>(an, 1) * vb);
+    t.heavy = reinterpret_cast<int64_t*>(take((rows + 1) * 8));
+    t.toff = reinterpret_cast<uint64_t*>(take((rows + 1) * 8));
+    t.cptr = reinterpret_cast<int64_t*>(take((rows + 1) * 8));
+    t.optr = reinterpret_cast<uint64_t*>(take((rows + 1) * 8));
+    t.rflops = reinterpret_cast<int64_t*>(take((rows + 1) * 8));
+    t.cnt = reinterpret_cast<int32_t*>(take((rows + 1) * 4));
+    const uint64_t used = static_cast<uint64_t>(m - slot_mem[t.slot]);
+    if (used > slot_bytes) fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY, "ring slot overflow");
+    // C region: c_cap column indices, then (256-byte aligned) c_cap values
+    t.c_cap = slot_bytes - used > 256 ? (slot_bytes - used - 256) / (ib + vb) : 0;
+    t.ccol = m;
+    t.cval = m + r256(t.c_cap * ib);
+    // upload (copy engine 0) once the slot's previous tile has drained
+    if (slot_free[t.slot]) AB2_CUDA(cudaStreamWaitEvent(st.h2d, slot_free[t.slot], 0));
+    AB2_CUDA(cudaMemcpyAsync(t.aptr, a.ptr + t.r0, (rows + 1) * 8, cudaMemcpyHostToDevice, st.h2d));
+    if (an) {
+      AB2_CUDA(cudaMemcpyAsync(t.acol, static_cast<const char*>(a.idx) + t.q0 * ib, an * ib, cudaMemcpyHostToDevice, st.h2d));
+      AB2_CUDA(cudaMemcpyAsync(t.aval, static_cast<const char*>(a.val) + t.q0 * vb, an * vb, cudaMemcpyHostToDevice, st.h2d));
+    }
+    rep.h2d_bytes += (rows + 1) * 8 + an * (ib + vb);
+    cudaEvent_t loaded = st.make();
+    AB2_CUDA(cudaEventRecord(loaded, st.h2d));
+    if (trace) {
+      t.tl_loaded = st.make_timed();
+      AB2_CUDA(cudaEventRecord(t.tl_loaded, st.h2d));
+    }
+    // size it on the device (sizing stream, so tile j's product never queues behind tile j+1's
+    // upload): row counts -> local exact offsets -> parts that fit the C region
+    cudaStream_t zs = st.aux;
+    AB2_CUDA(cudaStreamWaitEvent(zs, loaded, 0));
+    Ctl* c = d_ctl + t.slot * (kMaxParts + 1);
+    AB2_CUDA(cudaMemsetAsync(c, 0, sizeof(Ctl) * (kMaxParts + 1), zs));
+    StreamSwap swap(ctx, zs);
+    TileSym sy{};
+    sy.aptr = t.aptr;
+    sy.abase = t.q0;
+    sy.acol = t.acol;
+    sy.rows = static_cast<int64_t>(rows);
+    sy.cnt = t.cnt;
+    sy.rflops = t.rflops;
+    sy.heavy = t.heavy;
+    sy.ctl = c;
+    ctx.launches += tile_symbolic(ctx, *x, ib, sy);
+    const int64_t nb = (static_cast<int64_t>(rows) + kScanTile - 1) / kScanTile;
+    int64_t* part = reinterpret_cast<int64_t*>(t.optr);  // scan partials: optr is written later
+    if (rows > 0) {
+      k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, zs>>>(t.cnt, static_cast<int64_t>(rows), part);
+      k_scan_part<<<1, 1024, 0, zs>>>(part, nb, c);
+      k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, zs>>>(t.cnt, static_cast<int64_t>(rows), part, t.cptr);
+      ctx.launches += 3;
+    } else {
+      AB2_CUDA(cudaMemsetAsync(t.cptr, 0, 8, zs));
+    }
+    k_tile_report<<<1, 32, 0, zs>>>(c, t.cptr, static_cast<int64_t>(rows), t.c_cap, h_rep + t.slot);
+    AB2_CUDA(cudaGetLastError());
+    ctx.launches++;
+    t.sized = trace ? st.make_timed() : st.make();
+    AB2_CUDA(cudaEventRecord(t.sized, zs));
+    cursor = t.r1;
+    tiles.push_back(t);
+  };
+
+  size_t j = 0;
+  if (cursor < n) launch_tile();
+  while (j < tiles.size()) {
+    while (cursor < n && tiles.size() - j < nbuf) launch_tile();  // later tiles upload and size meanwhile
+    Tile& t = tiles[j];
+    AB2_CUDA(cudaEventSynchronize(t.sized));
+    const TileReport& r = h_rep[t.slot];
+    if (r.bad) fail(AIRES_B200_CAPACITY_EXCEEDED, r.bad == 2 ? "tile C row does not fit the slot's C region"
+                                                             : "tile sizing overflow");
+    const uint64_t rows = t.r1 - t.r0, tnnz = r.nnz;
+    flops += r.flops;
+    seen_a += t.q1 - t.q0;
+    seen_c += tnnz;
+    if (seen_a) rho = std::max(0.01, static_cast<double>(seen_c) / static_cast<double>(seen_a));
+    if (running + tnnz > bound) fail(AIRES_B200_CAPACITY_EXCEEDED, "C exceeds its bound");
+    const int n_parts = static_cast<int>(r.n_parts);
+    std::vector<long long> split(r.split, r.split + n_parts + 1), base(r.base, r.base + n_parts + 1);
+    cudaEvent_t prev_drain = nullptr;
+    Ctl* c = d_ctl + t.slot * (kMaxParts + 1);
+    for (int q = 0; q < n_parts; q++) {
+      const uint64_t pa = static_cast<uint64_t>(split[q]), pb = static_cast<uint64_t>(split[q + 1]);
+      const uint64_t pn = static_cast<uint64_t>(base[q + 1] - base[q]);
+      if (prev_drain) AB2_CUDA(cudaStreamWaitEvent(cs, prev_drain, 0));  // the C region is reused
+      TilePass tp{};
+      tp.aptr = t.aptr + pa;
+      tp.abase = t.q0;
+      tp.acol = t.acol;
+      tp.aval = t.aval;
+      tp.rows = static_cast<int64_t>(pb - pa);
+      tp.cpos = t.cptr + pa;
+      tp.cbase = base[q];
+      tp.ccol = t.ccol;
+      tp.cval = t.cval;
+      tp.c_cap = t.c_cap;
+      tp.heavy = t.heavy;
+      tp.cnt = reinterpret_cast<uint32_t*>(t.cnt) + pa;  // scratch (the counts are in cptr now)
+      tp.toff = t.toff;
+      tp.ctl = c + 1 + q;
+      ctx.launches += tile_product(ctx, *x, ib, tp);
+      {
+        const int g = static_cast<int>(std::min<uint64_t>((pb - pa + 256) / 256, static_cast<uint64_t>(ctx.sms) * 4));
+        k_part_ptr<<<g, 256, 0, cs>>>(t.cptr + pa, static_cast<int64_t>(pb - pa + 1), base[q], running, t.optr + pa,
+                                      c + 1 + q, d_bad);
+        AB2_CUDA(cudaGetLastError());
+        ctx.launches++;
+      }
+      cudaEvent_t computed = trace ? st.make_timed() : st.make();
+      AB2_CUDA(cudaEventRecord(computed, cs));
+      AB2_CUDA(cudaStreamWaitEvent(st.d2h, computed, 0));
+      AB2_CUDA(cudaMemcpyAsync(static_cast<uint64_t*>(optr) + t.r0 + pa, t.optr + pa, (pb - pa + 1) * 8,
+                               cudaMemcpyDeviceToHost, st.d2h));
+      if (pn) {
+        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oidx) + running * ib, t.ccol, pn * ib, cudaMemcpyDeviceToHost, st.d2h));
+        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oval) + running * vb, t.cval, pn * vb, cudaMemcpyDeviceToHost, st.d2h));
+      }
+      rep.d2h_bytes += (pb - pa + 1) * 8 + pn * (ib + vb);
+      prev_drain = trace ? st.make_timed() : st.make();
+      AB2_CUDA(cudaEventRecord(prev_drain, st.d2h));
+      if (trace) t.tl_computed = computed;
+      running += pn;
+      parts_total++;
+    }
+    t.parts = static_cast<uint64_t>(n_parts);
+    if (trace) t.tl_drained = prev_drain;
+    if (n_parts == 0) {  // rows without entries still get their row pointers
+      prev_drain = st.make();
+      AB2_CUDA(cudaEventRecord(prev_drain, st.d2h));
+    }
+    (void)rows;
+    slot_free[t.slot] = prev_drain;
+    j++;
+  }
+  AB2_CUDA(cudaEventRecord(t_p2, cs));
+  if (n == 0) static_cast<uint64_t*>(optr)[0] = 0;
+  cudaEvent_t e_d2h = st.make();
+  AB2_CUDA(cudaEventRecord(e_d2h, st.d2h));
+  AB2_CUDA(cudaStreamWaitEvent(cs, e_d2h, 0));
+  AB2_CUDA(cudaEventRecord(t_end, cs));
+  AB2_CUDA(cudaStreamSynchronize(cs));
+  {
+    unsigned long long hb = 0;
+    AB2_CUDA(cudaMemcpy(&hb, d_bad, 8, cudaMemcpyDeviceToHost));
+    if (hb == 2) fail(AIRES_B200_CUDA_ERROR, "numeric row counts disagree with the sizing pass");
+    if (hb) fail(AIRES_B200_CAPACITY_EXCEEDED, "tile output overflow");
+  }
+  if (trace) {
+    std::fprintf(stderr, "[ab2 capped] phase1 (X operand) %.3f ms, slot %llu bytes, %zu tiles\n",
+                 ms_between(t_begin, t_p1), static_cast<unsigned long long>(slot_bytes), tiles.size());
+    for (size_t q = 0; q < tiles.size(); q++) {
+      const Tile& t = tiles[q];
+      std::fprintf(stderr, "[ab2 capped] tile %3zu rows %8llu A %10llu  loaded %8.3f sized %8.3f computed %8.3f drained %8.3f  parts %llu\n",
+                   q, static_cast<unsigned long long>(t.r1 - t.r0), static_cast<unsigned long long>(t.q1 - t.q0),
+                   ms_between(t_begin, t.tl_loaded), ms_between(t_begin, t.sized),
+                   t.tl_computed ? ms_between(t_begin, t.tl_computed) : 0.0,
+                   t.tl_drained ? ms_between(t_begin, t.tl_drained) : 0.0, static_cast<unsigned long long>(t.parts));
+    }
+  }
+  rep.segments = parts_total;
+  rep.flops = flops;
+  rep.c_nnz = running;
+  rep.peak_device_bytes = arena.used + x_dev;
+  rep.phase1_ms = ms_between(t_begin, t_p1);
+  rep.phase2_ms = ms_between(t_p1, t_p2);
+  rep.phase3_ms = ms_between(t_p2, t_end);
+  rep.total_ms = ms_between(t_begin, t_end);
+  ctx.last_ms = rep.total_ms;
+  out.n_rows = n;
+  out.n_cols = static_cast<uint64_t>(x->n_cols);
+  out.nnz = running;
+  out.flops = flops;
+}
+
 }  // namespace
 
 void destroy_pipe_cache(void* p) { delete static_cast<PipeCacheImpl*>(p); }
@@ -418,6 +783,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   cudaStream_t cs = ctx.stream;
   Arena arena(*static_cast<PipeCacheImpl*>(ctx.pipe));
   Pinned pin;
+  SyncGuard sync{{cs, st.h2d, st.d2h, st.aux}};  // destroyed before pin (no copy outlives its buffers)
   cudaEvent_t t_begin = st.make_timed(), t_p1 = st.make_timed(), t_p2 = st.make_timed(), t_end = st.make_timed();
   pin.ensure(a.ptr, (n + 1) * 8);
   pin.ensure(static_cast<const char*>(a.idx) + p0 * ib, (pend - p0) * ib);
@@ -425,6 +791,11 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   if ((cfg.flags & AIRES_B200_RUN_STREAM_OUT) && cfg.device_budget == 0 && cfg.c_aware != 2 &&
       static_cast<int64_t>(b.n_cols) <= wide_threshold(mode)) {
     run_stream(ctx, a, b, mode, cfg.n_buffers ? nbuf : 3, out, rep, st, arena, pin);
+    return;
+  }
+  if ((cfg.flags & AIRES_B200_RUN_STREAM_OUT) && cfg.device_budget > 0 && cfg.c_aware == 1 &&
+      static_cast<int64_t>(b.n_cols) <= wide_threshold(mode)) {
+    run_stream_capped(ctx, a, b, mode, cfg.n_buffers ? nbuf : 3, cfg.device_budget, out, rep, st, arena, pin);
     return;
   }
 
@@ -798,18 +1169,19 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
       rep.merge_bytes += nf * (ib + vb);
       AB2_CUDA(cudaEventRecord(slot[s].loaded, st.h2d));
       AB2_CUDA(cudaStreamWaitEvent(cs, slot[s].loaded, 0));
-      // the trailing fragment goes back to the host once this tile is on the device
+      // the trailing fragment goes back to the host once this tile is on the device -- on its own
+      // stream, so the next upload waits for this fragment only (not behind earlier C drains)
       const uint64_t fb = j + 1 < mm.size() ? mm[j + 1].q_frag : pend;
       const uint64_t tail = m.q1 > fb ? m.q1 - fb : 0;
-      AB2_CUDA(cudaStreamWaitEvent(st.d2h, slot[s].loaded, 0));
+      AB2_CUDA(cudaStreamWaitEvent(st.aux, slot[s].loaded, 0));
       if (tail) {
         AB2_CUDA(cudaMemcpyAsync(merge_col, static_cast<char*>(slot[s].acol) + (fb - m.q_frag) * ib, tail * ib,
-                                 cudaMemcpyDeviceToHost, st.d2h));
+                                 cudaMemcpyDeviceToHost, st.aux));
         AB2_CUDA(cudaMemcpyAsync(merge_val, static_cast<char*>(slot[s].aval) + (fb - m.q_frag) * vb, tail * vb,
-                                 cudaMemcpyDeviceToHost, st.d2h));
+                                 cudaMemcpyDeviceToHost, st.aux));
         rep.d2h_bytes += tail * (ib + vb);
       }
-      AB2_CUDA(cudaEventRecord(frag_back, st.d2h));
+      AB2_CUDA(cudaEventRecord(frag_back, st.aux));
       TilePass t{};
       t.aptr = d_aptr + r0;
       t.abase = m.q_frag;

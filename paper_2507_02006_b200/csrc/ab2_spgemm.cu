@@ -338,7 +338,10 @@ int tile_symbolic_t(Ctx& ctx, const XOperand& x, const TileSym& t) {
   sp.num_heavy = t.heavy;  // unused: heavy_flops is never exceeded
   sp.heavy_flops = INT64_MAX;
   sp.ctl = t.ctl;
-  auto k = x.cslots ? k_symbolic<IdxT, kCSlotW> : k_symbolic<IdxT, 0>;
+  sp.xdesc = static_cast<const uint2*>(x.xdesc);
+  sp.xent = static_cast<const uint2*>(x.xent);
+  sp.w5 = x.W5;
+  auto k = x.cslots ? k_symbolic<IdxT, kCSlotW> : (x.ptr ? k_symbolic<IdxT, 0> : k_symbolic<IdxT, -1>);
   const size_t smem = 8 * static_cast<size_t>(sp.region_bytes);
   const int grid = occupancy_grid(k, 256, smem, ctx.sms);
   k<<<grid, 256, smem, ctx.stream>>>(sp, static_cast<const IdxT*>(t.acol));

@@ -212,11 +212,72 @@ def test_stream_out_edge_shapes():
     assert res.c.nnz() == 0 and res.c.row_ptr.shape[0] == 1
 
 
-def test_stream_out_ignored_when_capped():
-    # a capped budget keeps the exact protocol (C-aware tiles need the sizing pass)
+@pytest.mark.parametrize("frac", [0.5, 0.25, 0.125, 0.06])
+def test_stream_out_capped_single_pass(frac):
+    """capped + streamed output: each tile is sized on the device from the columns already in its
+    slot (no sizing pass over A), so every byte of A crosses the link exactly once; the tiny budgets
+    force tiles whose C is split into several parts.  fp64-exact: C bit-identical to the oracle."""
+    g, x = _graph(20_000, 300_000, 128)
+    wp, wi, wv, macs = _oracle(g, x)
+    a_b, c_b = _bytes(g, x, (wp, wi))
+    res = ab.run_aires(g, x, ab.MemoryBudget(int(3e6 + frac * (a_b + c_b))), stream_out=True, n_buffers=3)
+    assert res.report.segments >= 2
+    assert res.report.c_checksum == po.checksum(g.n_rows, x.n_cols, wp, wi, wv)
+    assert res.report.flops == macs
+    assert np.array_equal(res.c.row_ptr, wp) and np.array_equal(res.c.col_idx, wi)
+    base = 8 * (g.n_rows + 1) + 16 * g.nnz() + 8 * (x.n_rows + 1) + 16 * x.nnz()
+    # A once (the exact protocol sends its columns twice); each tile's row pointers include its end row
+    assert base <= res.report.ledger.h2d.bytes <= base + 8 * res.report.segments
+
+
+@pytest.mark.parametrize("n_buffers", [2, 3, 4])
+def test_stream_out_capped_fp32_matches_exact_protocol(n_buffers):
+    g, x = _graph(30_000, 400_000, 100, seed=4)
+    g32 = ab.CsrMatrix(g.n_rows, g.n_cols, g.row_ptr, g.col_idx.astype(np.uint32), g.values.astype(np.float32))
+    x32 = ab.CsrMatrix(x.n_rows, x.n_cols, x.row_ptr, x.col_idx.astype(np.uint32), x.values.astype(np.float32))
+    a_b, c_b = _bytes(g, x, (None, np.zeros(int(1.5 * g.nnz()))), vb=4)
+    budget = ab.MemoryBudget(int(2e6 + 0.2 * (a_b + c_b)))
+    exact = ab.run_aires(g32, x32, budget, n_buffers=n_buffers, with_checksum=False)
+    res = ab.run_aires(g32, x32, budget, n_buffers=n_buffers, with_checksum=False, stream_out=True)
+    assert res.report.segments >= 2
+    assert np.array_equal(res.c.row_ptr, exact.c.row_ptr)
+    assert np.array_equal(res.c.col_idx, exact.c.col_idx)
+    np.testing.assert_allclose(res.c.values, exact.c.values, rtol=2e-6)
+    assert res.report.flops == exact.report.flops
+    assert res.report.ledger.h2d.bytes < exact.report.ledger.h2d.bytes
+
+
+def test_stream_out_capped_edge_shapes():
+    g, x = _graph(4_000, 40_000, 64, seed=9)
+    lens = np.diff(g.row_ptr.astype(np.int64))
+    row_of = np.repeat(np.arange(g.n_rows), lens)
+    keep = (row_of >= 100) & (row_of < g.n_rows - 100)
+    lens[:100] = 0
+    lens[-100:] = 0
+    ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    g2 = ab.CsrMatrix(g.n_rows, g.n_cols, ptr, g.col_idx[keep], g.values[keep])
+    wp, wi, wv, _ = _oracle(g2, x)
+    res = ab.run_aires(g2, x, ab.MemoryBudget(1_500_000), stream_out=True)
+    assert res.report.segments >= 2
+    assert np.array_equal(res.c.row_ptr, wp) and np.array_equal(res.c.col_idx, wi)
+    assert res.report.c_checksum == po.checksum(g2.n_rows, x.n_cols, wp, wi, wv)
+    empty = ab.CsrMatrix(g.n_rows, g.n_cols, np.zeros(g.n_rows + 1, np.uint64), np.zeros(0, np.uint64),
+                         np.zeros(0, np.float64))
+    res = ab.run_aires(empty, x, ab.MemoryBudget(1_500_000), stream_out=True)
+    assert res.c.nnz() == 0 and not res.c.row_ptr.any()
+
+
+def test_stream_out_capped_budget_too_small_raises():
+    g, x = _graph(4_000, 40_000, 64, seed=9)
+    with pytest.raises(ab.AiresError) as e:
+        ab.run_aires(g, x, ab.MemoryBudget(100_000), stream_out=True)
+    assert e.value.code == ab.errc.insufficient_device_memory
+
+
+def test_stream_out_a_only_tiling_keeps_the_exact_protocol():
+    # c_aware=False (RoBW by A alone, the reference's admission) is not streamed
     g, x = _graph(20_000, 300_000, 128)
     wp, wi, wv, _ = _oracle(g, x)
     a_b, c_b = _bytes(g, x, (wp, wi))
-    res = ab.run_aires(g, x, ab.MemoryBudget(int(3e6 + 0.25 * (a_b + c_b))), stream_out=True)
-    assert res.report.segments >= 2
+    res = ab.run_aires(g, x, ab.MemoryBudget(int(3e6 + 2.0 * (a_b + c_b))), stream_out=True, c_aware=False)
     assert res.report.c_checksum == po.checksum(g.n_rows, x.n_cols, wp, wi, wv)

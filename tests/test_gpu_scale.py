@@ -66,6 +66,27 @@ def test_cfg3_capped_fp32_matches_oracle(frac, min_tiles):
     _check_fp32(res.c, want, macs, res.report.flops)
 
 
+@pytest.mark.parametrize("frac", [0.5, 0.25, 0.125])
+def test_cfg3_capped_streamed_fp32_matches_oracle(frac):
+    """bench.py's out-of-core sweep: capped, streamed output (A crosses the link once)"""
+    g, x, want, macs, _ = _inputs("cfg3")
+    res = ab.run_aires(_f32(g), _f32(x), _budget(g, x, want[1].shape[0], frac), n_buffers=3, with_checksum=False,
+                       stream_out=True)
+    assert res.report.segments >= 2
+    _check_fp32(res.c, want, macs, res.report.flops)
+    b_a = 8 * (g.n_rows + 1) + 8 * g.nnz()
+    b_x = 8 * (x.n_rows + 1) + 8 * x.nnz()
+    assert b_a + b_x <= res.report.ledger.h2d.bytes <= b_a + b_x + 8 * res.report.segments  # A crosses once
+
+
+def test_cfg2_capped_streamed_fp32_matches_oracle():
+    g, x, want, macs, _ = _inputs("cfg2")
+    res = ab.run_aires(_f32(g), _f32(x), _budget(g, x, want[1].shape[0], 0.25), n_buffers=3, with_checksum=False,
+                       stream_out=True)
+    assert res.report.segments >= 4
+    _check_fp32(res.c, want, macs, res.report.flops)
+
+
 def test_cfg3_capped_fp64_exact_checksum():
     g, x, want, macs, ck = _inputs("cfg3")
     res = ab.run_aires(g, x, _budget(g, x, want[1].shape[0], 0.25, vb=8), n_buffers=3)  # fp64 -> FP64_EXACT
