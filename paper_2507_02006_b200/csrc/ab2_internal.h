@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -39,6 +40,42 @@ struct DevBuf {
     return *this;
   }
   ~DevBuf() { release(); }
+};
+
+// One device allocation carved for a budgeted run: buffers the run keeps come from the bottom, build
+// temporaries from the top (dropped together once the build has finished on the device), so every
+// byte a run holds at once lies inside `size` and the high-water mark is `peak`.
+struct Region {
+  char* base = nullptr;
+  uint64_t size = 0, lo = 0, hi = 0, peak = 0;
+  void init(void* p, uint64_t n) {
+    base = static_cast<char*>(p);
+    size = n;
+    lo = 0;
+    hi = n;
+    peak = 0;
+  }
+  static uint64_t up(uint64_t b) { return (std::max<uint64_t>(b, 1) + 255) & ~uint64_t(255); }
+  void* keep(uint64_t bytes) {
+    bytes = up(bytes);
+    if (bytes > hi - lo)
+      fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY, "device budget of " + std::to_string(size) +
+                                                      " bytes exhausted (" + std::to_string(bytes) + " more needed)");
+    void* p = base + lo;
+    lo += bytes;
+    peak = std::max(peak, lo + (size - hi));
+    return p;
+  }
+  void* temp(uint64_t bytes) {
+    bytes = up(bytes);
+    if (bytes > hi - lo)
+      fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY, "device budget of " + std::to_string(size) +
+                                                      " bytes exhausted (" + std::to_string(bytes) + " more needed)");
+    hi -= bytes;
+    peak = std::max(peak, lo + (size - hi));
+    return base + hi;
+  }
+  void drop_temps() { hi = size; }
 };
 
 // Grow-only pinned host buffer.
@@ -120,8 +157,11 @@ enum OperandPlan : uint32_t {
 };
 // Widest X handled by the dense accumulator (wider operands run in column tiles).
 int64_t wide_threshold(uint32_t mode);
+// rg (budgeted runs): every device buffer of the build comes from the region -- the layouts the run
+// reads are kept, the raw upload and the scratch are temporaries dropped (after a stream sync) on return.
+struct Region;
 std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode, bool temp,
-                                       uint32_t plan = kPlanAuto);
+                                       uint32_t plan = kPlanAuto, Region* rg = nullptr);
 
 // C = A * X; A is a CSR rows view (host or device).
 void spgemm_rows(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_b200_output& out);

@@ -358,9 +358,10 @@ static __global__ void __launch_bounds__(1024) k_scan_part(int64_t* __restrict__
   if (threadIdx.x == 0) ctl->nnz = static_cast<unsigned long long>(carry);
 }
 
+template <class OutT = int64_t>
 static __global__ void __launch_bounds__(kScanThreads) k_scan_down(const int32_t* __restrict__ in, int64_t n,
                                                             const int64_t* __restrict__ part,
-                                                            int64_t* __restrict__ out) {
+                                                            OutT* __restrict__ out) {
   __shared__ int64_t tmp[32];
   int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile;
   // each thread owns kScanItems consecutive items
@@ -379,7 +380,7 @@ static __global__ void __launch_bounds__(kScanThreads) k_scan_down(const int32_t
   for (int i = 0; i < kScanItems; i++) {
     int64_t j = base + static_cast<int64_t>(threadIdx.x) * kScanItems + i;
     run += v[i];
-    if (j < n) out[j + 1] = run;
+    if (j < n) out[j + 1] = static_cast<OutT>(run);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = 0;
 }

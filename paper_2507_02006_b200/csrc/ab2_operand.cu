@@ -194,7 +194,7 @@ __global__ void k_x_pcount(const int64_t* __restrict__ xptr, int64_t K, int w5, 
 
 __global__ void k_x_pfill(const int64_t* __restrict__ xptr, const int32_t* __restrict__ xcol,
                           const float* __restrict__ xval, int64_t K, int w5, uint32_t trash,
-                          const int64_t* __restrict__ pstart, uint2* __restrict__ desc, uint2* __restrict__ ent,
+                          const uint32_t* __restrict__ pstart, uint2* __restrict__ desc, uint2* __restrict__ ent,
                           int64_t dummy) {
   if (blockIdx.x == 0 && threadIdx.x < w5) ent[dummy * w5 + threadIdx.x] = make_uint2(trash * 4u, kOneBits);
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k <= K;
@@ -344,7 +344,8 @@ int64_t wide_threshold(uint32_t mode) {
   return std::max<int64_t>(32, std::min<int64_t>(dense_max, env_int("AB2_WIDE_AT", dense_max)));
 }
 
-std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode, bool temp, uint32_t plan) {
+std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode, bool temp, uint32_t plan,
+                                       Region* rg) {
   if (b.layout != AIRES_B200_CSR && b.layout != AIRES_B200_CSC)
     fail(AIRES_B200_INVALID_ARGUMENT, "operand layout must be CSR or CSC");
   if ((b.idx_bytes != 4 && b.idx_bytes != 8) || (b.val_bytes != 4 && b.val_bytes != 8))
@@ -374,13 +375,19 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
   const uint64_t* dptr = b.ptr;
   const void* didx = b.idx;
   const void* dval = b.val;
+  // a budgeted lean build from a host CSR already in the canonical widths (u32 columns, fp32 values,
+  // ptr[0] = 0) converts the raw upload in place: it is the plain CSR the step list is built from
+  const bool lean = rg && (plan & kPlanLean) && (plan & kPlanStep) && !(plan & (kPlanSlots | kPlanCSlots));
+  bool in_place = false;
   if (b.location == AIRES_B200_HOST) {
     p0 = b.ptr[0];
     p1 = b.ptr[nptr - 1];
     if (p1 < p0 || p1 > b.span) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "operand pointer array exceeds its span");
-    uint64_t* up = ctx.x_ptr.as<uint64_t>(nptr);
-    void* ui = ctx.x_idx.get(std::max<uint64_t>(p1, 1) * b.idx_bytes);
-    void* uv = ctx.x_val.get(std::max<uint64_t>(p1, 1) * b.val_bytes);
+    in_place = lean && p0 == 0 && b.layout == AIRES_B200_CSR && b.idx_bytes == 4 && b.val_bytes == 4 &&
+               mode == AIRES_B200_MODE_FP32;
+    uint64_t* up = rg ? static_cast<uint64_t*>(rg->temp(nptr * 8)) : ctx.x_ptr.as<uint64_t>(nptr);
+    void* ui = rg ? rg->temp(std::max<uint64_t>(p1, 1) * b.idx_bytes) : ctx.x_idx.get(std::max<uint64_t>(p1, 1) * b.idx_bytes);
+    void* uv = rg ? rg->temp(std::max<uint64_t>(p1, 1) * b.val_bytes) : ctx.x_val.get(std::max<uint64_t>(p1, 1) * b.val_bytes);
     AB2_CUDA(cudaMemcpyAsync(up, b.ptr, nptr * 8, cudaMemcpyHostToDevice, ctx.stream));
     if (p1 > p0) {  // same absolute positions as on the host
       AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(ui) + p0 * b.idx_bytes,
@@ -410,15 +417,29 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
     plan = mode == AIRES_B200_MODE_FP32 && env_int("AB2_NUMERIC", 3) == 5 ? kPlanStep : kPlanSlots;
   if (mode != AIRES_B200_MODE_FP32) plan &= ~static_cast<uint32_t>(kPlanStep);
   auto alloc = [&](DevBuf& cache, size_t bytes) -> void* {
+    if (rg) {
+      x->bytes += Region::up(bytes);
+      return rg->keep(bytes);
+    }
     if (temp) {
       x->bytes += std::max<size_t>(bytes, 256);
       return cache.get(bytes);
     }
     return dmalloc(bytes, &x->bytes);
   };
-  x->ptr = alloc(ctx.xo_ptr, (x->K + 1) * 8);
-  x->col = alloc(ctx.xo_col, std::max<int64_t>(x->nnz, 1) * 4);
-  x->val = alloc(ctx.xo_val, std::max<int64_t>(x->nnz, 1) * vb);
+  if (in_place) {  // the raw upload (same positions, p0 = 0) becomes the plain CSR
+    x->ptr = const_cast<uint64_t*>(dptr);
+    x->col = const_cast<void*>(didx);
+    x->val = const_cast<void*>(dval);
+  } else if (lean) {  // the plain CSR is a build temporary
+    x->ptr = rg->temp((x->K + 1) * 8);
+    x->col = rg->temp(std::max<int64_t>(x->nnz, 1) * 4);
+    x->val = rg->temp(std::max<int64_t>(x->nnz, 1) * vb);
+  } else {
+    x->ptr = alloc(ctx.xo_ptr, (x->K + 1) * 8);
+    x->col = alloc(ctx.xo_col, std::max<int64_t>(x->nnz, 1) * 4);
+    x->val = alloc(ctx.xo_val, std::max<int64_t>(x->nnz, 1) * vb);
+  }
   if (mode == AIRES_B200_MODE_FP32)
     fill_dispatch<float>(ctx, *x, b, dptr, p0, didx, dval, ctl);
   else
@@ -493,18 +514,27 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
     const int64_t fw = env_int("AB2_W5", 0);
     if (fw == 2 || fw == 4 || fw == 8 || fw == 16 || fw == 32) w5 = static_cast<int>(fw);
     x->W5 = w5;
-    int32_t* pc = ctx.cnt.as<int32_t>(std::max<int64_t>(x->K, 1));
-    int64_t* ps = ctx.cptr.as<int64_t>(x->K + 1);
+    const int64_t nb = (x->K + kScanTile - 1) / kScanTile;
+    int32_t* pc = rg ? static_cast<int32_t*>(rg->temp(std::max<int64_t>(x->K, 1) * 4))
+                     : ctx.cnt.as<int32_t>(std::max<int64_t>(x->K, 1));
+    uint32_t* ps = rg ? static_cast<uint32_t*>(rg->temp((x->K + 1) * 4))
+                      : reinterpret_cast<uint32_t*>(ctx.cptr.as<int64_t>(x->K / 2 + 1));
+    int64_t* part = rg ? static_cast<int64_t*>(rg->temp(std::max<int64_t>(nb, 1) * 8))
+                       : ctx.scan_part.as<int64_t>(std::max<int64_t>(nb, 1));
     const int g = grid_for(std::max<int64_t>(x->K + 1, 1), 256, ctx.sms);
     k_x_pcount<<<g, 256, 0, ctx.stream>>>(static_cast<const int64_t*>(x->ptr), x->K, w5, pc);
-    const int64_t nb = (x->K + kScanTile - 1) / kScanTile;
-    int64_t* part = ctx.scan_part.as<int64_t>(std::max<int64_t>(nb, 1));
+    int64_t n_slots = 0;
     if (x->K > 0) {
       k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(pc, x->K, part);
       k_scan_part<<<1, 1024, 0, ctx.stream>>>(part, nb, ctl);
-      k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(pc, x->K, part, ps);
+      k_scan_down<uint32_t><<<static_cast<unsigned>(nb), kScanThreads, 0, ctx.stream>>>(pc, x->K, part, ps);
+      // the exact slot count (one readback) sizes the entry array
+      AB2_CUDA(cudaMemcpyAsync(&h->nnz, &ctl->nnz, 8, cudaMemcpyDeviceToHost, ctx.stream));
+      AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+      n_slots = static_cast<int64_t>(h->nnz);
     }
-    const int64_t slots_ub = x->nnz / w5 + x->K + 2;  // + the dummy slot
+    if (n_slots >= (int64_t(1) << 32) - 1) fail(AIRES_B200_CAPACITY_EXCEEDED, "feature step list exceeds 2^32 slots");
+    const int64_t slots_ub = n_slots + 1;  // + the dummy slot
     x->dummy_slot = slots_ub - 1;
     x->xdesc = alloc(ctx.xo_desc, (x->K + 1) * sizeof(uint2));
     x->xent = alloc(ctx.xo_ent, slots_ub * w5 * sizeof(uint2));
@@ -516,7 +546,13 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
     x->prep_launches += x->K > 0 ? 5 : 2;
   }
   x->prep_launches += (b.layout == AIRES_B200_CSR ? 1 : 6) + 2;
-  if ((plan & kPlanLean) && (plan & kPlanStep) && x->xdesc && !x->slots && !x->cslots && temp) {
+  if (rg) {
+    // the build's temporaries (raw upload, scratch, and the plain CSR of a lean build) go back to
+    // the region once the kernels reading them are done
+    AB2_CUDA(cudaStreamSynchronize(ctx.stream));
+    rg->drop_temps();
+    if (lean) x->ptr = x->col = x->val = nullptr;
+  } else if ((plan & kPlanLean) && (plan & kPlanStep) && x->xdesc && !x->slots && !x->cslots && temp) {
     // tight budgets: the step list is the only layout the product and the sizing kernels read, so
     // the plain CSR (the build's input) is released rather than held through the run
     AB2_CUDA(cudaStreamSynchronize(ctx.stream));

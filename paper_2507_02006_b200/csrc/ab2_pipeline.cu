@@ -84,6 +84,7 @@ struct PipeCacheImpl {
   cudaStream_t h2d = nullptr, d2h = nullptr, aux = nullptr;  // aux: sizing (capped streamed run), fragments (MaxMemory)
   std::vector<cudaEvent_t> ev, tev;  // disable-timing / timing
   std::vector<DevBuf> bufs;
+  DevBuf region;  // the capped streamed run's budget, carved by a Region
   PipeCacheImpl() {
     AB2_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
     AB2_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
@@ -482,24 +483,26 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
   // (the step list alone: the sizing kernel walks it too, so the plain CSR is released after the build)
   uint32_t plan = mode == AIRES_B200_MODE_FP32 && (xk + 1) * 16 * 8 * 8 > budget ? kPlanStep | kPlanLean : kPlanSlots;
   if (!(plan & kPlanLean) && xk > 0 && xnnz >= 4 * xk && xk * kCSlotW * 2 * 16 <= budget) plan |= kPlanCSlots;
-  auto x = make_operand(ctx, b, mode, /*temp=*/true, plan);
-  uint64_t x_dev = x->bytes;
-  if (b.location == AIRES_B200_HOST) {
-    const uint64_t raw = ctx.x_ptr.cap + ctx.x_idx.cap + ctx.x_val.cap;
-    x_dev = x_dev > raw ? x_dev - raw : 0;
+  // Everything the run holds on the device -- X's layouts, the build's temporaries (raw upload,
+  // scratch, the plain CSR of a lean build), the tile ring -- is carved from one budget-sized region
+  // (cached across calls, so no cudaMalloc / cudaFree on the run's path).
+  (void)arena;
+  Region rg;
+  rg.init(st.c.region.get(budget), budget);
+  auto x = make_operand(ctx, b, mode, /*temp=*/true, plan, &rg);
+  if (b.location == AIRES_B200_HOST)
     rep.h2d_bytes += xk * 8 + 8 + static_cast<uint64_t>(x->nnz) * (b.idx_bytes + b.val_bytes);
-  }
-  Ctl* d_ctl = static_cast<Ctl*>(arena.get(sizeof(Ctl) * nbuf * (kMaxParts + 1)));
-  auto* d_bad = static_cast<unsigned long long*>(arena.get(8));  // max of every part's ctl->bad_row
+  Ctl* d_ctl = static_cast<Ctl*>(rg.keep(sizeof(Ctl) * nbuf * (kMaxParts + 1)));
+  auto* d_bad = static_cast<unsigned long long*>(rg.keep(8));  // max of every part's ctl->bad_row
   AB2_CUDA(cudaMemsetAsync(d_bad, 0, 8, cs));
-  const uint64_t fixed = x_dev + arena.used + (64 << 10);
+  const uint64_t fixed = rg.lo + (64 << 10);
   if (budget <= fixed)
     fail(AIRES_B200_INSUFFICIENT_DEVICE_MEMORY, "device budget " + std::to_string(budget) +
                                                     " does not cover the resident operand and row arrays (" +
                                                     std::to_string(fixed) + " bytes)");
   const uint64_t slot_bytes = ((budget - fixed) / nbuf) & ~uint64_t(255);
   std::vector<char*> slot_mem(nbuf);
-  for (uint32_t s = 0; s < nbuf; s++) slot_mem[s] = static_cast<char*>(arena.get(slot_bytes));
+  for (uint32_t s = 0; s < nbuf; s++) slot_mem[s] = static_cast<char*>(rg.keep(slot_bytes));
   auto* h_rep = static_cast<TileReport*>(ctx.h_ctl.get(sizeof(TileReport) * nbuf));
   // the caller's allocator: an upper bound of nnz(C); the exact count is reported in out.nnz
   const uint64_t bound = c_bound(*x, n, pend - p0);
@@ -730,7 +733,7 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
   rep.segments = parts_total;
   rep.flops = flops;
   rep.c_nnz = running;
-  rep.peak_device_bytes = arena.used + x_dev;
+  rep.peak_device_bytes = rg.peak;
   rep.phase1_ms = ms_between(t_begin, t_p1);
   rep.phase2_ms = ms_between(t_p1, t_p2);
   rep.phase3_ms = ms_between(t_p2, t_end);

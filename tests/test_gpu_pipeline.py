@@ -244,7 +244,10 @@ def test_stream_out_capped_fp32_matches_exact_protocol(n_buffers):
     assert np.array_equal(res.c.col_idx, exact.c.col_idx)
     np.testing.assert_allclose(res.c.values, exact.c.values, rtol=2e-6)
     assert res.report.flops == exact.report.flops
-    assert res.report.ledger.h2d.bytes < exact.report.ledger.h2d.bytes
+    # A crosses the link once; each tile's row pointers include its end row
+    base = 8 * (g.n_rows + 1) + 8 * g.nnz() + 8 * (x.n_rows + 1) + 8 * x.nnz()
+    assert base <= res.report.ledger.h2d.bytes <= base + 8 * res.report.segments
+    assert res.report.ledger.h2d.bytes <= exact.report.ledger.h2d.bytes + 8 * res.report.segments
 
 
 def test_stream_out_capped_edge_shapes():
