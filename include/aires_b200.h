@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define AIRES_B200_ABI_VERSION 1
+#define AIRES_B200_ABI_VERSION 2
 
 /* status codes (1 + errc) */
 enum {
@@ -153,6 +153,32 @@ int aires_b200_robw_cuts(const uint64_t* row_ptr, uint64_t n_rows, uint64_t m_a,
                          uint64_t* cuts, uint64_t cap, uint64_t* n_segs, uint64_t* bad_row);
 
 /* ---- out-of-core run (Alg. 2 as a real multi-stream pipeline) ---------- */
+/*
+ * One measured event of a real run -- the TraceEvent of tiered_sim.hpp:60-68 with device clocks:
+ * timestamps are the completion times of CUDA events recorded on the stream that did the work,
+ * in ms after the run's first event.  Buffers are named the reference's way by the C++ glue:
+ * AIRES_B200_BUF_B -> "B", _A_TILE -> "a_tile_<index>", _C_BLOCK -> "C" (d2h of block <index>),
+ * _FRAGMENT -> "frag_<index>" (MaxMemory's returned row fragment), _A -> "A".
+ */
+enum { AIRES_B200_EV_TRANSFER = 0, AIRES_B200_EV_COMPUTE = 1, AIRES_B200_EV_ALLOC = 2, AIRES_B200_EV_FREE = 3 };
+enum { AIRES_B200_CH_GDS = 0, AIRES_B200_CH_S2H = 1, AIRES_B200_CH_H2D = 2, AIRES_B200_CH_D2H = 3 };
+enum { AIRES_B200_TIER_DEVICE = 0, AIRES_B200_TIER_HOST = 1, AIRES_B200_TIER_STORAGE = 2 };
+enum { AIRES_B200_BUF_B = 0, AIRES_B200_BUF_A_TILE = 1, AIRES_B200_BUF_C_BLOCK = 2, AIRES_B200_BUF_FRAGMENT = 3,
+       AIRES_B200_BUF_A = 4 /* A's row pointers / the sizing pass's column chunks -> "A" */ };
+typedef struct aires_b200_trace_event {
+  double timestamp_ms; /* completion, ms after the run's first event */
+  double duration_ms;  /* device time of the span (transfers, compute); 0 for alloc / free */
+  uint32_t kind;       /* AIRES_B200_EV_* (EventKind order) */
+  uint32_t phase;      /* 0, 1, 2 = Phase I, II, III */
+  uint32_t where;      /* transfers: AIRES_B200_CH_* (ChannelId order); otherwise AIRES_B200_TIER_* */
+  uint32_t buffer;     /* AIRES_B200_BUF_* */
+  uint64_t index;      /* tile / block index of the buffer */
+  uint64_t bytes;
+  uint64_t flops;
+} aires_b200_trace_event;
+/* Receives the whole trace once, sorted by timestamp, after the run completed. */
+typedef void (*aires_b200_trace_fn)(void* user, const aires_b200_trace_event* events, uint64_t n);
+
 typedef struct aires_b200_run_config {
   uint64_t device_budget; /* bytes the run may hold on the device at once (0 = no cap) */
   uint32_t mode;          /* AIRES_B200_MODE_* */
@@ -161,6 +187,8 @@ typedef struct aires_b200_run_config {
                                 returned to the host and re-sent, scheduler.hpp:174-293) */
   uint32_t n_buffers;     /* tile ring depth (default 2; 3 for streamed output) */
   uint32_t flags;         /* AIRES_B200_RUN_* bits (0 = the reference's exact-allocation protocol) */
+  aires_b200_trace_fn trace; /* optional: the run's measured trace (RunResult::trace) */
+  void* trace_user;
 } aires_b200_run_config;
 
 /* Streamed output (uncapped runs, device_budget 0): no sizing pass before the product.  c->alloc
@@ -182,6 +210,12 @@ typedef struct aires_b200_run_report {
   double phase2_ms;  /* tile streaming */
   double phase3_ms;  /* final drain / assembly */
   uint64_t merge_bytes; /* MaxMemory: fragment bytes re-sent after the host stitch (IoLedger::merge_bytes) */
+  /* ChannelTotals (tiered_sim.hpp:70-76) of the run: one transfer per tile upload / block drain */
+  uint64_t h2d_count;
+  uint64_t d2h_count;
+  double h2d_ms;        /* sum of the transfers' device durations */
+  double d2h_ms;
+  double merge_ms;      /* MaxMemory: fragment return + the re-sent share of uploads (RunReport::merge_seconds) */
 } aires_b200_run_report;
 
 /* A in host memory (CSR); B host or device; C written through c->alloc (host). */

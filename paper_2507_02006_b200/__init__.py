@@ -82,16 +82,29 @@ class _Output(C.Structure):
     ]
 
 
+ABI_VERSION = 2  # AIRES_B200_ABI_VERSION of include/aires_b200.h
+
+
+class _TraceEvent(C.Structure):
+    _fields_ = [("timestamp_ms", C.c_double), ("duration_ms", C.c_double), ("kind", C.c_uint32),
+                ("phase", C.c_uint32), ("where", C.c_uint32), ("buffer", C.c_uint32), ("index", C.c_uint64),
+                ("bytes", C.c_uint64), ("flops", C.c_uint64)]
+
+
+_TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(_TraceEvent), C.c_uint64)
+
+
 class _RunConfig(C.Structure):
     _fields_ = [("device_budget", C.c_uint64), ("mode", C.c_uint32), ("c_aware", C.c_uint32),
-                ("n_buffers", C.c_uint32), ("flags", C.c_uint32)]
+                ("n_buffers", C.c_uint32), ("flags", C.c_uint32), ("trace", _TRACE_FN), ("trace_user", C.c_void_p)]
 
 
 class _RunReport(C.Structure):
     _fields_ = [("segments", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("flops", C.c_uint64), ("c_nnz", C.c_uint64), ("peak_device_bytes", C.c_uint64),
                 ("total_ms", C.c_double), ("phase1_ms", C.c_double), ("phase2_ms", C.c_double),
-                ("phase3_ms", C.c_double), ("merge_bytes", C.c_uint64)]
+                ("phase3_ms", C.c_double), ("merge_bytes", C.c_uint64), ("h2d_count", C.c_uint64),
+                ("d2h_count", C.c_uint64), ("h2d_ms", C.c_double), ("d2h_ms", C.c_double), ("merge_ms", C.c_double)]
 
 
 _SEG_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64),
@@ -125,6 +138,8 @@ def lib() -> C.CDLL:
     L = C.CDLL(LIB_PATH)
     P = C.POINTER
     L.aires_b200_abi_version.restype = C.c_int
+    if L.aires_b200_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"{LIB_PATH} has ABI {L.aires_b200_abi_version()}, the bindings expect {ABI_VERSION}: rebuild")
     L.aires_b200_last_error.restype = C.c_char_p
     L.aires_b200_device_count.argtypes = [P(C.c_int)]
     L.aires_b200_set_device.argtypes = [C.c_int]
@@ -455,10 +470,40 @@ class RunReport:
 
 @dataclasses.dataclass
 class RunResult:
-    """scheduler.hpp:39-43 (trace: no simulator events; NVTX/ncu cover tracing on the device)."""
+    """scheduler.hpp:39-43; trace = the measured TraceEvents of the run (CUDA-event clocks)."""
     c: CsrMatrix
     report: RunReport
     trace: list
+
+
+@dataclasses.dataclass
+class TraceEvent:
+    """tiered_sim.hpp:60-68 with device clocks: timestamp = completion (s after the run's first
+    event); kind transfer/compute/alloc/free; phase I/II/III; where = channel or tier name."""
+    timestamp: float
+    kind: str
+    phase: str
+    where: str
+    buffer: str
+    bytes: int
+    flops: int
+    duration: float = 0.0
+
+
+_EV_KIND = ("transfer", "compute", "alloc", "free")
+_EV_PHASE = ("I", "II", "III")
+_EV_CH = ("gds", "s2h", "h2d", "d2h")
+_EV_TIER = ("device", "host", "storage")
+
+
+def _buffer_name(buf: int, index: int) -> str:
+    return ("B", f"a_tile_{index}", "C", f"frag_{index}", "A")[buf]
+
+
+def _trace_events(evs) -> list:
+    return [TraceEvent(e.timestamp_ms / 1e3, _EV_KIND[e.kind], _EV_PHASE[e.phase],
+                       _EV_CH[e.where] if e.kind == 0 else _EV_TIER[e.where], _buffer_name(e.buffer, e.index),
+                       int(e.bytes), int(e.flops), e.duration_ms / 1e3) for e in evs]
 
 
 def run_maxmemory(a: CsrMatrix, b, budget: MemoryBudget, cfg=None, mode: int = MODE_AUTO, n_buffers: int = 2,
@@ -498,20 +543,28 @@ def run_aires(a: CsrMatrix, b, budget: MemoryBudget, cfg=None, mode: int = MODE_
         am.val_bytes = keep_a[2].dtype.itemsize
     al = _HostAlloc(keep_a[1].dtype, vdt)
     out = al.output()
+    events = []
+
+    def _on_trace(_user, evs, n):
+        events.extend(_trace_events(evs[i] for i in range(n)))
+
+    trace_fn = _TRACE_FN(_on_trace)
     cfgc = _RunConfig(int(budget.device_total), mode, 2 if c_aware == 2 else int(bool(c_aware)),
-                      0 if stream_out and n_buffers == 2 else int(n_buffers), RUN_STREAM_OUT if stream_out else 0)
+                      0 if stream_out and n_buffers == 2 else int(n_buffers), RUN_STREAM_OUT if stream_out else 0,
+                      trace_fn, None)
     rep = _RunReport()
     _check(L.aires_b200_run(C.byref(am), C.byref(bm), C.byref(cfgc), C.byref(out), C.byref(rep)))
     c = CsrMatrix(a.n_rows, b.n_cols, al.ptr, al.idx[: out.nnz], al.val[: out.nnz])
     r = RunReport(budget_bytes=int(budget.device_total), total_s=rep.total_ms / 1e3, phase1_s=rep.phase1_ms / 1e3,
                   phase2_s=rep.phase2_ms / 1e3, phase3_s=rep.phase3_ms / 1e3, segments=int(rep.segments),
-                  flops=int(rep.flops))
-    r.ledger.h2d.bytes, r.ledger.d2h.bytes = int(rep.h2d_bytes), int(rep.d2h_bytes)
+                  flops=int(rep.flops), merge_seconds=rep.merge_ms / 1e3)
+    r.ledger.h2d = ChannelTotals(int(rep.h2d_count), int(rep.h2d_bytes), rep.h2d_ms / 1e3)
+    r.ledger.d2h = ChannelTotals(int(rep.d2h_count), int(rep.d2h_bytes), rep.d2h_ms / 1e3)
     r.ledger.peak_device_occupancy = int(rep.peak_device_bytes)
     r.ledger.merge_bytes = int(rep.merge_bytes)
     if with_checksum:
         r.c_checksum = checksum(c)
-    return RunResult(c, r, [])
+    return RunResult(c, r, events)
 
 
 # ---------------------------------------------------------------------------

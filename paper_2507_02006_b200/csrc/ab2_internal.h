@@ -50,9 +50,9 @@ struct Region {
   uint64_t size = 0, lo = 0, hi = 0, peak = 0;
   void init(void* p, uint64_t n) {
     base = static_cast<char*>(p);
-    size = n;
+    size = n & ~uint64_t(255);  // both ends 256-byte aligned
     lo = 0;
-    hi = n;
+    hi = size;
     peak = 0;
   }
   static uint64_t up(uint64_t b) { return (std::max<uint64_t>(b, 1) + 255) & ~uint64_t(255); }

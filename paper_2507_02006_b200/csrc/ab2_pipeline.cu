@@ -32,6 +32,8 @@
 #include <cstring>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ab2_internal.h"
 #include "ab2_kernels.cuh"
 
@@ -121,6 +123,94 @@ struct Streams {
     }
     return c.tev[nt++];
   }
+};
+
+// The measured trace of a run (RunResult::trace, tiered_sim.hpp:60-98): every transfer, compute span
+// and device allocation is bracketed by timed CUDA events on the stream that does the work, the
+// NVTX range of the enclosing phase marks the host side, and finish() turns the events into the
+// ChannelTotals of the report (count, bytes, seconds) and the time-sorted event list.
+struct Tracer {
+  struct Rec {
+    cudaEvent_t a, b;  // a == b for alloc / free
+    aires_b200_trace_event e;
+  };
+  Streams& st;
+  std::vector<Rec> recs;
+  uint32_t phase = 0;
+  explicit Tracer(Streams& s) : st(s) {}
+  void set_phase(uint32_t p, const char* name) {
+    if (phase_open) nvtxRangePop();
+    phase = p;
+    nvtxRangePushA(name);
+    phase_open = true;
+  }
+  ~Tracer() {
+    if (phase_open) nvtxRangePop();
+  }
+  // brackets the work fn() enqueues on stream s; returns the record (flops may be filled in later)
+  template <class F>
+  size_t span(cudaStream_t s, uint32_t kind, uint32_t where, uint32_t buf, uint64_t index, uint64_t bytes,
+              uint64_t flops, F&& fn) {
+    Rec r{st.make_timed(), st.make_timed(), {}};
+    r.e.kind = kind;
+    r.e.phase = phase;
+    r.e.where = where;
+    r.e.buffer = buf;
+    r.e.index = index;
+    r.e.bytes = bytes;
+    r.e.flops = flops;
+    AB2_CUDA(cudaEventRecord(r.a, s));
+    fn();
+    AB2_CUDA(cudaEventRecord(r.b, s));
+    recs.push_back(r);
+    return recs.size() - 1;
+  }
+  void point(cudaStream_t s, uint32_t kind, uint32_t buf, uint64_t index, uint64_t bytes) {
+    Rec r{st.make_timed(), nullptr, {}};
+    r.b = r.a;
+    r.e.kind = kind;
+    r.e.phase = phase;
+    r.e.where = AIRES_B200_TIER_DEVICE;
+    r.e.buffer = buf;
+    r.e.index = index;
+    r.e.bytes = bytes;
+    AB2_CUDA(cudaEventRecord(r.a, s));
+    recs.push_back(r);
+  }
+  // after the run's last synchronisation
+  // MaxMemory: records whose duration (times the share) is merge time -- fragment returns, re-sends
+  std::vector<std::pair<size_t, double>> merge_share;
+  void finish(cudaEvent_t t0, aires_b200_run_report& rep, const aires_b200_run_config& cfg) {
+    std::vector<aires_b200_trace_event> ev;
+    ev.reserve(recs.size());
+    rep.h2d_count = rep.d2h_count = 0;
+    rep.h2d_ms = rep.d2h_ms = 0.0;
+    for (Rec& r : recs) {
+      float t = 0.f, d = 0.f;
+      AB2_CUDA(cudaEventElapsedTime(&t, t0, r.b));
+      if (r.b != r.a) AB2_CUDA(cudaEventElapsedTime(&d, r.a, r.b));
+      r.e.timestamp_ms = std::max(0.0, static_cast<double>(t));
+      r.e.duration_ms = d;
+      if (r.e.kind == AIRES_B200_EV_TRANSFER && r.e.where == AIRES_B200_CH_H2D) {
+        rep.h2d_count++;
+        rep.h2d_ms += d;
+      } else if (r.e.kind == AIRES_B200_EV_TRANSFER && r.e.where == AIRES_B200_CH_D2H) {
+        rep.d2h_count++;
+        rep.d2h_ms += d;
+      }
+      ev.push_back(r.e);
+    }
+    rep.merge_ms = 0.0;
+    for (const auto& m : merge_share) rep.merge_ms += recs[m.first].e.duration_ms * m.second;
+    if (!cfg.trace) return;
+    std::stable_sort(ev.begin(), ev.end(), [](const aires_b200_trace_event& x, const aires_b200_trace_event& y) {
+      return x.timestamp_ms < y.timestamp_ms || (x.timestamp_ms == y.timestamp_ms && x.phase < y.phase);
+    });
+    cfg.trace(cfg.trace_user, ev.data(), ev.size());
+  }
+
+ private:
+  bool phase_open = false;
 };
 
 // Device allocations of the run (charged against the budget), from the cached grow-only buffers.
@@ -217,7 +307,8 @@ __global__ void k_tile_ptr(const int64_t* __restrict__ in, int64_t n, const Ctl*
 // first tile on -- with exact sizing first, D2H cannot start before every column of A has crossed
 // the link (the run's Phase I).  Same results as the exact run; out.nnz is the exact count.
 void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b, uint32_t mode, uint32_t nbuf,
-                aires_b200_output& out, aires_b200_run_report& rep, Streams& st, Arena& arena, Pinned& pin) {
+                aires_b200_output& out, aires_b200_run_report& rep, Streams& st, Arena& arena, Pinned& pin, Tracer& tr,
+                const aires_b200_run_config& cfg) {
   const uint32_t ib = a.idx_bytes, vb = mode == AIRES_B200_MODE_FP32 ? 4 : 8;
   const uint64_t n = a.n_rows;
   const uint64_t p0 = a.ptr[0], pend = a.ptr[n];
@@ -225,12 +316,21 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
   cudaEvent_t t_begin = st.make_timed(), t_p1 = st.make_timed(), t_p2 = st.make_timed(), t_end = st.make_timed();
   AB2_CUDA(cudaEventRecord(t_begin, cs));
   AB2_CUDA(cudaStreamWaitEvent(st.h2d, t_begin, 0));
-  auto x = make_operand(ctx, b, mode, /*temp=*/true, kPlanSlots);
-  if (b.location == AIRES_B200_HOST)
-    rep.h2d_bytes += (b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols) * 8 + 8 +
-                     static_cast<uint64_t>(x->nnz) * (b.idx_bytes + b.val_bytes);
+  tr.set_phase(0, "aires phase I (X operand, A row_ptr)");
+  std::unique_ptr<XOperand> x;
+  const uint64_t x_h2d = b.location == AIRES_B200_HOST
+                             ? (b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols) * 8 + 8 +
+                                   (b.ptr[b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols] - b.ptr[0]) *
+                                       (b.idx_bytes + b.val_bytes)
+                             : 0;
+  tr.span(cs, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_B, 0, x_h2d, 0,
+          [&] { x = make_operand(ctx, b, mode, /*temp=*/true, kPlanSlots); });
+  tr.point(cs, AIRES_B200_EV_ALLOC, AIRES_B200_BUF_B, 0, x->bytes);
+  rep.h2d_bytes += x_h2d;
   uint64_t* d_aptr = static_cast<uint64_t*>(arena.get((n + 1) * 8));
-  AB2_CUDA(cudaMemcpyAsync(d_aptr, a.ptr, (n + 1) * 8, cudaMemcpyHostToDevice, st.h2d));
+  tr.span(st.h2d, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_A, 0, (n + 1) * 8, 0, [&] {
+    AB2_CUDA(cudaMemcpyAsync(d_aptr, a.ptr, (n + 1) * 8, cudaMemcpyHostToDevice, st.h2d));
+  });
   rep.h2d_bytes += (n + 1) * 8;
   // row blocks of ~equal A nnz, the first one a quarter of the others (the D2H of C starts sooner)
   const uint64_t T = static_cast<uint64_t>(std::max<int64_t>(1, env_int("AB2_STREAM_TILES", 16)));
@@ -303,8 +403,11 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
   AB2_CUDA(cudaEventRecord(e_zero, cs));
   AB2_CUDA(cudaStreamWaitEvent(st.h2d, e_zero, 0));
   AB2_CUDA(cudaStreamWaitEvent(st.d2h, e_zero, 0));
+  tr.set_phase(1, "aires phase II (tiles)");
 
   uint64_t running = 0, flops = 0;
+  std::vector<size_t> compute_rec(n_tiles, 0);
+  std::vector<uint64_t> up_bytes(n_tiles, 0);
   auto drain = [&](uint64_t j) {
     Slot& s = slot[j % nbuf];
     AB2_CUDA(cudaEventSynchronize(s.computed));
@@ -313,13 +416,18 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
     const uint64_t r0 = cuts[j], rows = cuts[j + 1] - r0, nz = c[0];
     if (running + nz > bound) fail(AIRES_B200_CAPACITY_EXCEEDED, "C exceeds its bound");
     flops += c[1];
+    tr.recs[compute_rec[j]].e.flops = c[1];
     AB2_CUDA(cudaStreamWaitEvent(st.d2h, s.computed, 0));  // (already complete: the host waited on it)
-    AB2_CUDA(cudaMemcpyAsync(static_cast<uint64_t*>(optr) + r0, s.optr, (rows + 1) * 8, cudaMemcpyDeviceToHost, st.d2h));
-    if (nz) {
-      AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oidx) + running * ib, s.ccol, nz * ib, cudaMemcpyDeviceToHost, st.d2h));
-      AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oval) + running * vb, s.cval, nz * vb, cudaMemcpyDeviceToHost, st.d2h));
-    }
-    rep.d2h_bytes += (rows + 1) * 8 + nz * (ib + vb);
+    const uint64_t dn_bytes = (rows + 1) * 8 + nz * (ib + vb);
+    tr.span(st.d2h, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_D2H, AIRES_B200_BUF_C_BLOCK, j, dn_bytes, 0, [&] {
+      AB2_CUDA(cudaMemcpyAsync(static_cast<uint64_t*>(optr) + r0, s.optr, (rows + 1) * 8, cudaMemcpyDeviceToHost, st.d2h));
+      if (nz) {
+        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oidx) + running * ib, s.ccol, nz * ib, cudaMemcpyDeviceToHost, st.d2h));
+        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oval) + running * vb, s.cval, nz * vb, cudaMemcpyDeviceToHost, st.d2h));
+      }
+    });
+    rep.d2h_bytes += dn_bytes;
+    tr.point(st.d2h, AIRES_B200_EV_FREE, AIRES_B200_BUF_A_TILE, j, up_bytes[j]);
     AB2_CUDA(cudaEventRecord(s.drained, st.d2h));
     if (trace) AB2_CUDA(cudaEventRecord(tl[3 * j + 2], st.d2h));
     running += nz;
@@ -329,13 +437,17 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
     const uint64_t r0 = cuts[j], r1 = cuts[j + 1];
     const uint64_t q0 = a.ptr[r0], q1 = a.ptr[r1];
     if (j >= nbuf) AB2_CUDA(cudaStreamWaitEvent(st.h2d, s.drained, 0));
-    if (q1 > q0) {
-      AB2_CUDA(cudaMemcpyAsync(s.acol, static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib,
-                               cudaMemcpyHostToDevice, st.h2d));
-      AB2_CUDA(cudaMemcpyAsync(s.aval, static_cast<const char*>(a.val) + q0 * vb, (q1 - q0) * vb,
-                               cudaMemcpyHostToDevice, st.h2d));
-    }
-    rep.h2d_bytes += (q1 - q0) * (ib + vb);
+    up_bytes[j] = (q1 - q0) * (ib + vb);
+    tr.point(st.h2d, AIRES_B200_EV_ALLOC, AIRES_B200_BUF_A_TILE, j, up_bytes[j]);
+    tr.span(st.h2d, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_A_TILE, j, up_bytes[j], 0, [&] {
+      if (q1 > q0) {
+        AB2_CUDA(cudaMemcpyAsync(s.acol, static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib,
+                                 cudaMemcpyHostToDevice, st.h2d));
+        AB2_CUDA(cudaMemcpyAsync(s.aval, static_cast<const char*>(a.val) + q0 * vb, (q1 - q0) * vb,
+                                 cudaMemcpyHostToDevice, st.h2d));
+      }
+    });
+    rep.h2d_bytes += up_bytes[j];
     AB2_CUDA(cudaEventRecord(s.loaded, st.h2d));
     if (trace) AB2_CUDA(cudaEventRecord(tl[3 * j], st.h2d));
     AB2_CUDA(cudaStreamWaitEvent(cs, s.loaded, 0));
@@ -358,14 +470,14 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
     t.toff = s.toff;
     t.part = s.part;
     t.ctl = d_ctl + j;
-    ctx.launches += tile_product_staged(ctx, *x, ib, t);
-    {
+    compute_rec[j] = tr.span(cs, AIRES_B200_EV_COMPUTE, AIRES_B200_TIER_DEVICE, AIRES_B200_BUF_A_TILE, j, 0, 0, [&] {
+      ctx.launches += tile_product_staged(ctx, *x, ib, t);
       const int g = static_cast<int>(std::min<uint64_t>((r1 - r0 + 256) / 256, static_cast<uint64_t>(ctx.sms) * 4));
       k_tile_ptr<<<g, 256, 0, cs>>>(s.cptr, static_cast<int64_t>(r1 - r0 + 1), d_ctl + j, d_base + j, s.optr,
                                     h_rep + 3 * j);
       AB2_CUDA(cudaGetLastError());
       ctx.launches++;
-    }
+    });
     AB2_CUDA(cudaEventRecord(s.computed, cs));
     if (trace) AB2_CUDA(cudaEventRecord(tl[3 * j + 1], cs));
     if (j >= 1) drain(j - 1);
@@ -376,6 +488,8 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
   cudaEvent_t e_d2h = st.make();
   AB2_CUDA(cudaEventRecord(e_d2h, st.d2h));
   AB2_CUDA(cudaStreamWaitEvent(cs, e_d2h, 0));
+  tr.set_phase(2, "aires phase III (drain)");
+  tr.point(cs, AIRES_B200_EV_FREE, AIRES_B200_BUF_B, 0, x->bytes);
   AB2_CUDA(cudaEventRecord(t_end, cs));
   AB2_CUDA(cudaStreamSynchronize(cs));
   if (trace) {
@@ -389,6 +503,7 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
   rep.flops = flops;
   rep.c_nnz = running;
   rep.peak_device_bytes = arena.used + x->bytes;
+  tr.finish(t_begin, rep, cfg);
   rep.phase1_ms = ms_between(t_begin, t_p1);
   rep.phase2_ms = ms_between(t_p1, t_p2);
   rep.phase3_ms = ms_between(t_p2, t_end);
@@ -468,7 +583,7 @@ __global__ void k_tile_report(const Ctl* __restrict__ ctl, const int64_t* __rest
 // inside the tile), never a re-upload.  Slot layout: [A cols | A vals | per-row scratch | C region].
 void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b, uint32_t mode,
                        uint32_t nbuf, uint64_t budget, aires_b200_output& out, aires_b200_run_report& rep,
-                       Streams& st, Arena& arena, Pinned& pin) {
+                       Streams& st, Arena& arena, Pinned& pin, Tracer& tr, const aires_b200_run_config& cfg) {
   const uint32_t ib = a.idx_bytes, vb = mode == AIRES_B200_MODE_FP32 ? 4 : 8;
   const uint64_t n = a.n_rows;
   const uint64_t p0 = a.ptr[0], pend = a.ptr[n];
@@ -489,9 +604,14 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
   (void)arena;
   Region rg;
   rg.init(st.c.region.get(budget), budget);
-  auto x = make_operand(ctx, b, mode, /*temp=*/true, plan, &rg);
-  if (b.location == AIRES_B200_HOST)
-    rep.h2d_bytes += xk * 8 + 8 + static_cast<uint64_t>(x->nnz) * (b.idx_bytes + b.val_bytes);
+  tr.set_phase(0, "aires phase I (X operand)");
+  std::unique_ptr<XOperand> x;
+  const uint64_t x_h2d = b.location == AIRES_B200_HOST ? xk * 8 + 8 + xnnz * (b.idx_bytes + b.val_bytes) : 0;
+  tr.span(cs, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_B, 0, x_h2d, 0,
+          [&] { x = make_operand(ctx, b, mode, /*temp=*/true, plan, &rg); });
+  tr.point(cs, AIRES_B200_EV_ALLOC, AIRES_B200_BUF_B, 0, rg.lo);
+  const uint64_t x_keep = rg.lo;
+  rep.h2d_bytes += x_h2d;
   Ctl* d_ctl = static_cast<Ctl*>(rg.keep(sizeof(Ctl) * nbuf * (kMaxParts + 1)));
   auto* d_bad = static_cast<unsigned long long*>(rg.keep(8));  // max of every part's ctl->bad_row
   AB2_CUDA(cudaMemsetAsync(d_bad, 0, 8, cs));
@@ -513,6 +633,7 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
   pin.ensure(oidx, bound * ib);
   pin.ensure(oval, bound * vb);
   AB2_CUDA(cudaEventRecord(t_p1, cs));
+  tr.set_phase(1, "aires phase II (tiles)");
 
   auto r256 = [](uint64_t v) { return (v + 255) & ~uint64_t(255); };
   struct Tile {
@@ -528,6 +649,7 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
     cudaEvent_t sized;
     cudaEvent_t tl_loaded = nullptr, tl_computed = nullptr, tl_drained = nullptr;  // AB2_TRACE
     uint64_t parts = 0;
+    uint64_t up_bytes = 0;
   };
   // AB2_TRACE=1: per-tile device timeline (loaded / sized / last part computed / drained) on stderr
   const bool trace = env_int("AB2_TRACE", 0) != 0;
@@ -585,12 +707,18 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
     t.cval = m + r256(t.c_cap * ib);
     // upload (copy engine 0) once the slot's previous tile has drained
     if (slot_free[t.slot]) AB2_CUDA(cudaStreamWaitEvent(st.h2d, slot_free[t.slot], 0));
-    AB2_CUDA(cudaMemcpyAsync(t.aptr, a.ptr + t.r0, (rows + 1) * 8, cudaMemcpyHostToDevice, st.h2d));
-    if (an) {
-      AB2_CUDA(cudaMemcpyAsync(t.acol, static_cast<const char*>(a.idx) + t.q0 * ib, an * ib, cudaMemcpyHostToDevice, st.h2d));
-      AB2_CUDA(cudaMemcpyAsync(t.aval, static_cast<const char*>(a.val) + t.q0 * vb, an * vb, cudaMemcpyHostToDevice, st.h2d));
-    }
-    rep.h2d_bytes += (rows + 1) * 8 + an * (ib + vb);
+    const uint64_t up_bytes = (rows + 1) * 8 + an * (ib + vb);
+    const uint64_t j = tiles.size();
+    tr.point(st.h2d, AIRES_B200_EV_ALLOC, AIRES_B200_BUF_A_TILE, j, up_bytes);
+    tr.span(st.h2d, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_A_TILE, j, up_bytes, 0, [&] {
+      AB2_CUDA(cudaMemcpyAsync(t.aptr, a.ptr + t.r0, (rows + 1) * 8, cudaMemcpyHostToDevice, st.h2d));
+      if (an) {
+        AB2_CUDA(cudaMemcpyAsync(t.acol, static_cast<const char*>(a.idx) + t.q0 * ib, an * ib, cudaMemcpyHostToDevice, st.h2d));
+        AB2_CUDA(cudaMemcpyAsync(t.aval, static_cast<const char*>(a.val) + t.q0 * vb, an * vb, cudaMemcpyHostToDevice, st.h2d));
+      }
+    });
+    t.up_bytes = up_bytes;
+    rep.h2d_bytes += up_bytes;
     cudaEvent_t loaded = st.make();
     AB2_CUDA(cudaEventRecord(loaded, st.h2d));
     if (trace) {
@@ -604,29 +732,31 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
     Ctl* c = d_ctl + t.slot * (kMaxParts + 1);
     AB2_CUDA(cudaMemsetAsync(c, 0, sizeof(Ctl) * (kMaxParts + 1), zs));
     StreamSwap swap(ctx, zs);
-    TileSym sy{};
-    sy.aptr = t.aptr;
-    sy.abase = t.q0;
-    sy.acol = t.acol;
-    sy.rows = static_cast<int64_t>(rows);
-    sy.cnt = t.cnt;
-    sy.rflops = t.rflops;
-    sy.heavy = t.heavy;
-    sy.ctl = c;
-    ctx.launches += tile_symbolic(ctx, *x, ib, sy);
-    const int64_t nb = (static_cast<int64_t>(rows) + kScanTile - 1) / kScanTile;
-    int64_t* part = reinterpret_cast<int64_t*>(t.optr);  // scan partials: optr is written later
-    if (rows > 0) {
-      k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, zs>>>(t.cnt, static_cast<int64_t>(rows), part);
-      k_scan_part<<<1, 1024, 0, zs>>>(part, nb, c);
-      k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, zs>>>(t.cnt, static_cast<int64_t>(rows), part, t.cptr);
-      ctx.launches += 3;
-    } else {
-      AB2_CUDA(cudaMemsetAsync(t.cptr, 0, 8, zs));
-    }
-    k_tile_report<<<1, 32, 0, zs>>>(c, t.cptr, static_cast<int64_t>(rows), t.c_cap, h_rep + t.slot);
-    AB2_CUDA(cudaGetLastError());
-    ctx.launches++;
+    tr.span(zs, AIRES_B200_EV_COMPUTE, AIRES_B200_TIER_DEVICE, AIRES_B200_BUF_A_TILE, j, 0, 0, [&] {
+      TileSym sy{};
+      sy.aptr = t.aptr;
+      sy.abase = t.q0;
+      sy.acol = t.acol;
+      sy.rows = static_cast<int64_t>(rows);
+      sy.cnt = t.cnt;
+      sy.rflops = t.rflops;
+      sy.heavy = t.heavy;
+      sy.ctl = c;
+      ctx.launches += tile_symbolic(ctx, *x, ib, sy);
+      const int64_t nb = (static_cast<int64_t>(rows) + kScanTile - 1) / kScanTile;
+      int64_t* part = reinterpret_cast<int64_t*>(t.optr);  // scan partials: optr is written later
+      if (rows > 0) {
+        k_scan_reduce<<<static_cast<unsigned>(nb), kScanThreads, 0, zs>>>(t.cnt, static_cast<int64_t>(rows), part);
+        k_scan_part<<<1, 1024, 0, zs>>>(part, nb, c);
+        k_scan_down<<<static_cast<unsigned>(nb), kScanThreads, 0, zs>>>(t.cnt, static_cast<int64_t>(rows), part, t.cptr);
+        ctx.launches += 3;
+      } else {
+        AB2_CUDA(cudaMemsetAsync(t.cptr, 0, 8, zs));
+      }
+      k_tile_report<<<1, 32, 0, zs>>>(c, t.cptr, static_cast<int64_t>(rows), t.c_cap, h_rep + t.slot);
+      AB2_CUDA(cudaGetLastError());
+      ctx.launches++;
+    });
     t.sized = trace ? st.make_timed() : st.make();
     AB2_CUDA(cudaEventRecord(t.sized, zs));
     cursor = t.r1;
@@ -671,24 +801,28 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
       tp.cnt = reinterpret_cast<uint32_t*>(t.cnt) + pa;  // scratch (the counts are in cptr now)
       tp.toff = t.toff;
       tp.ctl = c + 1 + q;
-      ctx.launches += tile_product(ctx, *x, ib, tp);
-      {
+      tr.span(cs, AIRES_B200_EV_COMPUTE, AIRES_B200_TIER_DEVICE, AIRES_B200_BUF_A_TILE, j, 0, q == 0 ? r.flops : 0, [&] {
+        ctx.launches += tile_product(ctx, *x, ib, tp);
         const int g = static_cast<int>(std::min<uint64_t>((pb - pa + 256) / 256, static_cast<uint64_t>(ctx.sms) * 4));
         k_part_ptr<<<g, 256, 0, cs>>>(t.cptr + pa, static_cast<int64_t>(pb - pa + 1), base[q], running, t.optr + pa,
                                       c + 1 + q, d_bad);
         AB2_CUDA(cudaGetLastError());
         ctx.launches++;
-      }
+      });
       cudaEvent_t computed = trace ? st.make_timed() : st.make();
       AB2_CUDA(cudaEventRecord(computed, cs));
       AB2_CUDA(cudaStreamWaitEvent(st.d2h, computed, 0));
-      AB2_CUDA(cudaMemcpyAsync(static_cast<uint64_t*>(optr) + t.r0 + pa, t.optr + pa, (pb - pa + 1) * 8,
-                               cudaMemcpyDeviceToHost, st.d2h));
-      if (pn) {
-        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oidx) + running * ib, t.ccol, pn * ib, cudaMemcpyDeviceToHost, st.d2h));
-        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oval) + running * vb, t.cval, pn * vb, cudaMemcpyDeviceToHost, st.d2h));
-      }
-      rep.d2h_bytes += (pb - pa + 1) * 8 + pn * (ib + vb);
+      const uint64_t dn_bytes = (pb - pa + 1) * 8 + pn * (ib + vb);
+      tr.span(st.d2h, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_D2H, AIRES_B200_BUF_C_BLOCK, j, dn_bytes, 0, [&] {
+        AB2_CUDA(cudaMemcpyAsync(static_cast<uint64_t*>(optr) + t.r0 + pa, t.optr + pa, (pb - pa + 1) * 8,
+                                 cudaMemcpyDeviceToHost, st.d2h));
+        if (pn) {
+          AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oidx) + running * ib, t.ccol, pn * ib, cudaMemcpyDeviceToHost, st.d2h));
+          AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oval) + running * vb, t.cval, pn * vb, cudaMemcpyDeviceToHost, st.d2h));
+        }
+      });
+      rep.d2h_bytes += dn_bytes;
+      if (q + 1 == n_parts) tr.point(st.d2h, AIRES_B200_EV_FREE, AIRES_B200_BUF_A_TILE, j, t.up_bytes);
       prev_drain = trace ? st.make_timed() : st.make();
       AB2_CUDA(cudaEventRecord(prev_drain, st.d2h));
       if (trace) t.tl_computed = computed;
@@ -698,6 +832,7 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
     t.parts = static_cast<uint64_t>(n_parts);
     if (trace) t.tl_drained = prev_drain;
     if (n_parts == 0) {  // rows without entries still get their row pointers
+      tr.point(st.d2h, AIRES_B200_EV_FREE, AIRES_B200_BUF_A_TILE, j, t.up_bytes);
       prev_drain = st.make();
       AB2_CUDA(cudaEventRecord(prev_drain, st.d2h));
     }
@@ -710,6 +845,8 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
   cudaEvent_t e_d2h = st.make();
   AB2_CUDA(cudaEventRecord(e_d2h, st.d2h));
   AB2_CUDA(cudaStreamWaitEvent(cs, e_d2h, 0));
+  tr.set_phase(2, "aires phase III (drain)");
+  tr.point(cs, AIRES_B200_EV_FREE, AIRES_B200_BUF_B, 0, x_keep);
   AB2_CUDA(cudaEventRecord(t_end, cs));
   AB2_CUDA(cudaStreamSynchronize(cs));
   {
@@ -734,6 +871,7 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
   rep.flops = flops;
   rep.c_nnz = running;
   rep.peak_device_bytes = rg.peak;
+  tr.finish(t_begin, rep, cfg);
   rep.phase1_ms = ms_between(t_begin, t_p1);
   rep.phase2_ms = ms_between(t_p1, t_p2);
   rep.phase3_ms = ms_between(t_p2, t_end);
@@ -787,18 +925,19 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   Arena arena(*static_cast<PipeCacheImpl*>(ctx.pipe));
   Pinned pin;
   SyncGuard sync{{cs, st.h2d, st.d2h, st.aux}};  // destroyed before pin (no copy outlives its buffers)
+  Tracer tr(st);
   cudaEvent_t t_begin = st.make_timed(), t_p1 = st.make_timed(), t_p2 = st.make_timed(), t_end = st.make_timed();
   pin.ensure(a.ptr, (n + 1) * 8);
   pin.ensure(static_cast<const char*>(a.idx) + p0 * ib, (pend - p0) * ib);
   pin.ensure(static_cast<const char*>(a.val) + p0 * vb, (pend - p0) * vb);
   if ((cfg.flags & AIRES_B200_RUN_STREAM_OUT) && cfg.device_budget == 0 && cfg.c_aware != 2 &&
       static_cast<int64_t>(b.n_cols) <= wide_threshold(mode)) {
-    run_stream(ctx, a, b, mode, cfg.n_buffers ? nbuf : 3, out, rep, st, arena, pin);
+    run_stream(ctx, a, b, mode, cfg.n_buffers ? nbuf : 3, out, rep, st, arena, pin, tr, cfg);
     return;
   }
   if ((cfg.flags & AIRES_B200_RUN_STREAM_OUT) && cfg.device_budget > 0 && cfg.c_aware == 1 &&
       static_cast<int64_t>(b.n_cols) <= wide_threshold(mode)) {
-    run_stream_capped(ctx, a, b, mode, cfg.n_buffers ? nbuf : 3, cfg.device_budget, out, rep, st, arena, pin);
+    run_stream_capped(ctx, a, b, mode, cfg.n_buffers ? nbuf : 3, cfg.device_budget, out, rep, st, arena, pin, tr, cfg);
     return;
   }
 
@@ -806,6 +945,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   mark("pinned checks done");
   AB2_CUDA(cudaEventRecord(t_begin, cs));
   AB2_CUDA(cudaStreamWaitEvent(st.h2d, t_begin, 0));
+  tr.set_phase(0, "aires phase I (X operand, sizing pass)");
   // lean operand: the step-list layout (fp32) or W-slots (fp64-exact) plus the plain CSR, which
   // the sizing pass reads directly (the device staging of a host X's raw arrays is transient and
   // not charged to the budget)
@@ -821,7 +961,12 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
         env_int("AB2_RUN_CSLOTS", 1) != 0)
       plan |= kPlanCSlots;
   }
-  auto x = make_operand(ctx, b, mode, /*temp=*/true, plan);
+  std::unique_ptr<XOperand> x;
+  const uint64_t xk_ = b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols;
+  const uint64_t x_h2d =
+      b.location == AIRES_B200_HOST ? xk_ * 8 + 8 + (b.ptr[xk_] - b.ptr[0]) * (b.idx_bytes + b.val_bytes) : 0;
+  tr.span(cs, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_B, 0, x_h2d, 0,
+          [&] { x = make_operand(ctx, b, mode, /*temp=*/true, plan); });
   mark("operand built (host synced)");
   // Uncapped runs keep A's column indices resident and stream them right after X (X first: its
   // build synchronises the host once and must not queue behind A on the link).
@@ -838,9 +983,11 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
       early_cuts = {0, n};  // a row longer than the chunk target: one chunk
     for (size_t c = 0; c + 1 < early_cuts.size(); c++) {
       const uint64_t q0 = a.ptr[early_cuts[c]], q1 = a.ptr[early_cuts[c + 1]];
-      if (q1 > q0)
-        AB2_CUDA(cudaMemcpyAsync(d_acol_full + (q0 - p0) * ib, static_cast<const char*>(a.idx) + q0 * ib,
-                                 (q1 - q0) * ib, cudaMemcpyHostToDevice, st.h2d));
+      tr.span(st.h2d, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_A, c + 1, (q1 - q0) * ib, 0, [&] {
+        if (q1 > q0)
+          AB2_CUDA(cudaMemcpyAsync(d_acol_full + (q0 - p0) * ib, static_cast<const char*>(a.idx) + q0 * ib,
+                                   (q1 - q0) * ib, cudaMemcpyHostToDevice, st.h2d));
+      });
       early_ev.push_back(st.make());
       AB2_CUDA(cudaEventRecord(early_ev.back(), st.h2d));
     }
@@ -850,15 +997,16 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
     const uint64_t raw = ctx.x_ptr.cap + ctx.x_idx.cap + ctx.x_val.cap;
     x_dev = x_dev > raw ? x_dev - raw : 0;
   }
-  rep.h2d_bytes += b.location == AIRES_B200_HOST ? (b.layout == AIRES_B200_CSR ? b.n_rows : b.n_cols) * 8 + 8 +
-                                                       static_cast<uint64_t>(x->nnz) * (b.idx_bytes + b.val_bytes)
-                                                 : 0;
+  tr.point(cs, AIRES_B200_EV_ALLOC, AIRES_B200_BUF_B, 0, x_dev);
+  rep.h2d_bytes += x_h2d;
   // resident per-row arrays: A row_ptr, C row_ptr, counts
   mark("A columns enqueued");
   uint64_t* d_aptr = static_cast<uint64_t*>(arena.get((n + 1) * 8));
   int64_t* d_cptr = static_cast<int64_t*>(arena.get((n + 1) * 8));
   int32_t* d_cnt = static_cast<int32_t*>(arena.get(std::max<uint64_t>(n, 1) * 4));
-  AB2_CUDA(cudaMemcpyAsync(d_aptr, a.ptr, (n + 1) * 8, cudaMemcpyHostToDevice, st.h2d));
+  tr.span(st.h2d, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_A, 0, (n + 1) * 8, 0, [&] {
+    AB2_CUDA(cudaMemcpyAsync(d_aptr, a.ptr, (n + 1) * 8, cudaMemcpyHostToDevice, st.h2d));
+  });
   rep.h2d_bytes += (n + 1) * 8;
   cudaEvent_t e_ptr = st.make();
   AB2_CUDA(cudaEventRecord(e_ptr, st.h2d));
@@ -975,9 +1123,11 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
     if (early_cols) {
       AB2_CUDA(cudaStreamWaitEvent(cs, early_ev[c], 0));
     } else {
-      if (q1 > q0)
-        AB2_CUDA(cudaMemcpyAsync(slot[s].acol, static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib,
-                                 cudaMemcpyHostToDevice, st.h2d));
+      tr.span(st.h2d, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_A, c + 1, (q1 - q0) * ib, 0, [&] {
+        if (q1 > q0)
+          AB2_CUDA(cudaMemcpyAsync(slot[s].acol, static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib,
+                                   cudaMemcpyHostToDevice, st.h2d));
+      });
       AB2_CUDA(cudaEventRecord(slot[s].loaded, st.h2d));
       AB2_CUDA(cudaStreamWaitEvent(cs, slot[s].loaded, 0));
     }
@@ -990,7 +1140,8 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
     t.rflops = slot[s].rflops;
     t.heavy = slot[s].heavy;
     t.ctl = d_ctls + c;
-    ctx.launches += tile_symbolic(ctx, *x, ib, t);
+    tr.span(cs, AIRES_B200_EV_COMPUTE, AIRES_B200_TIER_DEVICE, AIRES_B200_BUF_A, c + 1, 0, 0,
+            [&] { ctx.launches += tile_symbolic(ctx, *x, ib, t); });
     AB2_CUDA(cudaEventRecord(slot[s].computed, cs));
   }
   // scan -> C row_ptr, total nnz and MACs
@@ -1025,7 +1176,9 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   pin.ensure(optr, (n + 1) * 8);
   pin.ensure(oidx, nnz * ib);
   pin.ensure(oval, nnz * vb);
-  AB2_CUDA(cudaMemcpyAsync(optr, d_cptr, (n + 1) * 8, cudaMemcpyDeviceToHost, cs));
+  tr.span(cs, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_D2H, AIRES_B200_BUF_C_BLOCK, 0, (n + 1) * 8, 0, [&] {
+    AB2_CUDA(cudaMemcpyAsync(optr, d_cptr, (n + 1) * 8, cudaMemcpyDeviceToHost, cs));
+  });
   AB2_CUDA(cudaStreamSynchronize(cs));
   rep.d2h_bytes += (n + 1) * 8;
   const uint64_t* cp = static_cast<const uint64_t*>(optr);
@@ -1143,6 +1296,8 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   mark("tiles cut");
   AB2_CUDA(cudaEventRecord(e_zero, cs));
   AB2_CUDA(cudaStreamWaitEvent(st.h2d, e_zero, 0));
+  tr.set_phase(1, "aires phase II (tiles)");
+  std::vector<size_t> compute_rec(n_tiles, 0);
   for (uint64_t j = 0; j < n_tiles; j++) {
     const uint32_t s = static_cast<uint32_t>(j % nbuf);
     const uint64_t r0 = cuts[j], r1 = cuts[j + 1];
@@ -1158,16 +1313,21 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
       carve(s, r1 - r0, m.q1 - m.q_frag, true, c1 - c0);
       if (j > 0) AB2_CUDA(cudaStreamWaitEvent(st.h2d, frag_back, 0));
       const uint64_t nf = m.q0 - m.q_frag, nr = m.q1 - m.q0;
-      if (nf) {
-        AB2_CUDA(cudaMemcpyAsync(slot[s].acol, merge_col, nf * ib, cudaMemcpyHostToDevice, st.h2d));
-        AB2_CUDA(cudaMemcpyAsync(slot[s].aval, merge_val, nf * vb, cudaMemcpyHostToDevice, st.h2d));
-      }
-      if (nr) {
-        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(slot[s].acol) + nf * ib, static_cast<const char*>(a.idx) + m.q0 * ib,
-                                 nr * ib, cudaMemcpyHostToDevice, st.h2d));
-        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(slot[s].aval) + nf * vb, static_cast<const char*>(a.val) + m.q0 * vb,
-                                 nr * vb, cudaMemcpyHostToDevice, st.h2d));
-      }
+      tr.point(st.h2d, AIRES_B200_EV_ALLOC, AIRES_B200_BUF_A_TILE, j, (nf + nr) * (ib + vb));
+      const size_t up = tr.span(st.h2d, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_A_TILE, j,
+                                (nf + nr) * (ib + vb), 0, [&] {
+        if (nf) {
+          AB2_CUDA(cudaMemcpyAsync(slot[s].acol, merge_col, nf * ib, cudaMemcpyHostToDevice, st.h2d));
+          AB2_CUDA(cudaMemcpyAsync(slot[s].aval, merge_val, nf * vb, cudaMemcpyHostToDevice, st.h2d));
+        }
+        if (nr) {
+          AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(slot[s].acol) + nf * ib, static_cast<const char*>(a.idx) + m.q0 * ib,
+                                   nr * ib, cudaMemcpyHostToDevice, st.h2d));
+          AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(slot[s].aval) + nf * vb, static_cast<const char*>(a.val) + m.q0 * vb,
+                                   nr * vb, cudaMemcpyHostToDevice, st.h2d));
+        }
+      });
+      if (nf) tr.merge_share.emplace_back(up, static_cast<double>(nf) / static_cast<double>(nf + nr));
       rep.h2d_bytes += (nf + nr) * (ib + vb);
       rep.merge_bytes += nf * (ib + vb);
       AB2_CUDA(cudaEventRecord(slot[s].loaded, st.h2d));
@@ -1178,10 +1338,14 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
       const uint64_t tail = m.q1 > fb ? m.q1 - fb : 0;
       AB2_CUDA(cudaStreamWaitEvent(st.aux, slot[s].loaded, 0));
       if (tail) {
-        AB2_CUDA(cudaMemcpyAsync(merge_col, static_cast<char*>(slot[s].acol) + (fb - m.q_frag) * ib, tail * ib,
-                                 cudaMemcpyDeviceToHost, st.aux));
-        AB2_CUDA(cudaMemcpyAsync(merge_val, static_cast<char*>(slot[s].aval) + (fb - m.q_frag) * vb, tail * vb,
-                                 cudaMemcpyDeviceToHost, st.aux));
+        const size_t fr = tr.span(st.aux, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_D2H, AIRES_B200_BUF_FRAGMENT, j,
+                                  tail * (ib + vb), 0, [&] {
+          AB2_CUDA(cudaMemcpyAsync(merge_col, static_cast<char*>(slot[s].acol) + (fb - m.q_frag) * ib, tail * ib,
+                                   cudaMemcpyDeviceToHost, st.aux));
+          AB2_CUDA(cudaMemcpyAsync(merge_val, static_cast<char*>(slot[s].aval) + (fb - m.q_frag) * vb, tail * vb,
+                                   cudaMemcpyDeviceToHost, st.aux));
+        });
+        tr.merge_share.emplace_back(fr, 1.0);
         rep.d2h_bytes += tail * (ib + vb);
       }
       AB2_CUDA(cudaEventRecord(frag_back, st.aux));
@@ -1200,28 +1364,35 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
       t.cnt = slot[s].cnt;
       t.toff = slot[s].toff;
       t.ctl = d_tctl + j;
-      ctx.launches += tile_product(ctx, *x, ib, t);
+      compute_rec[j] = tr.span(cs, AIRES_B200_EV_COMPUTE, AIRES_B200_TIER_DEVICE, AIRES_B200_BUF_A_TILE, j, 0, 0,
+                               [&] { ctx.launches += tile_product(ctx, *x, ib, t); });
       AB2_CUDA(cudaEventRecord(slot[s].computed, cs));
       AB2_CUDA(cudaStreamWaitEvent(st.d2h, slot[s].computed, 0));
-      if (c1 > c0) {
-        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oidx) + c0 * ib, slot[s].ccol, (c1 - c0) * ib,
-                                 cudaMemcpyDeviceToHost, st.d2h));
-        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oval) + c0 * vb, slot[s].cval, (c1 - c0) * vb,
-                                 cudaMemcpyDeviceToHost, st.d2h));
-      }
+      tr.span(st.d2h, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_D2H, AIRES_B200_BUF_C_BLOCK, j, (c1 - c0) * (ib + vb), 0, [&] {
+        if (c1 > c0) {
+          AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oidx) + c0 * ib, slot[s].ccol, (c1 - c0) * ib,
+                                   cudaMemcpyDeviceToHost, st.d2h));
+          AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oval) + c0 * vb, slot[s].cval, (c1 - c0) * vb,
+                                   cudaMemcpyDeviceToHost, st.d2h));
+        }
+      });
       rep.d2h_bytes += (c1 - c0) * (ib + vb);
+      tr.point(st.d2h, AIRES_B200_EV_FREE, AIRES_B200_BUF_A_TILE, j, (nf + nr) * (ib + vb));
       AB2_CUDA(cudaEventRecord(slot[s].drained, st.d2h));
       continue;
     }
     carve(s, r1 - r0, q1 - q0, true, c1 - c0);
     if (cols_resident) slot[s].acol = d_acol_full + (q0 - p0) * ib;
-    if (q1 > q0) {
-      if (!cols_resident)
-        AB2_CUDA(cudaMemcpyAsync(slot[s].acol, static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib,
+    tr.point(st.h2d, AIRES_B200_EV_ALLOC, AIRES_B200_BUF_A_TILE, j, (q1 - q0) * a_tile_bytes);
+    tr.span(st.h2d, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_A_TILE, j, (q1 - q0) * a_tile_bytes, 0, [&] {
+      if (q1 > q0) {
+        if (!cols_resident)
+          AB2_CUDA(cudaMemcpyAsync(slot[s].acol, static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib,
+                                   cudaMemcpyHostToDevice, st.h2d));
+        AB2_CUDA(cudaMemcpyAsync(slot[s].aval, static_cast<const char*>(a.val) + q0 * vb, (q1 - q0) * vb,
                                  cudaMemcpyHostToDevice, st.h2d));
-      AB2_CUDA(cudaMemcpyAsync(slot[s].aval, static_cast<const char*>(a.val) + q0 * vb, (q1 - q0) * vb,
-                               cudaMemcpyHostToDevice, st.h2d));
-    }
+      }
+    });
     rep.h2d_bytes += (q1 - q0) * a_tile_bytes;
     AB2_CUDA(cudaEventRecord(slot[s].loaded, st.h2d));
     AB2_CUDA(cudaStreamWaitEvent(cs, slot[s].loaded, 0));
@@ -1240,16 +1411,20 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
     t.cnt = slot[s].cnt;
     t.toff = slot[s].toff;
     t.ctl = d_tctl + j;
-    ctx.launches += tile_product(ctx, *x, ib, t);
+    compute_rec[j] = tr.span(cs, AIRES_B200_EV_COMPUTE, AIRES_B200_TIER_DEVICE, AIRES_B200_BUF_A_TILE, j, 0, 0,
+                             [&] { ctx.launches += tile_product(ctx, *x, ib, t); });
     AB2_CUDA(cudaEventRecord(slot[s].computed, cs));
     AB2_CUDA(cudaStreamWaitEvent(st.d2h, slot[s].computed, 0));
-    if (c1 > c0) {
-      AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oidx) + c0 * ib, slot[s].ccol, (c1 - c0) * ib,
-                               cudaMemcpyDeviceToHost, st.d2h));
-      AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oval) + c0 * vb, slot[s].cval, (c1 - c0) * vb,
-                               cudaMemcpyDeviceToHost, st.d2h));
-    }
+    tr.span(st.d2h, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_D2H, AIRES_B200_BUF_C_BLOCK, j, (c1 - c0) * (ib + vb), 0, [&] {
+      if (c1 > c0) {
+        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oidx) + c0 * ib, slot[s].ccol, (c1 - c0) * ib,
+                                 cudaMemcpyDeviceToHost, st.d2h));
+        AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oval) + c0 * vb, slot[s].cval, (c1 - c0) * vb,
+                                 cudaMemcpyDeviceToHost, st.d2h));
+      }
+    });
     rep.d2h_bytes += (c1 - c0) * (ib + vb);
+    tr.point(st.d2h, AIRES_B200_EV_FREE, AIRES_B200_BUF_A_TILE, j, (q1 - q0) * a_tile_bytes);
     AB2_CUDA(cudaEventRecord(slot[s].drained, st.d2h));
   }
   AB2_CUDA(cudaEventRecord(t_p2, cs));
@@ -1258,6 +1433,12 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   mark("phase II enqueued");
   AB2_CUDA(cudaStreamWaitEvent(cs, slot[0].drained, 0));
   for (uint32_t s = 0; s < nbuf; s++) AB2_CUDA(cudaStreamWaitEvent(cs, slot[s].drained, 0));
+  if (maxmem) {  // the fragment stream too
+    AB2_CUDA(cudaEventRecord(frag_back, st.aux));
+    AB2_CUDA(cudaStreamWaitEvent(cs, frag_back, 0));
+  }
+  tr.set_phase(2, "aires phase III (drain)");
+  tr.point(cs, AIRES_B200_EV_FREE, AIRES_B200_BUF_B, 0, x_dev);
   AB2_CUDA(cudaEventRecord(t_end, cs));
   std::vector<Ctl> h_t(std::max<uint64_t>(n_tiles, 1));
   AB2_CUDA(cudaMemcpyAsync(h_t.data(), d_tctl, sizeof(Ctl) * std::max<uint64_t>(n_tiles, 1), cudaMemcpyDeviceToHost, cs));
@@ -1272,6 +1453,8 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   rep.flops = flops;
   rep.c_nnz = nnz;
   rep.peak_device_bytes = arena.used + x_dev;
+  for (uint64_t j = 0; j < n_tiles; j++) tr.recs[compute_rec[j]].e.flops = h_t[j].flops;
+  tr.finish(t_begin, rep, cfg);
   rep.phase1_ms = ms_between(t_begin, t_p1);
   rep.phase2_ms = ms_between(t_p1, t_p2);
   rep.phase3_ms = ms_between(t_p2, t_end);

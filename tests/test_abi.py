@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version_and_status_mapping():
-    assert ab.lib().aires_b200_abi_version() == 1
+    assert ab.lib().aires_b200_abi_version() == ab.ABI_VERSION == 2
     # status = 1 + errc (error.hpp:9-27)
     e = ab.AiresError(8, "x")
     assert e.code == ab.errc.dimension_mismatch and str(e).startswith("dimension_mismatch")

@@ -260,13 +260,14 @@ def test_stream_out_capped_edge_shapes():
     ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
     g2 = ab.CsrMatrix(g.n_rows, g.n_cols, ptr, g.col_idx[keep], g.values[keep])
     wp, wi, wv, _ = _oracle(g2, x)
-    res = ab.run_aires(g2, x, ab.MemoryBudget(1_500_000), stream_out=True)
+    # (the budget covers X's fp64 layouts, ~1.4 MB, and its raw upload while the layouts are built)
+    res = ab.run_aires(g2, x, ab.MemoryBudget(2_600_000), stream_out=True)
     assert res.report.segments >= 2
     assert np.array_equal(res.c.row_ptr, wp) and np.array_equal(res.c.col_idx, wi)
     assert res.report.c_checksum == po.checksum(g2.n_rows, x.n_cols, wp, wi, wv)
     empty = ab.CsrMatrix(g.n_rows, g.n_cols, np.zeros(g.n_rows + 1, np.uint64), np.zeros(0, np.uint64),
                          np.zeros(0, np.float64))
-    res = ab.run_aires(empty, x, ab.MemoryBudget(1_500_000), stream_out=True)
+    res = ab.run_aires(empty, x, ab.MemoryBudget(2_600_000), stream_out=True)
     assert res.c.nnz() == 0 and not res.c.row_ptr.any()
 
 
@@ -284,3 +285,55 @@ def test_stream_out_a_only_tiling_keeps_the_exact_protocol():
     a_b, c_b = _bytes(g, x, (wp, wi))
     res = ab.run_aires(g, x, ab.MemoryBudget(int(3e6 + 2.0 * (a_b + c_b))), stream_out=True, c_aware=False)
     assert res.report.c_checksum == po.checksum(g.n_rows, x.n_cols, wp, wi, wv)
+
+
+def _audit(res, budget):
+    """audit_trace (tiered_sim.hpp:344-420) over the measured trace: per-channel transfer counts and
+    bytes equal the ledger, timestamps and phases monotone, frees matched, occupancy within budget."""
+    tr = res.trace
+    assert tr, "empty trace"
+    led = res.report.ledger
+    for ch, tot in (("h2d", led.h2d), ("d2h", led.d2h)):
+        xs = [e for e in tr if e.kind == "transfer" and e.where == ch]
+        assert len(xs) == tot.count and sum(e.bytes for e in xs) == tot.bytes, ch
+        assert tot.seconds > 0 and abs(sum(e.duration for e in xs) - tot.seconds) <= 1e-9 + 1e-6 * tot.seconds
+    ts = [e.timestamp for e in tr]
+    assert ts == sorted(ts)
+    ph = [("I", "II", "III").index(e.phase) for e in tr]
+    assert ph == sorted(ph)
+    live, occ, peak = {}, 0, 0
+    for e in tr:
+        if e.kind == "alloc" and e.where == "device":
+            assert e.buffer not in live
+            live[e.buffer] = e.bytes
+            occ += e.bytes
+            peak = max(peak, occ)
+        elif e.kind == "free" and e.where == "device":
+            assert live.pop(e.buffer) == e.bytes
+            occ -= e.bytes
+    assert not live and occ == 0
+    if budget:
+        assert peak <= budget
+    assert sum(e.flops for e in tr if e.kind == "compute") == res.report.flops
+    r = res.report
+    assert abs(r.total_s - (r.phase1_s + r.phase2_s + r.phase3_s)) <= 1e-6 * max(r.total_s, 1e-9) + 1e-9
+
+
+@pytest.mark.parametrize("proto", ["exact", "streamed", "capped", "capped_streamed", "maxmemory"])
+def test_run_trace_audits(proto):
+    g, x = _graph(20_000, 300_000, 128)
+    wp, wi, wv, macs = _oracle(g, x)
+    a_b, c_b = _bytes(g, x, (wp, wi))
+    budget = 0 if proto in ("exact", "streamed") else int(3e6 + 0.3 * (a_b + c_b))
+    if proto == "maxmemory":
+        res = ab.run_maxmemory(g, x, ab.MemoryBudget(budget), with_checksum=False)
+    else:
+        res = ab.run_aires(g, x, ab.MemoryBudget(budget), n_buffers=3, with_checksum=False,
+                           stream_out=proto in ("streamed", "capped_streamed"))
+    assert np.array_equal(res.c.row_ptr, wp) and np.array_equal(res.c.col_idx, wi)
+    assert res.report.flops == macs
+    _audit(res, budget)
+    if proto == "maxmemory" and res.report.ledger.merge_bytes:
+        assert res.report.merge_seconds > 0
+    elif proto != "maxmemory":
+        assert res.report.merge_seconds == 0.0
