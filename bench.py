@@ -376,7 +376,7 @@ def run_b200(args, cfg):
     # ---- e2e: the public out-of-core entry point with pinned host buffers ---------------------
     e2e = None
     if not args.skip_e2e:
-        e2e = e2e_leg(args, dev, L, ab, torch, blk, x, res32, tot_macs, dist, cdev)
+        e2e = e2e_leg(args, dev, L, ab, torch, blk, x, res32, tot_macs, dist, cdev, res64)
 
     # ---- CPU baseline (rank 0): the reference on a row sample, its rows checked against ours ----
     cpu = None
@@ -433,56 +433,77 @@ def link_bandwidth(dev, nbytes=512 << 20, reps=5):
 
 
 class HostOperands:
-    """Pinned host copies of an A block (u64 ptr, u32 idx, fp32 val) and of X, plus a pinned output
-    sized for `cap` nonzeros (or grown on demand) -- the buffers aires_b200_run sees."""
+    """Host copies of an A block and of X at the given widths (default u64 ptr, u32 idx, fp32 val,
+    page-locked), plus an output of the same widths sized for `cap` nonzeros (or grown on demand) --
+    the buffers aires_b200_run sees.  pinned=False: plain pageable numpy arrays, which the run
+    registers with the driver (cudaHostRegister) for the duration of every call, as it does for the
+    reference's std::vector containers behind the drop-in headers."""
 
-    def __init__(self, ab, torch, a, x, cap=0):
+    def __init__(self, ab, torch, a, x, cap=0, idx_dt=np.uint32, val_dt=np.float32, pinned=True):
         self.ab, self.torch = ab, torch
-        self.hA = [torch.from_numpy(np.ascontiguousarray(a.row_ptr, np.uint64).view(np.int64)).pin_memory(),
-                   torch.from_numpy(np.ascontiguousarray(a.col_idx, np.uint32).view(np.int32)).pin_memory(),
-                   torch.from_numpy(np.ascontiguousarray(a.values, np.float32)).pin_memory()]
-        self.hX = [torch.from_numpy(np.ascontiguousarray(x.row_ptr, np.uint64).view(np.int64)).pin_memory(),
-                   torch.from_numpy(np.ascontiguousarray(x.col_idx, np.uint32).view(np.int32)).pin_memory(),
-                   torch.from_numpy(np.ascontiguousarray(x.values, np.float32)).pin_memory()]
-        self.am = ab._Matrix(a.n_rows, a.n_cols, ab.CSR, ab.HOST, 4, 4, self.hA[0].data_ptr(), self.hA[1].data_ptr(),
-                             self.hA[2].data_ptr(), a.nnz())
-        self.xm = ab._Matrix(x.n_rows, x.n_cols, ab.CSR, ab.HOST, 4, 4, self.hX[0].data_ptr(), self.hX[1].data_ptr(),
-                             self.hX[2].data_ptr(), x.nnz())
+        self.pinned = pinned
+        self.idx_dt, self.val_dt = np.dtype(idx_dt), np.dtype(val_dt)
+        self.mode = ab.MODE_FP64_EXACT if self.val_dt == np.float64 else ab.MODE_FP32
+
+        def host(arr, dt):
+            arr = np.ascontiguousarray(arr, dt)
+            if not pinned:
+                return arr
+            return torch.from_numpy(arr.view({1: np.uint8, 4: np.int32, 8: np.int64}[arr.itemsize])
+                                    if arr.dtype.kind == "u" else arr).pin_memory()
+
+        def addr(t):
+            return t.ctypes.data if isinstance(t, np.ndarray) else t.data_ptr()
+
+        self.hA = [host(a.row_ptr, np.uint64), host(a.col_idx, self.idx_dt), host(a.values, self.val_dt)]
+        self.hX = [host(x.row_ptr, np.uint64), host(x.col_idx, self.idx_dt), host(x.values, self.val_dt)]
+        ib, vb = self.idx_dt.itemsize, self.val_dt.itemsize
+        self.am = ab._Matrix(a.n_rows, a.n_cols, ab.CSR, ab.HOST, ib, vb, addr(self.hA[0]), addr(self.hA[1]),
+                             addr(self.hA[2]), a.nnz())
+        self.xm = ab._Matrix(x.n_rows, x.n_cols, ab.CSR, ab.HOST, ib, vb, addr(self.hX[0]), addr(self.hX[1]),
+                             addr(self.hX[2]), x.nnz())
         self.rows = a.n_rows
         self.out_t = {}
         if cap:
             self._grow(a.n_rows, cap)
         self.fn = ab._ALLOC_FN(self._alloc)
-        self.out = ab._Output(ab.HOST, 4, 4, 0, self.fn, None, 0, 0, 0, 0)
+        self.out = ab._Output(ab.HOST, ib, vb, 0, self.fn, None, 0, 0, 0, 0)
 
     def _grow(self, rows, nnz):
         T = self.torch
-        self.out_t = {"ptr": T.empty(rows + 1, dtype=T.int64).pin_memory(),
-                      "idx": T.empty(max(nnz, 1), dtype=T.int32).pin_memory(),
-                      "val": T.empty(max(nnz, 1), dtype=T.float32).pin_memory(), "cap": nnz}
+        if self.pinned:
+            self.out_t = {"ptr": T.empty(rows + 1, dtype=T.int64).pin_memory(),
+                          "idx": T.empty(max(nnz, 1), dtype=T.int64 if self.idx_dt.itemsize == 8 else T.int32).pin_memory(),
+                          "val": T.empty(max(nnz, 1), dtype=T.float64 if self.val_dt.itemsize == 8 else T.float32).pin_memory(),
+                          "cap": nnz}
+        else:
+            self.out_t = {"ptr": np.empty(rows + 1, np.uint64), "idx": np.empty(max(nnz, 1), self.idx_dt),
+                          "val": np.empty(max(nnz, 1), self.val_dt), "cap": nnz}
 
     def _alloc(self, user, rows, nnz, pp, pi, pv):
         if self.out_t.get("cap", -1) < nnz:
             self._grow(rows, nnz)
-        pp[0], pi[0], pv[0] = (self.out_t["ptr"].data_ptr(), self.out_t["idx"].data_ptr(),
-                               self.out_t["val"].data_ptr())
+        addr = (lambda t: t.ctypes.data) if not self.pinned else (lambda t: t.data_ptr())
+        pp[0], pi[0], pv[0] = addr(self.out_t["ptr"]), addr(self.out_t["idx"]), addr(self.out_t["val"])
         return 0
 
     def run(self, budget=0, c_aware=1, n_buffers=0, flags=0):
         ab = self.ab
         rep = ab._RunReport()
-        cfg = ab._RunConfig(int(budget), ab.MODE_FP32, c_aware, n_buffers, flags)
+        cfg = ab._RunConfig(int(budget), self.mode, c_aware, n_buffers, flags)
         ab._check(ab.lib().aires_b200_run(C.byref(self.am), C.byref(self.xm), C.byref(cfg), C.byref(self.out),
                                           C.byref(rep)))
         return rep
 
     def result(self):
         z = int(self.out.nnz)
+        if not self.pinned:
+            return self.out_t["ptr"][: self.rows + 1], self.out_t["idx"][:z], self.out_t["val"][:z]
         return (self.out_t["ptr"][: self.rows + 1].numpy(), self.out_t["idx"][:z].numpy(),
                 self.out_t["val"][:z].numpy())
 
 
-def e2e_leg(args, dev, L, ab, torch, blk, x, res32, tot_macs, dist, cdev):
+def e2e_leg(args, dev, L, ab, torch, blk, x, res32, tot_macs, dist, cdev, res64=None):
     """run_aires (aires_b200_run) with pinned host A/X/C, uncapped: streamed output (the headline:
     no sizing pass, C drains while A still crosses) and, beside it, the exact-allocation protocol
     and the one-shot aires_b200_spgemm call with host buffers.  Wall clock per step (host time =
@@ -517,6 +538,40 @@ def e2e_leg(args, dev, L, ab, torch, blk, x, res32, tot_macs, dist, cdev):
     b_a = 8 * (blk.n_rows + 1) + 8 * blk.nnz()
     b_x = 8 * (x.n_rows + 1) + 8 * x.nnz()
     b_c = 8 * (blk.n_rows + 1) + 8 * int(h.out.nnz)
+    del h
+    # the drop-in's widths: the reference's CsrMatrix is u64 indices / f64 values (sparse.hpp:15-16)
+    # and its run_aires runs FP64_EXACT -- pinned buffers, then plain pageable arrays (registered with
+    # the driver inside every call, as std::vector storage is); checked bit for bit against the
+    # resident FP64_EXACT product when it ran
+    api = {}
+    for pinned in (True, False):
+        hw = HostOperands(ab, torch, blk, x, cap=max(c_bound, 1), idx_dt=np.uint64, val_dt=np.float64, pinned=pinned)
+        for _ in range(max(1, args.warmup)):
+            hw.run(flags=ab.RUN_STREAM_OUT)
+        w_ms, wrep = wall(lambda: hw.run(flags=ab.RUN_STREAM_OUT))
+        w_ms = max_over_ranks(w_ms, dist, cdev)
+        got = hw.result()
+        if res64 is not None:
+            chk_w = {"structure_equal": bool(np.array_equal(np.asarray(got[0], np.uint64), np.asarray(res64[0], np.uint64))
+                                             and np.array_equal(np.asarray(got[1], np.int64), np.asarray(res64[1], np.int64))),
+                     "values_bit_identical": bool(np.array_equal(np.asarray(got[2], np.float64).view(np.uint64),
+                                                                 np.asarray(res64[2], np.float64).view(np.uint64)))}
+            chk_w["checked"] = chk_w["structure_equal"] and chk_w["values_bit_identical"]
+        else:
+            chk_w = compare(*got, *res32)
+        b16 = 8 * (blk.n_rows + 1) + 16 * blk.nnz() + 8 * (x.n_rows + 1) + 16 * x.nnz()
+        c16 = 8 * (blk.n_rows + 1) + 16 * int(hw.out.nnz)
+        t16 = max(b16 / link["h2d"], c16 / link["d2h"]) / 1e6
+        api["pinned" if pinned else "pageable"] = {
+            "ms_per_step": round(w_ms, 3), "value": round(2.0 * tot_macs / (w_ms * 1e-3) / 1e9, 3),
+            "device_ms": round(wrep.total_ms, 3), "h2d_bytes_per_step": int(wrep.h2d_bytes),
+            "d2h_bytes_per_step": int(wrep.d2h_bytes), "segments": int(wrep.segments),
+            "link_frac": round(t16 / w_ms, 4), "checked": chk_w["checked"], "check": chk_w}
+        del hw
+    api["api"] = ("aires_b200_run, streamed output, FP64_EXACT, A/X/C host buffers at the reference's widths "
+                  "(u64 ptr, u64 idx, f64 val) -- what aires::run_aires behind the drop-in headers calls "
+                  "(it then adds the reference's c_checksum, a byte-serial FNV-1a on the host)")
+    api["roofline_basis"] = "max((B_A+B_X)/H2D, B_C/D2H) with B = 8(rows+1) + 16 nnz"
     t_alg = max((b_a + b_x) / link["h2d"], b_c / link["d2h"]) / 1e6
     e_ms_max = max_over_ranks(e_ms, dist, cdev)
     per_rank_frac = t_alg / e_ms
@@ -539,7 +594,8 @@ def e2e_leg(args, dev, L, ab, torch, blk, x, res32, tot_macs, dist, cdev):
                                "checked": chk_x["checked"]},
             "spgemm_call": {"api": "aires_b200_spgemm with host buffers (one-shot H2D, product, D2H)",
                             "ms_per_step": round(s_ms, 3), "value": round(2.0 * tot_macs / (s_ms * 1e-3) / 1e9, 3),
-                            "checked": chk_s["checked"]}}
+                            "checked": chk_s["checked"]},
+            "api_widths": api}
 
 
 def ooc_one(args, dev, ab, torch, g, x, frac, label, ref=None, maxmemory=False, link=None):

@@ -132,16 +132,28 @@ inline RunResult run_maxmemory_real(const CsrMatrix& a, const CscMatrix& b, cons
 
 #ifndef AIRES_B200_SIMULATED_RUN
 namespace aires {
-/// scheduler.hpp:72-168 -- the real pipeline, streamed output, ring of 3.
+/// scheduler.hpp:72-168 -- the real pipeline, streamed output, ring of 3.  Feature matrices wider
+/// than the device accumulator (aires_b200_run reports unsupported_format: the pipeline's tiles hold
+/// whole C rows) run on the reference scheduler with the B200 spgemm_block, which tiles B's columns.
 inline RunResult run_aires(const CsrMatrix& a, const CscMatrix& b, const MemoryBudget& budget,
                            const SimConfig& cfg) {
-  return b200::run_aires_real(a, b, budget, cfg, 3, true);
+  try {
+    return b200::run_aires_real(a, b, budget, cfg, 3, true);
+  } catch (const error& e) {
+    if (e.code() != errc::unsupported_format) throw;
+    return run_aires_simulated(a, b, budget, cfg);
+  }
 }
 
-/// scheduler.hpp:174-293 -- the real MaxMemory baseline.
+/// scheduler.hpp:174-293 -- the real MaxMemory baseline (wide features: as run_aires).
 inline RunResult run_maxmemory(const CsrMatrix& a, const CscMatrix& b, const MemoryBudget& budget,
                                const SimConfig& cfg) {
-  return b200::run_maxmemory_real(a, b, budget, cfg, 2);
+  try {
+    return b200::run_maxmemory_real(a, b, budget, cfg, 2);
+  } catch (const error& e) {
+    if (e.code() != errc::unsupported_format) throw;
+    return run_maxmemory_simulated(a, b, budget, cfg);
+  }
 }
 
 /// scheduler.hpp:295-299

@@ -170,6 +170,21 @@ TEST(RealDefault, EmptyOperandsStillProduceC) {
   }
 }
 
+// X wider than the fp64 device accumulator (4096 columns): the pipeline's tiles hold whole C rows,
+// so the default run_aires falls back to the reference scheduler with the B200 spgemm_block (which
+// tiles B's columns) -- same C as the in-core product.
+TEST(RealDefault, WideFeaturesFallBackToTheColumnTiledScheduler) {
+  CsrMatrix a = gen_symmetric(300, 0.03, 71);
+  CsrMatrix x = gen_features(300, 5000, 99.0, 72);
+  const CsrMatrix want = spgemm_full(a, x);
+  const CscMatrix b = csr_to_csc(x);
+  EXPECT_THROW(b200::run_aires_real(a, b, MemoryBudget{0}, SimConfig{}, 3, true), error);
+  SimConfig cfg;
+  RunResult r = run_aires(a, b, cfg.budget(), cfg);
+  EXPECT_TRUE(r.c == want);
+  EXPECT_EQ(r.report.c_checksum, checksum(want));
+}
+
 TEST(RealRun, DimensionMismatchThrows) {
   const Case c = make_case(500, 0.02, 16, 41);
   const CsrMatrix wrong = gen_features(499, 16, 95.0, 3);

@@ -65,6 +65,9 @@ def allgather_csr(row_ptr: np.ndarray, col_idx: np.ndarray, values: np.ndarray, 
     dev = device if device is not None else ("cuda" if dist.get_backend(group) == "nccl" else "cpu")
     rp = np.asarray(row_ptr, dtype=np.int64)
     rows, nnz = rp.shape[0] - 1, int(rp[-1] - rp[0])
+    # absolute row pointers (e.g. shard_rows' zero-copy blocks) address the block's entries from rp[0]
+    col_idx = np.asarray(col_idx)[int(rp[0]): int(rp[0]) + nnz]
+    values = np.asarray(values)[int(rp[0]): int(rp[0]) + nnz]
     meta = torch.tensor([rows, nnz], dtype=torch.int64, device=dev)
     metas = torch.zeros(world * 2, dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(metas, meta, group=group)

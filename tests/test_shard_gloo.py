@@ -54,6 +54,14 @@ def _worker(rank, world, port, q):
         g_rp, g_col, g_val = shard.allgather_csr(lp, li, lv)
         rc, (wp, wi, wv), _ = po.spgemm_rowwise(*a, 57, 40, 40, 23, *x)
         import torch
+        # absolute row pointers into the full arrays (shard_rows' zero-copy view) assemble the same C
+        base = 1000
+        ap = lp.astype(np.int64) + base
+        pad_i = np.concatenate([np.zeros(base, li.dtype), li, np.zeros(7, li.dtype)])
+        pad_v = np.concatenate([np.zeros(base, lv.dtype), lv, np.zeros(7, lv.dtype)])
+        a_rp, a_col, a_val = shard.allgather_csr(ap, pad_i, pad_v)
+        ok_abs = (np.array_equal(a_rp, wp) and np.array_equal(a_col.astype(np.uint64), wi)
+                  and np.array_equal(a_val.view(np.uint64), wv.view(np.uint64)))
         tp, ti, tv = shard.allgather_csr_torch(torch.from_numpy(lp.astype(np.int64)), torch.from_numpy(li.astype(np.int64)),
                                                torch.from_numpy(lv))
         ok = (total == wi.shape[0] and np.array_equal(g_rp, wp) and np.array_equal(g_col.astype(np.uint64), wi)
@@ -61,7 +69,7 @@ def _worker(rank, world, port, q):
               and np.array_equal(g_rows.astype(np.uint64), wp[cuts[rank]:cuts[rank + 1] + 1])
               and np.array_equal(tp.numpy().astype(np.uint64), wp) and np.array_equal(ti.numpy().astype(np.uint64), wi)
               and np.array_equal(tv.numpy().view(np.uint64), wv.view(np.uint64)))
-        q.put((rank, bool(ok)))
+        q.put((rank, bool(ok and ok_abs)))
     finally:
         dist.destroy_process_group()
 
