@@ -266,6 +266,29 @@ int aires_b200_layer_fused(const aires_b200_matrix* a_tilde, const aires_b200_ma
 uint64_t aires_b200_checksum(uint64_t n_rows, uint64_t n_cols, uint64_t nnz, const uint64_t* row_ptr,
                              const void* col_idx, uint32_t idx_bytes, const void* values, uint32_t val_bytes);
 
+/* ---- tuning options and test hooks (not part of the reference surface) --- */
+/*
+ * Per calling thread; every option has a measured default, so production callers set none.
+ * Unknown names return AIRES_B200_INVALID_ARGUMENT.  The library reads no environment variable
+ * for kernel choice or numerics (AB2_TRACE=1 only prints per-run device timelines to stderr).
+ *   heavy_deg (1024)        A rows above this degree are computed CTA-cooperatively
+ *   sym_heavy_deg (2048)    the same for the out-of-core sizing kernel
+ *   num_warps (4)           warps per CTA of the product kernel
+ *   short_rows (1)          rows with <= 32 terms take the register-sort path
+ *   slot_w (auto)           force the X slot width (2, 4, 8, 16)
+ *   numeric_kernel (3)      5: the fp32 step-list kernel instead of the W-slot kernel
+ *   n5_warps, w5            step-list kernel: warps per CTA, slot width
+ *   wide_at (8192 / 4096)   X column count from which products run in column tiles
+ *   wide_tile               column-tile width of those products
+ *   run_tiles (16), stream_tiles (16)  tiles of the uncapped exact / streamed runs
+ *   run_resident_cols (1)   uncapped exact runs keep A's columns on the device after sizing
+ *   run_cslots (1)          out-of-core sizing over 16-wide column slots when X rows average >= 4
+ *   combine_one_pass (1), combine_smem (1), combine_v4 (1), fused_reassoc (1)  GCN kernel paths
+ *   gds (0) / no_gds (0)    storage leg: force / forbid the cuFile attempt
+ */
+int aires_b200_set_option(const char* name, int64_t value);
+int aires_b200_clear_options(void);
+
 /* ---- timing helpers for harnesses (not part of the reference surface) --- */
 /* The cudaStream_t the calling thread's products run on (current device), so a harness can
    record CUDA events on the stream the kernels are launched on. */

@@ -13,6 +13,7 @@ every compute call raises.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import dataclasses
 import enum
@@ -141,6 +142,7 @@ def lib() -> C.CDLL:
     if L.aires_b200_abi_version() != ABI_VERSION:
         raise RuntimeError(f"{LIB_PATH} has ABI {L.aires_b200_abi_version()}, the bindings expect {ABI_VERSION}: rebuild")
     L.aires_b200_last_error.restype = C.c_char_p
+    L.aires_b200_set_option.argtypes = [C.c_char_p, C.c_int64]
     L.aires_b200_device_count.argtypes = [P(C.c_int)]
     L.aires_b200_set_device.argtypes = [C.c_int]
     L.aires_b200_spgemm.argtypes = [P(_Matrix), P(_Matrix), C.c_uint32, P(_Output)]
@@ -518,6 +520,26 @@ def run_maxmemory(a: CsrMatrix, b, budget: MemoryBudget, cfg=None, mode: int = M
 
 
 RUN_STREAM_OUT = 1  # aires_b200_run_config.flags: streamed output (include/aires_b200.h)
+
+
+def set_option(name: str, value: int) -> None:
+    """aires_b200_set_option: a tuning option / test hook for the calling thread (include/aires_b200.h)."""
+    _check(lib().aires_b200_set_option(name.encode(), int(value)))
+
+
+def clear_options() -> None:
+    _check(lib().aires_b200_clear_options())
+
+
+@contextlib.contextmanager
+def options(**kw):
+    """Temporarily sets tuning options / test hooks on this thread: `with ab.options(wide_at=64): ...`."""
+    try:
+        for k, v in kw.items():
+            set_option(k, v)
+        yield
+    finally:
+        clear_options()
 
 
 def run_aires(a: CsrMatrix, b, budget: MemoryBudget, cfg=None, mode: int = MODE_AUTO, c_aware: bool = True,

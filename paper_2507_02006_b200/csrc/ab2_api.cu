@@ -27,10 +27,38 @@ void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
   fail(code, std::string(cudaGetErrorString(e)) + " in " + what + " (" + file + ":" + std::to_string(line) + ")");
 }
 
-int64_t env_int(const char* name, int64_t def) {
-  const char* v = std::getenv(name);
-  if (!v || !*v) return def;
-  return std::strtoll(v, nullptr, 10);
+// Tuning options and test hooks (aires_b200_set_option): explicit, per calling thread, validated
+// against the list in aires_b200.h; nothing in the library reads the process environment except the
+// AB2_TRACE diagnostic timeline (stderr only, never numerics or kernel choice).
+namespace {
+const char* const kOptionNames[] = {
+    "heavy_deg",         "sym_heavy_deg",  "num_warps",         "short_rows", "slot_w",      "numeric_kernel",
+    "n5_warps",          "w5",             "wide_at",           "wide_tile",  "run_tiles",   "stream_tiles",
+    "run_resident_cols", "run_cslots",     "combine_one_pass",  "combine_smem", "combine_v4", "fused_reassoc",
+    "gds",               "no_gds"};
+thread_local std::vector<std::pair<std::string, int64_t>> t_options;
+}  // namespace
+
+std::vector<std::pair<std::string, int64_t>>& t_options_ref() { return t_options; }
+
+bool option_known(const char* name) {
+  for (const char* k : kOptionNames)
+    if (std::strcmp(k, name) == 0) return true;
+  return false;
+}
+
+int64_t option(const char* name, int64_t def) {
+  for (const auto& kv : t_options)
+    if (kv.first == name) return kv.second;
+  return def;
+}
+
+bool trace_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("AB2_TRACE");
+    return v && *v && std::strtoll(v, nullptr, 10) != 0;
+  }();
+  return on;
 }
 
 void* DevBuf::get(size_t bytes) {
@@ -137,6 +165,22 @@ struct aires_b200_operand_s {
 extern "C" {
 
 int aires_b200_abi_version(void) { return AIRES_B200_ABI_VERSION; }
+
+int aires_b200_set_option(const char* name, int64_t value) {
+  return ab2::guarded([&] {
+    if (!name || !ab2::option_known(name)) ab2::fail(AIRES_B200_INVALID_ARGUMENT, std::string("unknown option ") + (name ? name : "(null)"));
+    for (auto& kv : ab2::t_options_ref())
+      if (kv.first == name) {
+        kv.second = value;
+        return;
+      }
+    ab2::t_options_ref().emplace_back(name, value);
+  });
+}
+
+int aires_b200_clear_options(void) {
+  return ab2::guarded([&] { ab2::t_options_ref().clear(); });
+}
 
 const char* aires_b200_last_error(void) { return ab2::tl_error.c_str(); }
 

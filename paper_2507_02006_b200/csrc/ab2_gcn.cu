@@ -537,7 +537,7 @@ void combine_stage(Ctx& ctx, const Staged& s, int64_t rows, const V* w, int64_t 
   if constexpr (sizeof(V) == 4) {
     const int H = w_cols > 128 ? 2 : 1;
     const size_t smem4 = static_cast<size_t>(w_rows) * 128 * H * 4;
-    if (w_cols >= 96 && w_cols <= 256 && smem4 <= 200 * 1024 && env_int("AB2_COMBINE_V4", 1)) {
+    if (w_cols >= 96 && w_cols <= 256 && smem4 <= 200 * 1024 && option("combine_v4", 1)) {
       auto k = H == 2 ? k_combine_v4<IdxT, IdxO, 2> : k_combine_v4<IdxT, IdxO, 1>;
       AB2_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem4)));
       int nb = 0;
@@ -550,7 +550,7 @@ void combine_stage(Ctx& ctx, const Staged& s, int64_t rows, const V* w, int64_t 
       return;
     }
   }
-  const bool smem = static_cast<size_t>(w_rows * w_cols) * sizeof(V) <= 200 * 1024 && env_int("AB2_COMBINE_SMEM", 1);
+  const bool smem = static_cast<size_t>(w_rows * w_cols) * sizeof(V) <= 200 * 1024 && option("combine_smem", 1);
   if (smem)
     combine_launch2<V, IdxT, IdxO, J, false, true, true>(ctx, s, rows, w, w_rows, w_cols, cnt, nullptr, tcol, tval, ctl,
                                                           toff, t_cap);
@@ -562,7 +562,7 @@ void combine_stage(Ctx& ctx, const Staged& s, int64_t rows, const V* w, int64_t 
 template <class V, class IdxT, class IdxO, int J>
 void combine_launch(Ctx& ctx, const Staged& s, int64_t rows, const V* w, int64_t w_rows, int64_t w_cols, int32_t* cnt,
                     int64_t* optr, IdxO* ocol, V* oval, Ctl* ctl, bool fill) {
-  const bool smem = static_cast<size_t>(w_rows * w_cols) * sizeof(V) <= 200 * 1024 && env_int("AB2_COMBINE_SMEM", 1);
+  const bool smem = static_cast<size_t>(w_rows * w_cols) * sizeof(V) <= 200 * 1024 && option("combine_smem", 1);
   if (fill && smem)
     combine_launch2<V, IdxT, IdxO, J, true, true>(ctx, s, rows, w, w_rows, w_cols, cnt, optr, ocol, oval, ctl);
   else if (fill)
@@ -603,7 +603,7 @@ void combine_t(Ctx& ctx, const aires_b200_matrix& x, const void* w_in, uint64_t 
   // one pass when the output fits one column tile and its dense-bound staging fits in memory
   const uint64_t t_cap = combine_stage_cap(ctx, rows, static_cast<int64_t>(w_cols));
   const bool one_pass = rows > 0 && w_cols > 0 && static_cast<int64_t>(w_cols) <= 32 * std::max(J, 1) &&
-                        t_cap * (sizeof(IdxO) + sizeof(V)) <= (uint64_t(48) << 30) && env_int("AB2_COMBINE_ONE_PASS", 1);
+                        t_cap * (sizeof(IdxO) + sizeof(V)) <= (uint64_t(48) << 30) && option("combine_one_pass", 1);
   if (one_pass) {
     IdxO* tcol = static_cast<IdxO*>(ctx.t_col.get(t_cap * sizeof(IdxO)));
     V* tval = static_cast<V*>(ctx.t_val.get(t_cap * sizeof(V)));
@@ -1124,7 +1124,7 @@ void layer_fused(Ctx& ctx, const aires_b200_matrix& at, const aires_b200_matrix&
   const int64_t rows = static_cast<int64_t>(at.n_rows), K = static_cast<int64_t>(h.n_rows);
   int launches = 0;
   // W narrower than H: aggregate T = H·W instead of H (see k_hw / k_agg_t)
-  if (w_cols < h.n_cols && env_int("AB2_FUSED_REASSOC", 1) != 0) {
+  if (w_cols < h.n_cols && option("fused_reassoc", 1) != 0) {
     const int M4 = (M + 3) / 4;
     const size_t smem = static_cast<size_t>(M4) * w_cols * 32 * 16 + 8 * 128 * M4 * 4;
     if (smem <= 200 * 1024) {

@@ -245,6 +245,11 @@ int robw_cuts(Ctx& ctx, const uint64_t* row_ptr, uint64_t n_rows, uint64_t m_a, 
               uint64_t V, uint32_t location, uint64_t* cuts, uint64_t cap, uint64_t* n_segs,
               uint64_t* bad_row);
 
-int64_t env_int(const char* name, int64_t def);
+// Tuning option / test hook set through aires_b200_set_option (this thread), else def.
+int64_t option(const char* name, int64_t def);
+bool option_known(const char* name);
+std::vector<std::pair<std::string, int64_t>>& t_options_ref();
+// AB2_TRACE=1 in the environment: per-run device timelines on stderr (diagnostics only).
+bool trace_enabled();
 
 }  // namespace ab2

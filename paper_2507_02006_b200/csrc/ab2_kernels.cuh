@@ -1,22 +1,25 @@
-// ab2_kernels.cuh -- sm_100a kernels of the B200 AIRES A·X SpGEMM.
+// ab2_kernels.cuh -- sm_100a kernels of the B200 AIRES A·X SpGEMM shared by the in-core product and
+// the out-of-core pipeline.
 //
 // Replaces the reference's inner-product spgemm_block (spgemm.hpp:60-132):
-//   K_classify  : rows whose A-degree exceeds the warp budget -> CTA-wide symbolic list
-//   K_symbolic  : per-row nnz(C) = |U_k cols(X_k)| (byte flags in shared memory) and
-//                 per-row MACs (spgemm.hpp:94-109 counts; :51 flops)
-//   K_scan      : exclusive scan of the counts -> int64 C row_ptr (spgemm.hpp:107, :111)
-//   K_numeric   : per-row dense shared-memory accumulator, emitted in ascending column
-//                 order (spgemm.hpp:114-130; canonical, sparse.hpp:26-28)
+//   K_classify  : rows whose A-degree exceeds the warp budget -> CTA-wide (heavy) list
+//   K_numeric   : (ab2_numeric.cuh) one pass per row into a dense shared-memory accumulator,
+//                 counted and emitted in ascending column order (spgemm.hpp:114-130; canonical,
+//                 sparse.hpp:26-28) into a bump-allocated staging area
+//   K_scan      : exclusive scan of the row counts -> int64 C row_ptr (spgemm.hpp:107, :111)
+//   K_place     : staging -> exact CSR offsets (after the caller's exact allocation, :111-112)
+//   K_symbolic  : per-row nnz(C) = |U_k cols(X_k)| (byte flags in shared memory) and per-row MACs
+//                 -- only where C's sizes are needed before any product: the out-of-core tiles
+//                 (scheduler.hpp:103-139), each sized on the device before it is multiplied
 //
-// Work distribution: heavy rows (by A-degree for symbolic, by MACs for numeric) are
-// claimed first, one CTA per row; light rows then go one warp per row from a ticket
-// counter in batches.  No shared-memory fp atomics other than the fp32 CAS add (ATOMS
-// .CAST.SPIN, measured 11.7 SM-cycles per warp op on B200) and no MATCH.ANY (63).
+// Work distribution: heavy rows are claimed first, one CTA per row; light rows then go one warp per
+// row from a ticket counter in batches.  No shared-memory fp atomics (smem CAS add measured 11.7
+// SM-cycles per warp op on B200) and no MATCH.ANY.
 //
-// Accumulator marker: cells start at -0.0.  -0.0 + p == p for every p except p == -0.0,
-// so a cell reads -0.0 afterwards only if every contribution was -0.0; such rows are
-// detected by comparing the emitted count with the symbolic count and re-run by K_fix
-// with explicit marks and a +0.0 start (dot_row_col's `sum = 0.0`, spgemm.hpp:27).
+// Accumulator marker: cells start at -0.0.  -0.0 + p == p for every p except p == -0.0, so a cell
+// still reads -0.0 only if it got no contribution or only -0.0 ones; rows where a product can be
+// exactly zero (zero / tiny weights, zeros stored in X) are re-run on the explicit-mark path with a
+// +0.0 start (dot_row_col's `sum = 0.0; if (hit)`, spgemm.hpp:27-41) -- see ab2_numeric.cuh.
 #pragma once
 #include "ab2_common.cuh"
 #include "ab2_operand.cuh"

@@ -341,7 +341,7 @@ XOperand::~XOperand() {
 
 int64_t wide_threshold(uint32_t mode) {
   const int64_t dense_max = mode == AIRES_B200_MODE_FP32 ? kMaxDenseColsF32 : kMaxDenseColsF64;
-  return std::max<int64_t>(32, std::min<int64_t>(dense_max, env_int("AB2_WIDE_AT", dense_max)));
+  return std::max<int64_t>(32, std::min<int64_t>(dense_max, option("wide_at", dense_max)));
 }
 
 std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uint32_t mode, bool temp, uint32_t plan,
@@ -414,7 +414,7 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
   AB2_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), ctx.stream));
   const size_t vb = mode == AIRES_B200_MODE_FP32 ? 4 : 8;
   if (plan == kPlanAuto)
-    plan = mode == AIRES_B200_MODE_FP32 && env_int("AB2_NUMERIC", 3) == 5 ? kPlanStep : kPlanSlots;
+    plan = mode == AIRES_B200_MODE_FP32 && option("numeric_kernel", 3) == 5 ? kPlanStep : kPlanSlots;
   if (mode != AIRES_B200_MODE_FP32) plan &= ~static_cast<uint32_t>(kPlanStep);
   auto alloc = [&](DevBuf& cache, size_t bytes) -> void* {
     if (rg) {
@@ -487,7 +487,7 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
       W = widths[i];
       break;
     }
-  int64_t forced = env_int("AB2_SLOT_W", 0);
+  int64_t forced = option("slot_w", 0);
   if (forced == 2 || forced == 4 || forced == 8 || forced == 16) W = static_cast<int>(forced);
   x->W = W;
   if (x->wide) plan = 0;
@@ -511,7 +511,7 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
     int w5 = mean >= 4.0 ? 8 : (mean >= 2.0 ? 4 : 2);
     const int64_t stride = (x->n_cols + 1 + 31) & ~int64_t(31);
     while (w5 < 32 && (32 / w5) * stride * 4 > 24 * 1024) w5 *= 2;
-    const int64_t fw = env_int("AB2_W5", 0);
+    const int64_t fw = option("w5", 0);
     if (fw == 2 || fw == 4 || fw == 8 || fw == 16 || fw == 32) w5 = static_cast<int>(fw);
     x->W5 = w5;
     const int64_t nb = (x->K + kScanTile - 1) / kScanTile;

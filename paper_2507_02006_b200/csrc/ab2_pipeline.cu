@@ -333,7 +333,7 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
   });
   rep.h2d_bytes += (n + 1) * 8;
   // row blocks of ~equal A nnz, the first one a quarter of the others (the D2H of C starts sooner)
-  const uint64_t T = static_cast<uint64_t>(std::max<int64_t>(1, env_int("AB2_STREAM_TILES", 16)));
+  const uint64_t T = static_cast<uint64_t>(std::max<int64_t>(1, option("stream_tiles", 16)));
   std::vector<uint64_t> cuts{0};
   const double unit = static_cast<double>(pend - p0) / (static_cast<double>(T) - 0.75);
   for (uint64_t i = 1; i < T; i++) {
@@ -368,7 +368,7 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
     cudaEvent_t loaded, computed, drained;
   };
   // AB2_TRACE=1: per-tile device timeline (loaded / computed / drained, ms from the start) on stderr
-  const bool trace = env_int("AB2_TRACE", 0) != 0;
+  const bool trace = trace_enabled();
   std::vector<cudaEvent_t> tl;
   if (trace)
     for (uint64_t j = 0; j < 3 * n_tiles; j++) tl.push_back(st.make_timed());
@@ -652,7 +652,7 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
     uint64_t up_bytes = 0;
   };
   // AB2_TRACE=1: per-tile device timeline (loaded / sized / last part computed / drained) on stderr
-  const bool trace = env_int("AB2_TRACE", 0) != 0;
+  const bool trace = trace_enabled();
   std::vector<cudaEvent_t> slot_free(nbuf, nullptr);
   // C entries per A entry, observed; the first tile assumes the mean X row length
   double rho = std::max(0.05, std::min(static_cast<double>(x->n_cols),
@@ -911,7 +911,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   const uint32_t nbuf = std::max<uint32_t>(2, std::min<uint32_t>(cfg.n_buffers ? cfg.n_buffers : 2, 8));
   std::memset(&rep, 0, sizeof(rep));
   // AB2_TRACE=1: host-side milestones on stderr (where the wall time of a run goes)
-  const bool trace = env_int("AB2_TRACE", 0) != 0;
+  const bool trace = trace_enabled();
   const auto t_host0 = std::chrono::steady_clock::now();
   auto mark = [&](const char* what) {
     if (!trace) return;
@@ -958,7 +958,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
                                                         : b.span;
     const uint64_t cs_bytes = xk * kCSlotW * 2;
     if (xk > 0 && xnnz >= 4 * xk && (cfg.device_budget == 0 || cs_bytes * 16 <= cfg.device_budget) &&
-        env_int("AB2_RUN_CSLOTS", 1) != 0)
+        option("run_cslots", 1) != 0)
       plan |= kPlanCSlots;
   }
   std::unique_ptr<XOperand> x;
@@ -972,7 +972,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   // build synchronises the host once and must not queue behind A on the link).
   const uint64_t a_col_bytes = (pend - p0) * ib;
   const bool maxmem = cfg.c_aware == 2;  // the MaxMemory baseline (scheduler.hpp:174-293)
-  const bool early_cols = !maxmem && cfg.device_budget == 0 && env_int("AB2_RUN_RESIDENT_COLS", 1) != 0 && n > 0;
+  const bool early_cols = !maxmem && cfg.device_budget == 0 && option("run_resident_cols", 1) != 0 && n > 0;
   char* d_acol_full = nullptr;
   std::vector<uint64_t> early_cuts;
   std::vector<cudaEvent_t> early_ev;
@@ -1026,7 +1026,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   // A's column indices stay resident after the sizing pass when they take at most half of the
   // budget left (then Phase II streams only A's values): one column pass over the link instead of two
   const bool cols_resident =
-      early_cols || (!maxmem && env_int("AB2_RUN_RESIDENT_COLS", 1) != 0 && budget - fixed >= 2 * a_col_bytes + 4096);
+      early_cols || (!maxmem && option("run_resident_cols", 1) != 0 && budget - fixed >= 2 * a_col_bytes + 4096);
   if (cols_resident && !d_acol_full) d_acol_full = static_cast<char*>(arena.get(a_col_bytes));
   const uint64_t fixed2 = fixed + (cols_resident && !early_cols ? std::max<uint64_t>(a_col_bytes, 256) : 0);
   const uint64_t slot_budget = (budget - fixed2) / nbuf;
@@ -1192,7 +1192,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   uint64_t tile_budget = slot_budget;
   if (cfg.device_budget == 0) {
     const uint64_t p2_bytes = (pend - p0) * a_tile_bytes + nnz * (ib + vb) + n * row_bytes;
-    const uint64_t want = std::max<uint64_t>(env_int("AB2_RUN_TILES", 16), 1);
+    const uint64_t want = std::max<uint64_t>(option("run_tiles", 16), 1);
     tile_budget = std::min<uint64_t>(slot_budget, std::max<uint64_t>(p2_bytes / want, 64ull << 20));
   }
   // MaxMemory (partition.hpp:140-169): the element stream is cut at fixed byte boundaries, rows split

@@ -1,8 +1,8 @@
 // ab2_spgemm.cu -- host orchestration of one A·X product (spgemm_block, spgemm.hpp:60-132).
 //
-//   upload (host A only) -> K_classify -> K_symbolic -> K_scan -> [nnz readback, exact
-//   allocation through the caller's allocator, spgemm.hpp:111-112] -> K_numeric -> [K_fix]
-//   -> row_ptr copy -> (host C) D2H.
+//   upload (host A only) -> K_classify -> K_numeric (staging) -> K_scan -> [nnz readback, exact
+//   allocation through the caller's allocator, spgemm.hpp:111-112] -> K_place -> row_ptr copy
+//   -> (host C) D2H.  Operands wider than the dense accumulator run in column tiles (wide_product).
 #include <algorithm>
 #include <climits>
 #include <cmath>
@@ -46,7 +46,7 @@ void launch_numeric_w(Ctx& ctx, const Num3Args<V, IdxT>& p, int threads, size_t 
 
 template <class V, class IdxT>
 int numeric_warps(const Num3Args<V, IdxT>& p) {
-  int nw = std::min<int>(static_cast<int>(env_int("AB2_NUM_WARPS", 4)), AB2_NUM_MAXT / 32);
+  int nw = std::min<int>(static_cast<int>(option("num_warps", 4)), AB2_NUM_MAXT / 32);
   return std::max(1, std::min<int>(nw, static_cast<int>((200 * 1024) / p.warp_bytes)));
 }
 
@@ -69,7 +69,7 @@ void launch_numeric(Ctx& ctx, const Num3Args<V, IdxT>& p, int W, bool xz) {
 // k_numeric3 args.
 template <class IdxT, int W>
 void launch_numeric5_w(Ctx& ctx, const Num5Args<IdxT>& p, bool xz) {
-  int nw = static_cast<int>(env_int("AB2_N5_WARPS", AB2_N5_MAXT / 32));
+  int nw = static_cast<int>(option("n5_warps", AB2_N5_MAXT / 32));
   nw = std::max(1, std::min<int>({nw, AB2_N5_MAXT / 32, static_cast<int>((200 * 1024) / p.warp_bytes)}));
   const int threads = nw * 32;
   const size_t smem = static_cast<size_t>(nw) * p.warp_bytes;
@@ -167,7 +167,7 @@ Num3Args<V, IdxT> make_num3(const XOperand& x, const uint64_t* aptr, uint64_t ab
   np.tiny = x.xmin > 0 ? static_cast<V>((sizeof(V) == 4 ? std::ldexp(1.0, -147) : std::ldexp(1.0, -1072)) / x.xmin)
                        : V(0);
   np.stage_block = static_cast<uint32_t>(std::max<int64_t>(4096, 8 * static_cast<int64_t>(np.stride)));
-  np.pad0 = static_cast<int32_t>(env_int("AB2_SHORT", 1) != 0);
+  np.pad0 = static_cast<int32_t>(option("short_rows", 1) != 0);
   return np;
 }
 
@@ -177,7 +177,7 @@ Num3Args<V, IdxT> make_num3(const XOperand& x, const uint64_t* aptr, uint64_t ab
 template <class V, class IdxT>
 void launch_product(Ctx& ctx, const Num3Args<V, IdxT>& np, const XOperand& x) {
   if constexpr (std::is_same<V, float>::value) {
-    if (x.xdesc != nullptr && (x.slots == nullptr || env_int("AB2_NUMERIC", 3) == 5)) {
+    if (x.xdesc != nullptr && (x.slots == nullptr || option("numeric_kernel", 3) == 5)) {
       launch_numeric5<IdxT>(ctx, np, x);
       return;
     }
@@ -194,7 +194,7 @@ void run_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires_
   if (x.K >= (int64_t(1) << 31) / 16) fail(AIRES_B200_CAPACITY_EXCEEDED, "inner dimension too large for slot indexing");
   Ctl* ctl = ctx.ctl.as<Ctl>(1);
   Ctl* h = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));
-  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 1024);
+  const int64_t heavy_deg = option("heavy_deg", 1024);
   int64_t* heavy = ctx.sym_heavy.as<int64_t>(std::max<int64_t>(rows, 1));
   uint32_t* cnt = reinterpret_cast<uint32_t*>(ctx.cnt.as<int32_t>(std::max<int64_t>(rows, 1)));
   uint64_t* toff = reinterpret_cast<uint64_t*>(ctx.rflops.as<int64_t>(std::max<int64_t>(rows, 1)));
@@ -298,7 +298,7 @@ namespace {
 template <class V, class IdxT>
 int tile_product_t(Ctx& ctx, const XOperand& x, const TilePass& t) {
   if (t.rows <= 0) return 0;
-  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 1024);
+  const int64_t heavy_deg = option("heavy_deg", 1024);
   const int g = static_cast<int>(std::min<int64_t>((t.rows + 255) / 256, static_cast<int64_t>(ctx.sms) * 16));
   k_classify<<<g, 256, 0, ctx.stream>>>(t.aptr, t.rows, heavy_deg, t.heavy, t.ctl);
   AB2_CUDA(cudaGetLastError());
@@ -317,7 +317,7 @@ int tile_product_t(Ctx& ctx, const XOperand& x, const TilePass& t) {
 template <class IdxT>
 int tile_symbolic_t(Ctx& ctx, const XOperand& x, const TileSym& t) {
   if (t.rows <= 0) return 0;
-  const int64_t heavy_deg = env_int("AB2_SYM_HEAVY_DEG", 2048);
+  const int64_t heavy_deg = option("sym_heavy_deg", 2048);
   const int g = static_cast<int>(std::min<int64_t>((t.rows + 255) / 256, static_cast<int64_t>(ctx.sms) * 16));
   k_classify<<<g, 256, 0, ctx.stream>>>(t.aptr, t.rows, heavy_deg, t.heavy, t.ctl);
   AB2_CUDA(cudaGetLastError());
@@ -416,11 +416,11 @@ void wide_product(Ctx& ctx, const aires_b200_matrix& a, const XOperand& x, aires
                   const uint64_t* aptr, uint64_t abase, const IdxT* acol, const V* aval, uint64_t span_hint) {
   const int64_t rows = static_cast<int64_t>(a.n_rows);
   const int64_t n_cols = x.n_cols;
-  const int64_t tw = std::min<int64_t>(wide_threshold(x.mode), std::max<int64_t>(32, env_int("AB2_WIDE_TILE", 2048)));
+  const int64_t tw = std::min<int64_t>(wide_threshold(x.mode), std::max<int64_t>(32, option("wide_tile", 2048)));
   const int64_t T = (n_cols + tw - 1) / tw;
   const int64_t K = x.K;
   const uint32_t mode = x.mode;
-  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 1024);
+  const int64_t heavy_deg = option("heavy_deg", 1024);
   int64_t* heavy = ctx.sym_heavy.as<int64_t>(std::max<int64_t>(rows, 1));
   struct Tile {
     DevBuf ptr, col, val, cnt, toff, tcol, tval;
@@ -554,7 +554,7 @@ namespace {
 template <class V, class IdxT>
 int tile_product_staged_t(Ctx& ctx, const XOperand& x, const TileStaged& t) {
   if (t.rows <= 0) return 0;
-  const int64_t heavy_deg = env_int("AB2_HEAVY_DEG", 1024);
+  const int64_t heavy_deg = option("heavy_deg", 1024);
   const int g = static_cast<int>(std::min<int64_t>((t.rows + 255) / 256, static_cast<int64_t>(ctx.sms) * 16));
   k_classify<<<g, 256, 0, ctx.stream>>>(t.aptr, t.rows, heavy_deg, t.heavy, t.ctl);
   AB2_CUDA(cudaGetLastError());

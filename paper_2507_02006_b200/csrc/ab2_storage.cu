@@ -49,11 +49,11 @@ struct CuFileApi {
 
   bool load() {
     if (so) return open;
-    if (env_int("AB2_NO_GDS", 0)) return false;
+    if (option("no_gds", 0)) return false;
     // GPUDirect Storage needs the nvidia-fs kernel module; without it cuFileDriverOpen was measured
     // to block for minutes on the B200 boxes, so the driver is only opened when the module is
     // loaded (or AB2_GDS=1 forces the attempt).  Otherwise the pinned-host path is used.
-    if (::access("/proc/driver/nvidia-fs", F_OK) != 0 && env_int("AB2_GDS", 0) == 0) {
+    if (::access("/proc/driver/nvidia-fs", F_OK) != 0 && option("gds", 0) == 0) {
       so = reinterpret_cast<void*>(1);  // probed: unavailable
       return false;
     }

@@ -144,3 +144,14 @@ def test_matrix_container_round_trip(tmp_path):
     with pytest.raises(ab.AiresError) as e:
         ab.read_matrix(p)
     assert e.value.code == ab.errc.parse_error
+
+
+def test_options_are_explicit_and_validated():
+    # tuning options / test hooks go through aires_b200_set_option (no environment variables)
+    ab.set_option("heavy_deg", 512)
+    ab.clear_options()
+    with ab.options(stream_tiles=4, wide_at=64):
+        pass
+    with pytest.raises(ab.AiresError) as e:
+        ab.set_option("no_such_option", 1)
+    assert e.value.status == 102  # AIRES_B200_INVALID_ARGUMENT

@@ -227,14 +227,14 @@ def test_power_law_cfg1_shape(mode):
 
 
 @pytest.mark.parametrize("mode", [ab.MODE_FP64_EXACT, ab.MODE_FP32])
-def test_wide_operand_column_tiles(mode, monkeypatch):
+def test_wide_operand_column_tiles(mode):
     """X wider than the dense accumulator: the product runs in column tiles of X (the reference's
     B column tiling, spgemm.hpp:94-130) and must still match bit for bit (fp64) / 1e-5 (fp32)."""
     rng = np.random.default_rng(31)
     for nc, tile in ((12000, "2048"), (300, "64"), (97, "32")):
-        monkeypatch.setenv("AB2_WIDE_TILE", tile)
+        ab.set_option("wide_tile", int(tile))
         if nc < 4096:
-            monkeypatch.setenv("AB2_WIDE_AT", "64")
+            ab.set_option("wide_at", 64)
         a = random_csr(rng, 40, 50, 0.2)
         b = random_csr(rng, 50, nc, min(0.5, 30.0 / nc + 0.02))
         (wp, wi, wv), macs = oracle_product(40, 50, nc, a, b, inner=False)
@@ -350,14 +350,14 @@ def test_layer_fused_matches_unfused_chain(hcols, wcols):
 
 @pytest.mark.parametrize("cin,cout,path", [(100, 256, "v4"), (64, 130, "v4"), (40, 100, "v4"), (30, 96, "v4"),
                                            (100, 256, "scalar"), (64, 130, "two-pass"), (20, 300, "auto")])
-def test_combine_fp32_kernels_match_oracle(cin, cout, path, monkeypatch):
+def test_combine_fp32_kernels_match_oracle(cin, cout, path):
     """fp32 combine through each kernel path (LDS.128 one-pass for 96..256 output columns, the scalar
     one-pass, the two-pass count/fill) against the fp64 oracle: values within 1e-5 of the cell's
     scale sum |X|·|W|; only entries within that rounding of zero may flip across the ReLU."""
     if path == "scalar":
-        monkeypatch.setenv("AB2_COMBINE_V4", "0")
+        ab.set_option("combine_v4", 0)
     if path == "two-pass":
-        monkeypatch.setenv("AB2_COMBINE_ONE_PASS", "0")
+        ab.set_option("combine_one_pass", 0)
     rows = 5000
     x = ab.synth_features(rows, cin, 80.0, 11, idx_dtype=np.uint64)
     w = ab.gen_weights(cin, cout, 12)

@@ -52,8 +52,8 @@ def test_run_fp64_bit_exact_across_budgets(frac):
 
 
 @pytest.mark.parametrize("n_buffers,resident", [(2, "1"), (3, "0"), (4, "1"), (2, "0")])
-def test_run_fp32_tolerance_many_tiles(n_buffers, resident, monkeypatch):
-    monkeypatch.setenv("AB2_RUN_RESIDENT_COLS", resident)  # A columns kept on the device or re-streamed
+def test_run_fp32_tolerance_many_tiles(n_buffers, resident):
+    ab.set_option("run_resident_cols", int(resident))  # A columns kept on the device or re-streamed
     g, x = _graph(30_000, 400_000, 100, seed=4)
     wp, wi, wv, macs = _oracle(g, x)
     g32 = ab.CsrMatrix(g.n_rows, g.n_cols, g.row_ptr, g.col_idx.astype(np.uint32), g.values.astype(np.float32))
@@ -157,8 +157,8 @@ def test_maxmemory_baseline_same_result_more_traffic(frac):
 # ---- streamed output (AIRES_B200_RUN_STREAM_OUT): no sizing pass, C drained while A uploads ----
 
 @pytest.mark.parametrize("tiles", ["1", "5", "16", "300"])
-def test_stream_out_fp64_bit_exact(tiles, monkeypatch):
-    monkeypatch.setenv("AB2_STREAM_TILES", tiles)
+def test_stream_out_fp64_bit_exact(tiles):
+    ab.set_option("stream_tiles", int(tiles))
     g, x = _graph(20_000, 300_000, 128, seed=8)
     wp, wi, wv, macs = _oracle(g, x)
     res = ab.run_aires(g, x, ab.MemoryBudget(0), stream_out=True)
@@ -175,8 +175,8 @@ def test_stream_out_fp64_bit_exact(tiles, monkeypatch):
 
 
 @pytest.mark.parametrize("n_buffers", [2, 3, 4])
-def test_stream_out_fp32_matches_exact_protocol(n_buffers, monkeypatch):
-    monkeypatch.setenv("AB2_STREAM_TILES", "12")
+def test_stream_out_fp32_matches_exact_protocol(n_buffers):
+    ab.set_option("stream_tiles", 12)
     g, x = _graph(30_000, 400_000, 100, seed=4)
     g32 = ab.CsrMatrix(g.n_rows, g.n_cols, g.row_ptr, g.col_idx.astype(np.uint32), g.values.astype(np.float32))
     x32 = ab.CsrMatrix(x.n_rows, x.n_cols, x.row_ptr, x.col_idx.astype(np.uint32), x.values.astype(np.float32))
