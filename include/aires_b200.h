@@ -285,6 +285,8 @@ uint64_t aires_b200_checksum(uint64_t n_rows, uint64_t n_cols, uint64_t nnz, con
  *   run_cslots (1)          out-of-core sizing over 16-wide column slots when X rows average >= 4
  *   combine_one_pass (1), combine_smem (1), combine_v4 (1), fused_reassoc (1)  GCN kernel paths
  *   gds (0) / no_gds (0)    storage leg: force / forbid the cuFile attempt
+ *   stage_min_bytes (64 MiB) pageable host arrays at least this large move through pinned bounce
+ *                           slots (host copy threads) instead of being registered for the call
  */
 int aires_b200_set_option(const char* name, int64_t value);
 int aires_b200_clear_options(void);

@@ -29,7 +29,11 @@
 // (the operands arrive in host memory through the API).
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>
@@ -60,6 +64,172 @@ struct Pinned {
   }
 };
 
+bool is_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes at{};
+  const bool ok = cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type != cudaMemoryTypeUnregistered;
+  cudaGetLastError();
+  return ok;
+}
+
+// Host threads that copy between pageable caller arrays and pinned bounce buffers (Stager).
+struct CopyPool {
+  std::vector<std::thread> th;
+  std::mutex m;
+  std::condition_variable cv, idle;
+  std::vector<std::function<void()>> jobs;
+  size_t next = 0, left = 0;
+  uint64_t gen = 0;
+  bool stop = false;
+  explicit CopyPool(unsigned n) {
+    for (unsigned i = 0; i < n; i++)
+      th.emplace_back([this] {
+        uint64_t seen = 0;
+        for (;;) {
+          std::function<void()> job;
+          {
+            std::unique_lock<std::mutex> lk(m);
+            cv.wait(lk, [&] { return stop || (gen != seen && next < jobs.size()); });
+            if (stop) return;
+            job = jobs[next++];
+            if (next == jobs.size()) seen = gen;
+          }
+          job();
+          std::lock_guard<std::mutex> lk(m);
+          if (--left == 0) idle.notify_all();
+        }
+      });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(m);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : th) t.join();
+  }
+  // copies every (dst, src, bytes) in ~4 MB pieces across the pool and the calling thread
+  void copy(const std::vector<std::tuple<char*, const char*, uint64_t>>& segs) {
+    constexpr uint64_t kPiece = 4ull << 20;
+    std::vector<std::function<void()>> js;
+    for (const auto& sg : segs)
+      for (uint64_t o = 0; o < std::get<2>(sg); o += kPiece) {
+        const uint64_t n = std::min(kPiece, std::get<2>(sg) - o);
+        char* d = std::get<0>(sg) + o;
+        const char* s2 = std::get<1>(sg) + o;
+        js.emplace_back([d, s2, n] { std::memcpy(d, s2, n); });
+      }
+    if (js.empty()) return;
+    if (js.size() == 1 || th.empty()) {
+      for (auto& j : js) j();
+      return;
+    }
+    std::unique_lock<std::mutex> lk(m);
+    jobs = std::move(js);
+    next = 0;
+    left = jobs.size();
+    gen++;
+    cv.notify_all();
+    // the caller works too
+    while (next < jobs.size()) {
+      auto job = jobs[next++];
+      lk.unlock();
+      job();
+      lk.lock();
+      if (--left == 0) idle.notify_all();
+    }
+    idle.wait(lk, [&] { return left == 0; });
+    jobs.clear();
+  }
+};
+
+// Pageable caller arrays (the reference's std::vector storage behind the drop-in headers): instead of
+// registering gigabytes with the driver inside every call (cudaHostRegister pins page by page --
+// ~0.5 s for cfg2's A and C at the reference's widths), tiles travel through pinned bounce slots:
+// host threads copy a tile's A segments into an up-slot and the copy engine moves them to the device;
+// C parts come down into a down-slot and host threads copy them out once that DMA has completed
+// (before the slot is reused, or at the end of the run).  Page-locked caller buffers skip this.
+struct Stager {
+  struct Slot {
+    char* buf = nullptr;
+    uint64_t cap = 0;
+    cudaEvent_t done = nullptr;
+    bool armed = false;
+    std::vector<std::tuple<char*, const char*, uint64_t>> out;  // pending copy-outs (down slots)
+  };
+  CopyPool& pool;
+  std::vector<HostBuf>& ubuf;
+  std::vector<HostBuf>& dbuf;
+  std::vector<Slot> up, down;
+  size_t nu = 0, nd = 0;
+  Stager(CopyPool& p, std::vector<HostBuf>& u, std::vector<HostBuf>& d, uint32_t nbuf, std::vector<cudaEvent_t>& ev)
+      : pool(p), ubuf(u), dbuf(d), up(nbuf), down(nbuf) {
+    if (ubuf.size() < nbuf) ubuf.resize(nbuf);
+    if (dbuf.size() < nbuf) dbuf.resize(nbuf);
+    while (ev.size() < 2 * nbuf) {
+      cudaEvent_t e;
+      AB2_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev.push_back(e);
+    }
+    for (uint32_t i = 0; i < nbuf; i++) {
+      up[i].done = ev[i];
+      down[i].done = ev[nbuf + i];
+    }
+  }
+  // host -> device: segments (dev, host, bytes) through the next up-slot, queued on stream s
+  void h2d(const std::vector<std::tuple<char*, const char*, uint64_t>>& segs, cudaStream_t s) {
+    Slot& sl = up[nu % up.size()];
+    const uint32_t i = static_cast<uint32_t>(nu++ % up.size());
+    uint64_t total = 0;
+    for (const auto& g : segs) total += (std::get<2>(g) + 255) & ~uint64_t(255);
+    if (sl.armed) AB2_CUDA(cudaEventSynchronize(sl.done));  // its previous upload has left
+    sl.buf = static_cast<char*>(ubuf[i].get(total));
+    std::vector<std::tuple<char*, const char*, uint64_t>> in;
+    uint64_t o = 0;
+    for (const auto& g : segs) {
+      in.emplace_back(sl.buf + o, std::get<1>(g), std::get<2>(g));
+      o += (std::get<2>(g) + 255) & ~uint64_t(255);
+    }
+    pool.copy(in);
+    o = 0;
+    for (const auto& g : segs) {
+      if (std::get<2>(g)) AB2_CUDA(cudaMemcpyAsync(std::get<0>(g), sl.buf + o, std::get<2>(g), cudaMemcpyHostToDevice, s));
+      o += (std::get<2>(g) + 255) & ~uint64_t(255);
+    }
+    AB2_CUDA(cudaEventRecord(sl.done, s));
+    sl.armed = true;
+  }
+  // device -> host: segments (host, dev, bytes) into the next down-slot, queued on stream s; the
+  // host copies happen when the slot comes round again or at finish()
+  void d2h(const std::vector<std::tuple<char*, const char*, uint64_t>>& segs, cudaStream_t s) {
+    const uint32_t i = static_cast<uint32_t>(nd++ % down.size());
+    Slot& sl = down[i];
+    retire(sl);
+    uint64_t total = 0;
+    for (const auto& g : segs) total += (std::get<2>(g) + 255) & ~uint64_t(255);
+    sl.buf = static_cast<char*>(dbuf[i].get(total));
+    uint64_t o = 0;
+    for (const auto& g : segs) {
+      if (std::get<2>(g)) AB2_CUDA(cudaMemcpyAsync(sl.buf + o, std::get<1>(g), std::get<2>(g), cudaMemcpyDeviceToHost, s));
+      sl.out.emplace_back(std::get<0>(g), sl.buf + o, std::get<2>(g));
+      o += (std::get<2>(g) + 255) & ~uint64_t(255);
+    }
+    AB2_CUDA(cudaEventRecord(sl.done, s));
+    sl.armed = true;
+  }
+  void retire(Slot& sl) {
+    if (!sl.armed) return;
+    AB2_CUDA(cudaEventSynchronize(sl.done));
+    pool.copy(sl.out);
+    sl.out.clear();
+    sl.armed = false;
+  }
+  void finish() {
+    // oldest first, so the copies follow the order C arrived in
+    for (size_t k = 0; k < down.size(); k++) retire(down[(nd + k) % down.size()]);
+  }
+};
+
 // Routes the kernels a helper launches on ctx.stream to another stream for a scope.
 struct StreamSwap {
   Ctx& ctx;
@@ -87,6 +257,14 @@ struct PipeCacheImpl {
   std::vector<cudaEvent_t> ev, tev;  // disable-timing / timing
   std::vector<DevBuf> bufs;
   DevBuf region;  // the capped streamed run's budget, carved by a Region
+  // pageable caller arrays: pinned bounce slots and the host copy threads (Stager)
+  std::vector<HostBuf> bounce_up, bounce_down;
+  std::vector<cudaEvent_t> stage_ev;
+  std::unique_ptr<CopyPool> pool;
+  CopyPool& copy_pool() {
+    if (!pool) pool = std::make_unique<CopyPool>(std::max(1u, std::min(15u, std::thread::hardware_concurrency() - 1)));
+    return *pool;
+  }
   PipeCacheImpl() {
     AB2_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
     AB2_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
@@ -94,6 +272,8 @@ struct PipeCacheImpl {
     bufs.resize(32);
   }
   ~PipeCacheImpl() {
+    pool.reset();
+    for (auto e : stage_ev) cudaEventDestroy(e);
     for (auto e : ev) cudaEventDestroy(e);
     for (auto e : tev) cudaEventDestroy(e);
     if (h2d) cudaStreamDestroy(h2d);
@@ -308,7 +488,7 @@ __global__ void k_tile_ptr(const int64_t* __restrict__ in, int64_t n, const Ctl*
 // the link (the run's Phase I).  Same results as the exact run; out.nnz is the exact count.
 void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b, uint32_t mode, uint32_t nbuf,
                 aires_b200_output& out, aires_b200_run_report& rep, Streams& st, Arena& arena, Pinned& pin, Tracer& tr,
-                const aires_b200_run_config& cfg) {
+                const aires_b200_run_config& cfg, Stager& sg, bool stage_a) {
   const uint32_t ib = a.idx_bytes, vb = mode == AIRES_B200_MODE_FP32 ? 4 : 8;
   const uint64_t n = a.n_rows;
   const uint64_t p0 = a.ptr[0], pend = a.ptr[n];
@@ -356,9 +536,13 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
   void *optr = nullptr, *oidx = nullptr, *oval = nullptr;
   int rc = out.alloc(out.user, n, bound, &optr, &oidx, &oval);
   if (rc != 0) fail(rc, "output allocator failed for a bound of " + std::to_string(bound) + " nonzeros");
-  pin.ensure(optr, (n + 1) * 8);
-  pin.ensure(oidx, bound * ib);
-  pin.ensure(oval, bound * vb);
+  // pageable output arrays come down through the stager's pinned bounce slots
+  const bool stage_c = bound * (ib + vb) >= static_cast<uint64_t>(option("stage_min_bytes", 64ll << 20)) && (!is_pinned(oidx) || !is_pinned(oval) || !is_pinned(optr));
+  if (!stage_c) {
+    pin.ensure(optr, (n + 1) * 8);
+    pin.ensure(oidx, bound * ib);
+    pin.ensure(oval, bound * vb);
+  }
   struct Slot {
     void *acol, *aval, *tcol, *tval, *ccol, *cval;
     int64_t *cptr, *heavy, *part;
@@ -420,6 +604,14 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
     AB2_CUDA(cudaStreamWaitEvent(st.d2h, s.computed, 0));  // (already complete: the host waited on it)
     const uint64_t dn_bytes = (rows + 1) * 8 + nz * (ib + vb);
     tr.span(st.d2h, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_D2H, AIRES_B200_BUF_C_BLOCK, j, dn_bytes, 0, [&] {
+      if (stage_c) {
+        sg.d2h({{reinterpret_cast<char*>(static_cast<uint64_t*>(optr) + r0), reinterpret_cast<const char*>(s.optr),
+                 (rows + 1) * 8},
+                {static_cast<char*>(oidx) + running * ib, static_cast<const char*>(s.ccol), nz * ib},
+                {static_cast<char*>(oval) + running * vb, static_cast<const char*>(s.cval), nz * vb}},
+               st.d2h);
+        return;
+      }
       AB2_CUDA(cudaMemcpyAsync(static_cast<uint64_t*>(optr) + r0, s.optr, (rows + 1) * 8, cudaMemcpyDeviceToHost, st.d2h));
       if (nz) {
         AB2_CUDA(cudaMemcpyAsync(static_cast<char*>(oidx) + running * ib, s.ccol, nz * ib, cudaMemcpyDeviceToHost, st.d2h));
@@ -440,7 +632,11 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
     up_bytes[j] = (q1 - q0) * (ib + vb);
     tr.point(st.h2d, AIRES_B200_EV_ALLOC, AIRES_B200_BUF_A_TILE, j, up_bytes[j]);
     tr.span(st.h2d, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_A_TILE, j, up_bytes[j], 0, [&] {
-      if (q1 > q0) {
+      if (q1 > q0 && stage_a) {
+        sg.h2d({{static_cast<char*>(s.acol), static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib},
+                {static_cast<char*>(s.aval), static_cast<const char*>(a.val) + q0 * vb, (q1 - q0) * vb}},
+               st.h2d);
+      } else if (q1 > q0) {
         AB2_CUDA(cudaMemcpyAsync(s.acol, static_cast<const char*>(a.idx) + q0 * ib, (q1 - q0) * ib,
                                  cudaMemcpyHostToDevice, st.h2d));
         AB2_CUDA(cudaMemcpyAsync(s.aval, static_cast<const char*>(a.val) + q0 * vb, (q1 - q0) * vb,
@@ -492,6 +688,7 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
   tr.point(cs, AIRES_B200_EV_FREE, AIRES_B200_BUF_B, 0, x->bytes);
   AB2_CUDA(cudaEventRecord(t_end, cs));
   AB2_CUDA(cudaStreamSynchronize(cs));
+  sg.finish();  // pageable outputs: the last parts' host copies
   if (trace) {
     std::fprintf(stderr, "[ab2 stream] phase1 (X, A row_ptr) %.3f ms\n", ms_between(t_begin, t_p1));
     for (uint64_t j = 0; j < n_tiles; j++)
@@ -583,7 +780,8 @@ __global__ void k_tile_report(const Ctl* __restrict__ ctl, const int64_t* __rest
 // inside the tile), never a re-upload.  Slot layout: [A cols | A vals | per-row scratch | C region].
 void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b, uint32_t mode,
                        uint32_t nbuf, uint64_t budget, aires_b200_output& out, aires_b200_run_report& rep,
-                       Streams& st, Arena& arena, Pinned& pin, Tracer& tr, const aires_b200_run_config& cfg) {
+                       Streams& st, Arena& arena, Pinned& pin, Tracer& tr, const aires_b200_run_config& cfg, Stager& sg,
+                       bool stage_a) {
   const uint32_t ib = a.idx_bytes, vb = mode == AIRES_B200_MODE_FP32 ? 4 : 8;
   const uint64_t n = a.n_rows;
   const uint64_t p0 = a.ptr[0], pend = a.ptr[n];
@@ -629,9 +827,12 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
   void *optr = nullptr, *oidx = nullptr, *oval = nullptr;
   int rc = out.alloc(out.user, n, bound, &optr, &oidx, &oval);
   if (rc != 0) fail(rc, "output allocator failed for a bound of " + std::to_string(bound) + " nonzeros");
-  pin.ensure(optr, (n + 1) * 8);
-  pin.ensure(oidx, bound * ib);
-  pin.ensure(oval, bound * vb);
+  const bool stage_c = bound * (ib + vb) >= static_cast<uint64_t>(option("stage_min_bytes", 64ll << 20)) && (!is_pinned(oidx) || !is_pinned(oval) || !is_pinned(optr));
+  if (!stage_c) {
+    pin.ensure(optr, (n + 1) * 8);
+    pin.ensure(oidx, bound * ib);
+    pin.ensure(oval, bound * vb);
+  }
   AB2_CUDA(cudaEventRecord(t_p1, cs));
   tr.set_phase(1, "aires phase II (tiles)");
 
@@ -711,6 +912,13 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
     const uint64_t j = tiles.size();
     tr.point(st.h2d, AIRES_B200_EV_ALLOC, AIRES_B200_BUF_A_TILE, j, up_bytes);
     tr.span(st.h2d, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_H2D, AIRES_B200_BUF_A_TILE, j, up_bytes, 0, [&] {
+      if (stage_a) {
+        sg.h2d({{reinterpret_cast<char*>(t.aptr), reinterpret_cast<const char*>(a.ptr + t.r0), (rows + 1) * 8},
+                {t.acol, static_cast<const char*>(a.idx) + t.q0 * ib, an * ib},
+                {t.aval, static_cast<const char*>(a.val) + t.q0 * vb, an * vb}},
+               st.h2d);
+        return;
+      }
       AB2_CUDA(cudaMemcpyAsync(t.aptr, a.ptr + t.r0, (rows + 1) * 8, cudaMemcpyHostToDevice, st.h2d));
       if (an) {
         AB2_CUDA(cudaMemcpyAsync(t.acol, static_cast<const char*>(a.idx) + t.q0 * ib, an * ib, cudaMemcpyHostToDevice, st.h2d));
@@ -814,6 +1022,14 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
       AB2_CUDA(cudaStreamWaitEvent(st.d2h, computed, 0));
       const uint64_t dn_bytes = (pb - pa + 1) * 8 + pn * (ib + vb);
       tr.span(st.d2h, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_D2H, AIRES_B200_BUF_C_BLOCK, j, dn_bytes, 0, [&] {
+        if (stage_c) {
+          sg.d2h({{reinterpret_cast<char*>(static_cast<uint64_t*>(optr) + t.r0 + pa),
+                   reinterpret_cast<const char*>(t.optr + pa), (pb - pa + 1) * 8},
+                  {static_cast<char*>(oidx) + running * ib, t.ccol, pn * ib},
+                  {static_cast<char*>(oval) + running * vb, t.cval, pn * vb}},
+                 st.d2h);
+          return;
+        }
         AB2_CUDA(cudaMemcpyAsync(static_cast<uint64_t*>(optr) + t.r0 + pa, t.optr + pa, (pb - pa + 1) * 8,
                                  cudaMemcpyDeviceToHost, st.d2h));
         if (pn) {
@@ -849,6 +1065,7 @@ void run_stream_capped(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_ma
   tr.point(cs, AIRES_B200_EV_FREE, AIRES_B200_BUF_B, 0, x_keep);
   AB2_CUDA(cudaEventRecord(t_end, cs));
   AB2_CUDA(cudaStreamSynchronize(cs));
+  sg.finish();  // pageable outputs: the last parts' host copies
   {
     unsigned long long hb = 0;
     AB2_CUDA(cudaMemcpy(&hb, d_bad, 8, cudaMemcpyDeviceToHost));
@@ -927,17 +1144,32 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   SyncGuard sync{{cs, st.h2d, st.d2h, st.aux}};  // destroyed before pin (no copy outlives its buffers)
   Tracer tr(st);
   cudaEvent_t t_begin = st.make_timed(), t_p1 = st.make_timed(), t_p2 = st.make_timed(), t_end = st.make_timed();
+  // tiles hold whole C rows in the dense accumulator: wider features are the in-core product's
+  // column tiles (aires_b200_spgemm) -- the drop-in's run_aires falls back to the reference scheduler
+  if (static_cast<int64_t>(b.n_cols) > wide_threshold(mode))
+    fail(AIRES_B200_UNSUPPORTED_FORMAT, "run: feature matrix has " + std::to_string(b.n_cols) +
+                                            " columns; the out-of-core pipeline supports " +
+                                            std::to_string(wide_threshold(mode)));
+  const bool streamed = (cfg.flags & AIRES_B200_RUN_STREAM_OUT) && cfg.c_aware != 2 &&
+                        (cfg.device_budget == 0 || cfg.c_aware == 1) &&
+                        static_cast<int64_t>(b.n_cols) <= wide_threshold(mode);
+  // streamed runs move pageable A arrays through pinned bounce slots instead of registering them
+  const bool stage_a = streamed && (pend - p0) * (ib + vb) >= static_cast<uint64_t>(option("stage_min_bytes", 64ll << 20)) &&
+                       (!is_pinned(static_cast<const char*>(a.idx) + p0 * ib) ||
+                        !is_pinned(static_cast<const char*>(a.val) + p0 * vb));
   pin.ensure(a.ptr, (n + 1) * 8);
-  pin.ensure(static_cast<const char*>(a.idx) + p0 * ib, (pend - p0) * ib);
-  pin.ensure(static_cast<const char*>(a.val) + p0 * vb, (pend - p0) * vb);
-  if ((cfg.flags & AIRES_B200_RUN_STREAM_OUT) && cfg.device_budget == 0 && cfg.c_aware != 2 &&
-      static_cast<int64_t>(b.n_cols) <= wide_threshold(mode)) {
-    run_stream(ctx, a, b, mode, cfg.n_buffers ? nbuf : 3, out, rep, st, arena, pin, tr, cfg);
-    return;
+  if (!stage_a) {
+    pin.ensure(static_cast<const char*>(a.idx) + p0 * ib, (pend - p0) * ib);
+    pin.ensure(static_cast<const char*>(a.val) + p0 * vb, (pend - p0) * vb);
   }
-  if ((cfg.flags & AIRES_B200_RUN_STREAM_OUT) && cfg.device_budget > 0 && cfg.c_aware == 1 &&
-      static_cast<int64_t>(b.n_cols) <= wide_threshold(mode)) {
-    run_stream_capped(ctx, a, b, mode, cfg.n_buffers ? nbuf : 3, cfg.device_budget, out, rep, st, arena, pin, tr, cfg);
+  if (streamed) {
+    PipeCacheImpl& pc = *static_cast<PipeCacheImpl*>(ctx.pipe);
+    const uint32_t nb = cfg.n_buffers ? nbuf : 3;
+    Stager sg(pc.copy_pool(), pc.bounce_up, pc.bounce_down, nb, pc.stage_ev);
+    if (cfg.device_budget == 0)
+      run_stream(ctx, a, b, mode, nb, out, rep, st, arena, pin, tr, cfg, sg, stage_a);
+    else
+      run_stream_capped(ctx, a, b, mode, nb, cfg.device_budget, out, rep, st, arena, pin, tr, cfg, sg, stage_a);
     return;
   }
 

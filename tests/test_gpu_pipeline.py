@@ -337,3 +337,20 @@ def test_run_trace_audits(proto):
         assert res.report.merge_seconds > 0
     elif proto != "maxmemory":
         assert res.report.merge_seconds == 0.0
+
+
+@pytest.mark.parametrize("budget_frac", [0.0, 0.3])
+def test_pageable_arrays_through_bounce_slots(budget_frac):
+    """Pageable caller arrays (numpy here, std::vector behind the drop-in) move through pinned bounce
+    slots with host copy threads instead of being registered for the call (stage_min_bytes=0 forces
+    it at test size): C bit-identical to the oracle, every byte of A up once, C's tiles down in order."""
+    g, x = _graph(20_000, 300_000, 128, seed=12)
+    wp, wi, wv, macs = _oracle(g, x)
+    a_b, c_b = _bytes(g, x, (wp, wi))
+    budget = int(3e6 + budget_frac * (a_b + c_b)) if budget_frac else 0
+    with ab.options(stage_min_bytes=0, stream_tiles=7):
+        res = ab.run_aires(g, x, ab.MemoryBudget(budget), stream_out=True, n_buffers=3)
+    assert res.report.segments >= 2
+    assert np.array_equal(res.c.row_ptr, wp) and np.array_equal(res.c.col_idx, wi)
+    assert res.report.c_checksum == po.checksum(g.n_rows, x.n_cols, wp, wi, wv)
+    assert res.report.flops == macs
