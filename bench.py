@@ -283,6 +283,17 @@ def max_over_ranks(v: float, dist, cdev):
     return float(t.item())
 
 
+def gather_over_ranks(v: float, dist, cdev) -> list:
+    """Every rank's value (rank order), for per-rank figures on rank 0's line."""
+    if not dist:
+        return [v]
+    import torch
+    t = torch.tensor([float(v)], dtype=torch.float64, device=cdev)
+    out = torch.zeros(dist.get_world_size(), dtype=torch.float64, device=cdev)
+    dist.all_gather_into_tensor(out, t)
+    return [round(float(x), 4) for x in out.cpu()]
+
+
 def sum_over_ranks(v: int, dist, cdev):
     if not dist:
         return v
@@ -341,8 +352,8 @@ def run_b200(args, cfg):
     try:  # DRAM bytes of the dominant kernel from the committed ncu --set full capture (cfg2 fp32)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
-        if cfg is CONFIGS["cfg2"] and world == 1 and "k_numeric" in tj:
-            traffic = tj["k_numeric"]["dram_bytes"] if tj["k_numeric"].get("kernel") else None
+        if cfg is CONFIGS["cfg2"] and world == 1 and "k_numeric3" in tj:
+            traffic = int(tj["k_numeric3"]["dram_bytes"])
     except Exception:
         traffic = None
     roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
@@ -585,6 +596,7 @@ def e2e_leg(args, dev, L, ab, torch, blk, x, res32, tot_macs, dist, cdev, res64=
                          "link_gbs": {k: round(v, 2) for k, v in link.items()}, "t_roof_ms": round(t_alg, 3),
                          "frac": round(per_rank_frac, 4),
                          "frac_max_over_ranks": round(t_alg / e_ms_max, 4) if dist else None,
+                         "per_rank_frac": gather_over_ranks(per_rank_frac, dist, cdev) if dist else None,
                          "basis": "max((B_A+B_X)/measured pinned H2D, B_C/measured pinned D2H); B = 8(rows+1)+8nnz",
                          "bytes_moved_over_algorithmic": round((h2d + d2h) / (b_a + b_x + b_c), 4)},
             "exact_protocol": {"api": "aires_b200_run without streamed output (sizing pass over A's columns, "
@@ -713,7 +725,8 @@ def out_of_core_legs(args, dev, L, ab, torch, g2, x2, res2, rank, world, dist, c
            "runs": runs, "checked": all(r["checked"] for r in runs)}
     if world > 1:
         out["ms_max_over_ranks"] = max_over_ranks(runs[0]["ms"], dist, cdev)
-        out["per_rank_link_frac"] = runs[0]["roofline"]["frac"]
+        out["per_rank_ms"] = gather_over_ranks(runs[0]["ms"], dist, cdev)
+        out["per_rank_link_frac"] = gather_over_ranks(runs[0]["roofline"]["frac"], dist, cdev)
     return out
 
 

@@ -116,7 +116,13 @@ __global__ void k_len_hist(const int64_t* __restrict__ xptr, int64_t K,
   }
   int64_t m = c[4];
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(&h[4], static_cast<unsigned long long>(m));
+  __shared__ int64_t s_m[32];
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < static_cast<int>(blockDim.x >> 5); i++) m = max(m, s_m[i]);
+    atomicMax(&h[4], static_cast<unsigned long long>(m));
+  }
 }
 
 // Slot rows 0..K-1 from the plain CSR, plus the dummy row K (see ab2_operand.cuh).
@@ -140,7 +146,20 @@ __global__ void k_x_val_stats(const V* __restrict__ xval, const int64_t* __restr
     mn = min(mn, __shfl_xor_sync(kFull, mn, o));
     z |= __shfl_xor_sync(kFull, z, o);
   }
+  // one atomic per block (every warp of every block hitting one word serialised ~30 us at cfg2)
+  __shared__ unsigned long long s_mn[32];
+  __shared__ int s_z[32];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) {
+    s_mn[w] = mn;
+    s_z[w] = z;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < nw; i++) {
+      mn = min(mn, s_mn[i]);
+      z |= s_z[i];
+    }
     if (mn != ~0ull) atomicMin(&st[0], mn);
     if (z) st[1] = 1;
   }
@@ -450,14 +469,14 @@ std::unique_ptr<XOperand> make_operand(Ctx& ctx, const aires_b200_matrix& b, uin
   AB2_CUDA(cudaMemsetAsync(&ctl->bad_row + 0, 0, 8, ctx.stream));
   AB2_CUDA(cudaMemsetAsync(&ctl->flops, 0xff, 8, ctx.stream));  // min |x| bits
   {
-    const int g = grid_for(std::max<int64_t>(x->nnz, 1), 256, ctx.sms);
+    const int g = std::min(grid_for(std::max<int64_t>(x->nnz, 1), 256, ctx.sms), ctx.sms * 8);
     auto* xp = static_cast<const int64_t*>(x->ptr);
     if (mode == AIRES_B200_MODE_FP32)
       k_x_val_stats<float><<<g, 256, 0, ctx.stream>>>(static_cast<float*>(x->val), xp, x->K, &ctl->flops);
     else
       k_x_val_stats<double><<<g, 256, 0, ctx.stream>>>(static_cast<double*>(x->val), xp, x->K, &ctl->flops);
   }
-  k_len_hist<<<grid_for(std::max<int64_t>(x->K, 1), 256, ctx.sms), 256, 0, ctx.stream>>>(
+  k_len_hist<<<std::min(grid_for(std::max<int64_t>(x->K, 1), 256, ctx.sms), ctx.sms * 8), 256, 0, ctx.stream>>>(
       static_cast<int64_t*>(x->ptr), x->K, hist);
   AB2_CUDA(cudaGetLastError());
   Ctl* h = static_cast<Ctl*>(ctx.h_ctl.get(sizeof(Ctl)));

@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <chrono>
 #include <condition_variable>
+#include <exception>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -119,7 +120,34 @@ struct CopyPool {
         const char* s2 = std::get<1>(sg) + o;
         js.emplace_back([d, s2, n] { std::memcpy(d, s2, n); });
       }
+    run(std::move(js));
+  }
+  // widens `count` u16 column indices to u32 / u64 (out_bytes) in ~2M-entry pieces
+  void widen(char* dst, const uint16_t* src, uint64_t count, uint32_t out_bytes) {
+    constexpr uint64_t kPiece = 512ull << 10;
+    std::vector<std::function<void()>> js;
+    for (uint64_t o = 0; o < count; o += kPiece) {
+      const uint64_t n = std::min(kPiece, count - o);
+      if (out_bytes == 4) {
+        uint32_t* d = reinterpret_cast<uint32_t*>(dst) + o;
+        const uint16_t* q = src + o;
+        js.emplace_back([d, q, n] {
+          for (uint64_t i = 0; i < n; i++) d[i] = q[i];
+        });
+      } else {
+        uint64_t* d = reinterpret_cast<uint64_t*>(dst) + o;
+        const uint16_t* q = src + o;
+        js.emplace_back([d, q, n] {
+          for (uint64_t i = 0; i < n; i++) d[i] = q[i];
+        });
+      }
+    }
+    run(std::move(js));
+  }
+  std::mutex run_mu;  // one batch at a time (the pipeline thread's uploads, the stager's copy-outs)
+  void run(std::vector<std::function<void()>>&& js) {
     if (js.empty()) return;
+    std::lock_guard<std::mutex> batch(run_mu);
     if (js.size() == 1 || th.empty()) {
       for (auto& j : js) j();
       return;
@@ -152,29 +180,47 @@ struct CopyPool {
 struct Stager {
   struct Slot {
     char* buf = nullptr;
-    uint64_t cap = 0;
     cudaEvent_t done = nullptr;
     bool armed = false;
     std::vector<std::tuple<char*, const char*, uint64_t>> out;  // pending copy-outs (down slots)
+    std::vector<std::tuple<char*, const uint16_t*, uint64_t, uint32_t>> wide;  // pending u16 -> u32/u64 widenings
   };
   CopyPool& pool;
   std::vector<HostBuf>& ubuf;
   std::vector<HostBuf>& dbuf;
   std::vector<Slot> up, down;
   size_t nu = 0, nd = 0;
-  Stager(CopyPool& p, std::vector<HostBuf>& u, std::vector<HostBuf>& d, uint32_t nbuf, std::vector<cudaEvent_t>& ev)
-      : pool(p), ubuf(u), dbuf(d), up(nbuf), down(nbuf) {
+  int device = 0;
+  // down-slots are retired (DMA landed -> host copies) by a background thread, in arrival order,
+  // so the thread that queues the pipeline never stops for them
+  std::thread bg;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<uint32_t> fifo;
+  size_t head = 0;
+  bool stop = false;
+  std::exception_ptr err;
+  Stager(CopyPool& p, std::vector<HostBuf>& u, std::vector<HostBuf>& d, uint32_t nbuf, std::vector<cudaEvent_t>& ev,
+         int dev)
+      : pool(p), ubuf(u), dbuf(d), up(nbuf), down(2 * nbuf), device(dev) {
     if (ubuf.size() < nbuf) ubuf.resize(nbuf);
-    if (dbuf.size() < nbuf) dbuf.resize(nbuf);
-    while (ev.size() < 2 * nbuf) {
+    if (dbuf.size() < 2 * nbuf) dbuf.resize(2 * nbuf);
+    while (ev.size() < 3 * nbuf) {
       cudaEvent_t e;
       AB2_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       ev.push_back(e);
     }
-    for (uint32_t i = 0; i < nbuf; i++) {
-      up[i].done = ev[i];
-      down[i].done = ev[nbuf + i];
+    for (uint32_t i = 0; i < nbuf; i++) up[i].done = ev[i];
+    for (uint32_t i = 0; i < 2 * nbuf; i++) down[i].done = ev[nbuf + i];
+  }
+  ~Stager() { halt(); }
+  void halt() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
     }
+    cv.notify_all();
+    if (bg.joinable()) bg.join();
   }
   // host -> device: segments (dev, host, bytes) through the next up-slot, queued on stream s
   void h2d(const std::vector<std::tuple<char*, const char*, uint64_t>>& segs, cudaStream_t s) {
@@ -199,14 +245,21 @@ struct Stager {
     AB2_CUDA(cudaEventRecord(sl.done, s));
     sl.armed = true;
   }
-  // device -> host: segments (host, dev, bytes) into the next down-slot, queued on stream s; the
-  // host copies happen when the slot comes round again or at finish()
-  void d2h(const std::vector<std::tuple<char*, const char*, uint64_t>>& segs, cudaStream_t s) {
+  // device -> host: segments (host, dev, bytes) into the next down-slot, queued on stream s, plus
+  // `narrow` u16 column indices (host dst, device u16 src, count, host width 4 or 8) that the host
+  // widens; the background thread does the host side once the DMA has landed
+  void d2h(const std::vector<std::tuple<char*, const char*, uint64_t>>& segs, cudaStream_t s,
+           const std::vector<std::tuple<char*, const uint16_t*, uint64_t, uint32_t>>& narrow = {}) {
     const uint32_t i = static_cast<uint32_t>(nd++ % down.size());
     Slot& sl = down[i];
-    retire(sl);
+    {
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [&] { return !sl.armed || err; });
+      if (err) std::rethrow_exception(err);
+    }
     uint64_t total = 0;
     for (const auto& g : segs) total += (std::get<2>(g) + 255) & ~uint64_t(255);
+    for (const auto& g : narrow) total += (std::get<2>(g) * 2 + 255) & ~uint64_t(255);
     sl.buf = static_cast<char*>(dbuf[i].get(total));
     uint64_t o = 0;
     for (const auto& g : segs) {
@@ -214,19 +267,58 @@ struct Stager {
       sl.out.emplace_back(std::get<0>(g), sl.buf + o, std::get<2>(g));
       o += (std::get<2>(g) + 255) & ~uint64_t(255);
     }
+    for (const auto& g : narrow) {
+      if (std::get<2>(g))
+        AB2_CUDA(cudaMemcpyAsync(sl.buf + o, std::get<1>(g), std::get<2>(g) * 2, cudaMemcpyDeviceToHost, s));
+      sl.wide.emplace_back(std::get<0>(g), reinterpret_cast<const uint16_t*>(sl.buf + o), std::get<2>(g), std::get<3>(g));
+      o += (std::get<2>(g) * 2 + 255) & ~uint64_t(255);
+    }
     AB2_CUDA(cudaEventRecord(sl.done, s));
-    sl.armed = true;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      sl.armed = true;
+      fifo.push_back(i);
+    }
+    cv.notify_all();
+    if (!bg.joinable()) bg = std::thread([this] { loop(); });
   }
-  void retire(Slot& sl) {
-    if (!sl.armed) return;
-    AB2_CUDA(cudaEventSynchronize(sl.done));
-    pool.copy(sl.out);
-    sl.out.clear();
-    sl.armed = false;
+  void loop() {
+    cudaSetDevice(device);
+    for (;;) {
+      uint32_t i;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return stop || head < fifo.size(); });
+        if (head >= fifo.size()) return;
+        i = fifo[head];
+      }
+      Slot& sl = down[i];
+      try {
+        AB2_CUDA(cudaEventSynchronize(sl.done));
+        pool.copy(sl.out);
+        for (const auto& w : sl.wide) pool.widen(std::get<0>(w), std::get<1>(w), std::get<2>(w), std::get<3>(w));
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!err) err = std::current_exception();
+      }
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        sl.out.clear();
+        sl.wide.clear();
+        sl.armed = false;
+        head++;
+      }
+      cv.notify_all();
+    }
   }
+  // every queued copy-out done (call after the run's last synchronisation)
   void finish() {
-    // oldest first, so the copies follow the order C arrived in
-    for (size_t k = 0; k < down.size(); k++) retire(down[(nd + k) % down.size()]);
+    {
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [&] { return head >= fifo.size() || err; });
+    }
+    halt();
+    if (err) std::rethrow_exception(err);
   }
 };
 
@@ -478,6 +570,25 @@ __global__ void k_tile_ptr(const int64_t* __restrict__ in, int64_t n, const Ctl*
   }
 }
 
+// C's column indices on the wire: every feature column fits 16 bits (the dense accumulator is at most
+// 8192 wide), so a tile's columns cross the link as u16 and host threads widen them into the
+// caller's u32 / u64 array (CopyPool::widen) -- 2 bytes per C entry instead of 4 or 8 on the binding
+// D2H direction.  The count comes from the tile's Ctl (the device knows it before the host does).
+__global__ void k_narrow_cols(const void* __restrict__ in, uint32_t in_bytes, uint16_t* __restrict__ out,
+                              const Ctl* __restrict__ ctl) {
+  const uint64_t n = ctl->nnz;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  if (in_bytes == 4) {
+    const uint32_t* q = static_cast<const uint32_t*>(in);
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+      out[i] = static_cast<uint16_t>(q[i]);
+  } else {
+    const uint64_t* q = static_cast<const uint64_t*>(in);
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+      out[i] = static_cast<uint16_t>(q[i]);
+  }
+}
+
 // Streamed-output run (AIRES_B200_RUN_STREAM_OUT, uncapped): no sizing pass before the product.
 // The caller's allocator receives an upper bound of nnz(C) up front (min(rows * n_cols, nnz(A) *
 // longest X row)); A is cut into ~AB2_STREAM_TILES row blocks of equal nnz and every tile goes
@@ -543,8 +654,11 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
     pin.ensure(oidx, bound * ib);
     pin.ensure(oval, bound * vb);
   }
+  // C's columns cross the link as u16 (k_narrow_cols) unless the option turns it off
+  const bool narrow = x->n_cols <= 65536 && option("narrow_cols", 1) != 0;
   struct Slot {
     void *acol, *aval, *tcol, *tval, *ccol, *cval;
+    uint16_t* c16;
     int64_t *cptr, *heavy, *part;
     uint64_t* optr;
     uint32_t* cnt;
@@ -564,6 +678,7 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
     s.tval = arena.get(max_stage * vb);
     s.ccol = arena.get(max_cb * ib);
     s.cval = arena.get(max_cb * vb);
+    s.c16 = narrow ? static_cast<uint16_t*>(arena.get(max_cb * 2)) : nullptr;
     s.cptr = static_cast<int64_t*>(arena.get((max_rows + 1) * 8));
     s.optr = static_cast<uint64_t*>(arena.get((max_rows + 1) * 8));
     s.heavy = static_cast<int64_t*>(arena.get(max_rows * 8));
@@ -602,8 +717,22 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
     flops += c[1];
     tr.recs[compute_rec[j]].e.flops = c[1];
     AB2_CUDA(cudaStreamWaitEvent(st.d2h, s.computed, 0));  // (already complete: the host waited on it)
-    const uint64_t dn_bytes = (rows + 1) * 8 + nz * (ib + vb);
+    const uint64_t dn_bytes = (rows + 1) * 8 + nz * ((narrow ? 2 : ib) + vb);
     tr.span(st.d2h, AIRES_B200_EV_TRANSFER, AIRES_B200_CH_D2H, AIRES_B200_BUF_C_BLOCK, j, dn_bytes, 0, [&] {
+      if (narrow) {
+        std::vector<std::tuple<char*, const char*, uint64_t>> direct{
+            {reinterpret_cast<char*>(static_cast<uint64_t*>(optr) + r0), reinterpret_cast<const char*>(s.optr),
+             (rows + 1) * 8},
+            {static_cast<char*>(oval) + running * vb, static_cast<const char*>(s.cval), nz * vb}};
+        if (!stage_c) {
+          for (const auto& g : direct)
+            if (std::get<2>(g))
+              AB2_CUDA(cudaMemcpyAsync(std::get<0>(g), std::get<1>(g), std::get<2>(g), cudaMemcpyDeviceToHost, st.d2h));
+          direct.clear();
+        }
+        sg.d2h(direct, st.d2h, {{static_cast<char*>(oidx) + running * ib, s.c16, nz, ib}});
+        return;
+      }
       if (stage_c) {
         sg.d2h({{reinterpret_cast<char*>(static_cast<uint64_t*>(optr) + r0), reinterpret_cast<const char*>(s.optr),
                  (rows + 1) * 8},
@@ -673,6 +802,11 @@ void run_stream(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix& b
                                     h_rep + 3 * j);
       AB2_CUDA(cudaGetLastError());
       ctx.launches++;
+      if (narrow) {
+        k_narrow_cols<<<ctx.sms * 4, 256, 0, cs>>>(s.ccol, ib, s.c16, d_ctl + j);
+        AB2_CUDA(cudaGetLastError());
+        ctx.launches++;
+      }
     });
     AB2_CUDA(cudaEventRecord(s.computed, cs));
     if (trace) AB2_CUDA(cudaEventRecord(tl[3 * j + 1], cs));
@@ -1165,7 +1299,7 @@ void run_pipeline(Ctx& ctx, const aires_b200_matrix& a, const aires_b200_matrix&
   if (streamed) {
     PipeCacheImpl& pc = *static_cast<PipeCacheImpl*>(ctx.pipe);
     const uint32_t nb = cfg.n_buffers ? nbuf : 3;
-    Stager sg(pc.copy_pool(), pc.bounce_up, pc.bounce_down, nb, pc.stage_ev);
+    Stager sg(pc.copy_pool(), pc.bounce_up, pc.bounce_down, nb, pc.stage_ev, ctx.device);
     if (cfg.device_budget == 0)
       run_stream(ctx, a, b, mode, nb, out, rep, st, arena, pin, tr, cfg, sg, stage_a);
     else

@@ -171,7 +171,12 @@ def test_stream_out_fp64_bit_exact(tiles):
     # every byte crosses the link once: A (ptr, col, val) and X up, C (ptr, col, val) down
     base = 8 * (g.n_rows + 1) + 16 * g.nnz() + 8 * (x.n_rows + 1) + 16 * x.nnz()
     assert res.report.ledger.h2d.bytes == base
-    assert res.report.ledger.d2h.bytes >= 8 * (g.n_rows + 1) + 16 * wi.shape[0]
+    # C down once: row pointers, fp64 values, and the column indices as u16 on the wire (widened on the host)
+    assert res.report.ledger.d2h.bytes >= 8 * (g.n_rows + 1) + 10 * wi.shape[0]
+    with ab.options(narrow_cols=0, stream_tiles=int(tiles)):
+        wide = ab.run_aires(g, x, ab.MemoryBudget(0), stream_out=True)
+    assert wide.report.c_checksum == res.report.c_checksum
+    assert wide.report.ledger.d2h.bytes - res.report.ledger.d2h.bytes == 6 * wi.shape[0]
 
 
 @pytest.mark.parametrize("n_buffers", [2, 3, 4])

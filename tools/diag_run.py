@@ -1,5 +1,6 @@
 """Where the wall time of an aires_b200_run goes (cfg inputs, pinned host buffers).
-usage: python tools/diag_run.py [cfg2] [budget_MB] [stream]  (stream: AIRES_B200_RUN_STREAM_OUT)"""
+usage: [AB2_TRACE=1] python tools/diag_run.py [cfg2] [budget_MB] [stream] [name=value ...]
+(stream: AIRES_B200_RUN_STREAM_OUT; name=value: aires_b200_set_option, e.g. narrow_cols=0)"""
 import ctypes as C
 import os
 import sys
@@ -14,7 +15,7 @@ import bench  # noqa: E402
 import paper_2507_02006_b200 as ab  # noqa: E402
 
 cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg2"]
-g, st, x = bench.make_inputs(cfg, 0, 1)
+g, st, x = bench.make_inputs(cfg)
 L = ab.lib()
 hA = [torch.from_numpy(g.row_ptr.view(np.int64)).pin_memory(), torch.from_numpy(g.col_idx.view(np.int32)).pin_memory(),
       torch.from_numpy(g.values.astype(np.float32)).pin_memory()]
@@ -40,10 +41,12 @@ out = ab._Output(ab.HOST, 4, 4, 0, afn, None, 0, 0, 0, 0)
 budget = int(float(sys.argv[2]) * 1e6) if len(sys.argv) > 2 else 0
 flags = ab.RUN_STREAM_OUT if "stream" in sys.argv[3:] else 0
 nbuf = int(os.environ.get("NBUF", "0" if flags else "3"))
+for kv in sys.argv[3:]:
+    if "=" in kv:
+        k, v = kv.split("=")
+        ab.set_option(k, int(v))
 for it in range(4):
     rep = ab._RunReport()
-    if it == 3:
-        os.environ["AB2_TRACE"] = "1"
     t0 = time.perf_counter()
     ab._check(L.aires_b200_run(C.byref(am), C.byref(xm), C.byref(ab._RunConfig(budget, ab.MODE_FP32, 1, nbuf, flags)),
                                C.byref(out), C.byref(rep)))
