@@ -747,8 +747,34 @@ __global__ void __launch_bounds__(AB2_NUM_MAXT, (sizeof(V) == 8 || W == 16) ? AB
   unsigned long long my_nnz = 0, my_macs = 0;
   const unsigned long long n_heavy = p.ctl->n_sym_heavy;
 
-  // ---- Phase 1: heavy rows, one CTA per row ----
-  for (;;) {
+  // ---- Phase 1: heavy rows first (the long tail would otherwise finish last) ----
+  // fp64-exact: one warp per heavy row.  Each cell's terms must be added in ascending k, so a CTA
+  // could only split a row's columns -- every warp then walks (loads and steps over) every entry of
+  // the row; at cfg2 that replication made the pass 7.5 ms instead of 5.1 ms.
+  if constexpr (EXACT) {
+    V* hacc = warp_acc(warp);
+    for (;;) {
+      unsigned long long h = 0;
+      if (lane == 0) h = atomicAdd(&p.ctl->heavy_next, 1ull);
+      h = __shfl_sync(kFull, h, 0);
+      if (h >= n_heavy) break;
+      const int64_t r = p.heavy[h];
+      const uint64_t s = p.aptr[r] - p.abase, e = p.aptr[r + 1] - p.abase;
+      const uint32_t n = static_cast<uint32_t>(e - s);
+      bool zero = false;
+      my_macs += walk<V, IdxT, W, XZ>(p, p.acol + s, p.aval + s, n, 0, 1, hacc, warp_tab(warp), zero);
+      if (__any_sync(kFull, zero)) slow_row<V, IdxT, CS>(p, p.acol + s, p.aval + s, n, hacc, warp_mark(warp));
+      unsigned long long off;
+      const uint32_t cnt = fold_emit<V, CS>(p, hacc, 1, r, stage, off);
+      if (lane == 0) {
+        p.cnt[r] = cnt;
+        p.toff[r] = off;
+        my_nnz += cnt;
+      }
+    }
+  }
+  // fp32: one CTA per heavy row, the row's entries split over the warps (each its own copies)
+  for (; !EXACT;) {
     if (threadIdx.x == 0) {
       s_ticket = atomicAdd(&p.ctl->heavy_next, 1ull);
       s_zero = 0;
@@ -762,16 +788,7 @@ __global__ void __launch_bounds__(AB2_NUM_MAXT, (sizeof(V) == 8 || W == 16) ? AB
     const IdxT* ac = p.acol + s;
     const V* av = p.aval + s;
     bool zero = false;
-    if constexpr (EXACT) {
-      // column-owner split over one shared accumulator (warp 0's region)
-      const uint32_t span = ((n_cols + nw - 1) / nw + 31) & ~31;
-      const uint32_t c_lo = min(warp * span, static_cast<uint32_t>(n_cols));
-      const uint32_t c_hi = min(c_lo + span, static_cast<uint32_t>(n_cols));
-      const uint32_t m = walk_slots<V, IdxT, W, true, true, XZ>(p, ac, av, n, 0, 1, warp_acc(0), warp_tab(warp), c_lo, c_hi, zero);
-      if (warp == 0) my_macs += m;
-    } else {
-      my_macs += walk<V, IdxT, W, XZ>(p, ac, av, n, warp, nw, warp_acc(warp), warp_tab(warp), zero);
-    }
+    my_macs += walk<V, IdxT, W, XZ>(p, ac, av, n, warp, nw, warp_acc(warp), warp_tab(warp), zero);
     if (zero) s_zero = 1;
     __syncthreads();
     if (s_zero) {
