@@ -354,8 +354,9 @@ __device__ __forceinline__ uint32_t walk_pair(const Num3Args<float, IdxT>& p, co
 #pragma unroll
     for (int u = 0; u < 8; u++) any |= e[u].x;
     if (!__any_sync(kFull, (any & kSlotOvf) != 0u)) {
-      // Steps u and u+1 of one group may hit the same cell (different X rows): the RMWs are
-      // volatile shared accesses of one converged warp, issued and performed in program order.
+      // Steps u and u+1 of one group may hit the same cell (different X rows): a __syncwarp
+      // between the steps orders one step's stores before the next step's loads for every lane
+      // (racecheck-clean; the lanes of a step never share a cell).
 #pragma unroll
       for (int u = 0; u < 8; u++) {
         const uint32_t c = e[u].x;
@@ -365,8 +366,8 @@ __device__ __forceinline__ uint32_t walk_pair(const Num3Args<float, IdxT>& p, co
           smem_fma(copy_s + (c << 3), aa[u], __uint_as_float(e[u].y));
         }
         macs += real;
+        __syncwarp();
       }
-      __syncwarp();
       return;
     }
     // a row longer than 16: entry 15 is col = kSlotOvf | tail << 16 | trash with the tail's CSR
