@@ -288,6 +288,7 @@ uint64_t aires_b200_checksum(uint64_t n_rows, uint64_t n_cols, uint64_t nnz, con
  *   stage_min_bytes (64 MiB) pageable host arrays at least this large move through pinned bounce
  *                           slots (host copy threads) instead of being registered for the call
  *   narrow_cols (1)         streamed runs move C's column indices as u16 (host threads widen them)
+ *   hw_tensor (1)           fused layer: T = H·W on tcgen05 (3xTF32) when W has <= 48 columns
  */
 int aires_b200_set_option(const char* name, int64_t value);
 int aires_b200_clear_options(void);

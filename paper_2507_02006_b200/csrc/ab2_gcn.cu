@@ -986,6 +986,220 @@ __global__ void __launch_bounds__(256) k_agg_t(const uint64_t* __restrict__ aptr
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// T = H·W on the 5th-generation tensor cores (tcgen05.mma kind::tf32), for the reassociated layer's
+// narrow W (w_cols <= 48, h_cols <= 256).  fp32 accuracy from a 3xTF32 split: a = a_hi + a_lo with
+// a_hi the tf32 truncation, and T = A_hi·W_hi + A_hi·W_lo + A_lo·W_hi accumulated in fp32 (error
+// ~2^-21 of the cell's scale; the layer's tolerance is 1e-5).
+//
+// One persistent CTA per SM (512 threads), one 128-row tile of H at a time:
+//   shared: W^T hi / lo for all of K (N rows x K, K-major, 128-byte swizzle: 2 x 48 KB at N = 48),
+//           the tile's A hi / lo for one K half of 128 (2 x 64 KB), an mbarrier;
+//   TMEM:   the 128 x N fp32 accumulator (64 columns).
+// Per K half: zero A, densify the tile's CSR rows into the swizzled layout (warp w owns rows w + 16i;
+// the rows' offsets are read once per tile, then every row's next 32 entries are loaded together:
+// 16 loads per lane in flight), then one thread issues 16 K-steps x 3 MMAs and commits them to the
+// mbarrier; the epilogue reads the accumulator with tcgen05.ld (warp w: lane quarter w % 4, column
+// group w / 4) into T.
+// ---------------------------------------------------------------------------------------------
+namespace tc {
+constexpr int kRows = 128, kHalf = 128, kThreads = 512, kWarps = kThreads / 32, kRowsPerWarp = kRows / kWarps;
+__device__ __forceinline__ uint32_t swz(int m, int k) {  // byte offset of (row m, k < 32) in a K atom
+  return static_cast<uint32_t>((m >> 3) * 1024 + (m & 7) * 128 + ((((k >> 2) ^ (m & 7)) & 7) << 4) + (k & 3) * 4);
+}
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
+}
+__device__ __forceinline__ void split(float a, float& hi, float& lo) {
+  hi = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+  lo = a - hi;
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+               "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                 : "=r"(done)
+                 : "r"(mbar), "r"(phase)
+                 : "memory");
+}
+}  // namespace tc
+
+template <int N>
+__global__ void __launch_bounds__(tc::kThreads, 1)
+    k_hw_tc(const uint64_t* __restrict__ hptr, uint64_t hbase, const uint32_t* __restrict__ hcol,
+            const float* __restrict__ hval, int64_t K, int64_t h_cols, const float* __restrict__ w, int64_t w_cols,
+            int64_t tp, float* __restrict__ t, Ctl* __restrict__ ctl) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  const int katoms = static_cast<int>((h_cols + 31) / 32);  // K atoms of 32 (<= 8)
+  const uint32_t w_atom = N * 128;                           // bytes of one K atom of W^T
+  unsigned char* wt_hi = sm;
+  unsigned char* wt_lo = sm + 8 * w_atom;
+  unsigned char* a_hi = sm + 16 * w_atom;
+  unsigned char* a_lo = a_hi + 65536;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(a_lo + 65536);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 1);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // W^T, split, swizzled (zero beyond h_cols / w_cols)
+  for (int i = tid; i < N * katoms * 32; i += kThreads) {
+    const int n = i / (katoms * 32), k = i % (katoms * 32);
+    const float v = (n < w_cols && k < h_cols) ? w[static_cast<int64_t>(k) * w_cols + n] : 0.f;
+    float hi, lo;
+    split(v, hi, lo);
+    const uint32_t off = (k >> 5) * w_atom + swz(n, k & 31);
+    *reinterpret_cast<float*>(wt_hi + off) = hi;
+    *reinterpret_cast<float*>(wt_lo + off) = lo;
+  }
+  const uint32_t mbar_s = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
+  if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_s));
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+        static_cast<uint32_t>(__cvta_generic_to_shared(tslot))));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tslot;
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+                         (static_cast<uint32_t>(kRows >> 4) << 24);
+  const uint32_t ah_s = static_cast<uint32_t>(__cvta_generic_to_shared(a_hi));
+  const uint32_t al_s = static_cast<uint32_t>(__cvta_generic_to_shared(a_lo));
+  const uint32_t wh_s = static_cast<uint32_t>(__cvta_generic_to_shared(wt_hi));
+  const uint32_t wl_s = static_cast<uint32_t>(__cvta_generic_to_shared(wt_lo));
+  const int halves = (katoms + 3) / 4;
+  uint32_t phase = 0;
+  const int64_t ntiles = (K + kRows - 1) / kRows;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kRows;
+    const int rows = static_cast<int>(K - r0 < kRows ? K - r0 : kRows);
+    // this warp's rows: offsets relative to the tile's first entry (a tile holds <= 128 x 256 entries)
+    const int64_t tile_base = static_cast<int64_t>(hptr[r0] - hbase);
+    int32_t cur[kRowsPerWarp], end[kRowsPerWarp];
+#pragma unroll
+    for (int j = 0; j < kRowsPerWarp; j++) {
+      const int m = warp + kWarps * j;
+      cur[j] = end[j] = 0;
+      if (m < rows) {
+        cur[j] = static_cast<int32_t>(static_cast<int64_t>(hptr[r0 + m] - hbase) - tile_base);
+        end[j] = static_cast<int32_t>(static_cast<int64_t>(hptr[r0 + m + 1] - hbase) - tile_base);
+      }
+    }
+    const uint32_t* tcol = hcol + tile_base;
+    const float* tval = hval + tile_base;
+    for (int hf = 0; hf < halves; hf++) {
+      // zero this half of A (the previous MMAs that read it have completed: mbarrier waited below)
+      for (int i = tid; i < 2 * 65536 / 16; i += kThreads)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(ah_s + i * 16), "r"(0u) : "memory");
+      __syncthreads();
+      const uint32_t klo = static_cast<uint32_t>(hf * kHalf), khi = klo + kHalf;
+      for (;;) {
+        uint32_t c[kRowsPerWarp];
+        float v[kRowsPerWarp];
+#pragma unroll
+        for (int j = 0; j < kRowsPerWarp; j++) {
+          const int32_t i = cur[j] + lane;
+          c[j] = 0xffffffffu;
+          v[j] = 0.f;
+          if (i < end[j]) {
+            c[j] = __ldg(tcol + i);
+            v[j] = __ldg(tval + i);
+          }
+        }
+        bool more = false;
+#pragma unroll
+        for (int j = 0; j < kRowsPerWarp; j++) {
+          const int m = warp + kWarps * j;
+          const bool in = c[j] >= klo && c[j] < khi;  // (columns are sorted: the half's entries come first)
+          if (in) {
+            if (c[j] < static_cast<uint32_t>(h_cols)) {
+              float hi, lo;
+              split(v[j], hi, lo);
+              const uint32_t k = c[j] - klo;
+              const uint32_t off = (k >> 5) * 16384 + swz(m, static_cast<int>(k & 31));
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(ah_s + off), "f"(hi) : "memory");
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(al_s + off), "f"(lo) : "memory");
+            } else {
+              ctl->bad_row = 1;
+            }
+          }
+          const int took = __popc(__ballot_sync(0xffffffffu, in));
+          cur[j] += took;
+          more |= took == 32;
+        }
+        if (!__any_sync(0xffffffffu, more)) break;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        const int ksteps = min(16, (katoms - 4 * hf) * 4);
+        for (int kk = 0; kk < ksteps; kk++) {
+          const uint32_t ao = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t wo = (4 * hf + (kk >> 2)) * w_atom + (kk & 3) * 32;
+          const uint64_t dah = sw128_desc(ah_s + ao), dal = sw128_desc(al_s + ao);
+          const uint64_t dwh = sw128_desc(wh_s + wo), dwl = sw128_desc(wl_s + wo);
+          const uint32_t acc0 = (hf == 0 && kk == 0) ? 0u : 1u;
+          mma_tf32(tmem, dah, dwh, idesc, acc0);
+          mma_tf32(tmem, dah, dwl, idesc, 1u);
+          mma_tf32(tmem, dal, dwh, idesc, 1u);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar_s)
+                     : "memory");
+      }
+      mbar_wait(mbar_s, phase);
+      phase ^= 1u;
+    }
+    // epilogue: accumulator rows 32 (w % 4) + lane; warp group w / 4 takes N / 4 columns (x4 loads)
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    {
+      const int q = warp & 3, cg = warp >> 2;
+      const int m = 32 * q + lane;
+      constexpr int NQ = N / (kWarps / 4);  // 12 at N = 48
+      static_assert(NQ % 4 == 0, "column group must be whole x4 loads");
+#pragma unroll
+      for (int c0 = 0; c0 < NQ; c0 += 4) {
+        uint32_t r[4];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                     : "r"(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(cg * NQ + c0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (m < rows) {
+          float* dst = t + (r0 + m) * tp;
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const int col = cg * NQ + c0 + j;
+            if (col < w_cols) dst[col] = __uint_as_float(r[j]);
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();  // the accumulator is free for the next tile's MMAs
+  }
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+}
+
+void hw_tc_launch(Ctx& ctx, const Staged& hs, int64_t K, int64_t h_cols, const float* w, int64_t w_cols, int64_t tp,
+                  float* t, Ctl* ctl) {
+  constexpr int N = 48;
+  const size_t smem = 1024 + 16 * N * 128 + 2 * 65536 + 64;
+  AB2_CUDA(cudaFuncSetAttribute(k_hw_tc<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int64_t ntiles = (K + tc::kRows - 1) / tc::kRows;
+  if (ntiles > 0)
+    k_hw_tc<N><<<static_cast<int>(std::min<int64_t>(ntiles, ctx.sms)), tc::kThreads, smem, ctx.stream>>>(
+        hs.ptr, hs.base, static_cast<const uint32_t*>(hs.idx), static_cast<const float*>(hs.val), K, h_cols, w,
+        w_cols, tp, t, ctl);
+  AB2_CUDA(cudaGetLastError());
+}
+
 template <int M4, int JC>
 void hw_launch(Ctx& ctx, const Staged& hs, int64_t K, int64_t h_cols, const float4* wt4, int64_t w_cols, int64_t tp,
                float* t, Ctl* ctl) {
@@ -1135,9 +1349,14 @@ void layer_fused(Ctx& ctx, const aires_b200_matrix& at, const aires_b200_matrix&
         AB2_CUDA(cudaMemcpyAsync(dw, w, w_rows * w_cols * sizeof(float), cudaMemcpyHostToDevice, ctx.stream));
         wsrc = dw;
       }
-      float4* wt4 = static_cast<float4*>(ctx.xo_desc.get(static_cast<size_t>(M4) * w_cols * 32 * sizeof(float4)));
-      k_w_lane_major4<<<grid_of(static_cast<int64_t>(M4) * w_cols * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(
-          wsrc, static_cast<int64_t>(w_rows), static_cast<int64_t>(w_cols), M4, wt4);
+      // T = H·W on tcgen05 (3xTF32) when W fits the tensor-core kernel's 48 output columns
+      const bool tensor = w_cols <= 48 && h.n_cols <= 256 && option("hw_tensor", 1) != 0;
+      float4* wt4 = nullptr;
+      if (!tensor) {
+        wt4 = static_cast<float4*>(ctx.xo_desc.get(static_cast<size_t>(M4) * w_cols * 32 * sizeof(float4)));
+        k_w_lane_major4<<<grid_of(static_cast<int64_t>(M4) * w_cols * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(
+            wsrc, static_cast<int64_t>(w_rows), static_cast<int64_t>(w_cols), M4, wt4);
+      }
       const int64_t tp = (static_cast<int64_t>(w_cols) + 7) & ~int64_t(7);
       float* t = static_cast<float*>(ctx.xo_val.get(std::max<int64_t>(K, 1) * tp * sizeof(float)));
       float* dense = static_cast<float*>(ctx.t_val.get(std::max<int64_t>(rows, 1) * w_cols * sizeof(float)));
@@ -1147,11 +1366,15 @@ void layer_fused(Ctx& ctx, const aires_b200_matrix& at, const aires_b200_matrix&
       AB2_CUDA(cudaEventRecord(ctx.ev[0], ctx.stream));
       const int64_t hc = static_cast<int64_t>(h.n_cols), wc = static_cast<int64_t>(w_cols);
       // T = H·W is enqueued before Ã is staged: both stagings use the context's A buffers
-      switch (M4 * 8 + JC) {
+      if (tensor) {
+        hw_tc_launch(ctx, hs, K, hc, wsrc, wc, tp, t, ctl);
+      } else {
+        switch (M4 * 8 + JC) {
 #define AB2_RA(A, B) case A * 8 + B: hw_launch<A, B>(ctx, hs, K, hc, wt4, wc, tp, t, ctl); break;
-        AB2_RA(1, 1) AB2_RA(1, 2) AB2_RA(1, 3) AB2_RA(1, 4) AB2_RA(2, 1) AB2_RA(2, 2) AB2_RA(2, 3) AB2_RA(2, 4)
+          AB2_RA(1, 1) AB2_RA(1, 2) AB2_RA(1, 3) AB2_RA(1, 4) AB2_RA(2, 1) AB2_RA(2, 2) AB2_RA(2, 3) AB2_RA(2, 4)
 #undef AB2_RA
-        default: fail(AIRES_B200_UNSUPPORTED_FORMAT, "fused layer shape");
+          default: fail(AIRES_B200_UNSUPPORTED_FORMAT, "fused layer shape");
+        }
       }
       const Staged as = stage_csr(ctx, at);
       switch (JC) {

@@ -322,7 +322,7 @@ def test_layer_forward_two_layers_match_oracle():
     assert bits_equal(h2.values, want[2])
 
 
-@pytest.mark.parametrize("hcols,wcols", [(256, 47), (100, 128), (64, 8), (33, 40)])
+@pytest.mark.parametrize("hcols,wcols", [(256, 47), (100, 128), (64, 8), (33, 40), (200, 20), (160, 48)])
 def test_layer_fused_matches_unfused_chain(hcols, wcols):
     """ReLU((Ã·H)·W) fused (dense-ish H gathered as dense rows) against the fp64 oracle chain
     normalize -> row-wise A·H -> combine: values within 1e-5 relative to the cell's scale; entries
