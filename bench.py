@@ -902,6 +902,25 @@ def gcn_leg(args, dev, L, ab, torch):
         forward(rec)
     med = {k: round(float(np.median(v)), 3) for k, v in rec.items() if not k.startswith("(")}
     med_u = {k: round(float(np.median(v)), 3) for k, v in rec_u.items()}
+
+    def dense_h2():
+        o = o_h2
+        rows_n, z = int(o.out.n_rows), int(o.out.nnz)
+        ptr = o.t["ptr"][: rows_n + 1]
+        r = torch.repeat_interleave(torch.arange(rows_n, device=dev), ptr[1:] - ptr[:-1])
+        d = torch.zeros(rows_n, w2.shape[1], dtype=torch.float32, device=dev)
+        d[r, o.t["idx"][:z].long()] = o.t["val"][:z]
+        return d
+
+    # the fused layer 2 (tcgen05 T = H1·W2, then Ã·T) against the unfused chain (Ã·H1 on the SpGEMM
+    # path, then combine), outside the timed region
+    forward(fused=False)
+    want = dense_h2()
+    forward()
+    got = dense_h2()
+    err = float((got - want).abs().max()) / max(float(want.abs().max()), 1e-30)
+    check = {"layer2_fused_vs_unfused_max_abs_err_over_max": err, "tol": 1e-4, "checked": bool(err <= 1e-4)}
+    del want, got
     comb_flops = 2 * (int(o_c1.out.nnz) * 256 + int(o_c2.out.nnz) * 47)
     return {"workload": "cfg5 (1 GPU): 2-layer GCN forward on the ogbn-products shape, W1 100x256, W2 256x47 "
                         "(gen_weights seeds 4, 5), all operands device-resident, fp32",
@@ -914,7 +933,9 @@ def gcn_leg(args, dev, L, ab, torch):
             "gflops_combine_unfused": round(comb_flops / ((med_u["combine1"] + med_u["combine2"]) * 1e-3) / 1e9, 2),
             "layer2_fused_gflops": round((2.0 * macs2 + 2 * int(o_c2.out.nnz) * 47) / (med["layer2_fused"] * 1e-3) / 1e9, 2),
             "forward_ms": med["total"], "forward_ms_unfused": med_u["total"],
-            "layers_per_s": round(2.0 / (med["total"] * 1e-3), 2)}
+            "layers_per_s": round(2.0 / (med["total"] * 1e-3), 2),
+            "layer2": "T = H1·W2 on tcgen05 (kind::tf32, 3xTF32 split), then Ã·T", "check": check,
+            "checked": check["checked"]}
 
 
 # ---------------------------------------------------------------------------------------------

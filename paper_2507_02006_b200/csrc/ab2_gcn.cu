@@ -1102,38 +1102,46 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
       __syncthreads();
       const uint32_t klo = static_cast<uint32_t>(hf * kHalf), khi = klo + kHalf;
       for (;;) {
-        uint32_t c[kRowsPerWarp];
-        float v[kRowsPerWarp];
+        // the next 64 entries of each of the warp's rows: 2 x 8 x 2 loads per lane in flight
+        uint32_t c[2][kRowsPerWarp];
+        float v[2][kRowsPerWarp];
 #pragma unroll
-        for (int j = 0; j < kRowsPerWarp; j++) {
-          const int32_t i = cur[j] + lane;
-          c[j] = 0xffffffffu;
-          v[j] = 0.f;
-          if (i < end[j]) {
-            c[j] = __ldg(tcol + i);
-            v[j] = __ldg(tval + i);
+        for (int h2 = 0; h2 < 2; h2++)
+#pragma unroll
+          for (int j = 0; j < kRowsPerWarp; j++) {
+            const int32_t i = cur[j] + 32 * h2 + lane;
+            c[h2][j] = 0xffffffffu;
+            v[h2][j] = 0.f;
+            if (i < end[j]) {
+              c[h2][j] = __ldg(tcol + i);
+              v[h2][j] = __ldg(tval + i);
+            }
           }
-        }
         bool more = false;
 #pragma unroll
         for (int j = 0; j < kRowsPerWarp; j++) {
           const int m = warp + kWarps * j;
-          const bool in = c[j] >= klo && c[j] < khi;  // (columns are sorted: the half's entries come first)
-          if (in) {
-            if (c[j] < static_cast<uint32_t>(h_cols)) {
-              float hi, lo;
-              split(v[j], hi, lo);
-              const uint32_t k = c[j] - klo;
-              const uint32_t off = (k >> 5) * 16384 + swz(m, static_cast<int>(k & 31));
-              asm volatile("st.shared.f32 [%0], %1;" ::"r"(ah_s + off), "f"(hi) : "memory");
-              asm volatile("st.shared.f32 [%0], %1;" ::"r"(al_s + off), "f"(lo) : "memory");
-            } else {
-              ctl->bad_row = 1;
+          int took = 0;
+#pragma unroll
+          for (int h2 = 0; h2 < 2; h2++) {
+            const uint32_t cc = c[h2][j];
+            const bool in = cc >= klo && cc < khi;  // (columns are sorted: the half's entries come first)
+            if (in) {
+              if (cc < static_cast<uint32_t>(h_cols)) {
+                float hi, lo;
+                split(v[h2][j], hi, lo);
+                const uint32_t k = cc - klo;
+                const uint32_t off = (k >> 5) * 16384 + swz(m, static_cast<int>(k & 31));
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(ah_s + off), "f"(hi) : "memory");
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(al_s + off), "f"(lo) : "memory");
+              } else {
+                ctl->bad_row = 1;
+              }
             }
+            took += __popc(__ballot_sync(0xffffffffu, in));
           }
-          const int took = __popc(__ballot_sync(0xffffffffu, in));
           cur[j] += took;
-          more |= took == 32;
+          more |= took == 64;
         }
         if (!__any_sync(0xffffffffu, more)) break;
       }
