@@ -348,19 +348,24 @@ def run_b200(args, cfg):
     b_alg = algorithmic_bytes(blk.n_rows, blk.nnz(), K, x.nnz(), nnz_c, 4)
     num_ms = kern["numeric"]
     ach = b_alg / (num_ms * 1e-3) / 1e9
-    traffic = None
-    try:  # DRAM bytes of the dominant kernel from the committed ncu --set full capture (cfg2 fp32)
+    traffic, limiter = None, None
+    try:  # DRAM bytes and the limiting unit of the dominant kernel from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
         if cfg is CONFIGS["cfg2"] and world == 1 and "k_numeric3" in tj:
             traffic = int(tj["k_numeric3"]["dram_bytes"])
+            limiter = {"unit": "L1 data pipe (shared-memory RMW + X-slot gathers)",
+                       "pct_of_peak": tj["k_numeric3"].get("l1tex_data_pipe_lsu_wavefronts_pct_of_peak"),
+                       "dram_pct": tj["k_numeric3"].get("dram_throughput_pct"),
+                       "source": tj["k_numeric3"].get("source")}
     except Exception:
-        traffic = None
+        traffic, limiter = None, None
     roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
             "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write, one launch)",
             "kernel": "k_numeric (fp32 product pass)", "kernel_ms": round(num_ms, 4), "bytes_per_launch": b_alg,
             "bytes_basis": "8(rows+1)+8nnz over A block, X and C block (int64 ptr, int32 idx, fp32 val)",
             "peak_source": peak_src, "step_frac": round(b_alg / (ms_rank * 1e-3) / 1e9 / peak, 4),
+            "limiter": limiter,
             "kernel_ms_breakdown": {("place" if k == "symbolic" else k): round(v, 4) for k, v in kern.items()}}
     prod.free()
     torch.cuda.empty_cache()

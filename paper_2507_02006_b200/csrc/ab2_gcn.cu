@@ -1004,6 +1004,10 @@ __global__ void __launch_bounds__(256) k_agg_t(const uint64_t* __restrict__ aptr
 // ---------------------------------------------------------------------------------------------
 namespace tc {
 constexpr int kRows = 128, kHalf = 128, kThreads = 512, kWarps = kThreads / 32, kRowsPerWarp = kRows / kWarps;
+#ifndef AB2_HW_CHUNKS
+#define AB2_HW_CHUNKS 4
+#endif
+constexpr int kChunks = AB2_HW_CHUNKS;  // 32-entry chunks of every row loaded per densify round
 __device__ __forceinline__ uint32_t swz(int m, int k) {  // byte offset of (row m, k < 32) in a K atom
   return static_cast<uint32_t>((m >> 3) * 1024 + (m & 7) * 128 + ((((k >> 2) ^ (m & 7)) & 7) << 4) + (k & 3) * 4);
 }
@@ -1103,10 +1107,10 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
       const uint32_t klo = static_cast<uint32_t>(hf * kHalf), khi = klo + kHalf;
       for (;;) {
         // the next 64 entries of each of the warp's rows: 2 x 8 x 2 loads per lane in flight
-        uint32_t c[2][kRowsPerWarp];
-        float v[2][kRowsPerWarp];
+        uint32_t c[kChunks][kRowsPerWarp];
+        float v[kChunks][kRowsPerWarp];
 #pragma unroll
-        for (int h2 = 0; h2 < 2; h2++)
+        for (int h2 = 0; h2 < kChunks; h2++)
 #pragma unroll
           for (int j = 0; j < kRowsPerWarp; j++) {
             const int32_t i = cur[j] + 32 * h2 + lane;
@@ -1123,7 +1127,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
           const int m = warp + kWarps * j;
           int took = 0;
 #pragma unroll
-          for (int h2 = 0; h2 < 2; h2++) {
+          for (int h2 = 0; h2 < kChunks; h2++) {
             const uint32_t cc = c[h2][j];
             const bool in = cc >= klo && cc < khi;  // (columns are sorted: the half's entries come first)
             if (in) {
@@ -1141,7 +1145,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
             took += __popc(__ballot_sync(0xffffffffu, in));
           }
           cur[j] += took;
-          more |= took == 64;
+          more |= took == 32 * kChunks;
         }
         if (!__any_sync(0xffffffffu, more)) break;
       }
