@@ -922,8 +922,11 @@ __global__ void __launch_bounds__(256) k_hw(const uint64_t* __restrict__ hptr, u
 }
 
 // out[r, j] = ReLU(sum_k Ã[r, k] T[k, j]) as a dense row + the row's positive count (then scan +
-// k_compact_rows, as for k_agg_comb).  One warp per Ã row, lane l owns columns l + 32 jc; eight T rows
-// in flight per step.
+// k_compact_rows, as for k_agg_comb).  One warp per Ã row, lane l owns columns l + 32 jc; eight T
+// rows in flight per step.
+#ifndef AB2_AGG_INFLIGHT
+#define AB2_AGG_INFLIGHT 8  // T rows in flight per warp (16 measured slower: 102 registers, layer 2 9.3 -> 12.0 ms)
+#endif
 template <int JC>
 __global__ void __launch_bounds__(256) k_agg_t(const uint64_t* __restrict__ aptr, uint64_t abase,
                                                const uint32_t* __restrict__ acol, const float* __restrict__ aval,
@@ -951,10 +954,10 @@ __global__ void __launch_bounds__(256) k_agg_t(const uint64_t* __restrict__ aptr
       }
       const int n = static_cast<int>(e - b < 32 ? e - b : 32);
       int kk = 0;
-      for (; kk + 8 <= n; kk += 8) {
-        float x[8][JC], av[8];
+      for (; kk + AB2_AGG_INFLIGHT <= n; kk += AB2_AGG_INFLIGHT) {
+        float x[AB2_AGG_INFLIGHT][JC], av[AB2_AGG_INFLIGHT];
 #pragma unroll
-        for (int q = 0; q < 8; q++) {
+        for (int q = 0; q < AB2_AGG_INFLIGHT; q++) {
           const uint32_t kq = __shfl_sync(kFull, k, kk + q);
           av[q] = __shfl_sync(kFull, a, kk + q);
           const float* tr = t + static_cast<int64_t>(kq) * tp + lane;
@@ -962,7 +965,7 @@ __global__ void __launch_bounds__(256) k_agg_t(const uint64_t* __restrict__ aptr
           for (int jc = 0; jc < JC; jc++) x[q][jc] = mine[jc] ? __ldg(tr + 32 * jc) : 0.f;
         }
 #pragma unroll
-        for (int q = 0; q < 8; q++)
+        for (int q = 0; q < AB2_AGG_INFLIGHT; q++)
 #pragma unroll
           for (int jc = 0; jc < JC; jc++) acc[jc] = fmaf(av[q], x[q][jc], acc[jc]);
       }
