@@ -989,6 +989,117 @@ __global__ void __launch_bounds__(256) k_agg_t(const uint64_t* __restrict__ aptr
   }
 }
 
+// k_agg_t for T rows of <= 64 floats, with the gathers made asynchronous: k_agg_t holds its eight
+// in-flight T rows in registers, so the kernel is latency-bound (ncu: DRAM 21%, long-scoreboard
+// stalls, occupancy capped by registers).  Here each warp streams its Ã rows as 32-entry chunks; the
+// T rows of chunk i+1 are copied global -> shared with cp.async (no registers held) while chunk i is
+// summed from shared memory.  Same cells, same ascending-entry fmaf order as k_agg_t.
+constexpr int kAggWarps = 4;
+template <int JC>
+__global__ void __launch_bounds__(kAggWarps * 32) k_agg_t_cp(const uint64_t* __restrict__ aptr, uint64_t abase,
+                                                          const uint32_t* __restrict__ acol,
+                                                          const float* __restrict__ aval, int64_t rows, int64_t K,
+                                                          const float* __restrict__ t, int tp, int64_t w_cols,
+                                                          float* __restrict__ dense_out, int32_t* __restrict__ cnt) {
+  extern __shared__ __align__(16) float agg_smem[];
+  const int lane = lane_id();
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  float* const sb = agg_smem + static_cast<size_t>(threadIdx.x >> 5) * 2 * 32 * tp;  // two chunk buffers
+  const int tp4 = tp >> 2, piece = lane & 15, half = lane >> 4;
+  bool mine[JC];
+#pragma unroll
+  for (int jc = 0; jc < JC; jc++) mine[jc] = jc * 32 + lane < w_cols;
+
+  // chunk cursor: entries [b, min(b + 32, e)) of row r (an empty row is one empty chunk)
+  struct Cur {
+    int64_t r, b, e;
+  };
+  auto first = [&](int64_t r) -> Cur {
+    if (r >= rows) return Cur{r, 0, 0};
+    return Cur{r, static_cast<int64_t>(aptr[r] - abase), static_cast<int64_t>(aptr[r + 1] - abase)};
+  };
+  auto next = [&](const Cur& c) -> Cur {
+    if (c.b + 32 < c.e) return Cur{c.r, c.b + 32, c.e};
+    return first(c.r + nw);
+  };
+  // issue chunk c into buffer buf; returns this lane's Ã value for the chunk
+  auto issue = [&](const Cur& c, int buf) -> float {
+    float a = 0.f;
+    if (c.r < rows) {
+      const int n = static_cast<int>(c.e - c.b < 32 ? c.e - c.b : 32);
+      uint32_t k = 0;
+      if (lane < n) {
+        k = acol[c.b + lane];
+        a = aval[c.b + lane];
+        if (k >= K) a = 0.f, k = 0;
+      }
+      float* dst = sb + buf * 32 * tp;
+      for (int q = 0; q < n; q += 2) {
+        const int qq = q + half;
+        const uint32_t kq = __shfl_sync(kFull, k, qq & 31);
+        if (qq < n && piece < tp4) {
+          const float* src = t + static_cast<int64_t>(kq) * tp + piece * 4;
+          const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + qq * tp + piece * 4));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    return a;
+  };
+
+  float acc[JC];
+#pragma unroll
+  for (int jc = 0; jc < JC; jc++) acc[jc] = 0.f;
+  Cur c0 = first(wid), c1 = next(c0);
+  float a0 = issue(c0, 0), a1 = issue(c1, 1);
+  int buf = 0;
+  while (c0.r < rows) {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    const float* src = sb + buf * 32 * tp + lane;
+    const int n = static_cast<int>(c0.e - c0.b < 32 ? c0.e - c0.b : 32);
+    int q = 0;
+    for (; q + 8 <= n; q += 8) {
+      float x[8][JC], av[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        av[u] = __shfl_sync(kFull, a0, q + u);
+#pragma unroll
+        for (int jc = 0; jc < JC; jc++) x[u][jc] = mine[jc] ? src[(q + u) * tp + 32 * jc] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+#pragma unroll
+        for (int jc = 0; jc < JC; jc++) acc[jc] = fmaf(av[u], x[u][jc], acc[jc]);
+    }
+    for (; q < n; q++) {
+      const float aq = __shfl_sync(kFull, a0, q);
+#pragma unroll
+      for (int jc = 0; jc < JC; jc++)
+        if (mine[jc]) acc[jc] = fmaf(aq, src[q * tp + 32 * jc], acc[jc]);
+    }
+    if (c0.b + 32 >= c0.e) {  // last chunk of row c0.r
+      const int64_t r = c0.r;
+      int32_t count = 0;
+#pragma unroll
+      for (int jc = 0; jc < JC; jc++) {
+        const bool pos = mine[jc] && acc[jc] > 0.f;
+        if (mine[jc]) dense_out[r * w_cols + jc * 32 + lane] = pos ? acc[jc] : 0.f;
+        count += __popc(__ballot_sync(kFull, pos));
+        acc[jc] = 0.f;
+      }
+      if (lane == 0) cnt[r] = count;
+    }
+    __syncwarp();  // every lane is done reading this buffer before it is refilled
+    const Cur c2 = next(c1);
+    const float a2 = issue(c2, buf);
+    c0 = c1, c1 = c2, a0 = a1, a1 = a2, buf ^= 1;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------------------------
 // T = H·W on the 5th-generation tensor cores (tcgen05.mma kind::tf32), for the reassociated layer's
 // narrow W (w_cols <= 48, h_cols <= 256).  fp32 accuracy from a 3xTF32 split: a = a_hi + a_lo with
@@ -1240,6 +1351,23 @@ void agg_t_launch(Ctx& ctx, const Staged& as, int64_t rows, int64_t K, const flo
   AB2_CUDA(cudaGetLastError());
 }
 
+template <int JC>
+void agg_t_cp_launch(Ctx& ctx, const Staged& as, int64_t rows, int64_t K, const float* t, int64_t tp, int64_t w_cols,
+                     float* dense, int32_t* cnt) {
+  const int smem = kAggWarps * 2 * 32 * static_cast<int>(tp) * static_cast<int>(sizeof(float));
+  auto k1 = k_agg_t_cp<JC>;
+  AB2_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int nb = 0;
+  AB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k1, kAggWarps * 32, smem));
+  const int64_t want = (rows + kAggWarps - 1) / kAggWarps;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(std::max(nb, 1)) * ctx.sms)));
+  if (rows > 0)
+    k1<<<grid, kAggWarps * 32, smem, ctx.stream>>>(as.ptr, as.base, static_cast<const uint32_t*>(as.idx),
+                                                   static_cast<const float*>(as.val), rows, K, t, static_cast<int>(tp),
+                                                   w_cols, dense, cnt);
+  AB2_CUDA(cudaGetLastError());
+}
+
 }  // namespace
 
 void normalize_adjacency(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
@@ -1392,7 +1520,10 @@ void layer_fused(Ctx& ctx, const aires_b200_matrix& at, const aires_b200_matrix&
         }
       }
       const Staged as = stage_csr(ctx, at);
-      switch (JC) {
+      if (tp <= 64 && option("agg_async", 1) != 0) {
+        if (JC == 1) agg_t_cp_launch<1>(ctx, as, rows, K, t, tp, wc, dense, cnt);
+        else agg_t_cp_launch<2>(ctx, as, rows, K, t, tp, wc, dense, cnt);
+      } else switch (JC) {
         case 1: agg_t_launch<1>(ctx, as, rows, K, t, tp, wc, dense, cnt); break;
         case 2: agg_t_launch<2>(ctx, as, rows, K, t, tp, wc, dense, cnt); break;
         case 3: agg_t_launch<3>(ctx, as, rows, K, t, tp, wc, dense, cnt); break;
