@@ -792,16 +792,23 @@ __global__ void k_compact_rows(const float* __restrict__ dense, int64_t rows, in
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t r = wid; r < rows; r += nw) {
     int64_t o = optr[r];
-    for (int64_t j0 = 0; j0 < w_cols; j0 += 32) {
-      const int64_t j = j0 + lane;
-      const float v = j < w_cols ? dense[r * w_cols + j] : 0.f;
-      const unsigned m = __ballot_sync(kFull, v > 0.f);
-      if (v > 0.f) {
-        const int64_t d = o + __popc(m & ((1u << lane) - 1));
-        ocol[d] = static_cast<IdxO>(j);
-        oval[d] = v;
+    for (int64_t j0 = 0; j0 < w_cols; j0 += 128) {  // four 32-column chunks loaded before any is used
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int64_t j = j0 + 32 * u + lane;
+        v[u] = j < w_cols ? dense[r * w_cols + j] : 0.f;
       }
-      o += __popc(m);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const unsigned m = __ballot_sync(kFull, v[u] > 0.f);
+        if (v[u] > 0.f) {
+          const int64_t d = o + __popc(m & ((1u << lane) - 1));
+          ocol[d] = static_cast<IdxO>(j0 + 32 * u + lane);
+          oval[d] = v[u];
+        }
+        o += __popc(m);
+      }
     }
   }
 }
@@ -993,109 +1000,150 @@ __global__ void __launch_bounds__(256) k_agg_t(const uint64_t* __restrict__ aptr
 // in-flight T rows in registers, so the kernel is latency-bound (ncu: DRAM 21%, long-scoreboard
 // stalls, occupancy capped by registers).  Here each warp streams its Ã rows as 32-entry chunks; the
 // T rows of chunk i+1 are copied global -> shared with cp.async (no registers held) while chunk i is
-// summed from shared memory.  Same cells, same ascending-entry fmaf order as k_agg_t.
-constexpr int kAggWarps = 4;
-template <int JC>
+// summed from shared memory, and the Ã entries of chunk i+2 are loaded meanwhile.  TP is T's row
+// pitch (floats), K * TP < 2^32.  Same cells, same ascending-entry fmaf order as k_agg_t.
+#ifndef AB2_AGG_WARPS
+#define AB2_AGG_WARPS 4
+#endif
+#ifndef AB2_AGG_STAGES
+#define AB2_AGG_STAGES 2  // chunk buffers per warp (3: 8.8 ms, 4: 10.7 ms for cfg5 layer 2 -- fewer warps)
+#endif
+constexpr int kAggWarps = AB2_AGG_WARPS, kAggStages = AB2_AGG_STAGES;
+template <int TP>
 __global__ void __launch_bounds__(kAggWarps * 32) k_agg_t_cp(const uint64_t* __restrict__ aptr, uint64_t abase,
                                                           const uint32_t* __restrict__ acol,
                                                           const float* __restrict__ aval, int64_t rows, int64_t K,
-                                                          const float* __restrict__ t, int tp, int64_t w_cols,
+                                                          const float* __restrict__ t, int64_t w_cols,
                                                           float* __restrict__ dense_out, int32_t* __restrict__ cnt) {
+  constexpr int JC = (TP + 31) / 32, TP4 = TP / 4;
   extern __shared__ __align__(16) float agg_smem[];
   const int lane = lane_id();
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  float* const sb = agg_smem + static_cast<size_t>(threadIdx.x >> 5) * 2 * 32 * tp;  // two chunk buffers
-  const int tp4 = tp >> 2, piece = lane & 15, half = lane >> 4;
+  float* const sb = agg_smem + (threadIdx.x >> 5) * (kAggStages * 32 * TP);  // chunk ring
+  const int piece = lane & 15, half = lane >> 4;
   bool mine[JC];
 #pragma unroll
   for (int jc = 0; jc < JC; jc++) mine[jc] = jc * 32 + lane < w_cols;
 
-  // chunk cursor: entries [b, min(b + 32, e)) of row r (an empty row is one empty chunk)
+  // chunk cursor: entries [b, min(b + 32, e)) of row r (an empty row is one empty chunk).  A warp
+  // owns blocks of 32 consecutive rows (wid, wid + nw, ...): the block's row offsets are one
+  // coalesced load held by the lanes, and the following block's are loaded one block ahead, so
+  // stepping to the next row costs two shuffles instead of a dependent global load.
   struct Cur {
     int64_t r, b, e;
   };
+  int64_t rb = wid * 32;
+  uint64_t ps = 0, pe = 0, qs = 0, qe = 0;  // this block's / the next block's offsets (lane = row)
+  auto load_blk = [&](int64_t base, uint64_t& s0, uint64_t& e0) {
+    s0 = e0 = abase;
+    if (base + lane < rows) s0 = aptr[base + lane], e0 = aptr[base + lane + 1];
+  };
+  load_blk(rb, ps, pe);
+  load_blk(rb + 32 * nw, qs, qe);
   auto first = [&](int64_t r) -> Cur {
     if (r >= rows) return Cur{r, 0, 0};
-    return Cur{r, static_cast<int64_t>(aptr[r] - abase), static_cast<int64_t>(aptr[r + 1] - abase)};
+    if (r >= rb + 32) {  // entered the next block (r == rb + 32 nw)
+      rb = r, ps = qs, pe = qe;
+      load_blk(rb + 32 * nw, qs, qe);
+    }
+    const int l = static_cast<int>(r - rb);
+    return Cur{r, static_cast<int64_t>(__shfl_sync(kFull, ps, l) - abase),
+               static_cast<int64_t>(__shfl_sync(kFull, pe, l) - abase)};
   };
   auto next = [&](const Cur& c) -> Cur {
     if (c.b + 32 < c.e) return Cur{c.r, c.b + 32, c.e};
-    return first(c.r + nw);
+    return first(((c.r + 1) & 31) ? c.r + 1 : c.r + 1 + 32 * (nw - 1));
   };
-  // issue chunk c into buffer buf; returns this lane's Ã value for the chunk
-  auto issue = [&](const Cur& c, int buf) -> float {
-    float a = 0.f;
+  auto count = [](const Cur& c) { return static_cast<int>(c.e - c.b < 32 ? c.e - c.b : 32); };
+  auto load = [&](const Cur& c, uint32_t& k, float& a) {
+    k = 0, a = 0.f;
+    if (c.r < rows && lane < count(c)) k = acol[c.b + lane], a = aval[c.b + lane];
+  };
+  // copy chunk c's T rows into buffer buf (k, a: this lane's entry, loaded one step earlier)
+  auto issue = [&](const Cur& c, uint32_t k, float& a, int buf) {
     if (c.r < rows) {
-      const int n = static_cast<int>(c.e - c.b < 32 ? c.e - c.b : 32);
-      uint32_t k = 0;
-      if (lane < n) {
-        k = acol[c.b + lane];
-        a = aval[c.b + lane];
-        if (k >= K) a = 0.f, k = 0;
-      }
-      float* dst = sb + buf * 32 * tp;
+      const int n = count(c);
+      if (k >= K) a = 0.f, k = 0;
+      const uint32_t off = k * TP;
+      float* dst = sb + buf * (32 * TP) + piece * 4;
+#pragma unroll 4
       for (int q = 0; q < n; q += 2) {
         const int qq = q + half;
-        const uint32_t kq = __shfl_sync(kFull, k, qq & 31);
-        if (qq < n && piece < tp4) {
-          const float* src = t + static_cast<int64_t>(kq) * tp + piece * 4;
-          const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + qq * tp + piece * 4));
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+        const uint32_t o = __shfl_sync(kFull, off, qq & 31);
+        if (qq < n && piece < TP4) {
+          const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + qq * TP));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(t + o + piece * 4) : "memory");
         }
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    return a;
   };
 
   float acc[JC];
 #pragma unroll
   for (int jc = 0; jc < JC; jc++) acc[jc] = 0.f;
-  Cur c0 = first(wid), c1 = next(c0);
-  float a0 = issue(c0, 0), a1 = issue(c1, 1);
+  Cur c[kAggStages];
+  float ar[kAggStages];
+  c[0] = first(rb);
+#pragma unroll
+  for (int i = 1; i < kAggStages; i++) c[i] = next(c[i - 1]);
+#pragma unroll
+  for (int i = 0; i < kAggStages; i++) {
+    uint32_t k;
+    load(c[i], k, ar[i]);
+    issue(c[i], k, ar[i], i);
+  }
+  Cur cn = next(c[kAggStages - 1]);
+  uint32_t kn;
+  float an;
+  load(cn, kn, an);
   int buf = 0;
-  while (c0.r < rows) {
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
+  while (c[0].r < rows) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kAggStages - 1) : "memory");
     __syncwarp();
-    const float* src = sb + buf * 32 * tp + lane;
-    const int n = static_cast<int>(c0.e - c0.b < 32 ? c0.e - c0.b : 32);
+    const float* src = sb + buf * (32 * TP) + lane;
+    const int n = count(c[0]);
     int q = 0;
-    for (; q + 8 <= n; q += 8) {
+    for (; q + 8 <= n; q += 8, src += 8 * TP) {
       float x[8][JC], av[8];
 #pragma unroll
       for (int u = 0; u < 8; u++) {
-        av[u] = __shfl_sync(kFull, a0, q + u);
+        av[u] = __shfl_sync(kFull, ar[0], q + u);
 #pragma unroll
-        for (int jc = 0; jc < JC; jc++) x[u][jc] = mine[jc] ? src[(q + u) * tp + 32 * jc] : 0.f;
+        for (int jc = 0; jc < JC; jc++) x[u][jc] = mine[jc] ? src[u * TP + 32 * jc] : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < 8; u++)
 #pragma unroll
         for (int jc = 0; jc < JC; jc++) acc[jc] = fmaf(av[u], x[u][jc], acc[jc]);
     }
-    for (; q < n; q++) {
-      const float aq = __shfl_sync(kFull, a0, q);
+    for (; q < n; q++, src += TP) {
+      const float aq = __shfl_sync(kFull, ar[0], q);
 #pragma unroll
       for (int jc = 0; jc < JC; jc++)
-        if (mine[jc]) acc[jc] = fmaf(aq, src[q * tp + 32 * jc], acc[jc]);
+        if (mine[jc]) acc[jc] = fmaf(aq, src[32 * jc], acc[jc]);
     }
-    if (c0.b + 32 >= c0.e) {  // last chunk of row c0.r
-      const int64_t r = c0.r;
-      int32_t count = 0;
+    if (c[0].b + 32 >= c[0].e) {  // last chunk of row c[0].r
+      const int64_t r = c[0].r;
+      int32_t pos_count = 0;
 #pragma unroll
       for (int jc = 0; jc < JC; jc++) {
         const bool pos = mine[jc] && acc[jc] > 0.f;
         if (mine[jc]) dense_out[r * w_cols + jc * 32 + lane] = pos ? acc[jc] : 0.f;
-        count += __popc(__ballot_sync(kFull, pos));
+        pos_count += __popc(__ballot_sync(kFull, pos));
         acc[jc] = 0.f;
       }
-      if (lane == 0) cnt[r] = count;
+      if (lane == 0) cnt[r] = pos_count;
     }
     __syncwarp();  // every lane is done reading this buffer before it is refilled
-    const Cur c2 = next(c1);
-    const float a2 = issue(c2, buf);
-    c0 = c1, c1 = c2, a0 = a1, a1 = a2, buf ^= 1;
+    issue(cn, kn, an, buf);
+#pragma unroll
+    for (int i = 0; i + 1 < kAggStages; i++) c[i] = c[i + 1], ar[i] = ar[i + 1];
+    c[kAggStages - 1] = cn, ar[kAggStages - 1] = an;
+    cn = next(cn);
+    load(cn, kn, an);
+    buf = buf + 1 == kAggStages ? 0 : buf + 1;
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
@@ -1196,9 +1244,41 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
   const int halves = (katoms + 3) / 4;
   uint32_t phase = 0;
   const int64_t ntiles = (K + kRows - 1) / kRows;
+  // The tile loop is lock-step across the CTA (densify -> MMA -> epilogue), so the entries' load
+  // latency is exposed once per tile: one thread pulls the NEXT tile's row offsets and CSR entries
+  // into L2 with bulk prefetches (its offsets were read one tile earlier, so nothing waits).
+  const bool pf = tid == 32;
+  int64_t pf_b = 0, pf_e = 0;
+  auto pf_range = [&](int64_t tl) {
+    if (tl < ntiles) {
+      const int64_t q0 = tl * kRows, q1 = q0 + kRows < K ? q0 + kRows : K;
+      pf_b = static_cast<int64_t>(hptr[q0] - hbase), pf_e = static_cast<int64_t>(hptr[q1] - hbase);
+    } else {
+      pf_b = pf_e = 0;
+    }
+  };
+  auto bulk_pf = [](const void* p, int64_t bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+    for (uintptr_t x = a; x < e; x += 65536) {
+      const uint32_t n = static_cast<uint32_t>(e - x < 65536 ? e - x : 65536);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x), "r"(n) : "memory");
+    }
+  };
+  if (pf) pf_range(blockIdx.x + static_cast<int64_t>(gridDim.x));
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * kRows;
     const int rows = static_cast<int>(K - r0 < kRows ? K - r0 : kRows);
+    if (pf) {
+      const int64_t nt = tile + gridDim.x;
+      if (nt < ntiles && pf_e > pf_b) {
+        const int64_t q0 = nt * kRows, q1 = q0 + kRows < K ? q0 + kRows : K;
+        bulk_pf(hptr + q0, (q1 - q0 + 1) * 8);
+        bulk_pf(hcol + pf_b, (pf_e - pf_b) * 4);
+        bulk_pf(hval + pf_b, (pf_e - pf_b) * 4);
+      }
+      pf_range(nt + gridDim.x);
+    }
     // this warp's rows: offsets relative to the tile's first entry (a tile holds <= 128 x 256 entries)
     const int64_t tile_base = static_cast<int64_t>(hptr[r0] - hbase);
     int32_t cur[kRowsPerWarp], end[kRowsPerWarp];
@@ -1351,20 +1431,19 @@ void agg_t_launch(Ctx& ctx, const Staged& as, int64_t rows, int64_t K, const flo
   AB2_CUDA(cudaGetLastError());
 }
 
-template <int JC>
-void agg_t_cp_launch(Ctx& ctx, const Staged& as, int64_t rows, int64_t K, const float* t, int64_t tp, int64_t w_cols,
+template <int TP>
+void agg_t_cp_launch(Ctx& ctx, const Staged& as, int64_t rows, int64_t K, const float* t, int64_t w_cols,
                      float* dense, int32_t* cnt) {
-  const int smem = kAggWarps * 2 * 32 * static_cast<int>(tp) * static_cast<int>(sizeof(float));
-  auto k1 = k_agg_t_cp<JC>;
+  const int smem = kAggWarps * kAggStages * 32 * TP * static_cast<int>(sizeof(float));
+  auto k1 = k_agg_t_cp<TP>;
   AB2_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int nb = 0;
   AB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k1, kAggWarps * 32, smem));
-  const int64_t want = (rows + kAggWarps - 1) / kAggWarps;
+  const int64_t want = (rows + 32 * kAggWarps - 1) / (32 * kAggWarps);  // warps own 32-row blocks
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, static_cast<int64_t>(std::max(nb, 1)) * ctx.sms)));
   if (rows > 0)
     k1<<<grid, kAggWarps * 32, smem, ctx.stream>>>(as.ptr, as.base, static_cast<const uint32_t*>(as.idx),
-                                                   static_cast<const float*>(as.val), rows, K, t, static_cast<int>(tp),
-                                                   w_cols, dense, cnt);
+                                                   static_cast<const float*>(as.val), rows, K, t, w_cols, dense, cnt);
   AB2_CUDA(cudaGetLastError());
 }
 
@@ -1520,9 +1599,12 @@ void layer_fused(Ctx& ctx, const aires_b200_matrix& at, const aires_b200_matrix&
         }
       }
       const Staged as = stage_csr(ctx, at);
-      if (tp <= 64 && option("agg_async", 1) != 0) {
-        if (JC == 1) agg_t_cp_launch<1>(ctx, as, rows, K, t, tp, wc, dense, cnt);
-        else agg_t_cp_launch<2>(ctx, as, rows, K, t, tp, wc, dense, cnt);
+      if (tp <= 64 && K * tp < (int64_t(1) << 32) && option("agg_async", 1) != 0) {
+        switch (tp) {
+#define AB2_CP(TP) case TP: agg_t_cp_launch<TP>(ctx, as, rows, K, t, wc, dense, cnt); break;
+          AB2_CP(8) AB2_CP(16) AB2_CP(24) AB2_CP(32) AB2_CP(40) AB2_CP(48) AB2_CP(56) AB2_CP(64)
+#undef AB2_CP
+        }
       } else switch (JC) {
         case 1: agg_t_launch<1>(ctx, as, rows, K, t, tp, wc, dense, cnt); break;
         case 2: agg_t_launch<2>(ctx, as, rows, K, t, tp, wc, dense, cnt); break;
