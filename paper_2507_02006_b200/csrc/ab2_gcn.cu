@@ -998,17 +998,15 @@ __global__ void __launch_bounds__(256) k_agg_t(const uint64_t* __restrict__ aptr
 
 // k_agg_t for T rows of <= 64 floats, with the gathers made asynchronous: k_agg_t holds its eight
 // in-flight T rows in registers, so the kernel is latency-bound (ncu: DRAM 21%, long-scoreboard
-// stalls, occupancy capped by registers).  Here each warp streams its Ã rows as 32-entry chunks; the
-// T rows of chunk i+1 are copied global -> shared with cp.async (no registers held) while chunk i is
-// summed from shared memory, and the Ã entries of chunk i+2 are loaded meanwhile.  TP is T's row
-// pitch (floats), K * TP < 2^32.  Same cells, same ascending-entry fmaf order as k_agg_t.
+// stalls, occupancy capped by registers).  Here a warp owns blocks of 32 consecutive Ã rows (wid,
+// wid + nw, ...) and streams each block's entries as full 32-entry chunks across row boundaries (rows
+// average ~26 entries on GCN graphs); chunk i+1's T rows are copied global -> shared with cp.async (no
+// registers held) while chunk i is summed from shared memory.  A row's terms are added in ascending
+// entry order with fmaf, as in k_agg_t.  TP is T's row pitch (floats), K * TP < 2^32.
 #ifndef AB2_AGG_WARPS
 #define AB2_AGG_WARPS 4
 #endif
-#ifndef AB2_AGG_STAGES
-#define AB2_AGG_STAGES 2  // chunk buffers per warp (3: 8.8 ms, 4: 10.7 ms for cfg5 layer 2 -- fewer warps)
-#endif
-constexpr int kAggWarps = AB2_AGG_WARPS, kAggStages = AB2_AGG_STAGES;
+constexpr int kAggWarps = AB2_AGG_WARPS, kAggStages = 2;  // (3 / 4 buffers: fewer warps, slower)
 template <int TP>
 __global__ void __launch_bounds__(kAggWarps * 32) k_agg_t_cp(const uint64_t* __restrict__ aptr, uint64_t abase,
                                                           const uint32_t* __restrict__ acol,
@@ -1020,51 +1018,37 @@ __global__ void __launch_bounds__(kAggWarps * 32) k_agg_t_cp(const uint64_t* __r
   const int lane = lane_id();
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  float* const sb = agg_smem + (threadIdx.x >> 5) * (kAggStages * 32 * TP);  // chunk ring
+  float* const sb = agg_smem + (threadIdx.x >> 5) * (kAggStages * 32 * TP);
   const int piece = lane & 15, half = lane >> 4;
   bool mine[JC];
 #pragma unroll
   for (int jc = 0; jc < JC; jc++) mine[jc] = jc * 32 + lane < w_cols;
+  auto blk_end = [&](int64_t rb) { return rb + 32 < rows ? rb + 32 : rows; };
 
-  // chunk cursor: entries [b, min(b + 32, e)) of row r (an empty row is one empty chunk).  A warp
-  // owns blocks of 32 consecutive rows (wid, wid + nw, ...): the block's row offsets are one
-  // coalesced load held by the lanes, and the following block's are loaded one block ahead, so
-  // stepping to the next row costs two shuffles instead of a dependent global load.
-  struct Cur {
-    int64_t r, b, e;
-  };
-  int64_t rb = wid * 32;
-  uint64_t ps = 0, pe = 0, qs = 0, qe = 0;  // this block's / the next block's offsets (lane = row)
-  auto load_blk = [&](int64_t base, uint64_t& s0, uint64_t& e0) {
-    s0 = e0 = abase;
-    if (base + lane < rows) s0 = aptr[base + lane], e0 = aptr[base + lane + 1];
-  };
-  load_blk(rb, ps, pe);
-  load_blk(rb + 32 * nw, qs, qe);
-  auto first = [&](int64_t r) -> Cur {
-    if (r >= rows) return Cur{r, 0, 0};
-    if (r >= rb + 32) {  // entered the next block (r == rb + 32 nw)
-      rb = r, ps = qs, pe = qe;
-      load_blk(rb + 32 * nw, qs, qe);
+  // producer: chunks [b, min(b + 32, e)) of block rb's entry range [., e)
+  int64_t p_rb = wid * 32, p_b = 0, p_e = 0;
+  if (p_rb < rows) p_b = static_cast<int64_t>(aptr[p_rb] - abase), p_e = static_cast<int64_t>(aptr[blk_end(p_rb)] - abase);
+  // advance the producer to its next non-empty chunk; false when the warp's entries are exhausted
+  auto p_next = [&]() -> bool {
+    while (p_rb < rows && p_b >= p_e) {
+      p_rb += 32 * nw;
+      if (p_rb < rows) p_b = static_cast<int64_t>(aptr[p_rb] - abase), p_e = static_cast<int64_t>(aptr[blk_end(p_rb)] - abase);
     }
-    const int l = static_cast<int>(r - rb);
-    return Cur{r, static_cast<int64_t>(__shfl_sync(kFull, ps, l) - abase),
-               static_cast<int64_t>(__shfl_sync(kFull, pe, l) - abase)};
+    return p_rb < rows;
   };
-  auto next = [&](const Cur& c) -> Cur {
-    if (c.b + 32 < c.e) return Cur{c.r, c.b + 32, c.e};
-    return first(((c.r + 1) & 31) ? c.r + 1 : c.r + 1 + 32 * (nw - 1));
-  };
-  auto count = [](const Cur& c) { return static_cast<int>(c.e - c.b < 32 ? c.e - c.b : 32); };
-  auto load = [&](const Cur& c, uint32_t& k, float& a) {
-    k = 0, a = 0.f;
-    if (c.r < rows && lane < count(c)) k = acol[c.b + lane], a = aval[c.b + lane];
-  };
-  // copy chunk c's T rows into buffer buf (k, a: this lane's entry, loaded one step earlier)
-  auto issue = [&](const Cur& c, uint32_t k, float& a, int buf) {
-    if (c.r < rows) {
-      const int n = count(c);
-      if (k >= K) a = 0.f, k = 0;
+  // issue the producer's chunk into buffer buf (returns this lane's Ã value; entries [cb, ce))
+  auto issue = [&](int buf, int64_t& cb, int64_t& ce) -> float {
+    float a = 0.f;
+    cb = ce = -1;
+    if (p_next()) {
+      cb = p_b;
+      const int n = static_cast<int>(p_e - p_b < 32 ? p_e - p_b : 32);
+      uint32_t k = 0;
+      if (lane < n) {
+        k = acol[p_b + lane];
+        a = aval[p_b + lane];
+        if (k >= K) a = 0.f, k = 0;
+      }
       const uint32_t off = k * TP;
       float* dst = sb + buf * (32 * TP) + piece * 4;
 #pragma unroll 4
@@ -1076,74 +1060,73 @@ __global__ void __launch_bounds__(kAggWarps * 32) k_agg_t_cp(const uint64_t* __r
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(t + o + piece * 4) : "memory");
         }
       }
+      p_b += n;
+      ce = p_b;
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
+    return a;
   };
 
-  float acc[JC];
-#pragma unroll
-  for (int jc = 0; jc < JC; jc++) acc[jc] = 0.f;
-  Cur c[kAggStages];
-  float ar[kAggStages];
-  c[0] = first(rb);
-#pragma unroll
-  for (int i = 1; i < kAggStages; i++) c[i] = next(c[i - 1]);
-#pragma unroll
-  for (int i = 0; i < kAggStages; i++) {
-    uint32_t k;
-    load(c[i], k, ar[i]);
-    issue(c[i], k, ar[i], i);
-  }
-  Cur cn = next(c[kAggStages - 1]);
-  uint32_t kn;
-  float an;
-  load(cn, kn, an);
+  int64_t cb0, ce0, cb1, ce1;
+  float a0 = issue(0, cb0, ce0), a1 = issue(1, cb1, ce1);
   int buf = 0;
-  while (c[0].r < rows) {
-    asm volatile("cp.async.wait_group %0;" ::"n"(kAggStages - 1) : "memory");
-    __syncwarp();
-    const float* src = sb + buf * (32 * TP) + lane;
-    const int n = count(c[0]);
-    int q = 0;
-    for (; q + 8 <= n; q += 8, src += 8 * TP) {
-      float x[8][JC], av[8];
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+  __syncwarp();
+  // consumer: rows in order; entries [s, e) of row r come from the chunk at cb0 (buffer buf)
+  for (int64_t rb = wid * 32; rb < rows; rb += 32 * nw) {
+    const int nr = static_cast<int>(blk_end(rb) - rb);
+    uint64_t ps = 0, pe = 0;
+    if (lane < nr) ps = aptr[rb + lane], pe = aptr[rb + lane + 1];
+    for (int i = 0; i < nr; i++) {
+      int64_t s = static_cast<int64_t>(__shfl_sync(kFull, ps, i) - abase);
+      const int64_t e = static_cast<int64_t>(__shfl_sync(kFull, pe, i) - abase);
+      float acc[JC];
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
-        av[u] = __shfl_sync(kFull, ar[0], q + u);
+      for (int jc = 0; jc < JC; jc++) acc[jc] = 0.f;
+      while (s < e) {
+        if (s >= ce0) {  // chunk exhausted: refill its buffer, move to the next chunk
+          __syncwarp();
+          int64_t cb2, ce2;
+          const float a2 = issue(buf, cb2, ce2);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+          __syncwarp();
+          cb0 = cb1, ce0 = ce1, a0 = a1, cb1 = cb2, ce1 = ce2, a1 = a2, buf ^= 1;
+        }
+        const int q0 = static_cast<int>(s - cb0);
+        const int q1 = static_cast<int>((e < ce0 ? e : ce0) - cb0);
+        const float* src = sb + buf * (32 * TP) + lane;
+        int q = q0;
+        for (; q + 8 <= q1; q += 8) {
+          float x[8][JC], av[8];
 #pragma unroll
-        for (int jc = 0; jc < JC; jc++) x[u][jc] = mine[jc] ? src[u * TP + 32 * jc] : 0.f;
+          for (int u = 0; u < 8; u++) {
+            av[u] = __shfl_sync(kFull, a0, q + u);
+#pragma unroll
+            for (int jc = 0; jc < JC; jc++) x[u][jc] = mine[jc] ? src[(q + u) * TP + 32 * jc] : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; u++)
+#pragma unroll
+            for (int jc = 0; jc < JC; jc++) acc[jc] = fmaf(av[u], x[u][jc], acc[jc]);
+        }
+        for (; q < q1; q++) {
+          const float aq = __shfl_sync(kFull, a0, q);
+#pragma unroll
+          for (int jc = 0; jc < JC; jc++)
+            if (mine[jc]) acc[jc] = fmaf(aq, src[q * TP + 32 * jc], acc[jc]);
+        }
+        s = cb0 + q1;
       }
-#pragma unroll
-      for (int u = 0; u < 8; u++)
-#pragma unroll
-        for (int jc = 0; jc < JC; jc++) acc[jc] = fmaf(av[u], x[u][jc], acc[jc]);
-    }
-    for (; q < n; q++, src += TP) {
-      const float aq = __shfl_sync(kFull, ar[0], q);
-#pragma unroll
-      for (int jc = 0; jc < JC; jc++)
-        if (mine[jc]) acc[jc] = fmaf(aq, src[32 * jc], acc[jc]);
-    }
-    if (c[0].b + 32 >= c[0].e) {  // last chunk of row c[0].r
-      const int64_t r = c[0].r;
+      const int64_t r = rb + i;
       int32_t pos_count = 0;
 #pragma unroll
       for (int jc = 0; jc < JC; jc++) {
         const bool pos = mine[jc] && acc[jc] > 0.f;
         if (mine[jc]) dense_out[r * w_cols + jc * 32 + lane] = pos ? acc[jc] : 0.f;
         pos_count += __popc(__ballot_sync(kFull, pos));
-        acc[jc] = 0.f;
       }
       if (lane == 0) cnt[r] = pos_count;
     }
-    __syncwarp();  // every lane is done reading this buffer before it is refilled
-    issue(cn, kn, an, buf);
-#pragma unroll
-    for (int i = 0; i + 1 < kAggStages; i++) c[i] = c[i + 1], ar[i] = ar[i + 1];
-    c[kAggStages - 1] = cn, ar[kAggStages - 1] = an;
-    cn = next(cn);
-    load(cn, kn, an);
-    buf = buf + 1 == kAggStages ? 0 : buf + 1;
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }

@@ -348,6 +348,34 @@ def test_layer_fused_matches_unfused_chain(hcols, wcols):
         assert err <= 1e-5 * max(scale.get(key, 0.0), 1e-30), (key, want.get(key), have.get(key), scale.get(key))
 
 
+@pytest.mark.parametrize("wcols", [47, 20, 64])
+def test_layer_fused_gather_kernels_agree_on_sparse_blocks(wcols):
+    """The cp.async Ã·T gather (k_agg_t_cp: warps own 32-row blocks, entries streamed as chunks across
+    row boundaries) against the register gather (k_agg_t, option agg_async=0) on a graph where most
+    rows are empty, so warps own several blocks, some blocks have no entries and chunks end short of
+    32: same cells, same ascending-entry fmaf order -> bit-identical CSR."""
+    n = 300_000
+    rng = np.random.default_rng(17)
+    lens = np.zeros(n, dtype=np.int64)
+    live = np.arange(0, n, 20)
+    lens[live] = rng.integers(1, 70, live.size)
+    lens[123_456] = 0
+    lens[200_000:200_040] = 33  # a run of rows that straddle chunk boundaries
+    rp = np.zeros(n + 1, dtype=np.uint64)
+    rp[1:] = np.cumsum(lens)
+    cols = np.concatenate([np.sort(rng.choice(n, int(k), replace=False)) for k in lens if k]).astype(np.uint64)
+    a = ab.CsrMatrix(n, n, rp, cols, rng.random(cols.size) + 0.01)
+    h = ab.synth_features(n, 160, 50.0, 7, idx_dtype=np.uint64)
+    w = ab.gen_weights(160, wcols, 9)
+    got = ab.layer_fused(a, h, w)
+    ab.set_option("agg_async", 0)
+    want = ab.layer_fused(a, h, w)
+    assert np.array_equal(got.row_ptr, want.row_ptr)
+    assert np.array_equal(got.col_idx, want.col_idx)
+    assert np.array_equal(np.asarray(got.values).view(np.uint32), np.asarray(want.values).view(np.uint32))
+    assert got.row_ptr[-1] > 0
+
+
 @pytest.mark.parametrize("cin,cout,path", [(100, 256, "v4"), (64, 130, "v4"), (40, 100, "v4"), (30, 96, "v4"),
                                            (100, 256, "scalar"), (64, 130, "two-pass"), (20, 300, "auto")])
 def test_combine_fp32_kernels_match_oracle(cin, cout, path):
