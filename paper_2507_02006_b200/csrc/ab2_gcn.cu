@@ -1249,6 +1249,78 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
     }
   };
   if (pf) pf_range(blockIdx.x + static_cast<int64_t>(gridDim.x));
+  // densification state of the tile being loaded: this warp's rows (offsets relative to the tile's
+  // first entry; a tile holds <= 128 x 256 entries) and one round of entries in registers
+  int32_t cur[kRowsPerWarp], end[kRowsPerWarp];
+  const uint32_t* tcol = hcol;
+  const float* tval = hval;
+  uint32_t c[kChunks][kRowsPerWarp];
+  float v[kChunks][kRowsPerWarp];
+  auto setup_tile = [&](int64_t tl) {
+    const int64_t q0 = tl * kRows;
+    const int nrows = static_cast<int>(K - q0 < kRows ? K - q0 : kRows);
+    const int64_t tile_base = static_cast<int64_t>(hptr[q0] - hbase);
+#pragma unroll
+    for (int j = 0; j < kRowsPerWarp; j++) {
+      const int m = warp + kWarps * j;
+      cur[j] = end[j] = 0;
+      if (m < nrows) {
+        cur[j] = static_cast<int32_t>(static_cast<int64_t>(hptr[q0 + m] - hbase) - tile_base);
+        end[j] = static_cast<int32_t>(static_cast<int64_t>(hptr[q0 + m + 1] - hbase) - tile_base);
+      }
+    }
+    tcol = hcol + tile_base;
+    tval = hval + tile_base;
+  };
+  // the next 32 * kChunks entries of each of the warp's rows: kChunks x 8 x 2 loads per lane in flight
+  auto load_round = [&]() {
+#pragma unroll
+    for (int h2 = 0; h2 < kChunks; h2++)
+#pragma unroll
+      for (int j = 0; j < kRowsPerWarp; j++) {
+        const int32_t i = cur[j] + 32 * h2 + lane;
+        c[h2][j] = 0xffffffffu;
+        v[h2][j] = 0.f;
+        if (i < end[j]) {
+          c[h2][j] = __ldg(tcol + i);
+          v[h2][j] = __ldg(tval + i);
+        }
+      }
+  };
+  // scatter the round's entries of columns [klo, khi) into A; true if a row may have more of them
+  auto scatter = [&](uint32_t klo, uint32_t khi) -> bool {
+    bool more = false;
+#pragma unroll
+    for (int j = 0; j < kRowsPerWarp; j++) {
+      const int m = warp + kWarps * j;
+      int took = 0;
+#pragma unroll
+      for (int h2 = 0; h2 < kChunks; h2++) {
+        const uint32_t cc = c[h2][j];
+        const bool in = cc >= klo && cc < khi;  // (columns are sorted: the half's entries come first)
+        if (in) {
+          if (cc < static_cast<uint32_t>(h_cols)) {
+            float hi, lo;
+            split(v[h2][j], hi, lo);
+            const uint32_t k = cc - klo;
+            const uint32_t off = (k >> 5) * 16384 + swz(m, static_cast<int>(k & 31));
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(ah_s + off), "f"(hi) : "memory");
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(al_s + off), "f"(lo) : "memory");
+          } else {
+            ctl->bad_row = 1;
+          }
+        }
+        took += __popc(__ballot_sync(0xffffffffu, in));
+      }
+      cur[j] += took;
+      more |= took == 32 * kChunks;
+    }
+    return more;
+  };
+  if (static_cast<int64_t>(blockIdx.x) < ntiles) {
+    setup_tile(blockIdx.x);
+    load_round();
+  }
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t r0 = tile * kRows;
     const int rows = static_cast<int>(K - r0 < kRows ? K - r0 : kRows);
@@ -1262,69 +1334,26 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
       }
       pf_range(nt + gridDim.x);
     }
-    // this warp's rows: offsets relative to the tile's first entry (a tile holds <= 128 x 256 entries)
-    const int64_t tile_base = static_cast<int64_t>(hptr[r0] - hbase);
-    int32_t cur[kRowsPerWarp], end[kRowsPerWarp];
-#pragma unroll
-    for (int j = 0; j < kRowsPerWarp; j++) {
-      const int m = warp + kWarps * j;
-      cur[j] = end[j] = 0;
-      if (m < rows) {
-        cur[j] = static_cast<int32_t>(static_cast<int64_t>(hptr[r0 + m] - hbase) - tile_base);
-        end[j] = static_cast<int32_t>(static_cast<int64_t>(hptr[r0 + m + 1] - hbase) - tile_base);
-      }
-    }
-    const uint32_t* tcol = hcol + tile_base;
-    const float* tval = hval + tile_base;
     for (int hf = 0; hf < halves; hf++) {
-      // zero this half of A (the previous MMAs that read it have completed: mbarrier waited below)
-      for (int i = tid; i < 2 * 65536 / 16; i += kThreads)
-        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(ah_s + i * 16), "r"(0u) : "memory");
-      __syncthreads();
+      // zero this warp's rows of the half (the MMAs that read A have completed: mbarrier waited
+      // below) -- warp-local, so no CTA barrier between zeroing and the scatter
+#pragma unroll
+      for (int z = 0; z < (kRowsPerWarp * 4 * 2 * 128) / (32 * 16); z++) {
+        const int idx = z * 32 + lane;                       // 16-byte piece of (row j, atom, hi/lo)
+        const int j = idx >> 6, atom = (idx >> 3) & 3, lohi = (idx >> 5) & 1, pc = idx & 7;
+        const int m = warp + kWarps * j;
+        const uint32_t base = lohi ? al_s : ah_s;
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + atom * 16384 + (m >> 3) * 1024 +
+                                                                       (m & 7) * 128 + pc * 16),
+                     "r"(0u)
+                     : "memory");
+      }
+      __syncwarp();
       const uint32_t klo = static_cast<uint32_t>(hf * kHalf), khi = klo + kHalf;
-      for (;;) {
-        // the next 64 entries of each of the warp's rows: 2 x 8 x 2 loads per lane in flight
-        uint32_t c[kChunks][kRowsPerWarp];
-        float v[kChunks][kRowsPerWarp];
-#pragma unroll
-        for (int h2 = 0; h2 < kChunks; h2++)
-#pragma unroll
-          for (int j = 0; j < kRowsPerWarp; j++) {
-            const int32_t i = cur[j] + 32 * h2 + lane;
-            c[h2][j] = 0xffffffffu;
-            v[h2][j] = 0.f;
-            if (i < end[j]) {
-              c[h2][j] = __ldg(tcol + i);
-              v[h2][j] = __ldg(tval + i);
-            }
-          }
-        bool more = false;
-#pragma unroll
-        for (int j = 0; j < kRowsPerWarp; j++) {
-          const int m = warp + kWarps * j;
-          int took = 0;
-#pragma unroll
-          for (int h2 = 0; h2 < kChunks; h2++) {
-            const uint32_t cc = c[h2][j];
-            const bool in = cc >= klo && cc < khi;  // (columns are sorted: the half's entries come first)
-            if (in) {
-              if (cc < static_cast<uint32_t>(h_cols)) {
-                float hi, lo;
-                split(v[h2][j], hi, lo);
-                const uint32_t k = cc - klo;
-                const uint32_t off = (k >> 5) * 16384 + swz(m, static_cast<int>(k & 31));
-                asm volatile("st.shared.f32 [%0], %1;" ::"r"(ah_s + off), "f"(hi) : "memory");
-                asm volatile("st.shared.f32 [%0], %1;" ::"r"(al_s + off), "f"(lo) : "memory");
-              } else {
-                ctl->bad_row = 1;
-              }
-            }
-            took += __popc(__ballot_sync(0xffffffffu, in));
-          }
-          cur[j] += took;
-          more |= took == 32 * kChunks;
-        }
-        if (!__any_sync(0xffffffffu, more)) break;
+      bool more = scatter(klo, khi);
+      while (__any_sync(0xffffffffu, more)) {
+        load_round();
+        more = scatter(klo, khi);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
@@ -1343,6 +1372,13 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar_s)
                      : "memory");
       }
+      // while the MMAs run: the first entries of the next half, or of the next tile
+      if (hf + 1 < halves) {
+        load_round();
+      } else if (tile + gridDim.x < ntiles) {
+        setup_tile(tile + gridDim.x);
+        load_round();
+      }
       mbar_wait(mbar_s, phase);
       phase ^= 1u;
     }
@@ -1360,14 +1396,10 @@ __global__ void __launch_bounds__(tc::kThreads, 1)
                      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                      : "r"(tmem + (static_cast<uint32_t>(32 * q) << 16) + static_cast<uint32_t>(cg * NQ + c0)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (m < rows) {
-          float* dst = t + (r0 + m) * tp;
-#pragma unroll
-          for (int j = 0; j < 4; j++) {
-            const int col = cg * NQ + c0 + j;
-            if (col < w_cols) dst[col] = __uint_as_float(r[j]);
-          }
-        }
+        const int col = cg * NQ + c0;
+        if (m < rows && col < tp)  // tp is a multiple of 8: a group of 4 is wholly inside the pitch or not
+          *reinterpret_cast<float4*>(t + (r0 + m) * tp + col) =
+              make_float4(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3]));
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
