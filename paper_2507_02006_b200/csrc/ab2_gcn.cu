@@ -345,18 +345,35 @@ Staged stage_csr(Ctx& ctx, const aires_b200_matrix& m) {
   return s;
 }
 
-// Hands the result (device arrays ptr/idx/val) to the caller's allocator (host or device).
+// The result's arrays, allocated through the caller's allocator as soon as nnz is known: a device
+// result is written in place by the kernels (no staging copy of idx/val), a host result is built in
+// the context's buffers and copied down by deliver().
+template <class IdxO, class VO>
+struct OutBufs {
+  void *optr = nullptr, *oidx = nullptr, *oval = nullptr;
+  IdxO* col = nullptr;  // where the kernels write
+  VO* val = nullptr;
+  bool device = false;
+};
+template <class IdxO, class VO>
+OutBufs<IdxO, VO> out_alloc(Ctx& ctx, aires_b200_output& out, uint64_t rows, uint64_t nnz) {
+  OutBufs<IdxO, VO> o;
+  const int rc = out.alloc(out.user, rows, nnz, &o.optr, &o.oidx, &o.oval);
+  if (rc != 0) fail(rc, "output allocator failed for " + std::to_string(nnz) + " nonzeros");
+  o.device = out.location == AIRES_B200_DEVICE;
+  o.col = o.device ? static_cast<IdxO*>(o.oidx) : static_cast<IdxO*>(ctx.c_col.get(std::max<uint64_t>(nnz, 1) * sizeof(IdxO)));
+  o.val = o.device ? static_cast<VO*>(o.oval) : static_cast<VO*>(ctx.c_val.get(std::max<uint64_t>(nnz, 1) * sizeof(VO)));
+  return o;
+}
+// row_ptr (and, for a host result, idx/val) to the caller's arrays; waits for the stream.
 template <class IdxO, class VO>
 void deliver(Ctx& ctx, aires_b200_output& out, uint64_t rows, uint64_t cols, uint64_t nnz, const int64_t* dptr,
-             const IdxO* didx, const VO* dval) {
-  void *optr = nullptr, *oidx = nullptr, *oval = nullptr;
-  const int rc = out.alloc(out.user, rows, nnz, &optr, &oidx, &oval);
-  if (rc != 0) fail(rc, "output allocator failed for " + std::to_string(nnz) + " nonzeros");
-  const cudaMemcpyKind kind = out.location == AIRES_B200_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  AB2_CUDA(cudaMemcpyAsync(optr, dptr, (rows + 1) * 8, kind, ctx.stream));
-  if (nnz) {
-    AB2_CUDA(cudaMemcpyAsync(oidx, didx, nnz * sizeof(IdxO), kind, ctx.stream));
-    AB2_CUDA(cudaMemcpyAsync(oval, dval, nnz * sizeof(VO), kind, ctx.stream));
+             const OutBufs<IdxO, VO>& o) {
+  const cudaMemcpyKind kind = o.device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  AB2_CUDA(cudaMemcpyAsync(o.optr, dptr, (rows + 1) * 8, kind, ctx.stream));
+  if (nnz && !o.device) {
+    AB2_CUDA(cudaMemcpyAsync(o.oidx, o.col, nnz * sizeof(IdxO), kind, ctx.stream));
+    AB2_CUDA(cudaMemcpyAsync(o.oval, o.val, nnz * sizeof(VO), kind, ctx.stream));
   }
   AB2_CUDA(cudaStreamSynchronize(ctx.stream));
   out.n_rows = rows;
@@ -392,12 +409,13 @@ void normalize_t(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
   if (h->bad_row) fail(1 + 14, "adjacency weights must be nonnegative");  // errc::negative_weight
   if (h->n_fix) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "column index outside the square adjacency");
   const uint64_t nnz = n > 0 ? h->nnz : 0;
-  IdxO* ocol = static_cast<IdxO*>(ctx.c_col.get(std::max<uint64_t>(nnz, 1) * sizeof(IdxO)));
+  const OutBufs<IdxO, VO> ob = out_alloc<IdxO, VO>(ctx, out, static_cast<uint64_t>(n), nnz);
+  IdxO* ocol = ob.col;
   double* oval = static_cast<double*>(ctx.t_val.get(std::max<uint64_t>(nnz, 1) * 8));
   const bool flat = n < (int64_t(1) << 31);  // per-entry row ids for the flat scale pass
   int32_t* orow = flat ? static_cast<int32_t*>(ctx.t_col.get(std::max<uint64_t>(nnz, 1) * 4)) : nullptr;
   double* deg = static_cast<double*>(ctx.rflops.get(std::max<int64_t>(n, 1) * 8));
-  VO* outv = static_cast<VO*>(ctx.c_val.get(std::max<uint64_t>(nnz, 1) * sizeof(VO)));
+  VO* outv = ob.val;
   if (n > 0) {
     k_norm_fill<IdxT, VIn, IdxO><<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(s.ptr, s.base, col, val, n,
                                                                                        optr, ocol, oval, orow);
@@ -410,7 +428,7 @@ void normalize_t(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
     AB2_CUDA(cudaGetLastError());
     launches += 3;
   }
-  deliver<IdxO, VO>(ctx, out, static_cast<uint64_t>(n), static_cast<uint64_t>(n), nnz, optr, ocol, outv);
+  deliver<IdxO, VO>(ctx, out, static_cast<uint64_t>(n), static_cast<uint64_t>(n), nnz, optr, ob);
   ctx.launches = launches;
 }
 
@@ -623,15 +641,14 @@ void combine_t(Ctx& ctx, const aires_b200_matrix& x, const void* w_in, uint64_t 
     if (h->bad_row == 1) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "feature column outside the weight rows");
     if (h->bad_row) fail(AIRES_B200_CAPACITY_EXCEEDED, "combine staging overflow");
     const uint64_t nnz = h->nnz;
-    IdxO* ocol = static_cast<IdxO*>(ctx.c_col.get(std::max<uint64_t>(nnz, 1) * sizeof(IdxO)));
-    V* oval = static_cast<V*>(ctx.c_val.get(std::max<uint64_t>(nnz, 1) * sizeof(V)));
+    const OutBufs<IdxO, V> ob = out_alloc<IdxO, V>(ctx, out, static_cast<uint64_t>(rows), nnz);
     if (nnz) {
       k_place<V, IdxO><<<ctx.sms * 8, 256, 0, ctx.stream>>>(reinterpret_cast<const uint32_t*>(cnt), toff, optr, tcol,
-                                                           tval, rows, ocol, oval);
+                                                           tval, rows, ob.col, ob.val);
       AB2_CUDA(cudaGetLastError());
       launches++;
     }
-    deliver<IdxO, V>(ctx, out, static_cast<uint64_t>(rows), w_cols, nnz, optr, ocol, oval);
+    deliver<IdxO, V>(ctx, out, static_cast<uint64_t>(rows), w_cols, nnz, optr, ob);
     ctx.launches = launches;
     return;
   }
@@ -647,13 +664,12 @@ void combine_t(Ctx& ctx, const aires_b200_matrix& x, const void* w_in, uint64_t 
   AB2_CUDA(cudaStreamSynchronize(ctx.stream));
   if (h->bad_row) fail(AIRES_B200_INDEX_OUT_OF_RANGE, "feature column outside the weight rows");
   const uint64_t nnz = rows > 0 && w_cols > 0 ? h->nnz : 0;
-  IdxO* ocol = static_cast<IdxO*>(ctx.c_col.get(std::max<uint64_t>(nnz, 1) * sizeof(IdxO)));
-  V* oval = static_cast<V*>(ctx.c_val.get(std::max<uint64_t>(nnz, 1) * sizeof(V)));
+  const OutBufs<IdxO, V> ob = out_alloc<IdxO, V>(ctx, out, static_cast<uint64_t>(rows), nnz);
   if (nnz) {
-    run(true, ocol, oval);
+    run(true, ob.col, ob.val);
     launches++;
   }
-  deliver<IdxO, V>(ctx, out, static_cast<uint64_t>(rows), w_cols, nnz, optr, ocol, oval);
+  deliver<IdxO, V>(ctx, out, static_cast<uint64_t>(rows), w_cols, nnz, optr, ob);
   ctx.launches = launches;
 }
 
