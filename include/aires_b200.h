@@ -289,6 +289,7 @@ uint64_t aires_b200_checksum(uint64_t n_rows, uint64_t n_cols, uint64_t nnz, con
  *                           slots (host copy threads) instead of being registered for the call
  *   narrow_cols (1)         streamed runs move C's column indices as u16 (host threads widen them)
  *   hw_tensor (1)           fused layer: T = H·W on tcgen05 (3xTF32) when W has <= 48 columns
+ *   short_dense (1)         rows of <= 32 terms with <= 256 output columns: dense cells instead of a sort
  *   agg_async (1)           fused layer: Ã·T gathers T rows (<= 64 floats) with cp.async into shared memory
  */
 int aires_b200_set_option(const char* name, int64_t value);

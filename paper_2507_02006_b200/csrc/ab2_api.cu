@@ -35,7 +35,8 @@ const char* const kOptionNames[] = {
     "heavy_deg",         "sym_heavy_deg",  "num_warps",         "short_rows", "slot_w",      "numeric_kernel",
     "n5_warps",          "w5",             "wide_at",           "wide_tile",  "run_tiles",   "stream_tiles",
     "run_resident_cols", "run_cslots",     "combine_one_pass",  "combine_smem", "combine_v4", "fused_reassoc",
-    "gds",               "no_gds",         "stage_min_bytes",   "narrow_cols",       "hw_tensor",         "agg_async"};
+    "gds",               "no_gds",         "stage_min_bytes",   "narrow_cols",       "hw_tensor",         "agg_async",
+    "short_dense"};
 thread_local std::vector<std::pair<std::string, int64_t>> t_options;
 }  // namespace
 

@@ -64,7 +64,7 @@ struct Num3Args {
   int32_t stride;      // accumulator elements per copy (>= n_cols + 1, multiple of 32)
   int32_t copies;      // accumulator copies per warp
   int32_t warp_bytes;  // shared bytes per warp: copies*stride*sizeof(V) + stride marks + chunk table
-  int32_t pad0;          // 1: rows with <= 32 terms take the register sort path (short_row)
+  int32_t pad0;          // rows with <= 32 terms: 1 register sort (short_row), 2 dense cells (<= 256 columns)
   const int64_t* heavy;  // heavy rows (A-degree > heavy_deg)
   int64_t heavy_deg;
   uint32_t* cnt;         // per-row nnz
@@ -621,10 +621,18 @@ __device__ __forceinline__ V add_rn(V a, V b) {
     return __fadd_rn(a, b);
 }
 
-template <class V, class IdxT>
+//
+// Narrow outputs (<= 256 columns, e.g. the ogbn-products features): instead of the 32-key sort, lanes
+// holding the same column are grouped with match.any, each group's lowest lane sums the group's
+// terms in lane (= arrival) order and writes the sum into the warp's accumulator cell, the touched
+// columns are collected as bitmaps with redux.or, and the row is emitted in column order from the
+// bitmaps (the cells are reset to the sentinel as they are read).  Same sums, same order, same
+// structural zeros as the sorted form.
+template <class V, class IdxT, int CS = 1>
 __device__ __forceinline__ bool short_row(const Num3Args<V, IdxT>& p, const IdxT* __restrict__ ac,
                                           const V* __restrict__ av, uint32_t n, int64_t r, StageCursor& stage,
-                                          unsigned long long& my_nnz, unsigned long long& my_macs) {
+                                          unsigned long long& my_nnz, unsigned long long& my_macs,
+                                          V* acc = nullptr) {
   const int lane = lane_id();
   const uint64_t K = static_cast<uint64_t>(p.x.K);
   int64_t xs = 0;
@@ -660,6 +668,57 @@ __device__ __forceinline__ bool short_row(const Num3Args<V, IdxT>& p, const IdxT
     const int64_t q = xs_j + static_cast<int64_t>(t - ex_j);
     key = (static_cast<uint32_t>(p.x.col[q]) << 5) | t;
     v = mul_rn<V>(a_j, p.x.val[q]);
+  }
+  if (acc != nullptr) {  // narrow output: group by column, dense cells, bitmap emission
+    const bool real = t < T;
+    const uint32_t col = key >> 5;
+    const unsigned grp = __match_any_sync(kFull, real ? col : 0xffffffffu);
+    const bool lead = real && lane == __ffs(grp) - 1;
+    V sum = add_rn<V>(V(0), v);  // sum = 0.0; sum += term, then the group's later terms in order
+    unsigned rest = lead ? grp & (grp - 1) : 0u;
+    while (__any_sync(kFull, rest != 0)) {
+      const V ov = __shfl_sync(kFull, v, rest ? __ffs(rest) - 1 : lane);
+      if (rest) {
+        sum = add_rn<V>(sum, ov);
+        rest &= rest - 1;
+      }
+    }
+    if (lead) acc[CS * col] = sum;
+    const int nw = (p.x.n_cols + 31) >> 5;  // <= 8
+    unsigned bits[8];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+      bits[w] = 0;
+      if (w < nw) bits[w] = __reduce_or_sync(kFull, lead && (col >> 5) == static_cast<uint32_t>(w) ? 1u << (col & 31) : 0u);
+      cnt += __popc(bits[w]);
+    }
+    const unsigned long long off = out_offset(p, r, cnt, stage);
+    __syncwarp();
+    const bool fits = off <= p.t_cap && off + cnt <= p.t_cap;
+    uint32_t base = 0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+      if ((bits[w] >> lane) & 1u) {
+        const uint32_t c = 32 * w + lane;
+        if (fits) {
+          const unsigned long long pos = off + base + __popc(bits[w] & ((1u << lane) - 1));
+          p.tcol[pos] = static_cast<IdxT>(c);
+          p.tval[pos] = acc[CS * c];
+        }
+        acc[CS * c] = Sentinel<V>::value();
+      }
+      base += __popc(bits[w]);
+    }
+    __syncwarp();
+    if (!fits && lane == 0) atomicMax(&p.ctl->bad_row, 1ull);
+    if (lane == 0) {
+      p.cnt[r] = cnt;
+      p.toff[r] = off;
+      my_nnz += cnt;
+      my_macs += T;
+    }
+    return true;
   }
   // bitonic sort of the 32 (key, value) pairs, ascending
 #pragma unroll
@@ -836,7 +895,9 @@ __global__ void __launch_bounds__(AB2_NUM_MAXT, (sizeof(V) == 8 || W == 16) ? AB
       const uint32_t n = static_cast<uint32_t>(e - s);
       const IdxT* ac = p.acol + s;
       const V* av = p.aval + s;
-      if (p.pad0 && n <= 32 && short_row<V, IdxT>(p, ac, av, n, r, stage, my_nnz, my_macs)) continue;
+      if (p.pad0 && n <= 32 &&
+          short_row<V, IdxT, CS>(p, ac, av, n, r, stage, my_nnz, my_macs, p.pad0 == 2 ? acc : nullptr))
+        continue;
       bool zero = false;
       my_macs += walk<V, IdxT, W, XZ>(p, ac, av, n, 0, 1, acc, warp_tab(warp), zero);
       if (__any_sync(kFull, zero)) slow_row<V, IdxT, CS>(p, ac, av, n, acc, warp_mark(warp));

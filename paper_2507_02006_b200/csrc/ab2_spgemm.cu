@@ -167,7 +167,7 @@ Num3Args<V, IdxT> make_num3(const XOperand& x, const uint64_t* aptr, uint64_t ab
   np.tiny = x.xmin > 0 ? static_cast<V>((sizeof(V) == 4 ? std::ldexp(1.0, -147) : std::ldexp(1.0, -1072)) / x.xmin)
                        : V(0);
   np.stage_block = static_cast<uint32_t>(std::max<int64_t>(4096, 8 * static_cast<int64_t>(np.stride)));
-  np.pad0 = static_cast<int32_t>(option("short_rows", 1) != 0);
+  np.pad0 = option("short_rows", 1) == 0 ? 0 : (x.n_cols <= 256 && option("short_dense", 1) != 0 ? 2 : 1);
   return np;
 }
 
