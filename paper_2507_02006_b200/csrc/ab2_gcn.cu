@@ -94,50 +94,61 @@ __global__ void k_norm_fill(const uint64_t* __restrict__ ptr, uint64_t base, con
   }
 }
 
-// Rows of Â are short on GCN graphs (~26 entries on the products shape) with a power-law tail:
-// the degree sum takes one thread per row (a warp's 32 rows stream through L1 together, each
-// thread's loads run ahead of its arithmetic), and rows longer than kNormHeavy are handed to the
-// whole warp (coalesced 32-entry loads).  A warp per row left most lanes idle and issued the
-// per-row overhead 32 times (1.2 ms for the products-shaped Â); a thread per row alone serialised
-// the hub rows (0.94 ms); both together 0.73 ms.
+// Rows of Â are short on GCN graphs (~26 entries on the products shape) with a power-law tail. A warp
+// takes 32 consecutive rows (one per lane) and streams their contiguous entries through shared memory
+// in coalesced windows; each lane adds its own row's values left to right as the windows pass, so
+// the sum keeps the reference's order (gcn.hpp:61-64).  Rows longer than kNormHeavy are summed by the
+// whole warp instead (coalesced 32-entry loads, the next chunk in flight).  Earlier forms: a thread
+// per row reading its row from global (0.73 ms for the products-shaped Â: 32 rows' strided loads per
+// instruction), a warp per row (1.2 ms, lanes idle).
 constexpr int64_t kNormHeavy = 256;
+constexpr int kNormWin = 512, kNormWarps = 8;
 
-// weighted degrees, summed left to right (gcn.hpp:61-64), exact for any weights.
-__global__ void k_norm_degree(const int64_t* __restrict__ optr, const double* __restrict__ oval, int64_t n,
-                              double* __restrict__ deg) {
+// weighted degrees, summed left to right, exact for any weights.
+__global__ void __launch_bounds__(kNormWarps * 32) k_norm_degree(const int64_t* __restrict__ optr,
+                                                                  const double* __restrict__ oval, int64_t n,
+                                                                  double* __restrict__ deg) {
+  __shared__ double win[kNormWarps][kNormWin];
+  double* buf = win[threadIdx.x >> 5];
   const int lane = lane_id();
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t base = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) & ~int64_t(31); base < n;
-       base += stride) {
-    const int64_t r = base + lane;
+  const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t rb = wid * 32; rb < n; rb += nw * 32) {
+    const int64_t r = rb + lane;
     int64_t s = 0, e = 0;
-    if (r < n) {
-      s = optr[r];
-      e = optr[r + 1];
-    }
+    if (r < n) s = optr[r], e = optr[r + 1];
     const bool heavy = e - s > kNormHeavy;
-    if (r < n && !heavy) {
-      double d = 0.0;
-      int64_t k = s;
-      for (; k + 4 <= e; k += 4) {
-        const double v0 = oval[k], v1 = oval[k + 1], v2 = oval[k + 2], v3 = oval[k + 3];
-        d = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(d, v0), v1), v2), v3);
+    const int64_t S = optr[rb], E = optr[rb + 32 < n ? rb + 32 : n];
+    double d = 0.0;
+    int64_t pos = heavy ? e : s;
+    for (int64_t w0 = S; w0 < E; w0 += kNormWin) {
+      const int64_t w1 = w0 + kNormWin < E ? w0 + kNormWin : E;
+      if (__any_sync(kFull, pos < e && pos < w1)) {  // some light row has entries in this window
+#pragma unroll 4
+        for (int64_t i = w0 + lane; i < w1; i += 32) buf[i - w0] = oval[i];
+        __syncwarp();
+        const int64_t lim = e < w1 ? e : w1;
+        for (; pos + 4 <= lim; pos += 4) {  // loads ahead of the (ordered) adds
+          const double v0 = buf[pos - w0], v1 = buf[pos - w0 + 1], v2 = buf[pos - w0 + 2], v3 = buf[pos - w0 + 3];
+          d = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(d, v0), v1), v2), v3);
+        }
+        for (; pos < lim; pos++) d = __dadd_rn(d, buf[pos - w0]);
+        __syncwarp();
       }
-      for (; k < e; k++) d = __dadd_rn(d, oval[k]);
-      deg[r] = d;
     }
+    if (r < n && !heavy) deg[r] = d;
     for (unsigned hm = __ballot_sync(kFull, heavy); hm; hm &= hm - 1) {
       const int h = __ffs(hm) - 1;
       const int64_t hs = __shfl_sync(kFull, s, h), he = __shfl_sync(kFull, e, h);
-      double d = 0.0;
+      double hd = 0.0;
       double v = hs + lane < he ? oval[hs + lane] : 0.0;
       for (int64_t b = hs; b < he; b += 32) {
         const double nv = b + 32 + lane < he ? oval[b + 32 + lane] : 0.0;  // next chunk in flight
         const int m = static_cast<int>(he - b < 32 ? he - b : 32);
-        for (int i = 0; i < m; i++) d = __dadd_rn(d, __shfl_sync(kFull, v, i));
+        for (int i = 0; i < m; i++) hd = __dadd_rn(hd, __shfl_sync(kFull, v, i));
         v = nv;
       }
-      if (lane == h) deg[r] = d;
+      if (lane == h) deg[rb + h] = hd;
     }
   }
 }
@@ -419,7 +430,9 @@ void normalize_t(Ctx& ctx, const aires_b200_matrix& a, aires_b200_output& out) {
   if (n > 0) {
     k_norm_fill<IdxT, VIn, IdxO><<<grid_of(n * 32, 256, ctx.sms), 256, 0, ctx.stream>>>(s.ptr, s.base, col, val, n,
                                                                                        optr, ocol, oval, orow);
-    k_norm_degree<<<grid_of(n, 256, ctx.sms), 256, 0, ctx.stream>>>(optr, oval, n, deg);
+    k_norm_degree<<<static_cast<unsigned>(std::min<int64_t>((n + 32 * kNormWarps - 1) / (32 * kNormWarps),
+                                                            static_cast<int64_t>(ctx.sms) * 8)),
+                    kNormWarps * 32, 0, ctx.stream>>>(optr, oval, n, deg);
     if (flat)
       k_norm_scale_flat<IdxO, VO><<<grid_of(static_cast<int64_t>(nnz), 256, ctx.sms), 256, 0, ctx.stream>>>(
           orow, ocol, oval, deg, static_cast<int64_t>(nnz), outv);
