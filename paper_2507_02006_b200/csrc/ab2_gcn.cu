@@ -1035,7 +1035,11 @@ __global__ void __launch_bounds__(256) k_agg_t(const uint64_t* __restrict__ aptr
 #ifndef AB2_AGG_WARPS
 #define AB2_AGG_WARPS 4
 #endif
+#ifndef AB2_AGG_CH
+#define AB2_AGG_CH 32
+#endif
 constexpr int kAggWarps = AB2_AGG_WARPS, kAggStages = 2;  // (3 / 4 buffers: fewer warps, slower)
+constexpr int kAggCh = AB2_AGG_CH;  // entries per chunk (<= 32; cfg5 layer 2: 16 -> 6.54, 24 -> 6.18, 32 -> 6.20 ms)
 template <int TP>
 __global__ void __launch_bounds__(kAggWarps * 32) k_agg_t_cp(const uint64_t* __restrict__ aptr, uint64_t abase,
                                                           const uint32_t* __restrict__ acol,
@@ -1047,7 +1051,7 @@ __global__ void __launch_bounds__(kAggWarps * 32) k_agg_t_cp(const uint64_t* __r
   const int lane = lane_id();
   const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  float* const sb = agg_smem + (threadIdx.x >> 5) * (kAggStages * 32 * TP);
+  float* const sb = agg_smem + (threadIdx.x >> 5) * (kAggStages * kAggCh * TP);
   const int piece = lane & 15, half = lane >> 4;
   bool mine[JC];
 #pragma unroll
@@ -1071,7 +1075,7 @@ __global__ void __launch_bounds__(kAggWarps * 32) k_agg_t_cp(const uint64_t* __r
     cb = ce = -1;
     if (p_next()) {
       cb = p_b;
-      const int n = static_cast<int>(p_e - p_b < 32 ? p_e - p_b : 32);
+      const int n = static_cast<int>(p_e - p_b < kAggCh ? p_e - p_b : kAggCh);
       uint32_t k = 0;
       if (lane < n) {
         k = acol[p_b + lane];
@@ -1079,7 +1083,7 @@ __global__ void __launch_bounds__(kAggWarps * 32) k_agg_t_cp(const uint64_t* __r
         if (k >= K) a = 0.f, k = 0;
       }
       const uint32_t off = k * TP;
-      float* dst = sb + buf * (32 * TP) + piece * 4;
+      float* dst = sb + buf * (kAggCh * TP) + piece * 4;
 #pragma unroll 4
       for (int q = 0; q < n; q += 2) {
         const int qq = q + half;
@@ -1123,7 +1127,7 @@ __global__ void __launch_bounds__(kAggWarps * 32) k_agg_t_cp(const uint64_t* __r
         }
         const int q0 = static_cast<int>(s - cb0);
         const int q1 = static_cast<int>((e < ce0 ? e : ce0) - cb0);
-        const float* src = sb + buf * (32 * TP) + lane;
+        const float* src = sb + buf * (kAggCh * TP) + lane;
         int q = q0;
         for (; q + 8 <= q1; q += 8) {
           float x[8][JC], av[8];
@@ -1478,7 +1482,7 @@ void agg_t_launch(Ctx& ctx, const Staged& as, int64_t rows, int64_t K, const flo
 template <int TP>
 void agg_t_cp_launch(Ctx& ctx, const Staged& as, int64_t rows, int64_t K, const float* t, int64_t w_cols,
                      float* dense, int32_t* cnt) {
-  const int smem = kAggWarps * kAggStages * 32 * TP * static_cast<int>(sizeof(float));
+  const int smem = kAggWarps * kAggStages * kAggCh * TP * static_cast<int>(sizeof(float));
   auto k1 = k_agg_t_cp<TP>;
   AB2_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int nb = 0;
