@@ -256,6 +256,22 @@ def _gold_gcn():
     return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "gcn.npz"))
 
 
+@pytest.mark.parametrize("n,nnz,cap", [(60_000, 900_000, 3000), (5_000, 400_000, 5000)])
+def test_normalize_adjacency_matches_oracle_at_size(n, nnz, cap):
+    """normalize_adjacency on power-law graphs with hub rows (> 256 entries: the warp-summed degree
+    path) and warps whose 32 rows span several shared-memory windows: bit-identical to the oracle's
+    restatement of gcn.hpp:29-72, weighted edges (every value 1 + a random fraction)."""
+    a, _ = ab.synth_graph(n, nnz, degree_cap=cap, normalize=False, idx_dtype=np.uint64)
+    rng = np.random.default_rng(5)
+    a = ab.CsrMatrix(n, n, a.row_ptr, a.col_idx, 1.0 + rng.random(a.col_idx.size))
+    assert int(np.max(np.diff(a.row_ptr.astype(np.int64)))) > 256
+    t = ab.normalize_adjacency(a)
+    rc, (wp, wi, wv) = po.normalize_adjacency(n, a.row_ptr, a.col_idx, a.values)
+    assert rc == 0
+    assert np.array_equal(t.row_ptr, wp) and np.array_equal(t.col_idx, wi)
+    assert bits_equal(t.values, wv)
+
+
 def test_normalize_adjacency_matches_reference_goldens():
     """gcn.hpp:29-72 on the device: bit-identical to the reference (inserted and existing self loops,
     weighted edges, a 2-node graph)."""
