@@ -46,7 +46,11 @@ void launch_numeric_w(Ctx& ctx, const Num3Args<V, IdxT>& p, int threads, size_t 
 
 template <class V, class IdxT>
 int numeric_warps(const Num3Args<V, IdxT>& p) {
-  int nw = std::min<int>(static_cast<int>(option("num_warps", 4)), AB2_NUM_MAXT / 32);
+  // fp32 over 16-entry slots (walk_pair; cfg2): one-warp CTAs -- more resident warps, heavy rows one
+  // warp each -- measured 2.10 ms vs 2.13 (2 warps) and 2.20 (4 warps); fp64 is neutral and narrow
+  // slots (cfg3) prefer 4 (1.92 vs 1.94 ms at 2)
+  const int def = sizeof(V) == 4 && p.copies == 2 ? 1 : 4;
+  int nw = std::min<int>(static_cast<int>(option("num_warps", def)), AB2_NUM_MAXT / 32);
   return std::max(1, std::min<int>(nw, static_cast<int>((200 * 1024) / p.warp_bytes)));
 }
 
